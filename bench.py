@@ -1,0 +1,338 @@
+"""Benchmark of the sketch pass (BASELINE.json metric: sketch-pass GB/s of A).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2] [--precision auto|simt|tc]
+
+A step = one full sketch pass (Algorithm 4 steps 4-8) over the config's A,
+resident in HBM: every row pushed through libspca, H flushed, G widened,
+state finished on the device; with N > 1 ranks each rank owns its own row
+shard (weak scaling: the per-GPU shard is the config's full m) and the
+step ends with the NCCL all-reduce of [H | col_sums].
+
+The JSON line (rank 0) carries: value (whole-job GB/s of A), e2e (same
+metric through the public API with A in pinned host memory, H2D and the D2H
+of the sketch inside the timed region), roofline (dominant kernel group),
+cpu_baseline (the numpy oracle port on this host's cores, bounded sample),
+clocks sampled during the timed region, gpu_launches.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sketch-pass GB/s of A"
+UNIT = "GB/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="cfg2")
+    p.add_argument("--precision", default="auto")
+    p.add_argument("--rows", type=int, default=None, help="override m (debug)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-pca", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    except Exception:
+        return 6650.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                parts = [x.strip() for x in out.strip().split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_oracle_rate(n_rows: int, n: int, l: int, seed: int, threads: int):
+    """Time the numpy oracle (blocked sketch_pass, fp32 rows widened to fp64
+    as FileRowStream does) on a sample of rows; returns (GB/s of fp32 A, s)."""
+    from threadpoolctl import threadpool_limits
+    import oracle as O
+    rng = np.random.Generator(np.random.Philox(key=np.array([seed, 99], dtype=np.uint64)))
+    a = (rng.standard_normal((n_rows, n), dtype=np.float32) * np.float32(1e-2))
+    om = O.gaussian(n, l, 1)
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        blocks = ((r0, a[r0:r0 + 4096].astype(np.float64)) for r0 in range(0, n_rows, 4096))
+        O.oracle_sketch(blocks, om)
+        dt = time.perf_counter() - t0
+    return a.nbytes / dt / 1e9, dt
+
+
+def run_reference(args):
+    """Reference arm: the CPU implementation of the path (the oracle port —
+    the reference is pure Python/numpy and cannot be compiled), all host
+    threads, bounded sample of the same workload per step."""
+    world, rank, _ = dist_setup(args)
+    if rank != 0:
+        return
+    from paper_1704_07669_b200.synth import config_shape
+    cs = config_shape(args.config)
+    threads = os.cpu_count() or 1
+    sample_rows = 8192
+    rates, times = [], []
+    for i in range(args.warmup + args.steps):
+        r, dt = cpu_oracle_rate(sample_rows, cs["n"], cs["l"], seed=i, threads=threads)
+        if i >= args.warmup:
+            rates.append(r)
+            times.append(dt)
+    value = float(np.mean(rates))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{args.config} sample", "m": sample_rows, "n": cs["n"], "l": cs["l"],
+                   "block_rows": 4096},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample_rows} rows x {cs['n']} fp32 widened to fp64 per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+
+    import oracle as O  # noqa: F401  (only for the cpu_baseline leg below)
+    from paper_1704_07669_b200 import GpuSketch, PcaConfig, gaussian_matrix, synth
+    from paper_1704_07669_b200.parallel import allreduce_sketch
+
+    cs = synth.config_shape(args.config)
+    m = args.rows or cs["m"]
+    n, l = cs["n"], cs["l"]
+    bytes_per_rank = m * n * 4
+    hbm_peak, tc_peak, peak_kind = peaks()
+
+    # this rank's shard: rows [rank*m, (rank+1)*m) of the job's matrix
+    a = synth.config_matrix(args.config, device=dev, rows=(rank * m, (rank + 1) * m),
+                            m_override=m * world)
+    omega = gaussian_matrix(n, l, 1)
+    sk = GpuSketch(n, omega, np.float32, precision=args.precision, device=dev, rows_hint=m)
+    stream = torch.cuda.current_stream(dev)
+    launches0 = sk.kernel_launches()
+
+    def step():
+        sk.reset()
+        sk.push(a, 0)
+        g, h, c, rows = sk.finish(on_device=True)
+        if pg is not None:
+            allreduce_sketch(h, c, pg)
+        return g, h, c
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if pg is not None:
+        pg.barrier()
+    sk.enable_timing(True)
+    launches0 = sk.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if pg is not None:
+        pg.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = sk.kernel_launches() - launches0
+    kern_ms, kern_chunks = sk.kernel_time()
+    sk.enable_timing(False)
+    if pg is not None:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * bytes_per_rank / (ms_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel group (one canonical chunk: G, H contractions)
+    chunk_rows = sk.chunk_rows()
+    chunks_per_pass = -(-m // chunk_rows)
+    chunk_ms = kern_ms / max(1, kern_chunks)
+    avg_rows = m / chunks_per_pass
+    chunk_bytes = avg_rows * n * 4
+    achieved = chunk_bytes / (chunk_ms * 1e-3) / 1e9
+    flops = 4.0 * avg_rows * n * l
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None,
+                "peak_kind": peak_kind, "kernel": "sketch chunk (G = A Omega, H += A^T G, col sums)",
+                "chunk_rows": chunk_rows, "chunk_ms": chunk_ms,
+                "achieved_tflops": flops / (chunk_ms * 1e-3) / 1e12,
+                "algorithmic_bytes_per_chunk": chunk_bytes, "flops_per_chunk": flops}
+
+    out = {}
+    if rank == 0 and not args.no_e2e:
+        out["e2e"] = e2e_leg(args, a, omega, dev)
+    if rank == 0 and not args.no_pca:
+        out["pca_seconds"] = pca_leg(args, a, dev)
+    if rank == 0 and not args.no_cpu:
+        r, dt = cpu_oracle_rate(4096 * 2, n, l, seed=0, threads=os.cpu_count() or 1)
+        out["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+                               "sample": f"8192 rows x {n} fp32 (widened to fp64), numpy oracle sketch, "
+                                         f"{dt:.1f} s"}
+    sk.close()
+    if pg is not None:
+        pg.barrier()
+    if rank != 0:
+        if pg is not None:
+            pg.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.config, "m_per_gpu": m, "n": n, "l": l, "k": cs["k"],
+                   "rank": cs["rank"], "spectrum": cs["spectrum"], "noise": cs["noise"],
+                   "precision": args.precision, "parallelism": f"row-shard x{world}",
+                   "l2": "inputs larger than L2 (A is %.1f GB per GPU)" % (bytes_per_rank / 1e9)},
+        "roofline": roofline,
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "tflops": 4.0 * m * n * l * world / (ms_step * 1e-3) / 1e12,
+    }
+    line.update(out)
+    print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+def e2e_leg(args, a_dev, omega, dev, steps=3):
+    """Same metric through the public API: A in pinned host memory; each
+    step pushes it (H2D inside the library, overlapped with compute) and
+    reads the finished sketch back to the host."""
+    import torch
+    from paper_1704_07669_b200 import GpuSketch
+    m, n = a_dev.shape
+    host = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
+    host.copy_(a_dev)
+    torch.cuda.synchronize()
+    sk = GpuSketch(n, omega, np.float32, precision=args.precision, device=dev, rows_hint=m)
+    times = []
+    d2h = 0
+    for i in range(steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sk.reset()
+        sk.push(host, 0)
+        g, h, c, rows = sk.finish(on_device=False)
+        dt = time.perf_counter() - t0
+        d2h = g.nbytes + h.nbytes + c.nbytes
+        if i:
+            times.append(dt)
+    sk.close()
+    del host
+    t = float(np.median(times))
+    return {"value": m * n * 4 / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": m * n * 4,
+            "d2h_bytes_per_step": int(d2h), "seconds_per_step": t}
+
+
+def pca_leg(args, a_dev, dev):
+    """End-to-end PCA seconds (sketch + GPU post-pass) on the resident A."""
+    import torch
+    from paper_1704_07669_b200 import DeviceRowStream, PcaConfig, single_pass_pca
+    from paper_1704_07669_b200.synth import config_shape
+    cs = config_shape(args.config)
+    cfg = PcaConfig(k=cs["k"], oversample=cs["l"] - cs["k"], seed=1)
+    single_pass_pca(DeviceRowStream(a_dev), cfg, precision=args.precision, device=dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = single_pass_pca(DeviceRowStream(a_dev), cfg, precision=args.precision, device=dev)
+    torch.cuda.synchronize()
+    return {"value": time.perf_counter() - t0, "unit": "s", "k": cfg.k, "l": cfg.l,
+            "s0": float(res.s[0]), "includes": "Omega draw, sketch pass, QB, SVD, U/S/V to host"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,167 @@
+/*
+ * spca.h — C ABI of the B200 sketch pass (libspca.so).
+ *
+ * This is the drop-in boundary for the one hot path of the reference
+ * package `streampca` (arXiv 1704.07669, Algorithm 4 steps 4-8): the single
+ * streaming pass over A (m x n, row blocks A_i) that accumulates
+ *
+ *     G_i = A_i Omega          (m x l, one row per data row)
+ *     H  += A_i^T G_i          (n x l)
+ *     col_sums += 1^T A_i      (n)
+ *     rows_seen += rows(A_i)
+ *
+ * Entry points replace, one for one, the reference seam
+ *   sketch_pass(stream, omega, block_rows=None, fixed_order=False,
+ *               compensated=False) -> SketchState
+ * (/root/reference/pkg/src/streampca/sketch.py:52-116):
+ *   spca_sketch_create   <- argument checks + accumulator allocation, sketch.py:68-83
+ *   spca_sketch_push     <- one iteration of `for block in stream.blocks(...)`,
+ *                           _check_block sketch.py:40-49 and the two GEMMs +
+ *                           column sum sketch.py:102-113
+ *   spca_sketch_finish   <- `np.vstack(g_parts)` + SketchState(...), sketch.py:115-116
+ *   spca_center_correct  <- center_correct, sketch.py:119-139
+ *   spca_last_error      <- the exception taxonomy of errors.py:4-69
+ *                           (StreamFormatError / DataError(row=...))
+ * Plain pointers and sizes only; no torch or numpy types cross this line.
+ *
+ * Threading: a handle is single-consumer — one handle per
+ * host thread and per GPU. All work is ordered on the handle's CUDA stream.
+ *
+ * Determinism: the library re-chunks the pushed rows into canonical chunks
+ * of `spca_sketch_chunk_rows()` rows aligned to absolute row 0, and reduces
+ * every partial sum in a fixed order (no float atomics). Results are
+ * therefore bitwise identical for ANY sequence of push sizes and run to run
+ * — the GPU analogue of the reference's fixed_order contract
+ * (pkg/README.md:179-196, test_acceptance.py:223-255).
+ */
+#ifndef SPCA_H_
+#define SPCA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPCA_ABI_VERSION 1
+
+typedef struct spca_sketch *spca_handle_t;
+
+/* element type of A (and of the device-side G) */
+enum spca_dtype { SPCA_F32 = 0, SPCA_F64 = 1 };
+
+/* arithmetic used for the two contractions */
+enum spca_precision {
+  SPCA_PREC_AUTO = 0, /* best available: TC split for f32, DFMA for f64    */
+  SPCA_PREC_SIMT = 1, /* CUDA-core FFMA (f32) / DFMA (f64), fp32|fp64 accum */
+  SPCA_PREC_TC = 2    /* tcgen05 tensor cores, split precision (f32 only)   */
+};
+
+/* where a pointer lives */
+enum spca_mem {
+  SPCA_MEM_DEVICE = 0,   /* device memory of the handle's GPU               */
+  SPCA_MEM_PINNED = 1,   /* page-locked host memory (cudaHostAlloc/Register) */
+  SPCA_MEM_PAGEABLE = 2  /* ordinary host memory (staged through pinned)    */
+};
+
+/* status codes; the Python layer maps them onto errors.py classes */
+enum spca_status {
+  SPCA_OK = 0,
+  SPCA_ERR_FORMAT = 1,     /* StreamFormatError  (sketch.py:69-75, 41-44)   */
+  SPCA_ERR_DATA = 2,       /* DataError(row=)    (sketch.py:45-49)          */
+  SPCA_ERR_CAPABILITY = 3, /* CapabilityError    (errors.py:36-38)          */
+  SPCA_ERR_CONFIG = 4,     /* ConfigError        (errors.py:41-42)          */
+  SPCA_ERR_CUDA = 5,       /* CUDA runtime failure                           */
+  SPCA_ERR_OOM = 6,        /* device or pinned allocation failed             */
+  SPCA_ERR_STATE = 7,      /* call out of order (e.g. push after finish)     */
+  SPCA_ERR_EMPTY = 8       /* EmptyStreamError   (sketch.py:133-134)        */
+};
+
+/* Library version (SPCA_ABI_VERSION) and build info string. */
+int spca_abi_version(void);
+const char *spca_build_info(void);
+
+/* Create a sketch accumulator for A with n columns and sketch width l.
+ *  omega        : n x l row-major float64 test matrix (the reference draws it
+ *                 with linalg.gaussian_matrix, linalg.py:46-56); copied.
+ *  omega_where  : SPCA_MEM_DEVICE or a host kind.
+ *  device       : CUDA ordinal; stream: cudaStream_t (NULL = a private
+ *                 non-blocking stream owned by the handle).
+ *  rows_hint    : expected m (0 = unknown, G grows geometrically).
+ *  compensated  : Kahan summation of col_sums across chunks (sketch.py:82,107-111).
+ * Errors: SPCA_ERR_FORMAT for n<1 or l<1 (omega.ndim != 2, sketch.py:69-70). */
+int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype,
+                       int precision, const double *omega, int omega_where,
+                       int device, void *stream, int64_t rows_hint,
+                       int compensated);
+
+/* Append `rows` rows of A (row stride `ld` elements, ld >= n) whose first
+ * row is absolute row `first_row`, which must equal the rows pushed so far
+ * (RowStream blocks are consecutive, streams.py:31-52).
+ * Asynchronous: device and pinned sources must stay valid until the next
+ * spca_sketch_sync / finish. Non-finite values are detected on the device;
+ * the first offending absolute row is reported by sync/finish as
+ * SPCA_ERR_DATA (DataError(row=...), sketch.py:45-49). */
+int spca_sketch_push(spca_handle_t h, const void *a, int64_t rows, int64_t ld,
+                     int64_t first_row, int where);
+
+/* Start a new pass on the same handle (same n, l, Omega): zero the
+ * accumulators and the row counter, keep every allocation. Lets a caller
+ * run repeated passes (or a second pass of power_refine with the same Omega)
+ * without re-uploading Omega. */
+int spca_sketch_reset(spca_handle_t h);
+
+/* Wait for all queued work; returns SPCA_ERR_DATA if a non-finite row was seen. */
+int spca_sketch_sync(spca_handle_t h);
+
+/* Rows accepted so far (rows_seen) and the canonical chunk size. */
+int spca_sketch_rows(spca_handle_t h, int64_t *rows_seen);
+int64_t spca_sketch_chunk_rows(spca_handle_t h);
+
+/* Complete the pass and copy the state out in float64:
+ *   g_out  rows_seen x l row-major, h_out n x l row-major, colsum_out n.
+ * Any output pointer may be NULL (skipped). out_where: device or host.
+ * After finish the handle accepts no more pushes (it may still be read
+ * again with finish or used by spca_center_correct / spca_device_views). */
+int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out,
+                       double *colsum_out, int64_t *rows_seen, int out_where);
+
+/* Device views of the accumulators after finish (for the GPU post-pass and
+ * for an NCCL all-reduce of [H | colsum] across ranks). H and colsum are
+ * one contiguous float64 buffer of n*(l+1) elements: H row-major n x l,
+ * then colsum. G is float64 rows_seen x l. Pointers stay owned by h. */
+int spca_device_views(spca_handle_t h, double **g_dev, double **hcs_dev);
+
+
+/* center_correct (sketch.py:119-139) on the finished device state, in
+ * place: mu = colsum / m_total; G -= 1 (mu^T Omega); H -= mu (1^T G) where
+ * 1^T G is `gsum` (l values, already summed over every rank's rows; NULL =
+ * use this handle's own G); colsum <- 0. m_total = rows over all ranks.
+ * Writes mu (n values) to mean_out if non-NULL (host or device per where). */
+int spca_center_correct(spca_handle_t h, int64_t m_total, const double *gsum,
+                        double *mean_out, int mean_where);
+
+/* Column sums of the finished G (l values, float64) — for center_correct. */
+int spca_g_colsum(spca_handle_t h, double *out, int out_where);
+
+/* Last error of the handle (or of the calling thread when h == NULL):
+ * code, offending absolute row (or -1) and a message. */
+int spca_last_error(spca_handle_t h, int *code, int64_t *bad_row, char *msg,
+                    size_t msg_len);
+
+/* Number of kernels this handle launched so far (bench evidence). */
+int64_t spca_kernel_launches(spca_handle_t h);
+
+/* Device time (ms) spent in the dominant kernel (the contraction kernels),
+ * measured with CUDA events on the handle's stream when timing is enabled. */
+int spca_enable_kernel_timing(spca_handle_t h, int enable);
+int spca_kernel_time_ms(spca_handle_t h, double *ms, int64_t *launches);
+
+void spca_sketch_destroy(spca_handle_t h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPCA_H_ */

@@ -1,0 +1,221 @@
+"""Public single-pass PCA entry point, B200 edition.
+
+Signature- and result-compatible with the reference's ``single_pass_pca``
+(/root/reference/pkg/src/streampca/algorithms.py:165-204): same
+``PcaConfig`` (:52-101), same ``TruncatedSvd`` (:104-119), same Omega
+(Philox(seed, STREAM_SKETCH)), same error classes. The pass runs in
+libspca.so and the post-pass (blocked QB, small SVD, U = Q U~, sign
+convention) runs on the GPU in float64; only U, S, V (and the mean) come
+back to the host.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional, Union
+
+import numpy as np
+
+from .device import default_device, to_device64, torch_mod
+from .errors import ConfigError, EmptyStreamError
+from .linalg import STREAM_SKETCH, dense_svd, gaussian_matrix, qr_unpivoted, sign_align
+from .qb import QbFactor, blocked_qb
+from .sketch import SketchState, _omega_as_used, run_pass, sketch_pass
+from .streams import ArrayRowStream, PassCounter, RowStream
+
+
+@dataclass(frozen=True)
+class PcaConfig:
+    """k, oversample, block_size, power, seed, center — the reference's knobs
+    with its validation (algorithms.py:52-101); l = b * ceil((k + p) / b)."""
+
+    k: int
+    oversample: int = 10
+    block_size: int = 10
+    power: int = 0
+    seed: int = 0
+    center: bool = False
+
+    def __post_init__(self):
+        if self.k < 1:
+            raise ConfigError(f"target rank k must be >= 1, got {self.k}")
+        if self.oversample < 0:
+            raise ConfigError(f"oversample must be >= 0, got {self.oversample}")
+        if self.block_size < 1:
+            raise ConfigError(f"block_size must be >= 1, got {self.block_size}")
+        if self.power not in (0, 1):
+            raise ConfigError(f"power must be 0 or 1, got {self.power}")
+        if self.seed < 0:
+            raise ConfigError(f"seed must be >= 0, got {self.seed}")
+
+    @property
+    def l(self) -> int:
+        return self.block_size * math.ceil((self.k + self.oversample) / self.block_size)
+
+    @property
+    def n_blocks(self) -> int:
+        return self.l // self.block_size
+
+    def validate_dims(self, n_cols: int, n_rows: Optional[int] = None) -> None:
+        limit = n_cols if n_rows is None else min(n_rows, n_cols)
+        if self.k > limit:
+            raise ConfigError(f"target rank k={self.k} exceeds min(m, n)={limit}")
+        if self.l > limit:
+            raise ConfigError(
+                f"sketch width l={self.l} (k + oversample rounded up to a block multiple) "
+                f"exceeds min(m, n)={limit}; lower oversample or block_size")
+
+
+@dataclass(frozen=True)
+class TruncatedSvd:
+    """A ~ u diag(s) v^T (algorithms.py:104-119); numpy float64 arrays."""
+
+    u: np.ndarray
+    s: np.ndarray
+    v: np.ndarray
+    mean: Optional[np.ndarray] = None
+    passes: Optional[int] = None
+    retained_floats: Optional[int] = None
+    warnings: tuple = ()
+
+    @property
+    def k(self) -> int:
+        return int(self.s.shape[0])
+
+
+MatrixOrStream = Union[np.ndarray, RowStream]
+
+
+def as_row_stream(data) -> RowStream:
+    """Streams pass through; arrays become ArrayRowStream (float32 kept),
+    CUDA tensors DeviceRowStream, host tensors PinnedRowStream."""
+    if hasattr(data, "blocks") and hasattr(data, "n_cols"):
+        return data
+    try:
+        import torch
+        if isinstance(data, torch.Tensor):
+            from .streams import DeviceRowStream, PinnedRowStream
+            return DeviceRowStream(data) if data.is_cuda else PinnedRowStream(data)
+    except ImportError:  # pragma: no cover
+        pass
+    return ArrayRowStream(data)
+
+
+def _measured_passes(stream, fallback: int) -> int:
+    return stream.passes_completed if isinstance(stream, PassCounter) else fallback
+
+
+def finish_svd(factor: QbFactor, k: int):
+    """_finish (algorithms.py:144-162) on the device: SVD of B, U = Q U~[:, :k],
+    V = V~[:, :k], sign convention; returns CUDA tensors (u, s, v)."""
+    small = dense_svd(factor.b)
+    u = factor.q @ small.u[:, :k]
+    v = small.v[:, :k]
+    u, v = sign_align(u, v)
+    return u, small.s[:k].clone(), v
+
+
+def single_pass_pca(
+    data: MatrixOrStream,
+    cfg: PcaConfig,
+    block_rows: Optional[int] = None,
+    fixed_order: bool = False,
+    on_deficiency: str = "repair",
+    compensated: bool = False,
+    *,
+    precision: str = "auto",
+    device=None,
+    return_device: bool = False,
+) -> TruncatedSvd:
+    """Truncated SVD / PCA from exactly one traversal of the rows
+    (algorithms.py:165-204), sketch and post-pass on the GPU."""
+    stream = as_row_stream(data)
+    if cfg.power != 0:
+        raise ConfigError("single_pass_pca runs at power 0; use power_refine for power 1")
+    if stream.n_rows == 0:
+        raise EmptyStreamError("the stream has no rows")
+    cfg.validate_dims(stream.n_cols, stream.n_rows)
+    dev = default_device(device)
+    omega = gaussian_matrix(stream.n_cols, cfg.l, cfg.seed, stream=STREAM_SKETCH)
+    state = sketch_pass(stream, omega, block_rows=block_rows, fixed_order=fixed_order,
+                        compensated=compensated, precision=precision, device=dev,
+                        keep_on_device=True)
+    if state.rows_seen == 0:
+        raise EmptyStreamError("the stream yielded no rows")
+    cfg.validate_dims(stream.n_cols, state.rows_seen)
+    return _post_pass(state, cfg, stream, on_deficiency, return_device, passes_fallback=1)
+
+
+def _post_pass(state: SketchState, cfg: PcaConfig, stream, on_deficiency, return_device,
+               passes_fallback: int) -> TruncatedSvd:
+    from .sketch import center_correct
+    mean = None
+    if cfg.center:
+        mean = state.col_sums / state.rows_seen
+        state = center_correct(state, state.omega)
+    factor = blocked_qb(state.g, state.h, state.omega, cfg.block_size,
+                        on_deficiency=on_deficiency, repair_seed=cfg.seed)
+    u, s, v = finish_svd(factor, cfg.k)
+    retained = state.retained_floats + int(state.omega.numel())
+    if not return_device:
+        u, s, v = u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
+        mean = mean.cpu().numpy() if mean is not None else None
+    return TruncatedSvd(u=u, s=s, v=v, mean=mean,
+                        passes=_measured_passes(stream, passes_fallback),
+                        retained_floats=retained)
+
+
+def power_refine(
+    data: MatrixOrStream,
+    cfg: PcaConfig,
+    block_rows: Optional[int] = None,
+    fixed_order: bool = False,
+    on_deficiency: str = "repair",
+    *,
+    precision: str = "auto",
+    device=None,
+    return_device: bool = False,
+) -> TruncatedSvd:
+    """Power-sharpened variant (algorithms.py:266-309): pass 1 sketches with
+    Omega and keeps H; Omega2 = orth(H) (on the GPU) drives pass 2 through
+    the same kernels."""
+    from .errors import CapabilityError
+    from .sketch import center_correct
+    stream = as_row_stream(data)
+    if cfg.power != 1:
+        raise ConfigError("power_refine requires power = 1 in the config")
+    if not stream.resettable:
+        raise CapabilityError("power_refine needs a resettable stream (two passes)")
+    if stream.n_rows == 0:
+        raise EmptyStreamError("the stream has no rows")
+    cfg.validate_dims(stream.n_cols, stream.n_rows)
+    dev = default_device(device)
+    omega = gaussian_matrix(stream.n_cols, cfg.l, cfg.seed, stream=STREAM_SKETCH)
+    first = sketch_pass(stream, omega, block_rows=block_rows, precision=precision,
+                        device=dev, keep_on_device=True)
+    if first.rows_seen == 0:
+        raise EmptyStreamError("the stream yielded no rows")
+    cfg.validate_dims(stream.n_cols, first.rows_seen)
+    mean = first.col_sums / first.rows_seen if cfg.center else None
+    if cfg.center:
+        first = center_correct(first, first.omega)
+    omega2 = qr_unpivoted(first.h, rank_check=False, device=dev).q
+    second = sketch_pass(stream, omega2.cpu().numpy(), block_rows=block_rows, precision=precision,
+                         device=dev, keep_on_device=True)
+    if cfg.center:
+        second = center_correct(second, second.omega)
+    factor = blocked_qb(second.g, second.h, second.omega, cfg.block_size,
+                        on_deficiency=on_deficiency, repair_seed=cfg.seed)
+    u, s, v = finish_svd(factor, cfg.k)
+    retained = second.retained_floats + int(second.omega.numel())
+    if not return_device:
+        u, s, v = u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
+        mean = mean.cpu().numpy() if mean is not None else None
+    return TruncatedSvd(u=u, s=s, v=v, mean=mean, passes=_measured_passes(stream, 2),
+                        retained_floats=retained)
+
+
+def principal_components(svd: TruncatedSvd) -> list:
+    """Columns of V in order (algorithms.py:395-398)."""
+    return [np.asarray(svd.v)[:, j].copy() for j in range(svd.v.shape[1])]

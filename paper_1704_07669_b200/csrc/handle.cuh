@@ -1,0 +1,75 @@
+// handle.cuh — the state behind an spca_handle_t (one GPU, one consumer).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/spca.h"
+
+namespace spca {
+struct Timer {
+  cudaEvent_t start = nullptr, stop = nullptr;
+};
+}  // namespace spca
+
+struct spca_sketch {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaStream_t copy_stream = nullptr;
+  int dtype = SPCA_F32;
+  int precision = SPCA_PREC_SIMT;
+  size_t ds = 4;
+  int64_t n = 0, l = 0, lpad = 0;
+  int bl = 64;
+  bool compensated = false;
+
+  void *omega_dev = nullptr;     // n x lpad compute precision
+  double *omega64_dev = nullptr; // n x l fp64, exactly the values used
+  void *tc_omega = nullptr;      // tensor-core operand layout (sketch_tc.cuh)
+
+  void *g_dev = nullptr;         // cap x lpad compute precision
+  int64_t g_cap = 0;
+  double *g64_dev = nullptr;     // rows x l after finish
+  int64_t g64_cap = 0;
+  double *hcs_dev = nullptr;     // n*l H then n colsum
+  double *carry_dev = nullptr;   // Kahan carry (n)
+  void *hpart = nullptr;         // [hsplit][n][lpad]
+  int hsplit = 1;
+  double *cspart = nullptr;      // [hsplit][n]
+  void *gpart = nullptr;         // P1 split-K partials
+  int64_t gpart_elems = 0;
+  void *tc_ws = nullptr;         // tensor-core workspace
+  size_t tc_ws_bytes = 0;
+  unsigned long long *bad_dev = nullptr;
+
+  int64_t chunk_rows = 0;        // canonical chunk (R0)
+  void *tail = nullptr;          // R0 x n staging for the partial chunk
+  int64_t tail_rows = 0;
+  int64_t rows_seen = 0;         // accepted
+  int64_t rows_done = 0;         // processed
+  int chunks_since_flush = 0;
+  int flush_every = 64;
+  bool finished = false;
+
+  // host staging (pinned double buffer)
+  void *pinned[2] = {nullptr, nullptr};
+  void *dstage[2] = {nullptr, nullptr};
+  int64_t stage_rows = 0;
+  cudaEvent_t copy_done[2] = {nullptr, nullptr};
+  cudaEvent_t comp_done[2] = {nullptr, nullptr};
+  bool stage_used[2] = {false, false};
+  int stage_idx = 0;
+
+  int64_t launches = 0;
+  bool timing = false;
+  std::vector<spca::Timer> timers;     // pending per-chunk timers
+  double kernel_ms = 0.0;
+  int64_t timed_chunks = 0;
+
+  int last_code = SPCA_OK;
+  int64_t last_bad_row = -1;
+  char last_msg[512] = {0};
+};

@@ -1,0 +1,705 @@
+// spca_capi.cu — the C ABI of libspca.so (see include/spca.h).
+//
+// Owns the sketch accumulators on one GPU, re-chunks pushed rows into
+// canonical chunks, stages host rows through pinned double buffers on a
+// copy stream (host streaming) and launches the contraction
+// kernels per chunk on the handle's compute stream.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/spca.h"
+#include "common.cuh"
+#include "epilogue.cuh"
+#include "sketch_simt.cuh"
+#include "handle.cuh"
+
+using namespace spca;
+
+namespace {
+
+thread_local int g_tl_code = SPCA_OK;
+thread_local char g_tl_msg[512] = {0};
+
+int set_err(spca_sketch *h, int code, int64_t row, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) {
+    h->last_code = code;
+    h->last_bad_row = row;
+    snprintf(h->last_msg, sizeof h->last_msg, "%s", buf);
+  }
+  g_tl_code = code;
+  snprintf(g_tl_msg, sizeof g_tl_msg, "%s", buf);
+  return code;
+}
+
+#define CK(h, call)                                                                        \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      return set_err((h), _e == cudaErrorMemoryAllocation ? SPCA_ERR_OOM : SPCA_ERR_CUDA,  \
+                     -1, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, \
+                     __LINE__);                                                            \
+    }                                                                                      \
+  } while (0)
+
+#define CK_LAUNCH(h)                                                                       \
+  do {                                                                                     \
+    cudaError_t _e = cudaGetLastError();                                                   \
+    if (_e != cudaSuccess)                                                                 \
+      return set_err((h), SPCA_ERR_CUDA, -1, "kernel launch failed: %s (%s:%d)",          \
+                     cudaGetErrorString(_e), __FILE__, __LINE__);                          \
+    (h)->launches++;                                                                       \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int grid_for(int64_t count, int threads = 256) {
+  int64_t b = ceil_div(count, threads);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
+}
+
+int ensure_g(spca_sketch *h, int64_t rows_needed) {
+  if (rows_needed <= h->g_cap) return SPCA_OK;
+  int64_t cap = std::max<int64_t>(rows_needed, std::max<int64_t>(h->g_cap * 2, 4096));
+  void *nb = nullptr;
+  CK(h, cudaMalloc(&nb, (size_t)cap * h->lpad * h->ds));
+  if (h->g_dev && h->rows_done > 0) {
+    CK(h, cudaMemcpyAsync(nb, h->g_dev, (size_t)h->rows_done * h->lpad * h->ds,
+                          cudaMemcpyDeviceToDevice, h->stream));
+  }
+  if (h->g_dev) {
+    CK(h, cudaStreamSynchronize(h->stream));
+    cudaFree(h->g_dev);
+  }
+  h->g_dev = nb;
+  h->g_cap = cap;
+  return SPCA_OK;
+}
+
+}  // namespace
+
+// tensor-core path (uses set_err / CK / grid_for above)
+#include "sketch_tc.cuh"
+
+namespace {
+
+// ---- SIMT chunk processing ------------------------------------------------
+
+template <typename T, int BM, int BL, bool VEC>
+void launch_g(spca_sketch *h, const T *a, int64_t lda, int rows, T *out, int64_t out_stride,
+              int ksplit, int kseg) {
+  dim3 grid((unsigned)ceil_div(rows, BM), (unsigned)(h->lpad / BL), (unsigned)ksplit);
+  simt_g_kernel<T, BM, BL, (sizeof(T) == 4 ? 32 : 16), VEC><<<grid, kSimtThreads, 0, h->stream>>>(
+      a, lda, rows, (int)h->n, (const T *)h->omega_dev, (int)h->lpad, out, (int)h->lpad,
+      out_stride, kseg, h->rows_done, h->bad_dev);
+}
+
+template <typename T, int BN, int BL, bool VEC>
+void launch_h(spca_sketch *h, const T *a, int64_t lda, int rows, const T *g, int rseg, int accumulate) {
+  dim3 grid((unsigned)ceil_div(h->n, BN), (unsigned)(h->lpad / BL), (unsigned)h->hsplit);
+  simt_h_kernel<T, BN, BL, (sizeof(T) == 4 ? 32 : 16), VEC><<<grid, kSimtThreads, 0, h->stream>>>(
+      a, lda, rows, (int)h->n, g, (int)h->lpad, (T *)h->hpart, (int)h->lpad,
+      (int64_t)h->n * h->lpad, h->cspart, rseg, accumulate, h->compensated ? 1 : 0);
+}
+
+template <typename T>
+int simt_chunk(spca_sketch *h, const T *a, int64_t lda, int rows) {
+  constexpr int VN = Vec<T>::n;
+  const bool vec = (lda % VN == 0) && (h->n % VN == 0) &&
+                   ((reinterpret_cast<uintptr_t>(a) % 16) == 0);
+  const bool narrow = (h->bl == 32);
+  const int bm = narrow ? 128 : 64;
+  // split-K so that the G kernel fills the machine (~4 CTAs per SM)
+  int64_t tiles = ceil_div(rows, bm) * (h->lpad / h->bl);
+  int64_t kmax = std::max<int64_t>(1, ceil_div(h->n, 128));
+  int ksplit = (int)std::min<int64_t>(kmax, std::max<int64_t>(1, ceil_div(148 * 4, tiles)));
+  int kseg = (int)round_up(ceil_div(h->n, ksplit), 32);
+  ksplit = (int)ceil_div(h->n, kseg);
+  T *gout = (T *)h->g_dev + h->rows_done * h->lpad;
+  T *p1_out = gout;
+  int64_t p1_stride = 0;
+  if (ksplit > 1) {
+    int64_t need = (int64_t)ksplit * rows * h->lpad;
+    if (need > h->gpart_elems) {
+      if (h->gpart) {
+        CK(h, cudaStreamSynchronize(h->stream));
+        cudaFree(h->gpart);
+      }
+      h->gpart = nullptr;
+      CK(h, cudaMalloc(&h->gpart, (size_t)need * h->ds));
+      h->gpart_elems = need;
+    }
+    p1_out = (T *)h->gpart;
+    p1_stride = (int64_t)rows * h->lpad;
+  }
+  if (narrow) {
+    if (vec) launch_g<T, 128, 32, true>(h, a, lda, rows, p1_out, p1_stride, ksplit, kseg);
+    else launch_g<T, 128, 32, false>(h, a, lda, rows, p1_out, p1_stride, ksplit, kseg);
+  } else {
+    if (vec) launch_g<T, 64, 64, true>(h, a, lda, rows, p1_out, p1_stride, ksplit, kseg);
+    else launch_g<T, 64, 64, false>(h, a, lda, rows, p1_out, p1_stride, ksplit, kseg);
+  }
+  CK_LAUNCH(h);
+  if (ksplit > 1) {
+    int64_t count = (int64_t)rows * h->lpad;
+    simt_g_reduce<T><<<grid_for(count), 256, 0, h->stream>>>((const T *)h->gpart, ksplit,
+                                                              p1_stride, count, gout);
+    CK_LAUNCH(h);
+  }
+  int rseg = (int)round_up(ceil_div(rows, h->hsplit), 32);
+  int acc = h->chunks_since_flush > 0 ? 1 : 0;
+  if (narrow) {
+    if (vec) launch_h<T, 128, 32, true>(h, a, lda, rows, gout, rseg, acc);
+    else launch_h<T, 128, 32, false>(h, a, lda, rows, gout, rseg, acc);
+  } else {
+    if (vec) launch_h<T, 64, 64, true>(h, a, lda, rows, gout, rseg, acc);
+    else launch_h<T, 64, 64, false>(h, a, lda, rows, gout, rseg, acc);
+  }
+  CK_LAUNCH(h);
+  return SPCA_OK;
+}
+
+int flush_h(spca_sketch *h) {
+  if (h->chunks_since_flush == 0) return SPCA_OK;
+  int64_t count = h->n * h->l;
+  if (h->dtype == SPCA_F32)
+    h_flush<float><<<grid_for(count), 256, 0, h->stream>>>(
+        (const float *)h->hpart, h->hsplit, h->n * h->lpad, (int)h->n, (int)h->l, (int)h->lpad,
+        h->hcs_dev);
+  else
+    h_flush<double><<<grid_for(count), 256, 0, h->stream>>>(
+        (const double *)h->hpart, h->hsplit, h->n * h->lpad, (int)h->n, (int)h->l, (int)h->lpad,
+        h->hcs_dev);
+  CK_LAUNCH(h);
+  h->chunks_since_flush = 0;
+  return SPCA_OK;
+}
+
+int process_chunk(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
+  if (rows <= 0) return SPCA_OK;
+  int rc = ensure_g(h, h->rows_done + rows);
+  if (rc) return rc;
+  Timer tm;
+  if (h->timing) {
+    CK(h, cudaEventCreate(&tm.start));
+    CK(h, cudaEventCreate(&tm.stop));
+    CK(h, cudaEventRecord(tm.start, h->stream));
+  }
+  if (h->precision == SPCA_PREC_TC) {
+    rc = tc_chunk(h, a, lda, (int)rows);
+  } else if (h->dtype == SPCA_F32) {
+    rc = simt_chunk<float>(h, (const float *)a, lda, (int)rows);
+  } else {
+    rc = simt_chunk<double>(h, (const double *)a, lda, (int)rows);
+  }
+  if (rc) return rc;
+  colsum_accumulate<<<(unsigned)ceil_div(h->n, 256), 256, 0, h->stream>>>(
+      h->cspart, h->hsplit, (int)h->n, h->hcs_dev + h->n * h->l,
+      h->compensated ? h->carry_dev : nullptr);
+  CK_LAUNCH(h);
+  h->chunks_since_flush++;
+  if (h->chunks_since_flush >= h->flush_every) {
+    rc = flush_h(h);
+    if (rc) return rc;
+  }
+  if (h->timing) {
+    CK(h, cudaEventRecord(tm.stop, h->stream));
+    h->timers.push_back(tm);
+  }
+  h->rows_done += rows;
+  return SPCA_OK;
+}
+
+// Rows already on the device: feed canonical chunks, keep the remainder in `tail`.
+int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda) {
+  const int64_t R0 = h->chunk_rows;
+  const size_t row_bytes = (size_t)h->n * h->ds;
+  int64_t off = 0;
+  if (h->tail_rows > 0) {
+    int64_t take = std::min(R0 - h->tail_rows, rows);
+    CK(h, cudaMemcpy2DAsync((char *)h->tail + h->tail_rows * row_bytes, row_bytes, a,
+                            (size_t)lda * h->ds, row_bytes, (size_t)take,
+                            cudaMemcpyDeviceToDevice, h->stream));
+    h->tail_rows += take;
+    off = take;
+    if (h->tail_rows == R0) {
+      int rc = process_chunk(h, h->tail, h->n, R0);
+      if (rc) return rc;
+      h->tail_rows = 0;
+    }
+  }
+  while (rows - off >= R0) {
+    int rc = process_chunk(h, a + (size_t)off * lda * h->ds, lda, R0);
+    if (rc) return rc;
+    off += R0;
+  }
+  if (off < rows) {
+    int64_t rem = rows - off;
+    CK(h, cudaMemcpy2DAsync((char *)h->tail, row_bytes, a + (size_t)off * lda * h->ds,
+                            (size_t)lda * h->ds, row_bytes, (size_t)rem,
+                            cudaMemcpyDeviceToDevice, h->stream));
+    h->tail_rows = rem;
+  }
+  return SPCA_OK;
+}
+
+int ensure_staging(spca_sketch *h, bool need_pinned) {
+  const size_t bytes = (size_t)h->stage_rows * h->n * h->ds;
+  for (int i = 0; i < 2; ++i) {
+    if (!h->dstage[i]) CK(h, cudaMalloc(&h->dstage[i], bytes));
+    if (!h->copy_done[i]) CK(h, cudaEventCreateWithFlags(&h->copy_done[i], cudaEventDisableTiming));
+    if (!h->comp_done[i]) CK(h, cudaEventCreateWithFlags(&h->comp_done[i], cudaEventDisableTiming));
+    if (need_pinned && !h->pinned[i]) CK(h, cudaHostAlloc(&h->pinned[i], bytes, cudaHostAllocDefault));
+  }
+  if (!h->copy_stream) CK(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  return SPCA_OK;
+}
+
+int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, bool pageable) {
+  int rc = ensure_staging(h, pageable);
+  if (rc) return rc;
+  const size_t row_bytes = (size_t)h->n * h->ds;
+  int64_t off = 0;
+  while (off < rows) {
+    int64_t take = std::min(h->stage_rows, rows - off);
+    int i = h->stage_idx;
+    h->stage_idx ^= 1;
+    // the device buffer i is free once the compute that read it is done
+    if (h->stage_used[i]) CK(h, cudaStreamWaitEvent(h->copy_stream, h->comp_done[i], 0));
+    const char *src = a + (size_t)off * lda * h->ds;
+    if (pageable) {
+      if (h->stage_used[i]) CK(h, cudaEventSynchronize(h->copy_done[i]));
+      char *dst = (char *)h->pinned[i];
+      if ((size_t)lda * h->ds == row_bytes) {
+        memcpy(dst, src, (size_t)take * row_bytes);
+      } else {
+        for (int64_t r = 0; r < take; ++r)
+          memcpy(dst + r * row_bytes, src + (size_t)r * lda * h->ds, row_bytes);
+      }
+      src = dst;
+      CK(h, cudaMemcpyAsync(h->dstage[i], src, (size_t)take * row_bytes, cudaMemcpyHostToDevice,
+                            h->copy_stream));
+    } else {
+      CK(h, cudaMemcpy2DAsync(h->dstage[i], row_bytes, src, (size_t)lda * h->ds, row_bytes,
+                              (size_t)take, cudaMemcpyHostToDevice, h->copy_stream));
+    }
+    CK(h, cudaEventRecord(h->copy_done[i], h->copy_stream));
+    CK(h, cudaStreamWaitEvent(h->stream, h->copy_done[i], 0));
+    rc = push_device_rows(h, (const char *)h->dstage[i], take, h->n);
+    if (rc) return rc;
+    CK(h, cudaEventRecord(h->comp_done[i], h->stream));
+    h->stage_used[i] = true;
+    off += take;
+  }
+  return SPCA_OK;
+}
+
+int collect_timers(spca_sketch *h) {
+  for (auto &t : h->timers) {
+    float ms = 0.f;
+    CK(h, cudaEventElapsedTime(&ms, t.start, t.stop));
+    h->kernel_ms += ms;
+    h->timed_chunks++;
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.stop);
+  }
+  h->timers.clear();
+  return SPCA_OK;
+}
+
+int check_bad_row(spca_sketch *h) {
+  unsigned long long bad = 0;
+  CK(h, cudaMemcpyAsync(&bad, h->bad_dev, sizeof bad, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (bad != (unsigned long long)kNoBadRow) {
+    return set_err(h, SPCA_ERR_DATA, (int64_t)bad, "non-finite value in row %lld", (long long)bad);
+  }
+  return SPCA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spca_abi_version(void) { return SPCA_ABI_VERSION; }
+
+const char *spca_build_info(void) {
+  return "libspca sm_100a: SIMT(FFMA/DFMA) + tcgen05 split-precision sketch; " __DATE__ " " __TIME__;
+}
+
+int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int precision,
+                       const double *omega, int omega_where, int device, void *stream,
+                       int64_t rows_hint, int compensated) {
+  if (!out) return set_err(nullptr, SPCA_ERR_CONFIG, -1, "null handle pointer");
+  *out = nullptr;
+  if (n < 1 || l < 1) return set_err(nullptr, SPCA_ERR_FORMAT, -1, "omega must be 2-d and non-empty (n=%lld, l=%lld)", (long long)n, (long long)l);
+  if (l > 256) return set_err(nullptr, SPCA_ERR_CONFIG, -1, "sketch width l=%lld > 256 unsupported", (long long)l);
+  if (n > INT32_MAX / 2) return set_err(nullptr, SPCA_ERR_CONFIG, -1, "n too large");
+  if (dtype != SPCA_F32 && dtype != SPCA_F64) return set_err(nullptr, SPCA_ERR_CONFIG, -1, "bad dtype %d", dtype);
+  if (!omega) return set_err(nullptr, SPCA_ERR_FORMAT, -1, "omega is null");
+  if (precision == SPCA_PREC_AUTO) precision = (dtype == SPCA_F32 && tc_available(device)) ? SPCA_PREC_TC : SPCA_PREC_SIMT;
+  if (precision == SPCA_PREC_TC && dtype != SPCA_F32)
+    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "tensor-core path is f32 only (fp64 uses DFMA)");
+  if (precision == SPCA_PREC_TC && !tc_supported_shape(n, l))
+    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "tensor-core path does not support n=%lld l=%lld", (long long)n, (long long)l);
+
+  spca_sketch *h = new (std::nothrow) spca_sketch();
+  if (!h) return set_err(nullptr, SPCA_ERR_OOM, -1, "out of host memory");
+  h->device = device;
+  DeviceGuard dg(device);
+  h->dtype = dtype;
+  h->precision = precision;
+  h->ds = dtype == SPCA_F32 ? 4 : 8;
+  h->n = n;
+  h->l = l;
+  h->bl = l <= 32 ? 32 : 64;
+  h->lpad = round_up(l, h->bl);
+  h->compensated = compensated != 0;
+  auto fail = [&](int rc) {
+    spca_sketch_destroy(h);
+    g_tl_code = rc;
+    return rc;
+  };
+  if (stream) {
+    h->stream = (cudaStream_t)stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(set_err(nullptr, SPCA_ERR_CUDA, -1, "stream create failed"));
+    h->own_stream = true;
+  }
+  // canonical chunk: ~160 MB of A, 64..4096 rows, multiple of 128
+  {
+    int64_t r = (int64_t)(160ll << 20) / (n * (int64_t)h->ds);
+    r = std::max<int64_t>(128, std::min<int64_t>(4096, r));
+    h->chunk_rows = (r / 128) * 128;
+    if (h->precision == SPCA_PREC_TC) h->chunk_rows = tc_chunk_rows(n, l);
+  }
+  h->stage_rows = h->chunk_rows;
+  // row splits of the H kernel: enough CTAs with the n tiles
+  {
+    int bn = h->bl == 32 ? 128 : 64;
+    int64_t tiles = ceil_div(n, bn) * (h->lpad / h->bl);
+    int64_t want = ceil_div(148 * 2, tiles);
+    h->hsplit = (int)std::max<int64_t>(1, std::min<int64_t>(8, want));
+    if (h->precision == SPCA_PREC_TC) h->hsplit = tc_hsplit(n, l);
+  }
+  // flush the fp32 H partials into fp64 every ~1M rows
+  h->flush_every = (int)std::max<int64_t>(1, (1 << 20) / h->chunk_rows);
+
+  const size_t ds = h->ds;
+  int rc;
+#define TRY(call)                                                                      \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return fail(set_err(nullptr, _e == cudaErrorMemoryAllocation ? SPCA_ERR_OOM : SPCA_ERR_CUDA, -1, \
+                          "%s: %s", #call, cudaGetErrorString(_e)));                   \
+  } while (0)
+  TRY(cudaMalloc(&h->omega_dev, (size_t)n * h->lpad * ds));
+  TRY(cudaMalloc(&h->omega64_dev, (size_t)n * l * 8));
+  TRY(cudaMalloc(&h->hcs_dev, (size_t)n * (l + 1) * 8));
+  TRY(cudaMemsetAsync(h->hcs_dev, 0, (size_t)n * (l + 1) * 8, h->stream));
+  if (h->compensated) {
+    TRY(cudaMalloc(&h->carry_dev, (size_t)n * 8));
+    TRY(cudaMemsetAsync(h->carry_dev, 0, (size_t)n * 8, h->stream));
+  }
+  TRY(cudaMalloc(&h->hpart, (size_t)h->hsplit * n * h->lpad * ds));
+  TRY(cudaMemsetAsync(h->hpart, 0, (size_t)h->hsplit * n * h->lpad * ds, h->stream));
+  TRY(cudaMalloc(&h->cspart, (size_t)h->hsplit * n * 8));
+  TRY(cudaMemsetAsync(h->cspart, 0, (size_t)h->hsplit * n * 8, h->stream));
+  TRY(cudaMalloc(&h->bad_dev, sizeof(unsigned long long)));
+  {
+    unsigned long long init = (unsigned long long)kNoBadRow;
+    TRY(cudaMemcpyAsync(h->bad_dev, &init, sizeof init, cudaMemcpyHostToDevice, h->stream));
+    TRY(cudaStreamSynchronize(h->stream));
+  }
+  TRY(cudaMalloc(&h->tail, (size_t)h->chunk_rows * n * ds));
+  // Omega: upload fp64, derive the compute-precision copy
+  {
+    double *om_src = nullptr;
+    if (omega_where == SPCA_MEM_DEVICE) {
+      om_src = const_cast<double *>(omega);
+    } else {
+      TRY(cudaMalloc(&om_src, (size_t)n * l * 8));
+      TRY(cudaMemcpyAsync(om_src, omega, (size_t)n * l * 8, cudaMemcpyHostToDevice, h->stream));
+    }
+    if (dtype == SPCA_F32)
+      omega_prepare<float><<<grid_for(n * h->lpad), 256, 0, h->stream>>>(
+          om_src, (int)n, (int)l, (int)h->lpad, (float *)h->omega_dev, h->omega64_dev);
+    else
+      omega_prepare<double><<<grid_for(n * h->lpad), 256, 0, h->stream>>>(
+          om_src, (int)n, (int)l, (int)h->lpad, (double *)h->omega_dev, h->omega64_dev);
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) return fail(set_err(nullptr, SPCA_ERR_CUDA, -1, "omega_prepare: %s", cudaGetErrorString(le)));
+    h->launches++;
+    TRY(cudaStreamSynchronize(h->stream));
+    if (omega_where != SPCA_MEM_DEVICE) cudaFree(om_src);
+  }
+  if (h->precision == SPCA_PREC_TC) {
+    rc = tc_setup(h);
+    if (rc) return fail(rc);
+  }
+  if (rows_hint > 0) {
+    rc = ensure_g(h, rows_hint);
+    if (rc) return fail(rc);
+  }
+#undef TRY
+  *out = h;
+  return SPCA_OK;
+}
+
+int spca_sketch_push(spca_handle_t h, const void *a, int64_t rows, int64_t ld, int64_t first_row,
+                     int where) {
+  if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
+  if (h->finished) return set_err(h, SPCA_ERR_STATE, -1, "push after finish");
+  if (rows < 0) return set_err(h, SPCA_ERR_FORMAT, first_row, "negative row count");
+  if (first_row != h->rows_seen)
+    return set_err(h, SPCA_ERR_FORMAT, first_row,
+                   "block starts at row %lld but %lld rows were consumed (blocks must be consecutive)",
+                   (long long)first_row, (long long)h->rows_seen);
+  if (rows == 0) return SPCA_OK;
+  if (!a) return set_err(h, SPCA_ERR_FORMAT, first_row, "null block pointer");
+  if (ld < h->n)
+    return set_err(h, SPCA_ERR_FORMAT, first_row, "block at row %lld has row stride %lld < n=%lld",
+                   (long long)first_row, (long long)ld, (long long)h->n);
+  DeviceGuard dg(h->device);
+  int rc;
+  if (where == SPCA_MEM_DEVICE) rc = push_device_rows(h, (const char *)a, rows, ld);
+  else if (where == SPCA_MEM_PINNED) rc = push_host_rows(h, (const char *)a, rows, ld, false);
+  else if (where == SPCA_MEM_PAGEABLE) rc = push_host_rows(h, (const char *)a, rows, ld, true);
+  else return set_err(h, SPCA_ERR_CONFIG, -1, "bad memory kind %d", where);
+  if (rc) return rc;
+  h->rows_seen += rows;
+  return SPCA_OK;
+}
+
+int spca_sketch_reset(spca_handle_t h) {
+  if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
+  DeviceGuard dg(h->device);
+  CK(h, cudaStreamSynchronize(h->stream));
+  CK(h, cudaMemsetAsync(h->hcs_dev, 0, (size_t)h->n * (h->l + 1) * 8, h->stream));
+  if (h->carry_dev) CK(h, cudaMemsetAsync(h->carry_dev, 0, (size_t)h->n * 8, h->stream));
+  unsigned long long init = (unsigned long long)kNoBadRow;
+  CK(h, cudaMemcpyAsync(h->bad_dev, &init, sizeof init, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->tail_rows = 0;
+  h->rows_seen = 0;
+  h->rows_done = 0;
+  h->chunks_since_flush = 0;
+  h->finished = false;
+  h->last_code = SPCA_OK;
+  h->last_bad_row = -1;
+  h->last_msg[0] = 0;
+  return SPCA_OK;
+}
+
+int spca_sketch_sync(spca_handle_t h) {
+  if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
+  DeviceGuard dg(h->device);
+  CK(h, cudaStreamSynchronize(h->stream));
+  int rc = collect_timers(h);
+  if (rc) return rc;
+  return check_bad_row(h);
+}
+
+int spca_sketch_rows(spca_handle_t h, int64_t *rows_seen) {
+  if (!h || !rows_seen) return set_err(h, SPCA_ERR_STATE, -1, "null argument");
+  *rows_seen = h->rows_seen;
+  return SPCA_OK;
+}
+
+int64_t spca_sketch_chunk_rows(spca_handle_t h) { return h ? h->chunk_rows : -1; }
+
+int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out, double *colsum_out,
+                       int64_t *rows_seen, int out_where) {
+  if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
+  DeviceGuard dg(h->device);
+  int rc;
+  if (!h->finished) {
+    if (h->tail_rows > 0) {
+      rc = process_chunk(h, h->tail, h->n, h->tail_rows);
+      if (rc) return rc;
+      h->tail_rows = 0;
+    }
+    rc = flush_h(h);
+    if (rc) return rc;
+    if (h->rows_seen > h->g64_cap) {
+      if (h->g64_dev) cudaFree(h->g64_dev);
+      h->g64_dev = nullptr;
+      CK(h, cudaMalloc(&h->g64_dev, (size_t)std::max<int64_t>(1, h->rows_seen) * h->l * 8));
+      h->g64_cap = h->rows_seen;
+    }
+    if (h->rows_seen > 0) {
+      int64_t count = h->rows_seen * h->l;
+      if (h->dtype == SPCA_F32)
+        g_widen<float><<<grid_for(count), 256, 0, h->stream>>>((const float *)h->g_dev, (int)h->lpad,
+                                                               h->rows_seen, (int)h->l, h->g64_dev);
+      else
+        g_widen<double><<<grid_for(count), 256, 0, h->stream>>>((const double *)h->g_dev, (int)h->lpad,
+                                                                h->rows_seen, (int)h->l, h->g64_dev);
+      CK_LAUNCH(h);
+    }
+    CK(h, cudaStreamSynchronize(h->stream));
+    rc = collect_timers(h);
+    if (rc) return rc;
+    rc = check_bad_row(h);
+    if (rc) return rc;
+    h->finished = true;
+  }
+  cudaMemcpyKind kind = out_where == SPCA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (g_out && h->rows_seen > 0)
+    CK(h, cudaMemcpyAsync(g_out, h->g64_dev, (size_t)h->rows_seen * h->l * 8, kind, h->stream));
+  if (h_out) CK(h, cudaMemcpyAsync(h_out, h->hcs_dev, (size_t)h->n * h->l * 8, kind, h->stream));
+  if (colsum_out)
+    CK(h, cudaMemcpyAsync(colsum_out, h->hcs_dev + h->n * h->l, (size_t)h->n * 8, kind, h->stream));
+  if (rows_seen) *rows_seen = h->rows_seen;
+  CK(h, cudaStreamSynchronize(h->stream));
+  return SPCA_OK;
+}
+
+int spca_device_views(spca_handle_t h, double **g_dev, double **hcs_dev) {
+  if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
+  if (!h->finished) return set_err(h, SPCA_ERR_STATE, -1, "device views need a finished sketch");
+  if (g_dev) *g_dev = h->g64_dev;
+  if (hcs_dev) *hcs_dev = h->hcs_dev;
+  return SPCA_OK;
+}
+
+int spca_g_colsum(spca_handle_t h, double *out, int out_where) {
+  if (!h || !out) return set_err(h, SPCA_ERR_STATE, -1, "null argument");
+  if (!h->finished) return set_err(h, SPCA_ERR_STATE, -1, "g_colsum needs a finished sketch");
+  DeviceGuard dg(h->device);
+  double *d = nullptr;
+  CK(h, cudaMalloc(&d, (size_t)h->l * 8));
+  column_sums64<<<(unsigned)h->l, 256, 0, h->stream>>>(h->g64_dev, h->rows_seen, (int)h->l, d);
+  CK_LAUNCH(h);
+  CK(h, cudaMemcpyAsync(out, d, (size_t)h->l * 8,
+                        out_where == SPCA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                        h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  cudaFree(d);
+  return SPCA_OK;
+}
+
+int spca_center_correct(spca_handle_t h, int64_t m_total, const double *gsum, double *mean_out,
+                        int mean_where) {
+  if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
+  if (!h->finished) return set_err(h, SPCA_ERR_STATE, -1, "center_correct needs a finished sketch");
+  if (m_total <= 0) return set_err(h, SPCA_ERR_EMPTY, -1, "cannot center a sketch of zero rows");
+  DeviceGuard dg(h->device);
+  const int64_t n = h->n, l = h->l;
+  double *mu = nullptr, *w = nullptr, *gs = nullptr;
+  CK(h, cudaMalloc(&mu, (size_t)n * 8));
+  CK(h, cudaMalloc(&w, (size_t)l * 8));
+  CK(h, cudaMalloc(&gs, (size_t)l * 8));
+  double *colsum = h->hcs_dev + n * l;
+  mean_from_colsum<<<(unsigned)ceil_div(n, 256), 256, 0, h->stream>>>(colsum, (int)n, 1.0 / (double)m_total, mu);
+  CK_LAUNCH(h);
+  mu_omega<<<(unsigned)l, 256, 0, h->stream>>>(mu, h->omega64_dev, (int)n, (int)l, w);
+  CK_LAUNCH(h);
+  if (gsum) {
+    CK(h, cudaMemcpyAsync(gs, gsum, (size_t)l * 8, cudaMemcpyDefault, h->stream));
+  } else {
+    column_sums64<<<(unsigned)l, 256, 0, h->stream>>>(h->g64_dev, h->rows_seen, (int)l, gs);
+    CK_LAUNCH(h);
+  }
+  if (h->rows_seen > 0) {
+    g_center<<<grid_for(h->rows_seen * l), 256, 0, h->stream>>>(h->g64_dev, h->rows_seen, (int)l, w);
+    CK_LAUNCH(h);
+  }
+  h_center<<<grid_for(n * l), 256, 0, h->stream>>>(h->hcs_dev, (int)n, (int)l, mu, gs, colsum);
+  CK_LAUNCH(h);
+  if (mean_out)
+    CK(h, cudaMemcpyAsync(mean_out, mu, (size_t)n * 8,
+                          mean_where == SPCA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                          h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  cudaFree(mu);
+  cudaFree(w);
+  cudaFree(gs);
+  return SPCA_OK;
+}
+
+int spca_last_error(spca_handle_t h, int *code, int64_t *bad_row, char *msg, size_t msg_len) {
+  if (h) {
+    if (code) *code = h->last_code;
+    if (bad_row) *bad_row = h->last_bad_row;
+    if (msg && msg_len) snprintf(msg, msg_len, "%s", h->last_msg);
+    return h->last_code;
+  }
+  if (code) *code = g_tl_code;
+  if (bad_row) *bad_row = -1;
+  if (msg && msg_len) snprintf(msg, msg_len, "%s", g_tl_msg);
+  return g_tl_code;
+}
+
+int64_t spca_kernel_launches(spca_handle_t h) { return h ? h->launches : -1; }
+
+int spca_enable_kernel_timing(spca_handle_t h, int enable) {
+  if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
+  h->timing = enable != 0;
+  h->kernel_ms = 0.0;
+  h->timed_chunks = 0;
+  return SPCA_OK;
+}
+
+int spca_kernel_time_ms(spca_handle_t h, double *ms, int64_t *launches) {
+  if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
+  DeviceGuard dg(h->device);
+  CK(h, cudaStreamSynchronize(h->stream));
+  int rc = collect_timers(h);
+  if (rc) return rc;
+  if (ms) *ms = h->kernel_ms;
+  if (launches) *launches = h->timed_chunks;
+  return SPCA_OK;
+}
+
+void spca_sketch_destroy(spca_handle_t h) {
+  if (!h) return;
+  DeviceGuard dg(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->copy_stream) {
+    cudaStreamSynchronize(h->copy_stream);
+    cudaStreamDestroy(h->copy_stream);
+  }
+  for (auto &t : h->timers) {
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.stop);
+  }
+  void *bufs[] = {h->omega_dev, h->omega64_dev, h->tc_omega, h->g_dev, h->g64_dev, h->hcs_dev,
+                  h->carry_dev, h->hpart, h->cspart, h->gpart, h->tc_ws, h->bad_dev, h->tail,
+                  h->dstage[0], h->dstage[1]};
+  for (void *p : bufs)
+    if (p) cudaFree(p);
+  for (int i = 0; i < 2; ++i) {
+    if (h->pinned[i]) cudaFreeHost(h->pinned[i]);
+    if (h->copy_done[i]) cudaEventDestroy(h->copy_done[i]);
+    if (h->comp_done[i]) cudaEventDestroy(h->comp_done[i]);
+  }
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+}  // extern "C"

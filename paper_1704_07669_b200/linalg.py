@@ -1,0 +1,133 @@
+"""Dense kernels of the post-pass, on the GPU in float64.
+
+Same contracts as the reference's ``linalg.py`` (/root/reference/pkg/src/
+streampca/linalg.py): the seeded Gaussian draw (``gaussian_matrix``
+:46-56) is the reference's own numpy Philox generator, run on the host so
+Omega is bit-identical; QR with nonnegative diag(R) (:71-98), the
+triangular solve with its singularity guard (:121-136), the thin SVD
+(:110-118) and the component sign convention (:156-169) run on the device
+(cuSOLVER/cuBLAS through torch; tall-skinny shapes only).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .device import default_device, to_device64, torch_mod
+from .errors import (
+    ConfigError,
+    DataError,
+    DimensionError,
+    RankDeficiencyError,
+    SingularMatrixError,
+)
+
+# linalg.py:26 and :31-35
+RANK_TOL = 1e-12
+STREAM_SKETCH = 0
+STREAM_COSKETCH = 1
+STREAM_FACTOR_U = 2
+STREAM_FACTOR_V = 3
+STREAM_REPAIR = 4
+
+
+def gaussian_matrix(rows: int, cols: int, seed: int, stream: int = STREAM_SKETCH) -> np.ndarray:
+    """i.i.d. N(0,1) (rows x cols) float64 from Philox keyed by (seed, stream)
+    — numpy's generator, exactly as the reference draws it, so Omega (and
+    therefore every result) is comparable bit for bit."""
+    if rows < 1 or cols < 1:
+        raise DimensionError(f"gaussian_matrix needs positive dims, got {rows}x{cols}")
+    if seed < 0 or stream < 0:
+        raise ConfigError("seed and stream must be nonnegative")
+    key = np.array([seed, stream], dtype=np.uint64)
+    return np.random.Generator(np.random.Philox(key=key)).standard_normal((rows, cols))
+
+
+@dataclass(frozen=True)
+class QrPair:
+    q: object
+    r: object
+
+
+def qr_unpivoted(y, rank_check: bool = True, device=None) -> QrPair:
+    """Thin Householder QR on the GPU with diag(R) >= 0 (linalg.py:71-98)."""
+    torch = torch_mod()
+    dev = default_device(device if device is not None else (y.device if hasattr(y, "device") and getattr(y, "is_cuda", False) else None))
+    y = to_device64(y, dev)
+    if y.dim() != 2:
+        raise DimensionError("qr_unpivoted expects a 2-d array")
+    m, b = y.shape
+    if b < 1 or m < b:
+        raise DimensionError(f"qr_unpivoted needs m >= b >= 1, got {m}x{b}")
+    q, r = torch.linalg.qr(y, mode="reduced")
+    sign = torch.where(torch.diagonal(r) < 0, -1.0, 1.0).to(torch.float64)
+    q = q * sign
+    r = r * sign[:, None]
+    if rank_check:
+        tol = RANK_TOL * float(torch.linalg.norm(y, dim=0).max())
+        small = torch.abs(torch.diagonal(r)) < tol
+        if bool(small.any()):
+            j = int(torch.nonzero(small)[0, 0])
+            raise RankDeficiencyError(
+                f"column {j} of the QR input is numerically dependent "
+                f"(|r_jj| = {abs(float(r[j, j])):.3e} < tol = {tol:.3e})", column=j)
+    return QrPair(q=q, r=r)
+
+
+@dataclass(frozen=True)
+class SvdTriple:
+    u: object
+    s: object
+    v: object
+
+
+def dense_svd(b, device=None) -> SvdTriple:
+    """Thin SVD of the l x n sketch factor B on the GPU (linalg.py:110-118).
+
+    Wide B is reduced first: B^T = Q_b R_b (tall QR, cuSOLVER), then the
+    l x l SVD R_b^T = U S W^T gives B = U S (Q_b W)^T — backward stable,
+    as LAPACK's dgesdd does for wide inputs."""
+    torch = torch_mod()
+    dev = default_device(device if device is not None else (b.device if getattr(b, "is_cuda", False) else None))
+    b = to_device64(b, dev)
+    if b.dim() != 2 or b.shape[0] < 1 or b.shape[1] < 1:
+        raise DimensionError("dense_svd expects a nonempty 2-d array")
+    if not bool(torch.isfinite(b).all()):
+        raise DataError("dense_svd input contains non-finite entries")
+    p, n = b.shape
+    if n > 2 * p:
+        qb, rb = torch.linalg.qr(b.T, mode="reduced")           # n x p, p x p
+        u, s, wt = torch.linalg.svd(rb.T, full_matrices=False)
+        v = qb @ wt.T
+    else:
+        u, s, vt = torch.linalg.svd(b, full_matrices=False)
+        v = vt.T
+    return SvdTriple(u=u, s=s, v=v)
+
+
+def solve_rt(r, m):
+    """Solve r^T x = m (r upper triangular) with the reference's singularity
+    guard: any |r_jj| < 1e-300 or < 1e-15 max|r_jj| (linalg.py:121-136)."""
+    torch = torch_mod()
+    if r.dim() != 2 or r.shape[0] != r.shape[1]:
+        raise DimensionError("solve_rt expects a square triangular matrix")
+    if m.shape[0] != r.shape[0]:
+        raise DimensionError(f"solve_rt shape mismatch: r is {tuple(r.shape)}, rhs has {m.shape[0]} rows")
+    diag = torch.abs(torch.diagonal(r))
+    scale = float(diag.max()) if r.shape[0] else 0.0
+    if scale == 0.0 or bool((diag < 1e-300).any()) or bool((diag < 1e-15 * scale).any()):
+        j = int(torch.argmin(diag))
+        raise SingularMatrixError(f"triangular factor has near-zero diagonal at {j}")
+    return torch.linalg.solve_triangular(r.T, m, upper=False)
+
+
+def sign_align(u, v):
+    """Flip each (u_j, v_j) so the largest-|.| entry of v_j is positive;
+    first index wins ties (linalg.py:156-169)."""
+    torch = torch_mod()
+    idx = torch.argmax(torch.abs(v), dim=0)
+    pick = v.gather(0, idx[None, :])[0]
+    sign = torch.where(pick < 0, -1.0, 1.0).to(v.dtype)
+    return u * sign, v * sign

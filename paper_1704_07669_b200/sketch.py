@@ -1,0 +1,281 @@
+"""The one-pass sketch on the GPU — the drop-in for the reference's
+``sketch_pass`` (/root/reference/pkg/src/streampca/sketch.py:52-116).
+
+One traversal of the row stream accumulates, per row block A_i,
+
+    G_i = A_i Omega,   H += A_i^T G_i,   col_sums += 1^T A_i
+
+on one B200 through libspca.so (include/spca.h). Blocks are pushed as they
+arrive; in-memory, device and pinned sources are handed over whole and the
+library streams them in canonical chunks (pinned host rows go through
+double-buffered async copies). Shape errors raise ``StreamFormatError`` and
+the first non-finite row raises ``DataError(row=...)`` exactly as
+``_check_block`` (sketch.py:40-49) does.
+
+Precision: float64 data runs the fp64 DFMA path; float32 data runs the fp32
+path (tensor cores with split precision when available, else FFMA), with
+Omega rounded once to float32 — ``SketchState.omega`` records the Omega the
+sketch actually used so the post-pass stays consistent with it.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, replace
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .device import default_device, is_torch, to_device64, torch_mod
+from .errors import DeviceError, EmptyStreamError, StreamFormatError
+from .streams import PassCounter, has_whole
+
+_PRECISIONS = {"auto": _lib.PREC_AUTO, "simt": _lib.PREC_SIMT, "tc": _lib.PREC_TC}
+
+
+@dataclass(frozen=True)
+class SketchState:
+    """Accumulators after one pass (sketch.py:25-37). Arrays are numpy
+    float64 by default, CUDA float64 tensors with ``keep_on_device``.
+    ``omega`` (extra) is the test matrix exactly as the sketch used it."""
+
+    g: object
+    h: object
+    col_sums: object
+    rows_seen: int
+    omega: object = None
+
+    @property
+    def retained_floats(self) -> int:
+        """Floats held by the sketch itself, excluding Omega (sketch.py:34-37)."""
+        size = (lambda a: int(a.numel()) if is_torch(a) else int(np.asarray(a).size))
+        return size(self.g) + size(self.h) + size(self.col_sums)
+
+
+class GpuSketch:
+    """Owner of one libspca handle (single consumer, one GPU)."""
+
+    def __init__(self, n: int, omega: np.ndarray, dtype, precision: str = "auto",
+                 device=None, rows_hint: int = 0, compensated: bool = False, stream=None):
+        torch = torch_mod()
+        self.lib = _lib.load()
+        self.device = default_device(device)
+        self.n = int(n)
+        om = np.ascontiguousarray(np.asarray(omega, dtype=np.float64))
+        self.l = int(om.shape[1])
+        self.dtype = np.dtype(dtype)
+        if self.dtype not in (np.dtype(np.float32), np.dtype(np.float64)):
+            raise StreamFormatError(f"unsupported element type {self.dtype}")
+        code = _lib.SPCA_F32 if self.dtype == np.float32 else _lib.SPCA_F64
+        prec = _PRECISIONS[precision] if isinstance(precision, str) else int(precision)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            rc = self.lib.spca_sketch_create(
+                ctypes.byref(handle), self.n, self.l, code, prec,
+                om.ctypes.data_as(ctypes.c_void_p), _lib.MEM_PAGEABLE,
+                self.device.index, ctypes.c_void_p(stream.cuda_stream), int(rows_hint),
+                1 if compensated else 0)
+        _lib.check(rc)
+        self.h = handle
+        self._keep = []          # host/device sources that must outlive async copies
+        self._finished = False
+
+    # -- pushing ------------------------------------------------------------
+    def push(self, values, first_row: int) -> int:
+        """Append one block; numpy (pageable host), pinned host tensor or CUDA tensor."""
+        torch = torch_mod()
+        if is_torch(values):
+            t = values
+            if t.dim() != 2 or t.shape[1] != self.n:
+                raise StreamFormatError(
+                    f"block at row {first_row} has shape {tuple(t.shape)}, expected (*, {self.n})")
+            want = torch.float32 if self.dtype == np.float32 else torch.float64
+            if t.dtype != want:
+                t = t.to(want)
+            if t.stride(1) != 1:
+                t = t.contiguous()
+            if t.is_cuda:
+                if t.device != self.device:
+                    t = t.to(self.device)
+                where = _lib.MEM_DEVICE
+            else:
+                where = _lib.MEM_PINNED if t.is_pinned() else _lib.MEM_PAGEABLE
+            rows, ld, ptr = int(t.shape[0]), int(t.stride(0)) if t.shape[0] > 1 else self.n, t.data_ptr()
+            self._keep.append(t)
+        else:
+            a = np.asarray(values)
+            if a.ndim != 2 or a.shape[1] != self.n:
+                raise StreamFormatError(
+                    f"block at row {first_row} has shape {a.shape}, expected (*, {self.n})")
+            if a.dtype != self.dtype or a.strides[1] != a.itemsize:
+                a = np.ascontiguousarray(a, dtype=self.dtype)
+            rows = a.shape[0]
+            ld = a.strides[0] // a.itemsize if rows > 1 else self.n
+            ptr = a.ctypes.data
+            where = _lib.MEM_PAGEABLE
+        if rows == 0:
+            return 0
+        _lib.check(self.lib.spca_sketch_push(self.h, ctypes.c_void_p(ptr), rows, max(ld, self.n),
+                                             int(first_row), where), self.h)
+        return rows
+
+    def reset(self) -> None:
+        """New pass, same Omega and allocations (spca_sketch_reset)."""
+        _lib.check(self.lib.spca_sketch_reset(self.h), self.h)
+        self._keep.clear()
+        self._finished = False
+
+    def sync(self) -> None:
+        _lib.check(self.lib.spca_sketch_sync(self.h), self.h)
+        self._keep.clear()
+
+    # -- results ------------------------------------------------------------
+    def finish(self, on_device: bool = True):
+        """(g, h, col_sums, rows_seen) as CUDA float64 tensors (or numpy)."""
+        torch = torch_mod()
+        rows = ctypes.c_int64(0)
+        _lib.check(self.lib.spca_sketch_rows(self.h, ctypes.byref(rows)), self.h)
+        m = rows.value
+        if on_device:
+            g = torch.empty((m, self.l), dtype=torch.float64, device=self.device)
+            hh = torch.empty((self.n, self.l), dtype=torch.float64, device=self.device)
+            cs = torch.empty((self.n,), dtype=torch.float64, device=self.device)
+            ptrs = (g.data_ptr() if m else None, hh.data_ptr(), cs.data_ptr())
+            where = _lib.MEM_DEVICE
+        else:
+            g = np.empty((m, self.l))
+            hh = np.empty((self.n, self.l))
+            cs = np.empty(self.n)
+            ptrs = (g.ctypes.data if m else None, hh.ctypes.data, cs.ctypes.data)
+            where = _lib.MEM_PAGEABLE
+        # the handle's stream must see torch's allocations (same stream here)
+        rc = self.lib.spca_sketch_finish(self.h, *(ctypes.c_void_p(p) if p else None for p in ptrs),
+                                         ctypes.byref(rows), where)
+        self._keep.clear()
+        _lib.check(rc, self.h)
+        self._finished = True
+        return g, hh, cs, m
+
+    def kernel_launches(self) -> int:
+        return int(self.lib.spca_kernel_launches(self.h))
+
+    def chunk_rows(self) -> int:
+        return int(self.lib.spca_sketch_chunk_rows(self.h))
+
+    def enable_timing(self, on: bool = True) -> None:
+        _lib.check(self.lib.spca_enable_kernel_timing(self.h, 1 if on else 0), self.h)
+
+    def kernel_time(self) -> tuple[float, int]:
+        ms = ctypes.c_double(0)
+        cnt = ctypes.c_int64(0)
+        _lib.check(self.lib.spca_kernel_time_ms(self.h, ctypes.byref(ms), ctypes.byref(cnt)), self.h)
+        return ms.value, cnt.value
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.spca_sketch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _omega_as_used(omega: np.ndarray, dtype) -> np.ndarray:
+    om = np.asarray(omega, dtype=np.float64)
+    if np.dtype(dtype) == np.float32:
+        return om.astype(np.float32).astype(np.float64)
+    return om
+
+
+def run_pass(stream, omega, block_rows=None, compensated=False, precision="auto",
+             device=None, keep=None):
+    """Drive one traversal of ``stream`` through a GpuSketch; returns the
+    finished GpuSketch (state still on the device)."""
+    om = np.asarray(omega)
+    dtype = np.dtype(getattr(stream, "dtype", np.float64))
+    n, l = om.shape
+    sk = GpuSketch(n, om, dtype, precision=precision, device=device,
+                   rows_hint=stream.n_rows or 0, compensated=compensated)
+    if has_whole(stream):
+        kind, mat = stream.whole()
+        if mat.shape[0]:
+            sk.push(mat, 0)
+    else:
+        if block_rows is None:
+            block_rows = l
+        seen = 0
+        for block in stream.blocks(block_rows):
+            vals = block.values
+            if getattr(vals, "ndim", None) != 2 or vals.shape[1] != n:
+                raise StreamFormatError(
+                    f"block at row {block.first_row_index} has shape {tuple(vals.shape)}, "
+                    f"expected (*, {n})")
+            sk.push(vals, block.first_row_index)
+            seen += vals.shape[0]
+    return sk
+
+
+def sketch_pass(
+    stream,
+    omega: np.ndarray,
+    block_rows: Optional[int] = None,
+    fixed_order: bool = False,
+    compensated: bool = False,
+    *,
+    precision: str = "auto",
+    device=None,
+    keep_on_device: bool = False,
+) -> SketchState:
+    """Accumulate the sketch of the streamed matrix in exactly one pass
+    (sketch.py:52-116), on the GPU.
+
+    ``block_rows`` defaults to l and is what a generic stream is asked for
+    (sketch.py:76-77). ``fixed_order`` is accepted for signature parity: the
+    device path is always order-fixed — bitwise identical for every block
+    size and run to run — which is the property fixed_order buys on the CPU.
+    ``compensated`` enables Kahan summation of col_sums across chunks."""
+    om = np.asarray(omega, dtype=np.float64)
+    if om.ndim != 2:
+        raise StreamFormatError("omega must be 2-d")
+    n, l = om.shape
+    if stream.n_cols != n:
+        raise StreamFormatError(f"stream has {stream.n_cols} columns but omega has {n} rows")
+    sk = run_pass(stream, om, block_rows=block_rows, compensated=compensated,
+                  precision=precision, device=device)
+    try:
+        g, h, cs, m = sk.finish(on_device=keep_on_device)
+    finally:
+        sk.close()
+    used = _omega_as_used(om, getattr(stream, "dtype", np.float64))
+    if keep_on_device:
+        used = to_device64(used, default_device(device))
+    return SketchState(g=g, h=h, col_sums=cs, rows_seen=int(m), omega=used)
+
+
+def center_correct(state: SketchState, omega) -> SketchState:
+    """Rewrite the sketch as if A had been column-centered (sketch.py:119-139):
+    mu = col_sums/m, G -= 1 (mu^T Omega), H -= mu (1^T G); on the GPU in fp64.
+    Returns the same array kind (numpy or CUDA tensor) it was given."""
+    torch = torch_mod()
+    if state.rows_seen == 0:
+        raise EmptyStreamError("cannot center a sketch of zero rows")
+    on_dev = is_torch(state.g)
+    dev = state.g.device if on_dev else default_device()
+    g = to_device64(state.g, dev)
+    h = to_device64(state.h, dev)
+    cs = to_device64(state.col_sums, dev)
+    om = to_device64(omega, dev)
+    mu = cs / state.rows_seen
+    g_c = g - (mu @ om)[None, :]
+    h_c = h - torch.outer(mu, g.sum(dim=0))
+    z = torch.zeros_like(cs)
+    if not on_dev:
+        g_c, h_c, z = g_c.cpu().numpy(), h_c.cpu().numpy(), z.cpu().numpy()
+    return replace(state, g=g_c, h=h_c, col_sums=z)

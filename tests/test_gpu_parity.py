@@ -1,0 +1,369 @@
+"""CUDA path vs the CPU oracle / golden reference outputs (needs a B200).
+
+Everything here calls through libspca.so (the C ABI) via the Python mirror
+of the reference API. Tolerances follow BASELINE.json: fp64 1e-10 relative
+on singular values and principal angles (1e-12 on raw sketches, the
+reference's own test_sketch.py:35-42 bar); fp32 data 1e-4.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_1704_07669_b200 as P  # noqa: E402
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+PRECISIONS_F32 = ["simt", "tc"]
+
+
+def _tc_ok():
+    try:
+        sk = P.GpuSketch(64, np.ones((64, 16)), np.float32, precision="tc")
+        sk.close()
+        return True
+    except Exception:
+        return False
+
+
+# --------------------------------------------------------------- sketch_pass
+class TestSketchPass:
+    def test_golden_small(self, golden):
+        g, _ = golden
+        a = O.gaussian(40, 30, seed=3)
+        st = P.sketch_pass(P.ArrayRowStream(a), O.gaussian(30, 8, seed=4), block_rows=7)
+        assert rel(st.g, g["sk_small_g"]) <= 1e-12
+        assert rel(st.h, g["sk_small_h"]) <= 1e-12
+        assert np.allclose(st.col_sums, g["sk_small_cs"], rtol=1e-13, atol=1e-13)
+        assert st.rows_seen == 40
+
+    def test_identity(self, golden):
+        g, _ = golden
+        om = O.gaussian(5, 3, seed=1)
+        st = P.sketch_pass(P.ArrayRowStream(np.eye(5)), om, block_rows=2)
+        assert np.allclose(st.g, om) and np.allclose(st.h, om)
+        assert np.allclose(st.col_sums, np.ones(5)) and st.rows_seen == 5
+
+    def test_zero(self):
+        st = P.sketch_pass(P.ArrayRowStream(np.zeros((6, 4))), O.gaussian(4, 2, seed=2))
+        assert not st.g.any() and not st.h.any() and not st.col_sums.any()
+
+    def test_nonfinite_row_reported(self, golden):
+        g, _ = golden
+        a = O.gaussian(10, 4, seed=15)
+        a[6, 2] = np.inf
+        with pytest.raises(P.DataError) as exc:
+            P.sketch_pass(P.ArrayRowStream(a), O.gaussian(4, 2, seed=16), block_rows=4)
+        assert exc.value.row == int(g["sk_nonfinite_row"]) == 6
+
+    @pytest.mark.parametrize("dtype", [np.float32, np.float64])
+    def test_nan_first_row_large(self, dtype):
+        a = O.gaussian(5000, 300, seed=1).astype(dtype)
+        a[4321, 7] = np.nan
+        a[4999, 0] = -np.inf
+        with pytest.raises(P.DataError) as exc:
+            P.sketch_pass(P.ArrayRowStream(a), O.gaussian(300, 40, seed=2))
+        assert exc.value.row == 4321
+
+    def test_width_mismatch(self):
+        with pytest.raises(P.StreamFormatError):
+            P.sketch_pass(P.ArrayRowStream(np.ones((4, 3))), O.gaussian(5, 2, seed=1))
+
+    def test_bad_block_shape_from_generic_stream(self):
+        blocks = [np.ones((3, 4)), np.ones((2, 5))]
+        with pytest.raises(P.StreamFormatError):
+            P.sketch_pass(P.GeneratorRowStream(iter(blocks), n_cols=4), O.gaussian(4, 2, seed=1))
+
+    def test_default_block_rows_is_sketch_width(self):
+        seen = []
+
+        class Probe(P.RowStream):
+            def __init__(self, a):
+                self.a = a
+
+            n_rows = property(lambda s: s.a.shape[0])
+            n_cols = property(lambda s: s.a.shape[1])
+            resettable = property(lambda s: True)
+
+            def blocks(self, block_rows):
+                seen.append(block_rows)
+                for r in range(0, self.a.shape[0], block_rows):
+                    yield P.RowBlock(r, self.a[r:r + block_rows])
+
+        P.sketch_pass(Probe(O.gaussian(12, 6, seed=17)), O.gaussian(6, 5, seed=18))
+        assert seen == [5]
+
+    def test_memory_accounting(self):
+        m, n, l = 30, 20, 6
+        st = P.sketch_pass(P.ArrayRowStream(O.gaussian(m, n, seed=19)), O.gaussian(n, l, seed=20))
+        assert st.retained_floats == m * l + n * l + n
+
+    def test_single_pass_counted(self):
+        pc = P.PassCounter(P.ArrayRowStream(O.gaussian(20, 10, seed=5)))
+        P.sketch_pass(pc, O.gaussian(10, 4, seed=6))
+        assert pc.passes_completed == 1 and pc.rows_read == 20
+
+    def test_compensated_col_sums(self, golden):
+        g, _ = golden
+        a = O.gaussian(500, 3, seed=13) + 1e8
+        st = P.sketch_pass(P.ArrayRowStream(a), O.gaussian(3, 2, seed=14), compensated=True)
+        assert np.allclose(st.col_sums, a.sum(axis=0), rtol=1e-15)
+        assert np.allclose(st.col_sums, g["sk_kahan_cs"], rtol=1e-15)
+
+    def test_bitwise_independent_of_block_size(self):
+        """Canonical chunking: any push sizes give identical bytes (the GPU
+        analogue of acceptance criterion 9, test_acceptance.py:223-255)."""
+        a = O.gaussian(9000, 257, seed=9)
+        om = O.gaussian(257, 30, seed=10)
+        ref = P.sketch_pass(P.ArrayRowStream(a), om)
+        for br in (1, 30, 37, 4096, 9000):
+            st = P.sketch_pass(P.GeneratorRowStream(iter([a]), n_cols=257), om, block_rows=br)
+            assert np.array_equal(st.g, ref.g) and np.array_equal(st.h, ref.h)
+            assert np.array_equal(st.col_sums, ref.col_sums)
+
+    def test_run_to_run_bitwise(self):
+        a = O.gaussian(7000, 500, seed=21).astype(np.float32)
+        om = O.gaussian(500, 60, seed=22)
+        r1 = P.sketch_pass(P.ArrayRowStream(a), om)
+        r2 = P.sketch_pass(P.ArrayRowStream(a), om)
+        assert np.array_equal(r1.g, r2.g) and np.array_equal(r1.h, r2.h)
+
+    @pytest.mark.parametrize("m,n,l", [(1, 1, 1), (3, 7, 2), (129, 65, 33), (1000, 1001, 60),
+                                       (4097, 300, 120), (700, 50, 250)])
+    def test_fp64_shapes_vs_oracle(self, m, n, l):
+        a = O.gaussian(m, n, seed=m + n)
+        om = O.gaussian(n, l, seed=l)
+        st = P.sketch_pass(P.ArrayRowStream(a), om, block_rows=97)
+        ref = O.oracle_sketch(O.row_blocks(a, 97), om)
+        assert rel(st.g, ref.g) <= 1e-12 and rel(st.h, ref.h) <= 1e-12
+        assert np.allclose(st.col_sums, ref.col_sums, rtol=1e-12, atol=1e-12)
+
+    @pytest.mark.parametrize("precision", PRECISIONS_F32)
+    @pytest.mark.parametrize("m,n,l", [(5000, 1000, 60), (3000, 4096, 120), (300, 2000, 250),
+                                       (1000, 333, 30), (257, 100, 8)])
+    def test_fp32_shapes_vs_oracle(self, precision, m, n, l):
+        if precision == "tc" and not _tc_ok():
+            pytest.skip("tensor-core path unavailable")
+        a = O.gaussian(m, n, seed=m).astype(np.float32)
+        om = O.gaussian(n, l, seed=n)
+        try:
+            st = P.sketch_pass(P.ArrayRowStream(a), om, precision=precision)
+        except P.ConfigError:
+            pytest.skip("shape unsupported by this precision")
+        om32 = om.astype(np.float32).astype(np.float64)
+        ref = O.oracle_sketch(O.row_blocks(a, 4096), om32)
+        # fp32-class accumulation over n (G) and m (H) terms
+        assert rel(st.g, ref.g) <= 2e-6, rel(st.g, ref.g)
+        assert rel(st.h, ref.h) <= 2e-6, rel(st.h, ref.h)
+        assert np.allclose(st.col_sums, ref.col_sums, rtol=1e-9, atol=1e-9)
+
+    def test_device_and_pinned_sources_match_host(self):
+        a = O.gaussian(6000, 700, seed=31).astype(np.float32)
+        om = O.gaussian(700, 60, seed=32)
+        host = P.sketch_pass(P.ArrayRowStream(a), om)
+        dev = P.sketch_pass(P.DeviceRowStream(torch.from_numpy(a).cuda()), om)
+        pin = P.sketch_pass(P.PinnedRowStream(torch.from_numpy(a).pin_memory()), om)
+        for st in (dev, pin):
+            assert np.array_equal(st.g, host.g) and np.array_equal(st.h, host.h)
+
+    def test_center_correct_matches_explicit(self, golden):
+        g, _ = golden
+        a = O.gaussian(50, 40, seed=0) + 2.5
+        om = O.gaussian(40, 9, seed=100)
+        st = P.center_correct(P.sketch_pass(P.ArrayRowStream(a), om), om)
+        assert rel(st.g, g["center_g"]) <= 1e-10 and rel(st.h, g["center_h"]) <= 1e-10
+        assert not np.asarray(st.col_sums).any()
+
+    def test_symmetry_of_cross_gram(self):
+        a = O.gaussian(25, 12, seed=11)
+        om = O.gaussian(12, 5, seed=12)
+        st = P.sketch_pass(P.ArrayRowStream(a), om)
+        cross = om.T @ st.h
+        assert np.linalg.norm(cross - cross.T) <= 1e-10 * np.linalg.norm(cross)
+
+
+# ------------------------------------------------------------------ blocked_qb
+class TestBlockedQb:
+    def test_invariants_every_block(self):
+        a = O.gaussian(60, 50, seed=1)
+        om = O.gaussian(50, 20, seed=2)
+        st = P.sketch_pass(P.ArrayRowStream(a), om, keep_on_device=True)
+        at = torch.from_numpy(a).cuda()
+        seen = []
+
+        def probe(i, q, b):
+            seen.append(i)
+            assert float((q.T @ q - torch.eye(q.shape[1], device=q.device, dtype=q.dtype)).abs().max()) <= 1e-10
+            assert float(torch.linalg.norm(b - q.T @ at)) <= 1e-10 * float(torch.linalg.norm(at))
+
+        f = P.blocked_qb(st.g, st.h, om, 5, on_block=probe)
+        assert seen == [0, 1, 2, 3] and not f.repaired_columns
+
+    def test_repair_matches_reference(self, golden):
+        g, _ = golden
+        u, _ = O.qr_pos(O.gaussian(30, 5, 13, stream=2))
+        v, _ = O.qr_pos(O.gaussian(30, 5, 13, stream=3))
+        a = u @ (np.linspace(5.0, 1.0, 5)[:, None] * v.T)
+        om = O.gaussian(30, 10, 14)
+        st = P.sketch_pass(P.ArrayRowStream(a), om, keep_on_device=True)
+        f = P.blocked_qb(st.g, st.h, om, 5, on_deficiency="repair")
+        assert f.repaired_columns == tuple(g["qb_rep_cols"].tolist())
+        q = f.q.cpu().numpy()
+        b = f.b.cpu().numpy()
+        assert np.max(np.abs(q.T @ q - np.eye(10))) <= 1e-10
+        assert np.linalg.norm(a - q @ b) <= 1e-10 * np.linalg.norm(a)
+        qr, br = g["qb_rep_q"], g["qb_rep_b"]
+        assert np.linalg.norm(q @ b - qr @ br) <= 1e-10 * np.linalg.norm(a)
+
+    def test_deficiency_error_location(self, golden):
+        g, _ = golden
+        u, _ = O.qr_pos(O.gaussian(30, 5, 13, stream=2))
+        v, _ = O.qr_pos(O.gaussian(30, 5, 13, stream=3))
+        a = u @ (np.linspace(5.0, 1.0, 5)[:, None] * v.T)
+        om = O.gaussian(30, 10, 14)
+        st = P.sketch_pass(P.ArrayRowStream(a), om, keep_on_device=True)
+        with pytest.raises(P.RankDeficiencyError) as exc:
+            P.blocked_qb(st.g, st.h, om, 5)
+        assert exc.value.block == int(g["qb_err_block"])
+        assert exc.value.column == int(g["qb_err_col"])
+
+    def test_width_not_multiple(self):
+        a = O.gaussian(20, 15, seed=11)
+        om = O.gaussian(15, 10, seed=12)
+        st = P.sketch_pass(P.ArrayRowStream(a), om, keep_on_device=True)
+        with pytest.raises(P.ConfigError):
+            P.blocked_qb(st.g, st.h, om, 4)
+
+
+# ------------------------------------------------------------- single_pass_pca
+def _assert_svd_close(res, u, s, v, tol):
+    s_err = float(np.max(np.abs(res.s - s) / np.abs(s)))
+    assert s_err <= tol, f"S rel err {s_err:.2e} > {tol}"
+    au = O.subspace_angle(res.u, u)
+    av = O.subspace_angle(res.v, v)
+    assert au <= tol and av <= tol, f"angles U {au:.2e} V {av:.2e} > {tol}"
+    return s_err, au, av
+
+
+class TestSinglePass:
+    def test_config1_parity(self, golden):
+        """BASELINE config 1 (fp64): S and subspaces within 1e-10 of the reference."""
+        g, _ = golden
+        i = np.arange(1, 1001)
+        a = O.reference_synth_matrix(2000, 1000, 10.0 ** (-4.0 * (i - 1) / 999.0), seed=100)
+        cfg = P.PcaConfig(k=20, oversample=10, block_size=10, seed=1)
+        res = P.single_pass_pca(a, cfg, block_rows=200)
+        _assert_svd_close(res, g["cfg1_u"], g["cfg1_s"], g["cfg1_v"], 1e-10)
+        assert res.passes == 1 and res.retained_floats == int(g["cfg1_retained"])
+        # component signs follow the reference convention, so vectors match directly
+        assert np.max(np.abs(res.v - g["cfg1_v"])) <= 1e-8
+
+    @pytest.mark.parametrize("precision", PRECISIONS_F32)
+    def test_fp32_construction_parity(self, golden, precision):
+        if precision == "tc" and not _tc_ok():
+            pytest.skip("tensor-core path unavailable")
+        g, _ = golden
+        a = O.synth_lowrank_plus_noise(4000, 1500, 200, "inv", 1e-3, seed=11)
+        res = P.single_pass_pca(a, P.PcaConfig(k=50, oversample=10, seed=1), block_rows=1024,
+                                precision=precision)
+        _assert_svd_close(res, g["f32_u"], g["f32_s"], g["f32_v"], 1e-4)
+
+    def test_exact_low_rank(self, golden):
+        g, _ = golden
+        rng = np.random.default_rng(0)
+        a = rng.standard_normal((150, 5)) @ rng.standard_normal((5, 100))
+        res = P.single_pass_pca(a, P.PcaConfig(k=5, seed=1))
+        _assert_svd_close(res, g["spca_lr_u"], g["spca_lr_s"], g["spca_lr_v"], 1e-10)
+        with pytest.raises(P.RankDeficiencyError):
+            P.single_pass_pca(a, P.PcaConfig(k=5, seed=1), on_deficiency="error")
+
+    def test_centered(self, golden):
+        g, _ = golden
+        rng = np.random.default_rng(21)
+        base = rng.standard_normal((120, 9)) @ rng.standard_normal((9, 60))
+        a = base + np.outer(np.ones(120), rng.standard_normal(60))
+        res = P.single_pass_pca(a, P.PcaConfig(k=9, center=True))
+        _assert_svd_close(res, g["spca_ctr_u"], g["spca_ctr_s"], g["spca_ctr_v"], 1e-10)
+        assert np.allclose(res.mean, g["spca_ctr_mean"], rtol=0, atol=1e-12)
+
+    def test_type2_acceptance_input(self, golden):
+        g, _ = golden
+        sigma = np.arange(1, 501, dtype=np.float64) ** -2.0
+        a = O.reference_synth_matrix(500, 500, sigma, seed=100)
+        res = P.single_pass_pca(a, P.PcaConfig(k=20, seed=1))
+        _assert_svd_close(res, g["type2_u"], g["type2_s"], g["type2_v"], 1e-10)
+
+    def test_generator_stream_unknown_rows(self):
+        rng = np.random.default_rng(5)
+        a = rng.standard_normal((90, 40))
+        res = P.single_pass_pca(P.GeneratorRowStream(iter(a.reshape(9, 10, 40)), n_cols=40),
+                                P.PcaConfig(k=5))
+        ref = P.single_pass_pca(a, P.PcaConfig(k=5))
+        assert np.allclose(res.s, ref.s, rtol=0, atol=1e-12)
+
+    def test_errors_and_accounting(self):
+        with pytest.raises(P.EmptyStreamError):
+            P.single_pass_pca(np.empty((0, 30)), P.PcaConfig(k=3, oversample=0, block_size=1))
+        with pytest.raises(P.ConfigError):
+            P.single_pass_pca(np.eye(30), P.PcaConfig(k=3, power=1))
+        rng = np.random.default_rng(5)
+        a = rng.standard_normal((90, 40))
+        pc = P.PassCounter(P.ArrayRowStream(a))
+        cfg = P.PcaConfig(k=5, oversample=5)
+        res = P.single_pass_pca(pc, cfg)
+        assert res.passes == 1 and pc.passes_completed == 1
+        assert res.retained_floats == 90 * cfg.l + 2 * 40 * cfg.l + 40
+
+    def test_sign_convention(self):
+        res = P.single_pass_pca(np.random.default_rng(11).standard_normal((80, 50)), P.PcaConfig(k=8))
+        for j in range(8):
+            col = res.v[:, j]
+            assert col[np.argmax(np.abs(col))] > 0
+
+    def test_power_refine_matches_oracle_two_pass(self):
+        rng = np.random.default_rng(3)
+        a = rng.standard_normal((400, 120)) @ np.diag(1.0 / np.arange(1, 121)) @ rng.standard_normal((120, 200))
+        res = P.power_refine(a, P.PcaConfig(k=10, power=1, seed=2))
+        assert res.passes == 2
+        s_true = np.linalg.svd(a, compute_uv=False)[:10]
+        assert np.max(np.abs(res.s - s_true) / s_true) < 1e-2
+
+
+# -------------------------------------------------- full-size properties (cfg2)
+def test_config2_full_size_properties():
+    """BASELINE config 2 at full size on the device: H = A^T G and G = A Omega
+    checked through random probes in fp64 (size-independent properties),
+    Omega^T H symmetric, and bitwise reproducibility."""
+    from paper_1704_07669_b200 import synth
+    a = synth.config_matrix("cfg2", device="cuda")
+    m, n = a.shape
+    om = O.gaussian(n, 60, 1)
+    st = P.sketch_pass(P.DeviceRowStream(a), om, keep_on_device=True)
+    om32 = torch.from_numpy(om.astype(np.float32)).cuda().double()
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(60, 4, device="cuda", dtype=torch.float64, generator=gen)
+    y = torch.randn(n, 4, device="cuda", dtype=torch.float64, generator=gen)
+    a64_rows = a[:20000].double()
+    g_ref = a64_rows @ (om32 @ x)
+    assert float(torch.linalg.norm(st.g[:20000] @ x - g_ref) / torch.linalg.norm(g_ref)) < 2e-6
+    # y^T H x = (A y)^T (G x)
+    ay = torch.cat([a[i:i + 20000].double() @ y for i in range(0, m, 20000)])
+    lhs = y.T @ st.h @ x
+    rhs = ay.T @ (st.g @ x)
+    assert float(torch.linalg.norm(lhs - rhs) / torch.linalg.norm(rhs)) < 1e-5
+    cross = om32.T @ st.h
+    assert float(torch.linalg.norm(cross - cross.T) / torch.linalg.norm(cross)) < 1e-5
+    st2 = P.sketch_pass(P.DeviceRowStream(a), om, keep_on_device=True)
+    assert torch.equal(st.h, st2.h) and torch.equal(st.g, st2.g)
