@@ -1,6 +1,7 @@
 // handle.cuh — the state behind an spca_handle_t (one GPU, one consumer).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -28,7 +29,8 @@ struct spca_sketch {
 
   void *omega_dev = nullptr;     // n x lpad compute precision
   double *omega64_dev = nullptr; // n x l fp64, exactly the values used
-  void *tc_omega = nullptr;      // tensor-core operand layout (sketch_tc.cuh)
+  void *tc_omega = nullptr;      // Omega^T hi | lo (2 x lpad x n fp32, sketch_tc.cuh)
+  CUtensorMap tm_whi, tm_wlo;    // TMA maps over Omega^T hi / lo
 
   void *g_dev = nullptr;         // cap x lpad compute precision
   int64_t g_cap = 0;
@@ -41,7 +43,7 @@ struct spca_sketch {
   double *cspart = nullptr;      // [hsplit][n]
   void *gpart = nullptr;         // P1 split-K partials
   int64_t gpart_elems = 0;
-  void *tc_ws = nullptr;         // tensor-core workspace
+  void *tc_ws = nullptr;         // tensor-core workspace: G_hi | G_lo (2 x chunk x lpad)
   size_t tc_ws_bytes = 0;
   unsigned long long *bad_dev = nullptr;
 
@@ -52,6 +54,7 @@ struct spca_sketch {
   int64_t rows_done = 0;         // processed
   int chunks_since_flush = 0;
   int flush_every = 64;
+  int tc_debug = 0;              // SPCA_TC_DEBUG bitmask (profiling experiments only)
   bool finished = false;
 
   // host staging (pinned double buffer)

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -102,6 +103,7 @@ int ensure_g(spca_sketch *h, int64_t rows_needed) {
 
 // tensor-core path (uses set_err / CK / grid_for above)
 #include "sketch_tc.cuh"
+#include "tc_host.cuh"
 
 namespace {
 
@@ -407,6 +409,7 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
   }
   // flush the fp32 H partials into fp64 every ~1M rows
   h->flush_every = (int)std::max<int64_t>(1, (1 << 20) / h->chunk_rows);
+  if (const char *d = getenv("SPCA_TC_DEBUG")) h->tc_debug = atoi(d);
 
   const size_t ds = h->ds;
   int rc;

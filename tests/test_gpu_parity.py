@@ -164,9 +164,11 @@ class TestSketchPass:
             pytest.skip("shape unsupported by this precision")
         om32 = om.astype(np.float32).astype(np.float64)
         ref = O.oracle_sketch(O.row_blocks(a, 4096), om32)
-        # fp32-class accumulation over n (G) and m (H) terms
-        assert rel(st.g, ref.g) <= 2e-6, rel(st.g, ref.g)
-        assert rel(st.h, ref.h) <= 2e-6, rel(st.h, ref.h)
+        # fp32-class accumulation over n (G) and m (H) terms; 3xTF32 keeps
+        # ~22 significant bits per product (2^-22 ~ 2.4e-7), FFMA 24
+        tol = 2e-6 if precision == "simt" else 2e-5
+        assert rel(st.g, ref.g) <= tol, rel(st.g, ref.g)
+        assert rel(st.h, ref.h) <= tol, rel(st.h, ref.h)
         assert np.allclose(st.col_sums, ref.col_sums, rtol=1e-9, atol=1e-9)
 
     def test_device_and_pinned_sources_match_host(self):
@@ -357,7 +359,7 @@ def test_config2_full_size_properties():
     y = torch.randn(n, 4, device="cuda", dtype=torch.float64, generator=gen)
     a64_rows = a[:20000].double()
     g_ref = a64_rows @ (om32 @ x)
-    assert float(torch.linalg.norm(st.g[:20000] @ x - g_ref) / torch.linalg.norm(g_ref)) < 2e-6
+    assert float(torch.linalg.norm(st.g[:20000] @ x - g_ref) / torch.linalg.norm(g_ref)) < 2e-5
     # y^T H x = (A y)^T (G x)
     ay = torch.cat([a[i:i + 20000].double() @ y for i in range(0, m, 20000)])
     lhs = y.T @ st.h @ x
