@@ -55,6 +55,7 @@ struct spca_sketch {
   int chunks_since_flush = 0;
   int flush_every = 64;
   int tc_debug = 0;              // SPCA_TC_DEBUG bitmask (profiling experiments only)
+  unsigned long long *trace_g = nullptr, *trace_h = nullptr;  // SPCA_TC_TRACE timelines
   bool finished = false;
 
   // host staging (pinned double buffer)
@@ -68,7 +69,25 @@ struct spca_sketch {
 
   int64_t launches = 0;
   bool timing = false;
-  std::vector<spca::Timer> timers;     // pending per-chunk timers
+  std::vector<spca::Timer> timers;     // unused (kept for layout stability)
+  cudaEvent_t t_start = nullptr, t_stop = nullptr;  // kernel-group timing window
+  bool t_open = false;
+  int64_t t_chunks = 0;
+
+  // tensor-core path: the H contraction of chunk c runs on `hstream` while
+  // the G contraction of chunk c+1 runs on `stream` (two kernels in flight)
+  cudaStream_t hstream = nullptr;
+  cudaEvent_t ev_g[2] = {nullptr, nullptr};  // G^T slot ready (finalize done)
+  cudaEvent_t ev_h[2] = {nullptr, nullptr};  // G^T slot released (H done)
+  cudaEvent_t ev_join = nullptr;
+  bool h_used[2] = {false, false};
+  int64_t chunk_seq = 0;
+  // TMA descriptors cached per pushed source buffer (encoding is a driver
+  // call of several microseconds; a full-matrix push encodes once)
+  const void *src_ptr = nullptr;
+  int64_t src_rows = 0, src_lda = 0;
+  CUtensorMap src_tg, src_th;
+  CUtensorMap slot_tgh[2], slot_tgl[2];  // G^T slot descriptors for full chunks
   double kernel_ms = 0.0;
   int64_t timed_chunks = 0;
 

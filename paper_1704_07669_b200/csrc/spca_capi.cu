@@ -76,6 +76,17 @@ struct DeviceGuard {
   }
 };
 
+// stream that runs the H contraction and everything that depends on it
+cudaStream_t post_stream(const spca_sketch *h) { return h->hstream ? h->hstream : h->stream; }
+
+// make the main stream wait for all work queued on the H stream
+int join_h(spca_sketch *h) {
+  if (!h->hstream) return SPCA_OK;
+  CK(h, cudaEventRecord(h->ev_join, h->hstream));
+  CK(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+  return SPCA_OK;
+}
+
 int grid_for(int64_t count, int threads = 256) {
   int64_t b = ceil_div(count, threads);
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
@@ -187,11 +198,11 @@ int flush_h(spca_sketch *h) {
   if (h->chunks_since_flush == 0) return SPCA_OK;
   int64_t count = h->n * h->l;
   if (h->dtype == SPCA_F32)
-    h_flush<float><<<grid_for(count), 256, 0, h->stream>>>(
+    h_flush<float><<<grid_for(count), 256, 0, post_stream(h)>>>(
         (const float *)h->hpart, h->hsplit, h->n * h->lpad, (int)h->n, (int)h->l, (int)h->lpad,
         h->hcs_dev);
   else
-    h_flush<double><<<grid_for(count), 256, 0, h->stream>>>(
+    h_flush<double><<<grid_for(count), 256, 0, post_stream(h)>>>(
         (const double *)h->hpart, h->hsplit, h->n * h->lpad, (int)h->n, (int)h->l, (int)h->lpad,
         h->hcs_dev);
   CK_LAUNCH(h);
@@ -203,11 +214,12 @@ int process_chunk(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   if (rows <= 0) return SPCA_OK;
   int rc = ensure_g(h, h->rows_done + rows);
   if (rc) return rc;
-  Timer tm;
-  if (h->timing) {
-    CK(h, cudaEventCreate(&tm.start));
-    CK(h, cudaEventCreate(&tm.stop));
-    CK(h, cudaEventRecord(tm.start, h->stream));
+  if (h->timing && !h->t_open) {
+    if (!h->t_start) CK(h, cudaEventCreate(&h->t_start));
+    if (!h->t_stop) CK(h, cudaEventCreate(&h->t_stop));
+    CK(h, cudaEventRecord(h->t_start, h->stream));
+    h->t_open = true;
+    h->t_chunks = 0;
   }
   if (h->precision == SPCA_PREC_TC) {
     rc = tc_chunk(h, a, lda, (int)rows);
@@ -217,18 +229,24 @@ int process_chunk(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
     rc = simt_chunk<double>(h, (const double *)a, lda, (int)rows);
   }
   if (rc) return rc;
-  colsum_accumulate<<<(unsigned)ceil_div(h->n, 256), 256, 0, h->stream>>>(
+  // column sums and the H flush follow the H contraction on its stream
+  colsum_accumulate<<<(unsigned)ceil_div(h->n, 256), 256, 0, post_stream(h)>>>(
       h->cspart, h->hsplit, (int)h->n, h->hcs_dev + h->n * h->l,
       h->compensated ? h->carry_dev : nullptr);
   CK_LAUNCH(h);
+  if (h->hstream) {
+    const int slot = (int)((h->chunk_seq - 1) & 1);
+    CK(h, cudaEventRecord(h->ev_h[slot], h->hstream));
+    h->h_used[slot] = true;
+  }
   h->chunks_since_flush++;
   if (h->chunks_since_flush >= h->flush_every) {
     rc = flush_h(h);
     if (rc) return rc;
   }
   if (h->timing) {
-    CK(h, cudaEventRecord(tm.stop, h->stream));
-    h->timers.push_back(tm);
+    CK(h, cudaEventRecord(h->t_stop, post_stream(h)));
+    h->t_chunks++;
   }
   h->rows_done += rows;
   return SPCA_OK;
@@ -239,8 +257,14 @@ int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda) {
   const int64_t R0 = h->chunk_rows;
   const size_t row_bytes = (size_t)h->n * h->ds;
   int64_t off = 0;
+  if (h->precision == SPCA_PREC_TC) {
+    int rr = tc_register_source(h, a, rows, lda);
+    if (rr) return rr;
+  }
   if (h->tail_rows > 0) {
     int64_t take = std::min(R0 - h->tail_rows, rows);
+    int rj = join_h(h);  // the tail may still be read by an H contraction
+    if (rj) return rj;
     CK(h, cudaMemcpy2DAsync((char *)h->tail + h->tail_rows * row_bytes, row_bytes, a,
                             (size_t)lda * h->ds, row_bytes, (size_t)take,
                             cudaMemcpyDeviceToDevice, h->stream));
@@ -259,6 +283,8 @@ int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda) {
   }
   if (off < rows) {
     int64_t rem = rows - off;
+    int rj = join_h(h);
+    if (rj) return rj;
     CK(h, cudaMemcpy2DAsync((char *)h->tail, row_bytes, a + (size_t)off * lda * h->ds,
                             (size_t)lda * h->ds, row_bytes, (size_t)rem,
                             cudaMemcpyDeviceToDevice, h->stream));
@@ -311,6 +337,8 @@ int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, boo
     CK(h, cudaStreamWaitEvent(h->stream, h->copy_done[i], 0));
     rc = push_device_rows(h, (const char *)h->dstage[i], take, h->n);
     if (rc) return rc;
+    rc = join_h(h);  // staging buffer i is free once its H contraction ran too
+    if (rc) return rc;
     CK(h, cudaEventRecord(h->comp_done[i], h->stream));
     h->stage_used[i] = true;
     off += take;
@@ -319,15 +347,15 @@ int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, boo
 }
 
 int collect_timers(spca_sketch *h) {
-  for (auto &t : h->timers) {
+  if (h->t_open) {
     float ms = 0.f;
-    CK(h, cudaEventElapsedTime(&ms, t.start, t.stop));
+    CK(h, cudaEventSynchronize(h->t_stop));
+    CK(h, cudaEventElapsedTime(&ms, h->t_start, h->t_stop));
     h->kernel_ms += ms;
-    h->timed_chunks++;
-    cudaEventDestroy(t.start);
-    cudaEventDestroy(t.stop);
+    h->timed_chunks += h->t_chunks;
+    h->t_open = false;
+    h->t_chunks = 0;
   }
-  h->timers.clear();
   return SPCA_OK;
 }
 
@@ -501,6 +529,8 @@ int spca_sketch_push(spca_handle_t h, const void *a, int64_t rows, int64_t ld, i
 int spca_sketch_reset(spca_handle_t h) {
   if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
   DeviceGuard dg(h->device);
+  int rj = join_h(h);
+  if (rj) return rj;
   CK(h, cudaStreamSynchronize(h->stream));
   CK(h, cudaMemsetAsync(h->hcs_dev, 0, (size_t)h->n * (h->l + 1) * 8, h->stream));
   if (h->carry_dev) CK(h, cudaMemsetAsync(h->carry_dev, 0, (size_t)h->n * 8, h->stream));
@@ -521,6 +551,8 @@ int spca_sketch_reset(spca_handle_t h) {
 int spca_sketch_sync(spca_handle_t h) {
   if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
   DeviceGuard dg(h->device);
+  int rj = join_h(h);
+  if (rj) return rj;
   CK(h, cudaStreamSynchronize(h->stream));
   int rc = collect_timers(h);
   if (rc) return rc;
@@ -547,6 +579,8 @@ int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out, double *co
       h->tail_rows = 0;
     }
     rc = flush_h(h);
+    if (rc) return rc;
+    rc = join_h(h);
     if (rc) return rc;
     if (h->rows_seen > h->g64_cap) {
       if (h->g64_dev) cudaFree(h->g64_dev);
@@ -671,6 +705,8 @@ int spca_enable_kernel_timing(spca_handle_t h, int enable) {
 int spca_kernel_time_ms(spca_handle_t h, double *ms, int64_t *launches) {
   if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
   DeviceGuard dg(h->device);
+  int rj = join_h(h);
+  if (rj) return rj;
   CK(h, cudaStreamSynchronize(h->stream));
   int rc = collect_timers(h);
   if (rc) return rc;
@@ -679,10 +715,29 @@ int spca_kernel_time_ms(spca_handle_t h, double *ms, int64_t *launches) {
   return SPCA_OK;
 }
 
+// Profiling aid (not part of include/spca.h): copy the per-CTA globaltimer
+// stamps of the last tensor-core chunk (which: 0 = G kernel, 1 = H kernel).
+int spca_debug_trace(spca_handle_t h, int which, unsigned long long *out, int64_t count) {
+  if (!h) return SPCA_ERR_STATE;
+  unsigned long long *src = which == 0 ? h->trace_g : h->trace_h;
+  if (!src) return set_err(h, SPCA_ERR_STATE, -1, "tracing off (set SPCA_TC_TRACE)");
+  DeviceGuard dg(h->device);
+  CK(h, cudaStreamSynchronize(h->stream));
+  CK(h, cudaMemcpy(out, src, (size_t)std::min<int64_t>(count, kTraceTimeline + 4 * 1024) * 8,
+                   cudaMemcpyDeviceToHost));
+  return SPCA_OK;
+}
+
 void spca_sketch_destroy(spca_handle_t h) {
   if (!h) return;
   DeviceGuard dg(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->hstream) {
+    cudaStreamSynchronize(h->hstream);
+    if (h->hstream != h->stream) cudaStreamDestroy(h->hstream);
+  }
+  for (cudaEvent_t e : {h->ev_g[0], h->ev_g[1], h->ev_h[0], h->ev_h[1], h->ev_join, h->t_start, h->t_stop})
+    if (e) cudaEventDestroy(e);
   if (h->copy_stream) {
     cudaStreamSynchronize(h->copy_stream);
     cudaStreamDestroy(h->copy_stream);
@@ -693,7 +748,7 @@ void spca_sketch_destroy(spca_handle_t h) {
   }
   void *bufs[] = {h->omega_dev, h->omega64_dev, h->tc_omega, h->g_dev, h->g64_dev, h->hcs_dev,
                   h->carry_dev, h->hpart, h->cspart, h->gpart, h->tc_ws, h->bad_dev, h->tail,
-                  h->dstage[0], h->dstage[1]};
+                  h->dstage[0], h->dstage[1], h->trace_g, h->trace_h};
   for (void *p : bufs)
     if (p) cudaFree(p);
   for (int i = 0; i < 2; ++i) {

@@ -34,21 +34,27 @@ bool tc_available(int device) {
   return major == 10 && minor == 0 && tma_encoder() != nullptr;
 }
 
-bool tc_supported_shape(int64_t n, int64_t l) { return n >= 32 && n % 4 == 0 && l >= 1 && l <= 256; }
+// l <= 128: wider sketches (config 5's l = 250) use the SIMT kernels until the
+// promoted accumulators of an N = 256 tile fit the register budget.
+bool tc_supported_shape(int64_t n, int64_t l) { return n >= 32 && n % 4 == 0 && l >= 1 && l <= 128; }
 
-int tc_lpad(int64_t l) { return l <= 64 ? 64 : (l <= 128 ? 128 : 256); }
+int tc_lpad(int64_t l) { return l <= 64 ? 64 : 128; }
 
 // Canonical chunk: ~48 MB of A so the H kernel's re-read hits L2; whole
 // 128-row tiles.
 int64_t tc_chunk_rows(int64_t n, int64_t /*l*/) {
-  int64_t r = (int64_t)(48ll << 20) / (4 * n);
-  r = std::max<int64_t>(128, std::min<int64_t>(8192, r));
+  int64_t mb = 48;
+  if (const char *e = getenv("SPCA_TC_CHUNK_MB")) mb = std::max<int64_t>(1, atoll(e));  // tuning knob
+  int64_t r = (int64_t)(mb << 20) / (4 * n);
+  r = std::max<int64_t>(128, std::min<int64_t>(16384, r));
   return (r / 128) * 128;
 }
 
 int tc_hsplit(int64_t n, int64_t /*l*/) {
   int64_t tiles = ceil_div(n, 128);
-  return (int)std::max<int64_t>(1, std::min<int64_t>(8, 148 / tiles));
+  int64_t hs = std::max<int64_t>(1, std::min<int64_t>(8, 148 / tiles));
+  if (const char *e = getenv("SPCA_TC_HSPLIT")) hs = std::max<int64_t>(1, atoll(e));  // tuning knob
+  return (int)hs;
 }
 
 int encode_2d(spca_sketch *h, CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer,
@@ -74,9 +80,9 @@ int tc_set_smem_attrs() {
   static bool done = false;
   if (done) return 0;
   cudaError_t e1 = cudaFuncSetAttribute(tc_g_kernel<LPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)TcCfgG<LPAD>::SMEM);
+                                        (int)TcCfg<LPAD>::SMEM);
   cudaError_t e2 = cudaFuncSetAttribute(tc_h_kernel<LPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)TcCfgH<LPAD>::SMEM);
+                                        (int)TcCfg<LPAD>::SMEM);
   if (e1 != cudaSuccess || e2 != cudaSuccess) return 1;
   done = true;
   return 0;
@@ -96,7 +102,7 @@ int tc_setup(spca_sketch *h) {
     CK(h, cudaMalloc(&h->hpart, (size_t)h->hsplit * h->n * h->lpad * 4));
     CK(h, cudaMemsetAsync(h->hpart, 0, (size_t)h->hsplit * h->n * h->lpad * 4, h->stream));
   }
-  int bad = lp == 64 ? tc_set_smem_attrs<64>() : (lp == 128 ? tc_set_smem_attrs<128>() : tc_set_smem_attrs<256>());
+  int bad = lp == 64 ? tc_set_smem_attrs<64>() : tc_set_smem_attrs<128>();
   if (bad) return set_err(h, SPCA_ERR_CUDA, -1, "cannot raise dynamic shared memory for the tc kernels");
   CK(h, cudaMalloc(&h->tc_omega, (size_t)2 * h->lpad * h->n * 4));
   float *whi = (float *)h->tc_omega;
@@ -108,53 +114,130 @@ int tc_setup(spca_sketch *h) {
   if (rc) return rc;
   rc = encode_2d(h, &h->tm_wlo, wlo, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, h->lpad);
   if (rc) return rc;
-  h->tc_ws_bytes = (size_t)2 * h->chunk_rows * h->lpad * 4;
+  if (getenv("SPCA_TC_SERIAL"))  // profiling knob: run G and H on one stream
+    h->hstream = h->stream;
+  else
+    CK(h, cudaStreamCreateWithFlags(&h->hstream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    CK(h, cudaEventCreateWithFlags(&h->ev_g[i], cudaEventDisableTiming));
+    CK(h, cudaEventCreateWithFlags(&h->ev_h[i], cudaEventDisableTiming));
+  }
+  CK(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  // two G^T slots (hi | lo each), so G of chunk c+1 overlaps H of chunk c
+  h->tc_ws_bytes = (size_t)4 * h->chunk_rows * h->lpad * 4;
   CK(h, cudaMalloc(&h->tc_ws, h->tc_ws_bytes));
+  for (int slot = 0; slot < 2; ++slot) {
+    float *ghi = (float *)h->tc_ws + (size_t)slot * 2 * h->chunk_rows * h->lpad;
+    float *glo = ghi + (size_t)h->chunk_rows * h->lpad;
+    int rs = encode_2d(h, &h->slot_tgh[slot], ghi, (uint64_t)h->chunk_rows, (uint64_t)h->lpad,
+                       (uint64_t)h->chunk_rows * 4, 32, h->lpad);
+    if (rs) return rs;
+    rs = encode_2d(h, &h->slot_tgl[slot], glo, (uint64_t)h->chunk_rows, (uint64_t)h->lpad,
+                   (uint64_t)h->chunk_rows * 4, 32, h->lpad);
+    if (rs) return rs;
+  }
   int64_t tiles = ceil_div(h->chunk_rows, 128);
   int64_t ksplit_max = std::max<int64_t>(1, 148 / tiles) + 1;
   h->gpart_elems = ksplit_max * tiles * 128 * h->lpad;
   CK(h, cudaMalloc(&h->gpart, (size_t)h->gpart_elems * 4));
+  if (getenv("SPCA_TC_TRACE")) {
+    const size_t words = (size_t)kTraceTimeline + 4 * 1024;
+    CK(h, cudaMalloc(&h->trace_g, words * 8));
+    CK(h, cudaMalloc(&h->trace_h, words * 8));
+    std::vector<unsigned long long> init(words, 0ull);
+    for (size_t i = kTraceTimeline; i < words; i += 2) init[i] = ~0ull;  // span minima
+    CK(h, cudaMemcpy(h->trace_g, init.data(), words * 8, cudaMemcpyHostToDevice));
+    CK(h, cudaMemcpy(h->trace_h, init.data(), words * 8, cudaMemcpyHostToDevice));
+  }
   CK(h, cudaStreamSynchronize(h->stream));
   return SPCA_OK;
 }
 
 template <int LPAD>
 void tc_launch(spca_sketch *h, const CUtensorMap &ta_g, const CUtensorMap &ta_h, const CUtensorMap &tgh,
-               const CUtensorMap &tgl, int rows, int ksplit, int kseg, int rseg, float *gout,
-               float *ghi, float *glo, int accumulate, int64_t *launches, cudaError_t *err) {
+               const CUtensorMap &tgl, int row_base, int rows, int ksplit, int kseg, int rseg,
+               float *gout, float *ghi, float *glo, int accumulate, int slot, int64_t *launches,
+               cudaError_t *err) {
   const int tiles = (int)ceil_div(rows, 128);
   const int64_t gstride = (int64_t)tiles * 128 * LPAD;
-  tc_g_kernel<LPAD><<<dim3(tiles, ksplit), kTcThreads, TcCfgG<LPAD>::SMEM, h->stream>>>(
-      ta_g, h->tm_whi, h->tm_wlo, rows, (int)h->n, kseg, (float *)h->gpart, gstride, h->rows_done,
-      h->bad_dev, h->tc_debug);
+  // G^T slot reuse: the H pass that read this slot two chunks ago must be done
+  if (h->h_used[slot] && (*err = cudaStreamWaitEvent(h->stream, h->ev_h[slot], 0)) != cudaSuccess) return;
+  tc_g_kernel<LPAD><<<dim3(tiles, ksplit), kTcThreads, TcCfg<LPAD>::SMEM, h->stream>>>(
+      ta_g, h->tm_whi, h->tm_wlo, rows, (int)h->n, kseg, row_base, (float *)h->gpart, gstride,
+      h->rows_done, h->bad_dev, h->tc_debug, h->trace_g, (int)h->chunk_seq);
   if ((*err = cudaGetLastError()) != cudaSuccess) return;
   ++*launches;
   tc_g_finalize<<<dim3((unsigned)ceil_div(rows, 8), LPAD / 32), dim3(32, 8), 0, h->stream>>>(
       (const float *)h->gpart, ksplit, gstride, rows, LPAD, (int)h->chunk_rows, gout, ghi, glo);
   if ((*err = cudaGetLastError()) != cudaSuccess) return;
   ++*launches;
-  tc_h_kernel<LPAD><<<dim3((unsigned)ceil_div(h->n, 128), h->hsplit), kTcThreads, TcCfgH<LPAD>::SMEM,
-                      h->stream>>>(ta_h, tgh, tgl, rows, (int)h->n, rseg, (float *)h->hpart,
-                                   (int64_t)h->n * LPAD, h->cspart, accumulate, h->compensated ? 1 : 0);
+  if ((*err = cudaEventRecord(h->ev_g[slot], h->stream)) != cudaSuccess) return;
+  if ((*err = cudaStreamWaitEvent(h->hstream, h->ev_g[slot], 0)) != cudaSuccess) return;
+  // H of this chunk runs on the second stream, concurrently with G of the next
+  tc_h_kernel<LPAD><<<dim3((unsigned)ceil_div(h->n, 128), h->hsplit), kTcThreads, TcCfg<LPAD>::SMEM,
+                      h->hstream>>>(ta_h, tgh, tgl, rows, (int)h->n, rseg, row_base, (float *)h->hpart,
+                                    (int64_t)h->n * LPAD, h->cspart, accumulate, h->compensated ? 1 : 0,
+                                    h->tc_debug >> 8, h->trace_h, (int)h->chunk_seq);
   if ((*err = cudaGetLastError()) != cudaSuccess) return;
   ++*launches;
+}
+
+// Remember TMA descriptors over a pushed device buffer so its full chunks
+// are addressed by row offset without re-encoding.
+int tc_register_source(spca_sketch *h, const void *a, int64_t rows, int64_t lda) {
+  if (rows < h->chunk_rows || (lda % 4) != 0 || (reinterpret_cast<uintptr_t>(a) % 16) != 0 ||
+      rows > INT32_MAX) {
+    h->src_ptr = nullptr;
+    return SPCA_OK;
+  }
+  if (h->src_ptr == a && h->src_rows == rows && h->src_lda == lda) return SPCA_OK;
+  int rc = encode_2d(h, &h->src_tg, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)lda * 4, 32, 128);
+  if (rc) return rc;
+  rc = encode_2d(h, &h->src_th, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)lda * 4, 32, 32);
+  if (rc) return rc;
+  h->src_ptr = a;
+  h->src_rows = rows;
+  h->src_lda = lda;
+  return SPCA_OK;
 }
 
 int tc_chunk(spca_sketch *h, const void *a, int64_t lda, int rows) {
   if ((lda % 4) != 0 || (reinterpret_cast<uintptr_t>(a) % 16) != 0)
     return set_err(h, SPCA_ERR_CONFIG, -1, "tensor-core path needs 16-byte aligned rows");
-  CUtensorMap ta_g, ta_h, tgh, tgl;
-  int rc = encode_2d(h, &ta_g, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)lda * 4, 32, 128);
-  if (rc) return rc;
-  rc = encode_2d(h, &ta_h, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)lda * 4, 32, 32);
-  if (rc) return rc;
-  float *ghi = (float *)h->tc_ws;
+  const int slot = (int)(h->chunk_seq & 1);
+  float *ghi = (float *)h->tc_ws + (size_t)slot * 2 * h->chunk_rows * h->lpad;
   float *glo = ghi + (size_t)h->chunk_rows * h->lpad;
-  // G^T hi / lo: lpad rows of chunk_rows floats (rows of this chunk valid)
-  rc = encode_2d(h, &tgh, ghi, (uint64_t)rows, (uint64_t)h->lpad, (uint64_t)h->chunk_rows * 4, 32, h->lpad);
-  if (rc) return rc;
-  rc = encode_2d(h, &tgl, glo, (uint64_t)rows, (uint64_t)h->lpad, (uint64_t)h->chunk_rows * 4, 32, h->lpad);
-  if (rc) return rc;
+  CUtensorMap fa_g, fa_h, fg_h, fg_l;
+  const CUtensorMap *ta_g, *ta_h, *tgh, *tgl;
+  int row_base = 0;
+  const char *base = (const char *)h->src_ptr;
+  const int64_t row_bytes = lda * 4;
+  const bool full = rows == h->chunk_rows;
+  if (full && base && lda == h->src_lda && (const char *)a >= base &&
+      ((const char *)a - base) % row_bytes == 0 &&
+      ((const char *)a - base) / row_bytes + rows <= h->src_rows) {
+    row_base = (int)(((const char *)a - base) / row_bytes);
+    ta_g = &h->src_tg;
+    ta_h = &h->src_th;
+  } else {
+    int rc = encode_2d(h, &fa_g, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)row_bytes, 32, 128);
+    if (rc) return rc;
+    rc = encode_2d(h, &fa_h, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)row_bytes, 32, 32);
+    if (rc) return rc;
+    ta_g = &fa_g;
+    ta_h = &fa_h;
+  }
+  if (full) {
+    tgh = &h->slot_tgh[slot];
+    tgl = &h->slot_tgl[slot];
+  } else {  // partial chunk: rows beyond it must read as zeros (TMA out of bounds)
+    int rc = encode_2d(h, &fg_h, ghi, (uint64_t)rows, (uint64_t)h->lpad, (uint64_t)h->chunk_rows * 4, 32, h->lpad);
+    if (rc) return rc;
+    rc = encode_2d(h, &fg_l, glo, (uint64_t)rows, (uint64_t)h->lpad, (uint64_t)h->chunk_rows * 4, 32, h->lpad);
+    if (rc) return rc;
+    tgh = &fg_h;
+    tgl = &fg_l;
+  }
   const int64_t tiles = ceil_div(rows, 128);
   int ksplit = (int)std::max<int64_t>(1, 148 / tiles);
   int kseg = (int)round_up(ceil_div(h->n, ksplit), 32);
@@ -166,13 +249,14 @@ int tc_chunk(spca_sketch *h, const void *a, int64_t lda, int rows) {
   const int acc = h->chunks_since_flush > 0 ? 1 : 0;
   cudaError_t err = cudaSuccess;
   if (h->lpad == 64)
-    tc_launch<64>(h, ta_g, ta_h, tgh, tgl, rows, ksplit, kseg, rseg, gout, ghi, glo, acc, &h->launches, &err);
-  else if (h->lpad == 128)
-    tc_launch<128>(h, ta_g, ta_h, tgh, tgl, rows, ksplit, kseg, rseg, gout, ghi, glo, acc, &h->launches, &err);
+    tc_launch<64>(h, *ta_g, *ta_h, *tgh, *tgl, row_base, rows, ksplit, kseg, rseg, gout, ghi, glo, acc, slot,
+                  &h->launches, &err);
   else
-    tc_launch<256>(h, ta_g, ta_h, tgh, tgl, rows, ksplit, kseg, rseg, gout, ghi, glo, acc, &h->launches, &err);
+    tc_launch<128>(h, *ta_g, *ta_h, *tgh, *tgl, row_base, rows, ksplit, kseg, rseg, gout, ghi, glo, acc, slot,
+                   &h->launches, &err);
   if (err != cudaSuccess)
     return set_err(h, SPCA_ERR_CUDA, -1, "tc kernel launch failed: %s", cudaGetErrorString(err));
+  h->chunk_seq++;
   return SPCA_OK;
 }
 
