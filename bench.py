@@ -4,10 +4,10 @@
                     [--config cfg2] [--precision auto|simt|tc]
 
 A step = one full sketch pass (Algorithm 4 steps 4-8) over the config's A,
-resident in HBM: every row pushed through libspca, H flushed, G widened,
+resident in HBM: every row pushed through libspca, H flushed, G widened, the
 state finished on the device; with N > 1 ranks each rank owns its own row
-shard (weak scaling: the per-GPU shard is the config's full m) and the
-step ends with the NCCL all-reduce of [H | col_sums].
+shard (weak scaling: the per-GPU shard is the config's full m) and the step
+ends with the NCCL all-reduce of [H | col_sums | rows].
 
 The JSON line (rank 0) carries: value (whole-job GB/s of A), e2e (same
 metric through the public API with A in pinned host memory, H2D and the D2H
@@ -38,7 +38,7 @@ UNIT = "GB/s"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=40)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="cfg2")
@@ -51,16 +51,18 @@ def parse():
 
 
 def peaks():
+    """(hbm GB/s, bf16 dense TF/s burst, kind) from MEASURED_PEAKS.json."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             d = json.load(fh)
-        return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
     except Exception:
-        return 6650.0, 1400.0, "fallback"
+        return 6650.0, 1590.0, "fallback"
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons while the timed region runs."""
+    """nvidia-smi clocks + throttle reasons, streamed every 50 ms while the
+    timed region runs."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -69,46 +71,60 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
-        self._stop = threading.Event()
+        self.proc = None
         self._t = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
-                parts = [x.strip() for x in out.strip().split(",")]
-                if len(parts) >= 7:
-                    self.samples.append(parts)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _reader(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.strip().split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._reader, daemon=True)
+            self._t.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
+        if self.proc is not None:
+            time.sleep(0.06)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
         if self._t:
-            self._t.join(timeout=10)
+            self._t.join(timeout=5)
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(s[0]) for s in self.samples) if v]
+        mx = [v for v in (num(s[1]) for s in self.samples) if v]
+        pw = [v for v in (num(s[2]) for s in self.samples) if v]
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
                           if s[3 + i].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        busy = [v for v in sm if v > 0]
+        return {"sm_mhz": float(np.median(busy)), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_max": max(pw) if pw else None}
 
 
-def dist_setup(args):
+def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -133,9 +149,9 @@ def cpu_oracle_rate(n_rows: int, n: int, l: int, seed: int, threads: int):
 
 def run_reference(args):
     """Reference arm: the CPU implementation of the path (the oracle port —
-    the reference is pure Python/numpy and cannot be compiled), all host
-    threads, bounded sample of the same workload per step."""
-    world, rank, _ = dist_setup(args)
+    the reference is pure Python/numpy, nothing to compile), all host
+    threads, a bounded sample of the same workload per step."""
+    world, rank, _ = dist_setup()
     if rank != 0:
         return
     from paper_1704_07669_b200.synth import config_shape
@@ -143,29 +159,40 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     sample_rows = 8192
     rates, times = [], []
-    for i in range(args.warmup + args.steps):
+    for i in range(min(args.warmup, 3) + min(args.steps, 10)):
         r, dt = cpu_oracle_rate(sample_rows, cs["n"], cs["l"], seed=i, threads=threads)
-        if i >= args.warmup:
+        if i >= min(args.warmup, 3):
             rates.append(r)
             times.append(dt)
     value = float(np.mean(rates))
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(rates),
+        "warmup": min(args.warmup, 3), "ms_per_step": 1e3 * float(np.mean(times)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
         "config": {"workload": f"{args.config} sample", "m": sample_rows, "n": cs["n"], "l": cs["l"],
                    "block_rows": 4096},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample_rows} rows x {cs['n']} fp32 widened to fp64 per step"},
+                         "sample": f"{sample_rows} rows x {cs['n']} fp32 widened to fp64 per step "
+                                   "(numpy oracle of sketch.py:52-116, blocked path)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def profile_traffic(rows_per_chunk: float):
+    """dram read+write bytes of one chunk's G/H kernels, scaled from the
+    committed ncu --set full capture (profiles/ncu_summary.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
+            return json.load(fh)["dram_bytes_per_row"] * rows_per_chunk
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
-    world, rank, local = dist_setup(args)
+    world, rank, local = dist_setup()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
@@ -174,15 +201,14 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
 
-    import oracle as O  # noqa: F401  (only for the cpu_baseline leg below)
-    from paper_1704_07669_b200 import GpuSketch, PcaConfig, gaussian_matrix, synth
+    from paper_1704_07669_b200 import GpuSketch, gaussian_matrix, synth
     from paper_1704_07669_b200.parallel import allreduce_sketch
 
     cs = synth.config_shape(args.config)
     m = args.rows or cs["m"]
     n, l = cs["n"], cs["l"]
     bytes_per_rank = m * n * 4
-    hbm_peak, tc_peak, peak_kind = peaks()
+    hbm_peak, bf16_peak, peak_kind = peaks()
 
     # this rank's shard: rows [rank*m, (rank+1)*m) of the job's matrix
     a = synth.config_matrix(args.config, device=dev, rows=(rank * m, (rank + 1) * m),
@@ -190,14 +216,13 @@ def run_ours(args):
     omega = gaussian_matrix(n, l, 1)
     sk = GpuSketch(n, omega, np.float32, precision=args.precision, device=dev, rows_hint=m)
     stream = torch.cuda.current_stream(dev)
-    launches0 = sk.kernel_launches()
 
     def step():
         sk.reset()
         sk.push(a, 0)
         g, h, c, rows = sk.finish(on_device=True)
         if pg is not None:
-            allreduce_sketch(h, c, pg)
+            allreduce_sketch(h, c, pg, rows=rows)
         return g, h, c
 
     for _ in range(args.warmup):
@@ -229,20 +254,43 @@ def run_ours(args):
     ms_step = ms / args.steps
     value = world * bytes_per_rank / (ms_step * 1e-3) / 1e9
 
-    # roofline of the dominant kernel group (one canonical chunk: G, H contractions)
+    # Roofline of the dominant kernel group: one canonical chunk of the pass
+    # (G and H contractions + finalize + column sums), timed with CUDA events on
+    # the library's streams over the timed region (window per pass / chunks).
     chunk_rows = sk.chunk_rows()
     chunks_per_pass = -(-m // chunk_rows)
     chunk_ms = kern_ms / max(1, kern_chunks)
     avg_rows = m / chunks_per_pass
     chunk_bytes = avg_rows * n * 4
-    achieved = chunk_bytes / (chunk_ms * 1e-3) / 1e9
     flops = 4.0 * avg_rows * n * l
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None,
-                "peak_kind": peak_kind, "kernel": "sketch chunk (G = A Omega, H += A^T G, col sums)",
-                "chunk_rows": chunk_rows, "chunk_ms": chunk_ms,
-                "achieved_tflops": flops / (chunk_ms * 1e-3) / 1e12,
-                "algorithmic_bytes_per_chunk": chunk_bytes, "flops_per_chunk": flops}
+    used_tc = (args.precision in ("auto", "tc")) and l <= 128
+    if used_tc:
+        peak_tf = bf16_peak / 2.0 / 3.0   # 3xTF32: tf32 = bf16/2, three products
+        peak_desc = "3xTF32 effective = measured bf16 burst / 2 (tf32) / 3 (products)"
+    else:
+        peak_tf = 148 * 128 * 2 * 1.965e9 / 1e12  # FFMA nominal
+        peak_desc = "FFMA nominal (148 SMs x 128 lanes x 2 x 1965 MHz)"
+    hbm_floor = chunk_bytes / (hbm_peak * 1e9)
+    tc_floor = flops / (peak_tf * 1e12)
+    achieved_tf = flops / (chunk_ms * 1e-3) / 1e12
+    achieved_gbs = chunk_bytes / (chunk_ms * 1e-3) / 1e9
+    if tc_floor >= hbm_floor:
+        roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": achieved_tf / peak_tf}
+    else:
+        roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved_gbs / hbm_peak}
+    roofline.update({
+        "traffic": profile_traffic(avg_rows) if used_tc else None,
+        "peak_kind": peak_kind, "peak_desc": peak_desc,
+        "kernel": "sketch chunk: tc_g_kernel + tc_g_finalize + tc_h_kernel + colsum" if used_tc
+                  else "sketch chunk: simt_g_kernel + simt_h_kernel + colsum",
+        "chunk_rows": chunk_rows, "chunk_ms": chunk_ms,
+        "hbm": {"achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved_gbs / hbm_peak},
+        "algorithmic_bytes_per_chunk": chunk_bytes, "flops_per_chunk": flops,
+        "floors_ms_per_chunk": {"hbm": hbm_floor * 1e3, "tensor": tc_floor * 1e3},
+    })
 
     out = {}
     if rank == 0 and not args.no_e2e:
@@ -267,7 +315,8 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.config, "m_per_gpu": m, "n": n, "l": l, "k": cs["k"],
                    "rank": cs["rank"], "spectrum": cs["spectrum"], "noise": cs["noise"],
-                   "precision": args.precision, "parallelism": f"row-shard x{world}",
+                   "precision": "3xTF32 tcgen05" if used_tc else "FFMA",
+                   "parallelism": f"row-shard x{world}",
                    "l2": "inputs larger than L2 (A is %.1f GB per GPU)" % (bytes_per_rank / 1e9)},
         "roofline": roofline,
         "clocks": clk.summary(),

@@ -40,10 +40,11 @@ bool tc_supported_shape(int64_t n, int64_t l) { return n >= 32 && n % 4 == 0 && 
 
 int tc_lpad(int64_t l) { return l <= 64 ? 64 : 128; }
 
-// Canonical chunk: ~48 MB of A so the H kernel's re-read hits L2; whole
-// 128-row tiles.
+// Canonical chunk: large (up to 16384 rows, ~640 MB) so the per-kernel ramp
+// and tail amortise; measured on B200 this beats L2-resident chunks, whose
+// G/H kernels are too short to reach steady state. Whole 128-row tiles.
 int64_t tc_chunk_rows(int64_t n, int64_t /*l*/) {
-  int64_t mb = 48;
+  int64_t mb = 640;
   if (const char *e = getenv("SPCA_TC_CHUNK_MB")) mb = std::max<int64_t>(1, atoll(e));  // tuning knob
   int64_t r = (int64_t)(mb << 20) / (4 * n);
   r = std::max<int64_t>(128, std::min<int64_t>(16384, r));
@@ -51,8 +52,10 @@ int64_t tc_chunk_rows(int64_t n, int64_t /*l*/) {
 }
 
 int tc_hsplit(int64_t n, int64_t /*l*/) {
+  // about two waves of H tiles over the 148 SMs (the G kernel of the next
+  // chunk fills the gaps from the other stream)
   int64_t tiles = ceil_div(n, 128);
-  int64_t hs = std::max<int64_t>(1, std::min<int64_t>(8, 148 / tiles));
+  int64_t hs = std::max<int64_t>(1, std::min<int64_t>(8, (2 * 148 + tiles / 2) / tiles));
   if (const char *e = getenv("SPCA_TC_HSPLIT")) hs = std::max<int64_t>(1, atoll(e));  // tuning knob
   return (int)hs;
 }
