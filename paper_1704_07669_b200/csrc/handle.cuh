@@ -31,6 +31,7 @@ struct spca_sketch {
   double *omega64_dev = nullptr; // n x l fp64, exactly the values used
   void *tc_omega = nullptr;      // Omega^T hi | lo (2 x lpad x n fp32, sketch_tc.cuh)
   CUtensorMap tm_whi, tm_wlo;    // TMA maps over Omega^T hi / lo
+  CUtensorMap tm_gT;             // TMA map over the G^T hi / lo slots (sketch_fused.cuh)
 
   void *g_dev = nullptr;         // cap x lpad compute precision
   int64_t g_cap = 0;
@@ -43,8 +44,12 @@ struct spca_sketch {
   double *cspart = nullptr;      // [hsplit][n]
   void *gpart = nullptr;         // P1 split-K partials
   int64_t gpart_elems = 0;
-  void *tc_ws = nullptr;         // tensor-core workspace: G_hi | G_lo (2 x chunk x lpad)
+  void *tc_ws = nullptr;         // tensor-core G^T slots [kSlots][2][lpad][R0]
   size_t tc_ws_bytes = 0;
+  int *tc_ctr = nullptr;         // per-launch ordering counters of the pass kernel
+  int64_t tc_ctr_chunks = 0;     // chunks one launch may cover
+  int num_sms = 148;
+  int max_pairs = 74;             // co-resident CTA pairs of the pass kernel
   unsigned long long *bad_dev = nullptr;
 
   int64_t chunk_rows = 0;        // canonical chunk (R0)
@@ -55,7 +60,7 @@ struct spca_sketch {
   int chunks_since_flush = 0;
   int flush_every = 64;
   int tc_debug = 0;              // SPCA_TC_DEBUG bitmask (profiling experiments only)
-  unsigned long long *trace_g = nullptr, *trace_h = nullptr;  // SPCA_TC_TRACE timelines
+  unsigned long long *trace = nullptr;  // SPCA_TC_TRACE per-CTA timeline
   bool finished = false;
 
   // host staging (pinned double buffer)
@@ -74,20 +79,11 @@ struct spca_sketch {
   bool t_open = false;
   int64_t t_chunks = 0;
 
-  // tensor-core path: the H contraction of chunk c runs on `hstream` while
-  // the G contraction of chunk c+1 runs on `stream` (two kernels in flight)
-  cudaStream_t hstream = nullptr;
-  cudaEvent_t ev_g[2] = {nullptr, nullptr};  // G^T slot ready (finalize done)
-  cudaEvent_t ev_h[2] = {nullptr, nullptr};  // G^T slot released (H done)
-  cudaEvent_t ev_join = nullptr;
-  bool h_used[2] = {false, false};
-  int64_t chunk_seq = 0;
   // TMA descriptors cached per pushed source buffer (encoding is a driver
   // call of several microseconds; a full-matrix push encodes once)
   const void *src_ptr = nullptr;
   int64_t src_rows = 0, src_lda = 0;
   CUtensorMap src_tg, src_th;
-  CUtensorMap slot_tgh[2], slot_tgl[2];  // G^T slot descriptors for full chunks
   double kernel_ms = 0.0;
   int64_t timed_chunks = 0;
 

@@ -1,0 +1,602 @@
+// sketch_fused.cuh — the single-read tensor-core sketch pass (sm_100a, fp32).
+//
+// One persistent kernel per push walks the pushed rows in canonical chunks of
+// R0 rows small enough to stay resident in the 126 MB L2 (R0 * n * 4 B ~ 40 MB)
+// and computes, per chunk c (reference sketch.py:85-113, paper Alg. 4 steps 5-7):
+//
+//   G_c = A_c Omega          ("G units": 128-row tile x K segment of n)
+//   H  += A_c^T G_c          ("H units": 128-column tile x row segment of R0)
+//   col_sums += 1^T A_c      (inside the H units)
+//
+// A_c is read from HBM once, by the G units (TMA, L2 evict_last); the H units
+// re-read it from L2 one stage later (evict_first). The units form one global
+// sequence of stages {G(s), H(s-1)}, s = 0..C, dealt round robin to CTA
+// pairs (clusters of 2, one CTA per SM), so the H contraction of chunk c
+// overlaps the G contraction of chunk c+1 inside one launch and every pair
+// does the same work over a push. A pair unit covers two adjacent tiles (one
+// per CTA) that share the B operand: the leader CTA issues M = 256 pair MMAs
+// (cta_group::2), each CTA holding its own A tile in TMEM and half of B in
+// shared memory (sketch_tc.cuh).
+//
+// Ordering between CTAs uses counters in global memory (acquire / release);
+// every wait points at units dealt no later than the waiting one, so with all
+// CTAs resident the pass cannot deadlock:
+//   * G(c, t, seg) writes its K-split partial into slot c % kSlots, counts
+//     itself in seg_cnt[c][t], waits until all S segments of the tile are
+//     there, then reduces ITS slice of the tile's rows over the S partials
+//     in fixed order -> G rows (output) and the split G^T hi / lo operands,
+//     and counts the slice in ready[c]. Partial and G^T slots are reused
+//     kSlots chunks later, after ready / hdone of that chunk say so.
+//   * H(c, x, rs) loads its B operand (G^T of chunk c) once ready[c] counts
+//     every slice; it adds its fp32 partial into the running H and its column
+//     sums into the fp64 running sums in chunk order (hseq[x]), so results
+//     are bitwise reproducible and independent of how rows were pushed.
+//
+// Warp roles per CTA (sketch_tc.cuh): A producer, MMA issuer (leader only),
+// B producer, converters (tf32 split into TMEM, accumulator promotion) and
+// epilogue warps, which take each finished unit from a staging tile in
+// shared memory so the converters go straight on with the next unit.
+#pragma once
+
+#include "sketch_tc.cuh"
+
+namespace spca {
+
+constexpr int kSlots = 3;      // chunks whose G partials / G^T may be in flight
+
+// optional timeline (SPCA_TC_TRACE): per CTA kTraceStride globaltimer stamps:
+// [0] start, [1] end, then per unit i < kTraceUnits, 8 stamps at 8 + 8i:
+//   0 converters start, 1 converters' main loop done, 2 staged for the epilogue,
+//   3 epilogue took it, 4 epilogue done, 5 MMA first issue, 6 MMA last issue,
+//   7 B producer passed its dependency wait
+constexpr int kTraceStride = 1024;
+constexpr int kTraceUnits = 127;
+constexpr int kTraceWords = 256 * kTraceStride;
+#define SPCA_TRACE(i, k)                                                         \
+  do {                                                                           \
+    if (trace && (i) < kTraceUnits) trace[8 + 8 * (i) + (k)] = ptx::globaltimer(); \
+  } while (0)
+
+struct FusedSched {
+  int C;          // chunks in this launch
+  int R0;         // canonical chunk rows (multiple of 256)
+  int rows_last;  // rows of the last chunk (<= R0)
+  int T, Tl;      // 256-row tile pairs of a full / the last chunk
+  int nt, ntl;    // real 128-row tiles of a full / the last chunk
+  int S, kseg;    // G: K segments over n, K blocks per segment
+  int nkb;        // K blocks over n
+  int X, nx;      // H: 256-column tile pairs, real 128-column tiles over n
+  int RS, hseg;   // H: row segments per chunk, K blocks per segment
+  int total;      // pair units in this launch
+};
+
+struct FusedArgs {
+  FusedSched s;
+  int n;
+  int row_base;             // first launch row in the A tensor maps
+  float *gpart;             // [kSlots][2T][S][128][LPAD] K-split partials
+  float *gT;                // [kSlots][2][LPAD][R0] G^T hi, lo
+  float *g_out;             // G rows of this launch, [rows][LPAD]
+  float *hpart;             // [n][LPAD] running H (fp32, flushed to fp64 by the host)
+  double *colsum;           // [n] running column sums (fp64)
+  double *carry;            // [n] Kahan carry, or null
+  int *seg_cnt;             // [C][2T] partials written per tile
+  int *ready;               // [C] reduced row slices
+  int *hdone;               // [C] finished H units
+  int *hseq;                // [2X] H units applied to column tile x (chunk-major)
+  int accumulate;           // H of the launch's first chunk adds to hpart
+  int64_t first_row;        // global index of the launch's first row
+  unsigned long long *bad_row;
+  unsigned long long *trace;  // null unless profiling
+  int dbg;                    // profiling knobs (SPCA_TC_DEBUG), 0 in production:
+                              // 1 converters skip the split, 2 no MMAs, 4 no B loads, 8 no A loads
+};
+
+struct FusedUnit {
+  int kind;   // 0 = G, 1 = H
+  int c;      // chunk
+  int a, b;   // G: tile pair, segment; H: column-tile pair, row segment
+  int k0, nk; // first K block and count (G: over n; H: over the chunk's rows)
+  int rows;   // rows of chunk c
+};
+
+__host__ __device__ inline int fused_total(const FusedSched &s) {
+  const int XR = s.X * s.RS;
+  const int g0 = (s.C == 1 ? s.Tl : s.T) * s.S;
+  const int mid = s.C > 2 ? (s.C - 2) * (s.T * s.S + XR) : 0;
+  const int last = s.C >= 2 ? s.Tl * s.S + XR : 0;
+  return g0 + mid + last + XR;
+}
+
+__host__ __device__ __forceinline__ FusedUnit fused_decode(const FusedSched &s, int u) {
+  const int TS = s.T * s.S, XR = s.X * s.RS;
+  int kind = 0, c = 0, r = u;
+  const int g0 = (s.C == 1 ? s.Tl : s.T) * s.S;
+  if (u >= g0) {
+    u -= g0;
+    const int F = TS + XR;
+    const int nmid = s.C > 2 ? s.C - 2 : 0;
+    if (u < nmid * F) {  // stage 1 + u / F: G(stage) then H(stage - 1)
+      const int st = 1 + u / F;
+      r = u - (st - 1) * F;
+      if (r < TS) {
+        c = st;
+      } else {
+        kind = 1;
+        c = st - 1;
+        r -= TS;
+      }
+    } else {
+      u -= nmid * F;
+      const int TlS = s.Tl * s.S;
+      if (s.C >= 2 && u < TlS + XR) {  // stage C - 1
+        if (u < TlS) {
+          c = s.C - 1;
+          r = u;
+        } else {
+          kind = 1;
+          c = s.C - 2;
+          r = u - TlS;
+        }
+      } else {  // stage C: H of the last chunk
+        if (s.C >= 2) u -= TlS + XR;
+        kind = 1;
+        c = s.C - 1;
+        r = u;
+      }
+    }
+  }
+  FusedUnit f;
+  f.kind = kind;
+  f.c = c;
+  f.rows = c == s.C - 1 ? s.rows_last : s.R0;
+  if (kind == 0) {
+    f.a = r / s.S;
+    f.b = r - f.a * s.S;
+    f.k0 = f.b * s.kseg;
+    f.nk = min(s.kseg, s.nkb - f.k0);
+  } else {  // row-segment major: consecutive units of one column tile are X apart
+    f.b = r / s.X;
+    f.a = r - f.b * s.X;
+    f.k0 = f.b * s.hseg;
+    f.nk = max(0, min(s.hseg, (f.rows + 31) / 32 - f.k0));
+  }
+  return f;
+}
+
+__device__ __forceinline__ int fused_real_tiles(const FusedSched &s, int c) {
+  return c == s.C - 1 ? s.ntl : s.nt;
+}
+
+template <int LPAD>
+struct PairBars {
+  using C = TcCfg<LPAD>;
+  uint64_t a_full[C::NA], a_empty[C::NA];  // local: A producer <-> converters
+  uint64_t b_full[C::NB];                  // leader: both CTAs' B halves landed
+  uint64_t b_empty[C::NB];                 // each CTA: MMAs done with the B stage
+  uint64_t t_full[C::NT];                  // leader: both CTAs' converters stored the stage
+  uint64_t t_empty[C::NT];                 // each CTA: MMAs done with the TMEM stage
+  uint64_t acc_full[2];                    // each CTA: accumulator period complete
+  uint64_t acc_empty[2];                   // leader: both CTAs folded the period
+  uint64_t epi_full, epi_empty;            // local: converters <-> epilogue staging
+  uint32_t tmem_base;
+};
+
+template <int LPAD>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
+tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ CUtensorMap tAh,
+               const __grid_constant__ CUtensorMap tWhi, const __grid_constant__ CUtensorMap tWlo,
+               const __grid_constant__ CUtensorMap tGT, const FusedArgs args) {
+  using C = TcCfg<LPAD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ PairBars<LPAD> bars;
+  __shared__ float stg_chk[2 * 128];   // G: per half, NaN iff the row holds a non-finite value
+  __shared__ double stg_cs[2 * 128];   // H: per half, column-sum partial
+  const FusedSched &sc = args.s;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_rank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  unsigned long long *trace = args.trace ? args.trace + (size_t)blockIdx.x * kTraceStride : nullptr;
+  if (trace && threadIdx.x == 0) trace[0] = ptx::globaltimer();
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NA; ++s) {
+      ptx::mbar_init(&bars.a_full[s], 1);
+      ptx::mbar_init(&bars.a_empty[s], kTcConv / 64);  // one converter group per block
+    }
+    for (int s = 0; s < C::NB; ++s) {
+      ptx::mbar_init(&bars.b_full[s], 1);
+      ptx::mbar_init(&bars.b_empty[s], 1);
+    }
+    for (int s = 0; s < C::NT; ++s) {
+      ptx::mbar_init(&bars.t_full[s], 2 * kTcConv / 64);  // one group in each CTA
+      ptx::mbar_init(&bars.t_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&bars.acc_full[s], 1);
+      ptx::mbar_init(&bars.acc_empty[s], 2 * kTcConv / 32);
+    }
+    ptx::mbar_init(&bars.epi_full, kTcConv);
+    ptx::mbar_init(&bars.epi_empty, kTcEpi);
+    ptx::fence_mbar_init();
+    ptx::tma_prefetch(&tAg);
+    ptx::tma_prefetch(&tAh);
+    ptx::tma_prefetch(&tWhi);
+    ptx::tma_prefetch(&tWlo);
+    ptx::tma_prefetch(&tGT);
+  }
+  if (warp == 1) ptx::tmem_alloc2(&bars.tmem_base, kTmemCols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();  // both CTAs' barriers exist before any cross-CTA arrive
+  ptx::tc_fence_after();
+  const uint32_t tmem = bars.tmem_base;
+
+  if (warp == 0) {  // ---------------------------------------------- A producer
+    const uint64_t keep = ptx::policy_evict_last(), drop = ptx::policy_evict_first();
+    int gkb = 0;
+#pragma unroll 1
+    for (int u = cid; u < sc.total; u += ncl) {
+      const FusedUnit f = fused_decode(sc, u);
+      const int rbase = args.row_base + f.c * sc.R0;
+      const int tile = 2 * f.a + (int)rank;
+#pragma unroll 1
+      for (int kb = 0; kb < f.nk; ++kb, ++gkb) {
+        const int s = gkb % C::NA;
+        if (gkb >= C::NA) ptx::mbar_wait(&bars.a_empty[s], ((gkb / C::NA) - 1) & 1);
+        if (ptx::elect_one()) {
+          uint8_t *st = smem + s * C::A_BYTES;
+          if (args.dbg & 8) {
+            ptx::mbar_arrive(&bars.a_full[s]);
+          } else {
+            ptx::mbar_arrive_expect_tx(&bars.a_full[s], C::A_BYTES);
+            if (f.kind == 0) {  // 128 rows x 32 k, row-major (swizzled)
+              ptx::tma_load_2d_hint(st, &tAg, &bars.a_full[s], (f.k0 + kb) * 32, rbase + tile * 128, keep);
+            } else {            // 32 rows x 128 columns, one unswizzled box
+              ptx::tma_load_2d_hint(st, &tAh, &bars.a_full[s], tile * 128, rbase + (f.k0 + kb) * 32, drop);
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 2) {  // ---------------------------------- B producer (half)
+    const uint64_t keep = ptx::policy_evict_last();
+    int gkb = 0, ui = 0;
+#pragma unroll 1
+    for (int u = cid; u < sc.total; u += ncl, ++ui) {
+      const FusedUnit f = fused_decode(sc, u);
+      const int gslot = f.c % kSlots;
+      if (f.kind == 1 && f.nk > 0) {  // G^T of chunk c must be complete
+        if (ptx::elect_one()) {
+          ptx::spin_until_geq(&args.ready[f.c], fused_real_tiles(sc, f.c) * sc.S);
+          ptx::fence_proxy_async_global();
+        }
+        __syncwarp();
+      }
+      if (lane == 0) SPCA_TRACE(ui, 7);
+#pragma unroll 1
+      for (int kb = 0; kb < f.nk; ++kb, ++gkb) {
+        const int s = gkb % C::NB;
+        if (gkb >= C::NB) ptx::mbar_wait(&bars.b_empty[s], ((gkb / C::NB) - 1) & 1);
+        if (ptx::elect_one()) {
+          uint8_t *st = smem + C::B_OFF + s * C::B_STAGE;
+          const uint32_t bar = ptx::mapa(ptx::smem_u32(&bars.b_full[s]), 0);
+          const int k = (f.k0 + kb) * 32;
+          if (args.dbg & 4) {
+            if (rank == 0) ptx::mbar_arrive(&bars.b_full[s]);
+          } else {
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&bars.b_full[s], 2 * C::B_STAGE);
+          if (f.kind == 0) {
+            if constexpr (C::FOUR) {
+              ptx::tma_load_2d_pair(st, rank == 0 ? &tWhi : &tWlo, bar, k, 0, keep);
+            } else {
+              ptx::tma_load_2d_pair(st, &tWhi, bar, k, 64 * (int)rank, keep);
+              ptx::tma_load_2d_pair(st + C::BH_BYTES, &tWlo, bar, k, 64 * (int)rank, keep);
+            }
+          } else {
+            if constexpr (C::FOUR) {
+              ptx::tma_load_2d_pair(st, &tGT, bar, k, (2 * gslot + (int)rank) * 64, keep);
+            } else {
+              ptx::tma_load_2d_pair(st, &tGT, bar, k, 2 * gslot * LPAD + 64 * (int)rank, keep);
+              ptx::tma_load_2d_pair(st + C::BH_BYTES, &tGT, bar, k, (2 * gslot + 1) * LPAD + 64 * (int)rank, keep);
+            }
+          }
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {  // ------------------------- MMA issuer (leader CTA)
+    if (rank == 0) {
+      int gkb = 0, gq = 0, ui = 0;
+#pragma unroll 1
+      for (int u = cid; u < sc.total; u += ncl, ++ui) {
+        const FusedUnit f = fused_decode(sc, u);
+#pragma unroll 1
+        for (int kb = 0; kb < f.nk; ++kb, ++gkb) {
+          if (lane == 0 && kb == 1) SPCA_TRACE(ui, 5);
+          if (lane == 0 && kb == f.nk - 1) SPCA_TRACE(ui, 6);
+          const int ts = gkb % C::NT, bs = gkb % C::NB;
+          const int q = gq + kb / kPromote, buf = q & 1;
+          const bool first = (kb % kPromote) == 0;
+          if (first && q >= 2) ptx::mbar_wait_cluster(&bars.acc_empty[buf], ((q >> 1) - 1) & 1);
+          ptx::mbar_wait_cluster(&bars.t_full[ts], (gkb / C::NT) & 1);
+          ptx::mbar_wait_cluster(&bars.b_full[bs], (gkb / C::NB) & 1);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+            if (!(args.dbg & 2))
+              tc_mma_stage2<LPAD>(tmem, tmem + buf * C::ACC_COLS, ts,
+                                  ptx::smem_u32(smem + C::B_OFF + bs * C::B_STAGE), first);
+            ptx::mma2_commit_both(&bars.t_empty[ts]);
+            ptx::mma2_commit_both(&bars.b_empty[bs]);
+            if ((kb % kPromote) == kPromote - 1 || kb == f.nk - 1) ptx::mma2_commit_both(&bars.acc_full[buf]);
+          }
+          __syncwarp();
+        }
+        gq += (f.nk + kPromote - 1) / kPromote;
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {  // ------------ converters and promotion
+    const int ct = threadIdx.x - 128;
+    const int t = ct & 127;    // TMEM lane: G row / H column within the tile
+    const int half = ct >> 7;  // which 16 of the 32 K values, which half of the outputs
+    const uint32_t lane_base = tmem + ((uint32_t)(t & ~31) << 16);
+    const uint32_t tfull_l = ptx::mapa(ptx::smem_u32(&bars.t_full[0]), 0);
+    const uint32_t accempty_l = ptx::mapa(ptx::smem_u32(&bars.acc_empty[0]), 0);
+    const uint32_t stg_row = ptx::smem_u32(smem + C::STG_OFF + t * LPAD * 4);
+    int gkb = 0, gq = 0, ui = 0;
+#pragma unroll 1
+    for (int u = cid; u < sc.total; u += ncl, ++ui) {
+      const FusedUnit f = fused_decode(sc, u);
+      float racc[C::HALF_COLS];
+#pragma unroll
+      for (int i = 0; i < C::HALF_COLS; ++i) racc[i] = 0.f;
+      float chk = 0.f;            // G: NaN iff this row holds a non-finite value
+      float cs = 0.f, cc = 0.f;   // H: column sum (fp32 Kahan over the unit)
+      const int nq = (f.nk + kPromote - 1) / kPromote;
+      int promoted = 0;
+      if (ct == 0) SPCA_TRACE(ui, 0);
+      // fold accumulator period qg into racc, hand the accumulator back to the MMAs
+      auto promote = [&](int qg) {
+        const int buf = qg & 1;
+        ptx::mbar_wait(&bars.acc_full[buf], (qg >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t base = lane_base + buf * C::ACC_COLS + half * C::HALF_COLS;
+#pragma unroll
+        for (int c0 = 0; c0 < C::HALF_COLS; c0 += 16) {
+          float v[16];
+          ptx::tmem_ld16(base + c0, v);
+          if constexpr (C::FOUR) {  // the A * W_lo half of the accumulator
+            float w[16];
+            ptx::tmem_ld16(base + LPAD + c0, w);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += w[i];
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) racc[c0 + i] += v[i];
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(accempty_l + 8 * buf);
+      };
+      // The two converter groups take alternate K blocks (group `half` the blocks
+      // of its parity, all 32 K values of its row / column), so each warp has two
+      // MMA periods of time per block; promotion still splits the output columns.
+#pragma unroll 1
+      for (int kb = half; kb < f.nk; kb += 2) {
+        const int gk = gkb + kb;
+        const int s = gk % C::NA, ts = gk % C::NT;
+        ptx::mbar_wait(&bars.a_full[s], (gk / C::NA) & 1);
+        // the TMEM stage must be free before the first store
+        if (gk >= C::NT) ptx::mbar_wait(&bars.t_empty[ts], ((gk / C::NT) - 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t tst = lane_base + C::A_TMEM + 64 * ts;
+        if (args.dbg & 1) {
+          __syncwarp();
+        } else if (f.kind == 0) {
+          const uint32_t row = ptx::smem_u32(smem + s * C::A_BYTES + t * 128);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            float4 v[4];
+            float hi[16], lo[16];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) v[q4] = ptx::lds128(row + (((4 * hh + q4) ^ (t & 7)) << 4));
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              chk = fmaf(v[q4].x, 0.f, fmaf(v[q4].y, 0.f, fmaf(v[q4].z, 0.f, fmaf(v[q4].w, 0.f, chk))));
+              split3(v[q4].x, hi[4 * q4 + 0], lo[4 * q4 + 0]);
+              split3(v[q4].y, hi[4 * q4 + 1], lo[4 * q4 + 1]);
+              split3(v[q4].z, hi[4 * q4 + 2], lo[4 * q4 + 2]);
+              split3(v[q4].w, hi[4 * q4 + 3], lo[4 * q4 + 3]);
+            }
+            ptx::tmem_st16(tst + 16 * hh, hi);
+            ptx::tmem_st16(tst + 32 + 16 * hh, lo);
+          }
+        } else {
+          const uint32_t raw = ptx::smem_u32(smem + s * C::A_BYTES + t * 4);  // column t
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            float v[16], hi[16], lo[16];
+#pragma unroll
+            for (int kq = 0; kq < 16; ++kq) v[kq] = ptx::lds32(raw + (16 * hh + kq) * 512);
+#pragma unroll
+            for (int kq = 0; kq < 16; ++kq) split3(v[kq], hi[kq], lo[kq]);
+            float p8[8];  // pairwise sum of the 16 values, then one Kahan step
+#pragma unroll
+            for (int i = 0; i < 8; ++i) p8[i] = v[2 * i] + v[2 * i + 1];
+            const float blk = ((p8[0] + p8[1]) + (p8[2] + p8[3])) + ((p8[4] + p8[5]) + (p8[6] + p8[7]));
+            const float y = blk - cc;
+            const float tt = cs + y;
+            cc = (tt - cs) - y;
+            cs = tt;
+            ptx::tmem_st16(tst + 16 * hh, hi);
+            ptx::tmem_st16(tst + 32 + 16 * hh, lo);
+          }
+        }
+        // every lane's loads were consumed by the split above: the landing slot
+        // can go back to TMA (one lane's arrive would not order the other lanes'
+        // outstanding shared loads against the next TMA write)
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&bars.a_empty[s]);
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(tfull_l + 8 * ts);
+        // fold the period before the one this block closes (the MMAs run ahead)
+        if ((kb % kPromote) == kPromote - 2 + half && kb >= kPromote) promote(gq + promoted++);
+      }
+      gkb += f.nk;
+      for (; promoted < nq; ++promoted) promote(gq + promoted);
+      gq += nq;
+      if (ct == 0) SPCA_TRACE(ui, 1);
+      // stage the result for the epilogue warps (16-byte chunks XOR-swizzled by row)
+      if (ui >= 1) ptx::mbar_wait(&bars.epi_empty, (ui - 1) & 1);
+      if (ct == 0) SPCA_TRACE(ui, 2);
+#pragma unroll
+      for (int i = 0; i < C::HALF_COLS / 4; ++i) {
+        const int q = half * (C::HALF_COLS / 4) + i;
+        ptx::st_shared_v4(stg_row + ((q ^ (t & 7)) << 4),
+                          make_float4(racc[4 * i], racc[4 * i + 1], racc[4 * i + 2], racc[4 * i + 3]));
+      }
+      if (f.kind == 0)
+        stg_chk[half * 128 + t] = chk;
+      else
+        stg_cs[half * 128 + t] = (double)cs - (double)cc;
+      ptx::mbar_arrive(&bars.epi_full);
+    }
+  } else if (warp >= 12) {  // ------------------------------------ epilogue
+    const int e = threadIdx.x - kTcEpiBase;  // row (G) / column (H) of the tile
+    constexpr int NQ = LPAD / 4;             // 16-byte chunks per row
+    const uint32_t srow = ptx::smem_u32(smem + C::STG_OFF + e * LPAD * 4);
+    const int twoT = 2 * sc.T;
+    int ui = 0;
+#pragma unroll 1
+    for (int u = cid; u < sc.total; u += ncl, ++ui) {
+      const FusedUnit f = fused_decode(sc, u);
+      const int tile = 2 * f.a + (int)rank;
+      ptx::mbar_wait(&bars.epi_full, ui & 1);
+      if (e == 0) SPCA_TRACE(ui, 3);
+      if (f.kind == 0) {  // ---------------------------------- G epilogue
+        const int gslot = f.c % kSlots;
+        const bool real = tile < fused_real_tiles(sc, f.c);
+        const int row = tile * 128 + e;
+        float chk = 0.f;
+        if (real) {
+          // the partial slot was last used kSlots chunks ago: its slices must be reduced
+          if (f.c >= kSlots && e == 0) ptx::spin_until_geq(&args.ready[f.c - kSlots], sc.nt * sc.S);
+          ptx::named_bar(2, kTcEpi);
+          float4 *gp = reinterpret_cast<float4 *>(
+              args.gpart + ((((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 + e) * LPAD);
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) gp[q] = ptx::lds128(srow + ((q ^ (e & 7)) << 4));
+          chk = stg_chk[e] + stg_chk[128 + e];
+        }
+        ptx::mbar_arrive(&bars.epi_empty);
+        if (real) {
+          if (!(chk == 0.f) && row < f.rows)
+            report_bad_row(args.bad_row, args.first_row + (int64_t)f.c * sc.R0 + row);
+          // every writer fences its own stores before the count (a fence by one
+          // thread does not drain the other warps' outstanding stores)
+          __threadfence();
+          ptx::named_bar(2, kTcEpi);
+          int *cnt = &args.seg_cnt[f.c * twoT + tile];
+          if (e == 0) {
+            atomicAdd(cnt, 1);
+            ptx::spin_until_geq(cnt, sc.S);  // every segment's partial is in
+            if (f.c >= kSlots) ptx::spin_until_geq(&args.hdone[f.c - kSlots], sc.nx * sc.RS);
+          }
+          ptx::named_bar(2, kTcEpi);
+          // reduce this segment's slice of the tile's rows over the S partials (fixed order)
+          const int r0 = (f.b * 128) / sc.S, r1 = ((f.b + 1) * 128) / sc.S;
+          const float *p0 = args.gpart + (((size_t)gslot * twoT + tile) * sc.S) * 128 * LPAD;
+          float *ghi = args.gT + (size_t)(2 * gslot) * LPAD * sc.R0;
+          float *glo = ghi + (size_t)LPAD * sc.R0;
+          const int items = (r1 - r0) * NQ;
+#pragma unroll 1
+          for (int it = e; it < items; it += kTcEpi) {
+            const int r = r0 + it / NQ, q = it % NQ;
+            // partials of other CTAs: read through L2 (.cg), never a stale L1 line
+            const float4 *src = reinterpret_cast<const float4 *>(p0 + (size_t)r * LPAD) + q;
+            float4 acc = __ldcg(src);
+            for (int z = 1; z < sc.S; ++z) {
+              const float4 b4 = __ldcg(src + (size_t)z * 128 * NQ);
+              acc.x += b4.x; acc.y += b4.y; acc.z += b4.z; acc.w += b4.w;
+            }
+            const int rc = tile * 128 + r;  // row within the chunk
+            const bool valid = rc < f.rows;
+            if (valid) reinterpret_cast<float4 *>(args.g_out + ((int64_t)f.c * sc.R0 + rc) * LPAD)[q] = acc;
+            const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float h1 = 0.f, l1 = 0.f;
+              if (valid) split3(a4[j], h1, l1);
+              ghi[(size_t)(4 * q + j) * sc.R0 + rc] = h1;
+              glo[(size_t)(4 * q + j) * sc.R0 + rc] = l1;
+            }
+          }
+          ptx::fence_proxy_async_global();
+          __threadfence();
+          ptx::named_bar(2, kTcEpi);
+          if (e == 0) atomicAdd(&args.ready[f.c], 1);
+        }
+      } else {  // ------------------------------------------------ H epilogue
+        const bool real = tile < sc.nx;
+        const int seq = f.c * sc.RS + f.b;
+        const int col = tile * 128 + e;
+        double csv = 0.0;
+        if (real) {
+          if (e == 0) ptx::spin_until_geq(&args.hseq[tile], seq);
+          ptx::named_bar(2, kTcEpi);
+          if (col < args.n) {
+            float4 *hp = reinterpret_cast<float4 *>(args.hpart + (int64_t)col * LPAD);
+            const bool overwrite = !args.accumulate && seq == 0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              float4 w = ptx::lds128(srow + ((q ^ (e & 7)) << 4));
+              if (!overwrite) {
+                const float4 o = __ldcg(hp + q);
+                w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+              }
+              hp[q] = w;
+            }
+          }
+          csv = stg_cs[e] + stg_cs[128 + e];
+        }
+        ptx::mbar_arrive(&bars.epi_empty);
+        if (real) {
+          if (col < args.n) {
+            if (args.carry) {
+              const double y = csv - __ldcg(args.carry + col);
+              const double s0 = __ldcg(args.colsum + col);
+              const double tt = s0 + y;
+              args.carry[col] = (tt - s0) - y;
+              args.colsum[col] = tt;
+            } else {
+              args.colsum[col] = __ldcg(args.colsum + col) + csv;
+            }
+          }
+          __threadfence();
+          ptx::named_bar(2, kTcEpi);
+          if (e == 0) {
+            ptx::st_release(&args.hseq[tile], seq + 1);
+            atomicAdd(&args.hdone[f.c], 1);
+          }
+        }
+      }
+      if (e == 0) SPCA_TRACE(ui, 4);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();  // the peer's TMEM and barriers stay live until the leader is done
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc2(tmem, kTmemCols);
+  }
+  if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
+}
+
+}  // namespace spca

@@ -76,17 +76,6 @@ struct DeviceGuard {
   }
 };
 
-// stream that runs the H contraction and everything that depends on it
-cudaStream_t post_stream(const spca_sketch *h) { return h->hstream ? h->hstream : h->stream; }
-
-// make the main stream wait for all work queued on the H stream
-int join_h(spca_sketch *h) {
-  if (!h->hstream) return SPCA_OK;
-  CK(h, cudaEventRecord(h->ev_join, h->hstream));
-  CK(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
-  return SPCA_OK;
-}
-
 int grid_for(int64_t count, int threads = 256) {
   int64_t b = ceil_div(count, threads);
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
@@ -113,7 +102,7 @@ int ensure_g(spca_sketch *h, int64_t rows_needed) {
 }  // namespace
 
 // tensor-core path (uses set_err / CK / grid_for above)
-#include "sketch_tc.cuh"
+#include "sketch_fused.cuh"
 #include "tc_host.cuh"
 
 namespace {
@@ -198,11 +187,11 @@ int flush_h(spca_sketch *h) {
   if (h->chunks_since_flush == 0) return SPCA_OK;
   int64_t count = h->n * h->l;
   if (h->dtype == SPCA_F32)
-    h_flush<float><<<grid_for(count), 256, 0, post_stream(h)>>>(
+    h_flush<float><<<grid_for(count), 256, 0, h->stream>>>(
         (const float *)h->hpart, h->hsplit, h->n * h->lpad, (int)h->n, (int)h->l, (int)h->lpad,
         h->hcs_dev);
   else
-    h_flush<double><<<grid_for(count), 256, 0, post_stream(h)>>>(
+    h_flush<double><<<grid_for(count), 256, 0, h->stream>>>(
         (const double *)h->hpart, h->hsplit, h->n * h->lpad, (int)h->n, (int)h->l, (int)h->lpad,
         h->hcs_dev);
   CK_LAUNCH(h);
@@ -210,46 +199,72 @@ int flush_h(spca_sketch *h) {
   return SPCA_OK;
 }
 
+void open_timing(spca_sketch *h) {
+  if (h->timing && !h->t_open) {
+    if (!h->t_start) cudaEventCreate(&h->t_start);
+    if (!h->t_stop) cudaEventCreate(&h->t_stop);
+    cudaEventRecord(h->t_start, h->stream);
+    h->t_open = true;
+    h->t_chunks = 0;
+  }
+}
+
+int close_timing(spca_sketch *h, int64_t chunks) {
+  if (h->timing) {
+    CK(h, cudaEventRecord(h->t_stop, h->stream));
+    h->t_chunks += chunks;
+  }
+  return SPCA_OK;
+}
+
+// SIMT path: one canonical chunk (G, H, column sums), flush every ~1M rows
 int process_chunk(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   if (rows <= 0) return SPCA_OK;
   int rc = ensure_g(h, h->rows_done + rows);
   if (rc) return rc;
-  if (h->timing && !h->t_open) {
-    if (!h->t_start) CK(h, cudaEventCreate(&h->t_start));
-    if (!h->t_stop) CK(h, cudaEventCreate(&h->t_stop));
-    CK(h, cudaEventRecord(h->t_start, h->stream));
-    h->t_open = true;
-    h->t_chunks = 0;
-  }
-  if (h->precision == SPCA_PREC_TC) {
-    rc = tc_chunk(h, a, lda, (int)rows);
-  } else if (h->dtype == SPCA_F32) {
+  open_timing(h);
+  if (h->dtype == SPCA_F32) {
     rc = simt_chunk<float>(h, (const float *)a, lda, (int)rows);
   } else {
     rc = simt_chunk<double>(h, (const double *)a, lda, (int)rows);
   }
   if (rc) return rc;
-  // column sums and the H flush follow the H contraction on its stream
-  colsum_accumulate<<<(unsigned)ceil_div(h->n, 256), 256, 0, post_stream(h)>>>(
+  colsum_accumulate<<<(unsigned)ceil_div(h->n, 256), 256, 0, h->stream>>>(
       h->cspart, h->hsplit, (int)h->n, h->hcs_dev + h->n * h->l,
       h->compensated ? h->carry_dev : nullptr);
   CK_LAUNCH(h);
-  if (h->hstream) {
-    const int slot = (int)((h->chunk_seq - 1) & 1);
-    CK(h, cudaEventRecord(h->ev_h[slot], h->hstream));
-    h->h_used[slot] = true;
-  }
   h->chunks_since_flush++;
   if (h->chunks_since_flush >= h->flush_every) {
     rc = flush_h(h);
     if (rc) return rc;
   }
-  if (h->timing) {
-    CK(h, cudaEventRecord(h->t_stop, post_stream(h)));
-    h->t_chunks++;
-  }
+  rc = close_timing(h, 1);
+  if (rc) return rc;
   h->rows_done += rows;
   return SPCA_OK;
+}
+
+// Tensor-core path: `rows` rows (whole canonical chunks, or the final partial
+// chunk) through the pass kernel, in launches that end at H flush points.
+int process_rows_tc(spca_sketch *h, const char *a, int64_t lda, int64_t rows) {
+  int rc = ensure_g(h, h->rows_done + rows);
+  if (rc) return rc;
+  open_timing(h);
+  int64_t off = 0, chunks = 0;
+  while (off < rows) {
+    const int64_t room = std::max<int64_t>(1, h->flush_every - h->chunks_since_flush);
+    const int64_t take = std::min<int64_t>(rows - off, room * h->chunk_rows);
+    rc = tc_launch_rows(h, a + (size_t)off * lda * 4, lda, take);
+    if (rc) return rc;
+    h->rows_done += take;
+    chunks += ceil_div(take, h->chunk_rows);
+    off += take;
+    if (h->chunks_since_flush >= h->flush_every) {
+      rc = flush_h(h);
+      if (rc) return rc;
+    }
+  }
+  return close_timing(h, chunks);
 }
 
 // Rows already on the device: feed canonical chunks, keep the remainder in `tail`.
@@ -263,17 +278,24 @@ int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda) {
   }
   if (h->tail_rows > 0) {
     int64_t take = std::min(R0 - h->tail_rows, rows);
-    int rj = join_h(h);  // the tail may still be read by an H contraction
-    if (rj) return rj;
     CK(h, cudaMemcpy2DAsync((char *)h->tail + h->tail_rows * row_bytes, row_bytes, a,
                             (size_t)lda * h->ds, row_bytes, (size_t)take,
                             cudaMemcpyDeviceToDevice, h->stream));
     h->tail_rows += take;
     off = take;
     if (h->tail_rows == R0) {
-      int rc = process_chunk(h, h->tail, h->n, R0);
+      int rc = h->precision == SPCA_PREC_TC ? process_rows_tc(h, (const char *)h->tail, h->n, R0)
+                                            : process_chunk(h, h->tail, h->n, R0);
       if (rc) return rc;
       h->tail_rows = 0;
+    }
+  }
+  if (h->precision == SPCA_PREC_TC) {  // all whole chunks in one go
+    const int64_t whole = ((rows - off) / R0) * R0;
+    if (whole > 0) {
+      int rc = process_rows_tc(h, a + (size_t)off * lda * h->ds, lda, whole);
+      if (rc) return rc;
+      off += whole;
     }
   }
   while (rows - off >= R0) {
@@ -283,8 +305,6 @@ int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda) {
   }
   if (off < rows) {
     int64_t rem = rows - off;
-    int rj = join_h(h);
-    if (rj) return rj;
     CK(h, cudaMemcpy2DAsync((char *)h->tail, row_bytes, a + (size_t)off * lda * h->ds,
                             (size_t)lda * h->ds, row_bytes, (size_t)rem,
                             cudaMemcpyDeviceToDevice, h->stream));
@@ -336,8 +356,6 @@ int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, boo
     CK(h, cudaEventRecord(h->copy_done[i], h->copy_stream));
     CK(h, cudaStreamWaitEvent(h->stream, h->copy_done[i], 0));
     rc = push_device_rows(h, (const char *)h->dstage[i], take, h->n);
-    if (rc) return rc;
-    rc = join_h(h);  // staging buffer i is free once its H contraction ran too
     if (rc) return rc;
     CK(h, cudaEventRecord(h->comp_done[i], h->stream));
     h->stage_used[i] = true;
@@ -427,13 +445,15 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
     if (h->precision == SPCA_PREC_TC) h->chunk_rows = tc_chunk_rows(n, l);
   }
   h->stage_rows = h->chunk_rows;
+  if (h->precision == SPCA_PREC_TC)  // host staging in ~512 MB pieces: many chunks per launch
+    h->stage_rows = h->chunk_rows * std::max<int64_t>(1, (512ll << 20) / (h->chunk_rows * n * 4));
   // row splits of the H kernel: enough CTAs with the n tiles
   {
     int bn = h->bl == 32 ? 128 : 64;
     int64_t tiles = ceil_div(n, bn) * (h->lpad / h->bl);
     int64_t want = ceil_div(148 * 2, tiles);
     h->hsplit = (int)std::max<int64_t>(1, std::min<int64_t>(8, want));
-    if (h->precision == SPCA_PREC_TC) h->hsplit = tc_hsplit(n, l);
+    if (h->precision == SPCA_PREC_TC) h->hsplit = 1;  // the pass kernel keeps one running H
   }
   // flush the fp32 H partials into fp64 every ~1M rows
   h->flush_every = (int)std::max<int64_t>(1, (1 << 20) / h->chunk_rows);
@@ -529,8 +549,6 @@ int spca_sketch_push(spca_handle_t h, const void *a, int64_t rows, int64_t ld, i
 int spca_sketch_reset(spca_handle_t h) {
   if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
   DeviceGuard dg(h->device);
-  int rj = join_h(h);
-  if (rj) return rj;
   CK(h, cudaStreamSynchronize(h->stream));
   CK(h, cudaMemsetAsync(h->hcs_dev, 0, (size_t)h->n * (h->l + 1) * 8, h->stream));
   if (h->carry_dev) CK(h, cudaMemsetAsync(h->carry_dev, 0, (size_t)h->n * 8, h->stream));
@@ -551,8 +569,6 @@ int spca_sketch_reset(spca_handle_t h) {
 int spca_sketch_sync(spca_handle_t h) {
   if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
   DeviceGuard dg(h->device);
-  int rj = join_h(h);
-  if (rj) return rj;
   CK(h, cudaStreamSynchronize(h->stream));
   int rc = collect_timers(h);
   if (rc) return rc;
@@ -574,13 +590,12 @@ int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out, double *co
   int rc;
   if (!h->finished) {
     if (h->tail_rows > 0) {
-      rc = process_chunk(h, h->tail, h->n, h->tail_rows);
+      rc = h->precision == SPCA_PREC_TC ? process_rows_tc(h, (const char *)h->tail, h->n, h->tail_rows)
+                                        : process_chunk(h, h->tail, h->n, h->tail_rows);
       if (rc) return rc;
       h->tail_rows = 0;
     }
     rc = flush_h(h);
-    if (rc) return rc;
-    rc = join_h(h);
     if (rc) return rc;
     if (h->rows_seen > h->g64_cap) {
       if (h->g64_dev) cudaFree(h->g64_dev);
@@ -705,8 +720,6 @@ int spca_enable_kernel_timing(spca_handle_t h, int enable) {
 int spca_kernel_time_ms(spca_handle_t h, double *ms, int64_t *launches) {
   if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
   DeviceGuard dg(h->device);
-  int rj = join_h(h);
-  if (rj) return rj;
   CK(h, cudaStreamSynchronize(h->stream));
   int rc = collect_timers(h);
   if (rc) return rc;
@@ -715,16 +728,25 @@ int spca_kernel_time_ms(spca_handle_t h, double *ms, int64_t *launches) {
   return SPCA_OK;
 }
 
-// Profiling aid (not part of include/spca.h): copy the per-CTA globaltimer
-// stamps of the last tensor-core chunk (which: 0 = G kernel, 1 = H kernel).
+// Profiling aid (not part of include/spca.h): copy the per-CTA timeline of
+// the last pass-kernel launch (sketch_fused.cuh kTraceStride layout).
 int spca_debug_trace(spca_handle_t h, int which, unsigned long long *out, int64_t count) {
   if (!h) return SPCA_ERR_STATE;
-  unsigned long long *src = which == 0 ? h->trace_g : h->trace_h;
-  if (!src) return set_err(h, SPCA_ERR_STATE, -1, "tracing off (set SPCA_TC_TRACE)");
+  (void)which;
+  if (!h->trace) return set_err(h, SPCA_ERR_STATE, -1, "tracing off (set SPCA_TC_TRACE)");
   DeviceGuard dg(h->device);
   CK(h, cudaStreamSynchronize(h->stream));
-  CK(h, cudaMemcpy(out, src, (size_t)std::min<int64_t>(count, kTraceTimeline + 4 * 1024) * 8,
-                   cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(out, h->trace, (size_t)std::min<int64_t>(count, kTraceWords) * 8, cudaMemcpyDeviceToHost));
+  return SPCA_OK;
+}
+
+// Profiling aid (not part of include/spca.h): copy the pass kernel's K-split
+// partial slots ([kSlots][2T][S][128][lpad] fp32).
+int spca_debug_gpart(spca_handle_t h, float *out, int64_t count) {
+  if (!h || !h->gpart) return SPCA_ERR_STATE;
+  DeviceGuard dg(h->device);
+  CK(h, cudaStreamSynchronize(h->stream));
+  CK(h, cudaMemcpy(out, h->gpart, (size_t)std::min<int64_t>(count, h->gpart_elems) * 4, cudaMemcpyDeviceToHost));
   return SPCA_OK;
 }
 
@@ -732,11 +754,7 @@ void spca_sketch_destroy(spca_handle_t h) {
   if (!h) return;
   DeviceGuard dg(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  if (h->hstream) {
-    cudaStreamSynchronize(h->hstream);
-    if (h->hstream != h->stream) cudaStreamDestroy(h->hstream);
-  }
-  for (cudaEvent_t e : {h->ev_g[0], h->ev_g[1], h->ev_h[0], h->ev_h[1], h->ev_join, h->t_start, h->t_stop})
+  for (cudaEvent_t e : {h->t_start, h->t_stop})
     if (e) cudaEventDestroy(e);
   if (h->copy_stream) {
     cudaStreamSynchronize(h->copy_stream);
@@ -748,7 +766,7 @@ void spca_sketch_destroy(spca_handle_t h) {
   }
   void *bufs[] = {h->omega_dev, h->omega64_dev, h->tc_omega, h->g_dev, h->g64_dev, h->hcs_dev,
                   h->carry_dev, h->hpart, h->cspart, h->gpart, h->tc_ws, h->bad_dev, h->tail,
-                  h->dstage[0], h->dstage[1], h->trace_g, h->trace_h};
+                  h->dstage[0], h->dstage[1], h->trace, h->tc_ctr};
   for (void *p : bufs)
     if (p) cudaFree(p);
   for (int i = 0; i < 2; ++i) {

@@ -40,28 +40,47 @@ bool tc_supported_shape(int64_t n, int64_t l) { return n >= 32 && n % 4 == 0 && 
 
 int tc_lpad(int64_t l) { return l <= 64 ? 64 : 128; }
 
-// Canonical chunk: large (up to 16384 rows, ~640 MB) so the per-kernel ramp
-// and tail amortise; measured on B200 this beats L2-resident chunks, whose
-// G/H kernels are too short to reach steady state. Whole 128-row tiles.
+// Canonical chunk of the single-read pass: A_c is read from HBM by the G
+// units and again from L2 by the H units one stage later, so about two
+// chunks must stay resident in the 126 MB L2: R0 * n * 4 B ~ 40 MB by default
+// (SPCA_TC_CHUNK_MB). Whole 256-row tile pairs, at most 8192 rows.
 int64_t tc_chunk_rows(int64_t n, int64_t /*l*/) {
-  int64_t mb = 640;
+  int64_t mb = 40;
   if (const char *e = getenv("SPCA_TC_CHUNK_MB")) mb = std::max<int64_t>(1, atoll(e));  // tuning knob
   int64_t r = (int64_t)(mb << 20) / (4 * n);
-  r = std::max<int64_t>(128, std::min<int64_t>(16384, r));
-  return (r / 128) * 128;
+  r = std::max<int64_t>(256, std::min<int64_t>(8192, r));
+  return (r / 256) * 256;
 }
 
-int tc_hsplit(int64_t n, int64_t /*l*/) {
-  // about two waves of H tiles over the 148 SMs (the G kernel of the next
-  // chunk fills the gaps from the other stream)
-  int64_t tiles = ceil_div(n, 128);
-  int64_t hs = std::max<int64_t>(1, std::min<int64_t>(8, (2 * 148 + tiles / 2) / tiles));
-  if (const char *e = getenv("SPCA_TC_HSPLIT")) hs = std::max<int64_t>(1, atoll(e));  // tuning knob
-  return (int)hs;
+// K blocks (32 deep) per work unit: the G units split n, the H units split a
+// chunk's rows, both into pieces of about this size.
+int tc_unit_kb() {
+  int u = 32;
+  if (const char *e = getenv("SPCA_TC_UNIT_KB")) u = std::max(1, atoi(e));  // tuning knob
+  return u;
+}
+
+FusedSched tc_base_sched(const spca_sketch *h) {
+  FusedSched s{};
+  const int U = tc_unit_kb();
+  s.R0 = (int)h->chunk_rows;
+  s.nt = s.R0 / 128;
+  s.T = s.nt / 2;
+  s.nkb = (int)ceil_div(h->n, 32);
+  s.S = (int)ceil_div(s.nkb, U);
+  s.kseg = (int)ceil_div(s.nkb, s.S);
+  s.S = (int)ceil_div(s.nkb, s.kseg);
+  s.nx = (int)ceil_div(h->n, 128);
+  s.X = (int)ceil_div(s.nx, 2);
+  const int rkb = s.R0 / 32;
+  s.RS = (int)ceil_div(rkb, U);
+  s.hseg = (int)ceil_div(rkb, s.RS);
+  s.RS = (int)ceil_div(rkb, s.hseg);
+  return s;
 }
 
 int encode_2d(spca_sketch *h, CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer,
-              uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+              uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, bool swizzle = true) {
   EncodeTiledFn enc = tma_encoder();
   if (!enc) return set_err(h, SPCA_ERR_CUDA, -1, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
@@ -69,7 +88,8 @@ int encode_2d(spca_sketch *h, CUtensorMap *map, const void *ptr, uint64_t inner,
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(ptr), dims, strides, box,
-                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return set_err(h, SPCA_ERR_CUDA, -1, "tensor map encode failed (%d): dims %llu x %llu stride %llu",
@@ -82,19 +102,37 @@ template <int LPAD>
 int tc_set_smem_attrs() {
   static bool done = false;
   if (done) return 0;
-  cudaError_t e1 = cudaFuncSetAttribute(tc_g_kernel<LPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)TcCfg<LPAD>::SMEM);
-  cudaError_t e2 = cudaFuncSetAttribute(tc_h_kernel<LPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)TcCfg<LPAD>::SMEM);
-  if (e1 != cudaSuccess || e2 != cudaSuccess) return 1;
+  if (cudaFuncSetAttribute(tc_pass_kernel<LPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)TcCfg<LPAD>::SMEM) != cudaSuccess)
+    return 1;
   done = true;
   return 0;
+}
+
+// CTA pairs that can be resident at once: the persistent pass needs every
+// CTA of its grid co-resident (its inter-CTA waits assume it).
+template <int LPAD>
+int tc_max_pairs() {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2, 1, 1);
+  cfg.blockDim = dim3(kTcThreads, 1, 1);
+  cfg.dynamicSmemBytes = TcCfg<LPAD>::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, tc_pass_kernel<LPAD>, &cfg) != cudaSuccess) return 0;
+  return nc;
 }
 
 int tc_setup(spca_sketch *h) {
   const int lp = tc_lpad(h->l);
   if (lp != h->lpad) {
-    // the SIMT layout padded l to 32/64; the tensor-core path needs 64/128/256
+    // the SIMT layout padded l to 32/64; the tensor-core path needs 64/128
     h->lpad = lp;
     h->bl = 64;
     cudaFree(h->omega_dev);
@@ -102,87 +140,43 @@ int tc_setup(spca_sketch *h) {
     cudaFree(h->hpart);
     h->hpart = nullptr;
     CK(h, cudaMalloc(&h->omega_dev, (size_t)h->n * h->lpad * 4));
-    CK(h, cudaMalloc(&h->hpart, (size_t)h->hsplit * h->n * h->lpad * 4));
-    CK(h, cudaMemsetAsync(h->hpart, 0, (size_t)h->hsplit * h->n * h->lpad * 4, h->stream));
+    CK(h, cudaMalloc(&h->hpart, (size_t)h->n * h->lpad * 4));
+    CK(h, cudaMemsetAsync(h->hpart, 0, (size_t)h->n * h->lpad * 4, h->stream));
   }
   int bad = lp == 64 ? tc_set_smem_attrs<64>() : tc_set_smem_attrs<128>();
-  if (bad) return set_err(h, SPCA_ERR_CUDA, -1, "cannot raise dynamic shared memory for the tc kernels");
+  if (bad) return set_err(h, SPCA_ERR_CUDA, -1, "cannot raise dynamic shared memory for the tc kernel");
+  CK(h, cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
+  h->max_pairs = lp == 64 ? tc_max_pairs<64>() : tc_max_pairs<128>();
+  if (h->max_pairs < 1) return set_err(h, SPCA_ERR_CUDA, -1, "no CTA pair of the pass kernel fits an SM pair");
   CK(h, cudaMalloc(&h->tc_omega, (size_t)2 * h->lpad * h->n * 4));
   float *whi = (float *)h->tc_omega;
   float *wlo = whi + (size_t)h->lpad * h->n;
   tc_omega_prepare<<<grid_for((int64_t)h->lpad * h->n), 256, 0, h->stream>>>(
       h->omega64_dev, (int)h->n, (int)h->l, (int)h->lpad, whi, wlo);
   CK_LAUNCH(h);
-  int rc = encode_2d(h, &h->tm_whi, whi, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, h->lpad);
+  // B tiles are loaded as 64-row halves (one per CTA of a pair)
+  int rc = encode_2d(h, &h->tm_whi, whi, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, 64);
   if (rc) return rc;
-  rc = encode_2d(h, &h->tm_wlo, wlo, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, h->lpad);
+  rc = encode_2d(h, &h->tm_wlo, wlo, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, 64);
   if (rc) return rc;
-  if (getenv("SPCA_TC_SERIAL"))  // profiling knob: run G and H on one stream
-    h->hstream = h->stream;
-  else
-    CK(h, cudaStreamCreateWithFlags(&h->hstream, cudaStreamNonBlocking));
-  for (int i = 0; i < 2; ++i) {
-    CK(h, cudaEventCreateWithFlags(&h->ev_g[i], cudaEventDisableTiming));
-    CK(h, cudaEventCreateWithFlags(&h->ev_h[i], cudaEventDisableTiming));
-  }
-  CK(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
-  // two G^T slots (hi | lo each), so G of chunk c+1 overlaps H of chunk c
-  h->tc_ws_bytes = (size_t)4 * h->chunk_rows * h->lpad * 4;
+  const FusedSched s = tc_base_sched(h);
+  // G^T hi / lo of kSlots chunks: [kSlots][2][lpad][R0], one TMA map
+  h->tc_ws_bytes = (size_t)kSlots * 2 * h->lpad * s.R0 * 4;
   CK(h, cudaMalloc(&h->tc_ws, h->tc_ws_bytes));
-  for (int slot = 0; slot < 2; ++slot) {
-    float *ghi = (float *)h->tc_ws + (size_t)slot * 2 * h->chunk_rows * h->lpad;
-    float *glo = ghi + (size_t)h->chunk_rows * h->lpad;
-    int rs = encode_2d(h, &h->slot_tgh[slot], ghi, (uint64_t)h->chunk_rows, (uint64_t)h->lpad,
-                       (uint64_t)h->chunk_rows * 4, 32, h->lpad);
-    if (rs) return rs;
-    rs = encode_2d(h, &h->slot_tgl[slot], glo, (uint64_t)h->chunk_rows, (uint64_t)h->lpad,
-                   (uint64_t)h->chunk_rows * 4, 32, h->lpad);
-    if (rs) return rs;
-  }
-  int64_t tiles = ceil_div(h->chunk_rows, 128);
-  int64_t ksplit_max = std::max<int64_t>(1, 148 / tiles) + 1;
-  h->gpart_elems = ksplit_max * tiles * 128 * h->lpad;
+  rc = encode_2d(h, &h->tm_gT, h->tc_ws, (uint64_t)s.R0, (uint64_t)kSlots * 2 * h->lpad, (uint64_t)s.R0 * 4,
+                 32, 64);
+  if (rc) return rc;
+  h->gpart_elems = (int64_t)kSlots * 2 * s.T * s.S * 128 * h->lpad;
   CK(h, cudaMalloc(&h->gpart, (size_t)h->gpart_elems * 4));
+  // ordering counters of one launch (at most flush_every chunks)
+  h->tc_ctr_chunks = h->flush_every;
+  CK(h, cudaMalloc(&h->tc_ctr, (size_t)(h->tc_ctr_chunks * (2 * s.T + 2) + 2 * s.X) * 4));
   if (getenv("SPCA_TC_TRACE")) {
-    const size_t words = (size_t)kTraceTimeline + 4 * 1024;
-    CK(h, cudaMalloc(&h->trace_g, words * 8));
-    CK(h, cudaMalloc(&h->trace_h, words * 8));
-    std::vector<unsigned long long> init(words, 0ull);
-    for (size_t i = kTraceTimeline; i < words; i += 2) init[i] = ~0ull;  // span minima
-    CK(h, cudaMemcpy(h->trace_g, init.data(), words * 8, cudaMemcpyHostToDevice));
-    CK(h, cudaMemcpy(h->trace_h, init.data(), words * 8, cudaMemcpyHostToDevice));
+    CK(h, cudaMalloc(&h->trace, (size_t)kTraceWords * 8));
+    CK(h, cudaMemsetAsync(h->trace, 0, (size_t)kTraceWords * 8, h->stream));
   }
   CK(h, cudaStreamSynchronize(h->stream));
   return SPCA_OK;
-}
-
-template <int LPAD>
-void tc_launch(spca_sketch *h, const CUtensorMap &ta_g, const CUtensorMap &ta_h, const CUtensorMap &tgh,
-               const CUtensorMap &tgl, int row_base, int rows, int ksplit, int kseg, int rseg,
-               float *gout, float *ghi, float *glo, int accumulate, int slot, int64_t *launches,
-               cudaError_t *err) {
-  const int tiles = (int)ceil_div(rows, 128);
-  const int64_t gstride = (int64_t)tiles * 128 * LPAD;
-  // G^T slot reuse: the H pass that read this slot two chunks ago must be done
-  if (h->h_used[slot] && (*err = cudaStreamWaitEvent(h->stream, h->ev_h[slot], 0)) != cudaSuccess) return;
-  tc_g_kernel<LPAD><<<dim3(tiles, ksplit), kTcThreads, TcCfg<LPAD>::SMEM, h->stream>>>(
-      ta_g, h->tm_whi, h->tm_wlo, rows, (int)h->n, kseg, row_base, (float *)h->gpart, gstride,
-      h->rows_done, h->bad_dev, h->tc_debug, h->trace_g, (int)h->chunk_seq);
-  if ((*err = cudaGetLastError()) != cudaSuccess) return;
-  ++*launches;
-  tc_g_finalize<<<dim3((unsigned)ceil_div(rows, 8), LPAD / 32), dim3(32, 8), 0, h->stream>>>(
-      (const float *)h->gpart, ksplit, gstride, rows, LPAD, (int)h->chunk_rows, gout, ghi, glo);
-  if ((*err = cudaGetLastError()) != cudaSuccess) return;
-  ++*launches;
-  if ((*err = cudaEventRecord(h->ev_g[slot], h->stream)) != cudaSuccess) return;
-  if ((*err = cudaStreamWaitEvent(h->hstream, h->ev_g[slot], 0)) != cudaSuccess) return;
-  // H of this chunk runs on the second stream, concurrently with G of the next
-  tc_h_kernel<LPAD><<<dim3((unsigned)ceil_div(h->n, 128), h->hsplit), kTcThreads, TcCfg<LPAD>::SMEM,
-                      h->hstream>>>(ta_h, tgh, tgl, rows, (int)h->n, rseg, row_base, (float *)h->hpart,
-                                    (int64_t)h->n * LPAD, h->cspart, accumulate, h->compensated ? 1 : 0,
-                                    h->tc_debug >> 8, h->trace_h, (int)h->chunk_seq);
-  if ((*err = cudaGetLastError()) != cudaSuccess) return;
-  ++*launches;
 }
 
 // Remember TMA descriptors over a pushed device buffer so its full chunks
@@ -196,7 +190,7 @@ int tc_register_source(spca_sketch *h, const void *a, int64_t rows, int64_t lda)
   if (h->src_ptr == a && h->src_rows == rows && h->src_lda == lda) return SPCA_OK;
   int rc = encode_2d(h, &h->src_tg, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)lda * 4, 32, 128);
   if (rc) return rc;
-  rc = encode_2d(h, &h->src_th, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)lda * 4, 32, 32);
+  rc = encode_2d(h, &h->src_th, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)lda * 4, 128, 32, false);
   if (rc) return rc;
   h->src_ptr = a;
   h->src_rows = rows;
@@ -204,62 +198,67 @@ int tc_register_source(spca_sketch *h, const void *a, int64_t rows, int64_t lda)
   return SPCA_OK;
 }
 
-int tc_chunk(spca_sketch *h, const void *a, int64_t lda, int rows) {
+// One launch of the pass kernel over `rows` rows at `a` (a whole number of
+// canonical chunks, or one partial chunk at the end of the stream).
+int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   if ((lda % 4) != 0 || (reinterpret_cast<uintptr_t>(a) % 16) != 0)
     return set_err(h, SPCA_ERR_CONFIG, -1, "tensor-core path needs 16-byte aligned rows");
-  const int slot = (int)(h->chunk_seq & 1);
-  float *ghi = (float *)h->tc_ws + (size_t)slot * 2 * h->chunk_rows * h->lpad;
-  float *glo = ghi + (size_t)h->chunk_rows * h->lpad;
-  CUtensorMap fa_g, fa_h, fg_h, fg_l;
-  const CUtensorMap *ta_g, *ta_h, *tgh, *tgl;
+  FusedSched s = tc_base_sched(h);
+  s.C = (int)ceil_div(rows, s.R0);
+  s.rows_last = (int)(rows - (int64_t)(s.C - 1) * s.R0);
+  s.ntl = (int)ceil_div(s.rows_last, 128);
+  s.Tl = (int)ceil_div(s.ntl, 2);
+  s.total = fused_total(s);
+  if (s.C > h->tc_ctr_chunks) return set_err(h, SPCA_ERR_STATE, -1, "tc launch exceeds its counters");
+  CUtensorMap fa_g, fa_h;
+  const CUtensorMap *ta_g, *ta_h;
   int row_base = 0;
   const char *base = (const char *)h->src_ptr;
   const int64_t row_bytes = lda * 4;
-  const bool full = rows == h->chunk_rows;
-  if (full && base && lda == h->src_lda && (const char *)a >= base &&
+  if (s.rows_last == s.R0 && base && lda == h->src_lda && (const char *)a >= base &&
       ((const char *)a - base) % row_bytes == 0 &&
       ((const char *)a - base) / row_bytes + rows <= h->src_rows) {
     row_base = (int)(((const char *)a - base) / row_bytes);
     ta_g = &h->src_tg;
     ta_h = &h->src_th;
-  } else {
+  } else {  // rows beyond the launch must read as zeros (TMA out of bounds)
     int rc = encode_2d(h, &fa_g, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)row_bytes, 32, 128);
     if (rc) return rc;
-    rc = encode_2d(h, &fa_h, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)row_bytes, 32, 32);
+    rc = encode_2d(h, &fa_h, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)row_bytes, 128, 32, false);
     if (rc) return rc;
     ta_g = &fa_g;
     ta_h = &fa_h;
   }
-  if (full) {
-    tgh = &h->slot_tgh[slot];
-    tgl = &h->slot_tgl[slot];
-  } else {  // partial chunk: rows beyond it must read as zeros (TMA out of bounds)
-    int rc = encode_2d(h, &fg_h, ghi, (uint64_t)rows, (uint64_t)h->lpad, (uint64_t)h->chunk_rows * 4, 32, h->lpad);
-    if (rc) return rc;
-    rc = encode_2d(h, &fg_l, glo, (uint64_t)rows, (uint64_t)h->lpad, (uint64_t)h->chunk_rows * 4, 32, h->lpad);
-    if (rc) return rc;
-    tgh = &fg_h;
-    tgl = &fg_l;
-  }
-  const int64_t tiles = ceil_div(rows, 128);
-  int ksplit = (int)std::max<int64_t>(1, 148 / tiles);
-  int kseg = (int)round_up(ceil_div(h->n, ksplit), 32);
-  ksplit = (int)ceil_div(h->n, kseg);
-  if ((int64_t)ksplit * tiles * 128 * h->lpad > h->gpart_elems)
-    return set_err(h, SPCA_ERR_STATE, -1, "tc workspace too small");
-  const int rseg = (int)round_up(ceil_div(rows, h->hsplit), 32);
-  float *gout = (float *)h->g_dev + h->rows_done * h->lpad;
-  const int acc = h->chunks_since_flush > 0 ? 1 : 0;
-  cudaError_t err = cudaSuccess;
+  const size_t ctr_words = (size_t)s.C * (2 * s.T + 2) + 2 * s.X;
+  CK(h, cudaMemsetAsync(h->tc_ctr, 0, ctr_words * 4, h->stream));
+  FusedArgs args{};
+  args.s = s;
+  args.n = (int)h->n;
+  args.row_base = row_base;
+  args.gpart = (float *)h->gpart;
+  args.gT = (float *)h->tc_ws;
+  args.g_out = (float *)h->g_dev + h->rows_done * h->lpad;
+  args.hpart = (float *)h->hpart;
+  args.colsum = h->hcs_dev + h->n * h->l;
+  args.carry = h->compensated ? h->carry_dev : nullptr;
+  args.seg_cnt = h->tc_ctr;
+  args.ready = h->tc_ctr + (size_t)s.C * 2 * s.T;
+  args.hdone = args.ready + s.C;
+  args.hseq = args.hdone + s.C;
+  args.accumulate = h->chunks_since_flush > 0 ? 1 : 0;
+  args.first_row = h->rows_done;
+  args.bad_row = h->bad_dev;
+  args.trace = h->trace;
+  args.dbg = h->tc_debug;
+  const int grid = 2 * std::max(1, std::min(h->max_pairs, s.total));
   if (h->lpad == 64)
-    tc_launch<64>(h, *ta_g, *ta_h, *tgh, *tgl, row_base, rows, ksplit, kseg, rseg, gout, ghi, glo, acc, slot,
-                  &h->launches, &err);
+    tc_pass_kernel<64><<<grid, kTcThreads, TcCfg<64>::SMEM, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo,
+                                                                         h->tm_gT, args);
   else
-    tc_launch<128>(h, *ta_g, *ta_h, *tgh, *tgl, row_base, rows, ksplit, kseg, rseg, gout, ghi, glo, acc, slot,
-                   &h->launches, &err);
-  if (err != cudaSuccess)
-    return set_err(h, SPCA_ERR_CUDA, -1, "tc kernel launch failed: %s", cudaGetErrorString(err));
-  h->chunk_seq++;
+    tc_pass_kernel<128><<<grid, kTcThreads, TcCfg<128>::SMEM, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo,
+                                                                           h->tm_gT, args);
+  CK_LAUNCH(h);
+  h->chunks_since_flush += s.C;
   return SPCA_OK;
 }
 

@@ -169,7 +169,12 @@ class TestSketchPass:
         tol = 2e-6 if precision == "simt" else 2e-5
         assert rel(st.g, ref.g) <= tol, rel(st.g, ref.g)
         assert rel(st.h, ref.h) <= tol, rel(st.h, ref.h)
-        assert np.allclose(st.col_sums, ref.col_sums, rtol=1e-9, atol=1e-9)
+        # column sums: exact fp64 on the SIMT path; the tensor-core pass sums each
+        # unit's rows in fp32 (pairwise + Kahan, ~2 ulp of sum|a|) and the units in
+        # fp64, i.e. ~1e-7 of the column's absolute sum
+        cs_tol = 1e-9 if precision == "simt" else 1e-6
+        scale = np.abs(a).astype(np.float64).sum(axis=0)
+        assert np.all(np.abs(st.col_sums - ref.col_sums) <= cs_tol * scale + 1e-12)
 
     def test_device_and_pinned_sources_match_host(self):
         a = O.gaussian(6000, 700, seed=31).astype(np.float32)
