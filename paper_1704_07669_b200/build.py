@@ -29,6 +29,8 @@ FLAGS = [
     "--expt-relaxed-constexpr",
     "-Xptxas", "-v",
 ]
+if os.environ.get("SPCA_BUILD_FINE_TRACE"):  # profiling builds: per-K-block clock64 stamps
+    FLAGS.append("-DSPCA_FINE_TRACE")
 
 
 def _stale() -> bool:

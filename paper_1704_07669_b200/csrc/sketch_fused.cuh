@@ -42,16 +42,19 @@
 
 namespace spca {
 
-constexpr int kSlots = 3;      // chunks whose G partials / G^T may be in flight
+constexpr int kMaxLag = 3;               // largest stage lag D of the H units
+constexpr int kSlots = kMaxLag + 2;      // chunks whose G partials / G^T may be in flight
 
 // optional timeline (SPCA_TC_TRACE): per CTA kTraceStride globaltimer stamps:
 // [0] start, [1] end, then per unit i < kTraceUnits, 8 stamps at 8 + 8i:
-//   0 converters start, 1 converters' main loop done, 2 staged for the epilogue,
-//   3 epilogue took it, 4 epilogue done, 5 MMA first issue, 6 MMA last issue,
-//   7 B producer passed its dependency wait
+//   0 converters start, 1 converters' main loop done, 2 promoters staged the result,
+//   3 epilogue took it, 4 epilogue done, 5 MMA first issue, 6 promoters folded the
+//   last period (MMA done), 7 B producer passed its dependency wait
 constexpr int kTraceStride = 1024;
 constexpr int kTraceUnits = 127;
-constexpr int kTraceWords = 256 * kTraceStride;
+constexpr int kTraceMma = 2048;  // leader of pair 0: 4 stamps for each of its first K blocks
+constexpr int kTraceConv = 1024;  // converter thread 0 of CTA 0: 6 stamps for each of its first blocks
+constexpr int kTraceWords = 256 * kTraceStride + 4 * kTraceMma + 6 * kTraceConv + kTraceMma;
 #define SPCA_TRACE(i, k)                                                         \
   do {                                                                           \
     if (trace && (i) < kTraceUnits) trace[8 + 8 * (i) + (k)] = ptx::globaltimer(); \
@@ -67,6 +70,7 @@ struct FusedSched {
   int nkb;        // K blocks over n
   int X, nx;      // H: 256-column tile pairs, real 128-column tiles over n
   int RS, hseg;   // H: row segments per chunk, K blocks per segment
+  int D;          // stage lag of a chunk's H units behind its G units
   int total;      // pair units in this launch
 };
 
@@ -86,10 +90,13 @@ struct FusedArgs {
   int *hseq;                // [2X] H units applied to column tile x (chunk-major)
   int accumulate;           // H of the launch's first chunk adds to hpart
   int64_t first_row;        // global index of the launch's first row
+  const float *a;           // the launch's rows (row_base = 0) and their stride, for the
+  int64_t lda;              //   exact non-finite re-check of a flagged row
   unsigned long long *bad_row;
   unsigned long long *trace;  // null unless profiling
   int dbg;                    // profiling knobs (SPCA_TC_DEBUG), 0 in production:
                               // 1 converters skip the split, 2 no MMAs, 4 no B loads, 8 no A loads
+
 };
 
 struct FusedUnit {
@@ -100,50 +107,60 @@ struct FusedUnit {
   int rows;   // rows of chunk c
 };
 
+// Stage s holds G(s) (if s < C) and H(s - D) (if 0 <= s - D < C): the H
+// units of a chunk come D stages after its G units, which leaves the G^T
+// reduction of the chunk D - 1 stages of slack (A of D + 1 chunks in L2).
 __host__ __device__ inline int fused_total(const FusedSched &s) {
-  const int XR = s.X * s.RS;
-  const int g0 = (s.C == 1 ? s.Tl : s.T) * s.S;
-  const int mid = s.C > 2 ? (s.C - 2) * (s.T * s.S + XR) : 0;
-  const int last = s.C >= 2 ? s.Tl * s.S + XR : 0;
-  return g0 + mid + last + XR;
+  const int TS = s.T * s.S, TlS = s.Tl * s.S, XR = s.X * s.RS;
+  return (s.C - 1) * TS + TlS + s.C * XR;
 }
 
 __host__ __device__ __forceinline__ FusedUnit fused_decode(const FusedSched &s, int u) {
-  const int TS = s.T * s.S, XR = s.X * s.RS;
-  int kind = 0, c = 0, r = u;
-  const int g0 = (s.C == 1 ? s.Tl : s.T) * s.S;
-  if (u >= g0) {
-    u -= g0;
-    const int F = TS + XR;
-    const int nmid = s.C > 2 ? s.C - 2 : 0;
-    if (u < nmid * F) {  // stage 1 + u / F: G(stage) then H(stage - 1)
-      const int st = 1 + u / F;
-      r = u - (st - 1) * F;
-      if (r < TS) {
-        c = st;
-      } else {
-        kind = 1;
-        c = st - 1;
-        r -= TS;
-      }
-    } else {
-      u -= nmid * F;
-      const int TlS = s.Tl * s.S;
-      if (s.C >= 2 && u < TlS + XR) {  // stage C - 1
-        if (u < TlS) {
-          c = s.C - 1;
-          r = u;
+  const int TS = s.T * s.S, TlS = s.Tl * s.S, XR = s.X * s.RS, F = TS + XR, D = s.D;
+  int kind = 0, c = 0, r = 0;
+  // region 1: stages 0 .. min(C, D) - 1, G units only
+  const int size1 = s.C <= D ? (s.C - 1) * TS + TlS : D * TS;
+  if (u < size1) {
+    c = min(u / TS, s.C - 1);
+    r = u - c * TS;
+  } else {
+    u -= size1;
+    const int n2 = s.C > D ? s.C - D : 0;  // region 2: stages D .. C - 1, G(s) then H(s - D)
+    bool done = false;
+    if (n2 > 0) {
+      if (u < (n2 - 1) * F) {
+        const int st = D + u / F;
+        r = u - (st - D) * F;
+        if (r < TS) {
+          c = st;
         } else {
           kind = 1;
-          c = s.C - 2;
-          r = u - TlS;
+          c = st - D;
+          r -= TS;
         }
-      } else {  // stage C: H of the last chunk
-        if (s.C >= 2) u -= TlS + XR;
-        kind = 1;
-        c = s.C - 1;
-        r = u;
+        done = true;
+      } else {
+        u -= (n2 - 1) * F;
+        if (u < TlS + XR) {
+          if (u < TlS) {
+            c = s.C - 1;
+            r = u;
+          } else {
+            kind = 1;
+            c = s.C - 1 - D;
+            r = u - TlS;
+          }
+          done = true;
+        } else {
+          u -= TlS + XR;
+        }
       }
+    }
+    if (!done) {  // region 3: stages max(C, D) .. C + D - 1, H units only
+      const int st = (s.C > D ? s.C : D) + u / XR;
+      kind = 1;
+      c = st - D;
+      r = u % XR;
     }
   }
   FusedUnit f;
@@ -172,10 +189,10 @@ template <int LPAD>
 struct PairBars {
   using C = TcCfg<LPAD>;
   uint64_t a_full[C::NA], a_empty[C::NA];  // local: A producer <-> converters
+  uint64_t kb_full[C::NS];                 // leader: both CTAs' converters stored the TMEM stage
+  uint64_t kb_empty[C::NS];                // each CTA: MMAs done with the TMEM stage
   uint64_t b_full[C::NB];                  // leader: both CTAs' B halves landed
   uint64_t b_empty[C::NB];                 // each CTA: MMAs done with the B stage
-  uint64_t t_full[C::NT];                  // leader: both CTAs' converters stored the stage
-  uint64_t t_empty[C::NT];                 // each CTA: MMAs done with the TMEM stage
   uint64_t acc_full[2];                    // each CTA: accumulator period complete
   uint64_t acc_empty[2];                   // leader: both CTAs folded the period
   uint64_t epi_full, epi_empty;            // local: converters <-> epilogue staging
@@ -183,7 +200,7 @@ struct PairBars {
 };
 
 template <int LPAD>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<LPAD>::THREADS, 1)
 tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ CUtensorMap tAh,
                const __grid_constant__ CUtensorMap tWhi, const __grid_constant__ CUtensorMap tWlo,
                const __grid_constant__ CUtensorMap tGT, const FusedArgs args) {
@@ -191,8 +208,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ PairBars<LPAD> bars;
-  __shared__ float stg_chk[2 * 128];   // G: per half, NaN iff the row holds a non-finite value
-  __shared__ double stg_cs[2 * 128];   // H: per half, column-sum partial
+  __shared__ double stg_cs[kGroups * 128];  // H: per converter group, column-sum partial
   const FusedSched &sc = args.s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -204,21 +220,21 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NA; ++s) {
       ptx::mbar_init(&bars.a_full[s], 1);
-      ptx::mbar_init(&bars.a_empty[s], kTcConv / 64);  // one converter group per block
+      ptx::mbar_init(&bars.a_empty[s], 4);  // the four warps of one converter group
+    }
+    for (int s = 0; s < C::NS; ++s) {
+      ptx::mbar_init(&bars.kb_full[s], 2 * 4);  // one converter group (4 warps) in each CTA
+      ptx::mbar_init(&bars.kb_empty[s], 1);
     }
     for (int s = 0; s < C::NB; ++s) {
       ptx::mbar_init(&bars.b_full[s], 1);
       ptx::mbar_init(&bars.b_empty[s], 1);
     }
-    for (int s = 0; s < C::NT; ++s) {
-      ptx::mbar_init(&bars.t_full[s], 2 * kTcConv / 64);  // one group in each CTA
-      ptx::mbar_init(&bars.t_empty[s], 1);
-    }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&bars.acc_full[s], 1);
-      ptx::mbar_init(&bars.acc_empty[s], 2 * kTcConv / 32);
+      ptx::mbar_init(&bars.acc_empty[s], 2 * C::PROMO_WARPS);
     }
-    ptx::mbar_init(&bars.epi_full, kTcConv);
+    ptx::mbar_init(&bars.epi_full, kTcConv + 32 * C::PROMO_WARPS);  // converters (column sums) + promoters
     ptx::mbar_init(&bars.epi_empty, kTcEpi);
     ptx::fence_mbar_init();
     ptx::tma_prefetch(&tAg);
@@ -289,48 +305,71 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             if (rank == 0) ptx::mbar_arrive(&bars.b_full[s]);
           } else {
           if (rank == 0) ptx::mbar_arrive_expect_tx(&bars.b_full[s], 2 * C::B_STAGE);
-          if (f.kind == 0) {
-            if constexpr (C::FOUR) {
-              ptx::tma_load_2d_pair(st, rank == 0 ? &tWhi : &tWlo, bar, k, 0, keep);
-            } else {
-              ptx::tma_load_2d_pair(st, &tWhi, bar, k, 64 * (int)rank, keep);
-              ptx::tma_load_2d_pair(st + C::BH_BYTES, &tWlo, bar, k, 64 * (int)rank, keep);
-            }
+          constexpr int HR = LPAD / 2;  // rows per B box
+          // rows of W_hi / W_lo in the maps: Omega^T (G units) or G^T slot (H units)
+          const CUtensorMap *mh = f.kind == 0 ? &tWhi : &tGT, *ml = f.kind == 0 ? &tWlo : &tGT;
+          const int yh = f.kind == 0 ? 0 : 2 * gslot * LPAD, yl = f.kind == 0 ? 0 : (2 * gslot + 1) * LPAD;
+          if constexpr (C::STACKED) {
+            const CUtensorMap *m01 = rank == 0 ? mh : ml;
+            const int y01 = rank == 0 ? yh : yl;
+            ptx::tma_load_2d_pair(st, m01, bar, k, y01, keep);
+            ptx::tma_load_2d_pair(st + C::BH_BYTES, m01, bar, k, y01 + HR, keep);
+            ptx::tma_load_2d_pair(st + 2 * C::BH_BYTES, mh, bar, k, yh + HR * (int)rank, keep);
           } else {
-            if constexpr (C::FOUR) {
-              ptx::tma_load_2d_pair(st, &tGT, bar, k, (2 * gslot + (int)rank) * 64, keep);
-            } else {
-              ptx::tma_load_2d_pair(st, &tGT, bar, k, 2 * gslot * LPAD + 64 * (int)rank, keep);
-              ptx::tma_load_2d_pair(st + C::BH_BYTES, &tGT, bar, k, (2 * gslot + 1) * LPAD + 64 * (int)rank, keep);
-            }
+            ptx::tma_load_2d_pair(st, mh, bar, k, yh + HR * (int)rank, keep);
+            ptx::tma_load_2d_pair(st + C::BH_BYTES, ml, bar, k, yl + HR * (int)rank, keep);
           }
           }
         }
         __syncwarp();
       }
     }
+#ifdef SPCA_FINE_TRACE
+  } else if (warp == 3) {  // profiling: completion time of each K block's MMAs (pair 0, leader)
+    if (trace && cid == 0 && rank == 0 && lane == 0) {
+      unsigned long long *ct_ = args.trace + 256 * kTraceStride + 4 * kTraceMma + 6 * kTraceConv;
+      int gkb = 0;
+      for (int u = cid; u < sc.total && gkb < kTraceMma; u += ncl) {
+        const FusedUnit f = fused_decode(sc, u);
+        for (int kb = 0; kb < f.nk && gkb < kTraceMma; ++kb, ++gkb) {
+          ptx::mbar_wait(&bars.kb_empty[gkb % C::NS], (gkb / C::NS) & 1);
+          ct_[gkb] = clock64();
+        }
+      }
+    }
+#endif
   } else if (warp == 1) {  // ------------------------- MMA issuer (leader CTA)
     if (rank == 0) {
+      const uint64_t bdesc0 = ptx::sdesc_sw128(ptx::smem_u32(smem + C::B_OFF), 16, 1024);
       int gkb = 0, gq = 0, ui = 0;
 #pragma unroll 1
       for (int u = cid; u < sc.total; u += ncl, ++ui) {
         const FusedUnit f = fused_decode(sc, u);
 #pragma unroll 1
         for (int kb = 0; kb < f.nk; ++kb, ++gkb) {
-          if (lane == 0 && kb == 1) SPCA_TRACE(ui, 5);
-          if (lane == 0 && kb == f.nk - 1) SPCA_TRACE(ui, 6);
-          const int ts = gkb % C::NT, bs = gkb % C::NB;
+          if (lane == 0 && kb == 0) SPCA_TRACE(ui, 5);
+          const int ks = gkb % C::NS, bs = gkb % C::NB;
           const int q = gq + kb / kPromote, buf = q & 1;
           const bool first = (kb % kPromote) == 0;
-          if (first && q >= 2) ptx::mbar_wait_cluster(&bars.acc_empty[buf], ((q >> 1) - 1) & 1);
-          ptx::mbar_wait_cluster(&bars.t_full[ts], (gkb / C::NT) & 1);
-          ptx::mbar_wait_cluster(&bars.b_full[bs], (gkb / C::NB) & 1);
+#ifdef SPCA_FINE_TRACE
+          unsigned long long *mt = (trace && cid == 0 && lane == 0 && gkb < kTraceMma)
+                                       ? args.trace + 256 * kTraceStride + 4 * gkb : nullptr;
+#else
+          constexpr unsigned long long *mt = nullptr;
+#endif
+          if (mt) mt[0] = clock64();
+          if (first && q >= 2) ptx::mbar_wait(&bars.acc_empty[buf], ((q >> 1) - 1) & 1);
+          if (mt) mt[1] = clock64();
+          ptx::mbar_wait(&bars.kb_full[ks], (gkb / C::NS) & 1);
+          if (mt) mt[2] = clock64();
+          ptx::mbar_wait(&bars.b_full[bs], (gkb / C::NB) & 1);
+          if (mt) mt[3] = clock64();
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
             if (!(args.dbg & 2))
-              tc_mma_stage2<LPAD>(tmem, tmem + buf * C::ACC_COLS, ts,
-                                  ptx::smem_u32(smem + C::B_OFF + bs * C::B_STAGE), first);
-            ptx::mma2_commit_both(&bars.t_empty[ts]);
+              tc_mma_stage2<LPAD>(tmem + C::A_TMEM + 64 * ks, tmem + buf * C::ACC_COLS,
+                                  bdesc0 + (uint64_t)((bs * C::B_STAGE) >> 4), first);
+            ptx::mma2_commit_both(&bars.kb_empty[ks]);
             ptx::mma2_commit_both(&bars.b_empty[bs]);
             if ((kb % kPromote) == kPromote - 1 || kb == f.nk - 1) ptx::mma2_commit_both(&bars.acc_full[buf]);
           }
@@ -339,101 +378,67 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         gq += (f.nk + kPromote - 1) / kPromote;
       }
     }
-  } else if (warp >= 4 && warp < 12) {  // ------------ converters and promotion
+  } else if (warp >= 4 && warp < 4 + kTcConv / 32) {  // -------------------- converters
     const int ct = threadIdx.x - 128;
     const int t = ct & 127;    // TMEM lane: G row / H column within the tile
-    const int half = ct >> 7;  // which 16 of the 32 K values, which half of the outputs
+    const int grp = ct >> 7;   // converts the K blocks kb = grp (mod kGroups)
     const uint32_t lane_base = tmem + ((uint32_t)(t & ~31) << 16);
-    const uint32_t tfull_l = ptx::mapa(ptx::smem_u32(&bars.t_full[0]), 0);
-    const uint32_t accempty_l = ptx::mapa(ptx::smem_u32(&bars.acc_empty[0]), 0);
-    const uint32_t stg_row = ptx::smem_u32(smem + C::STG_OFF + t * LPAD * 4);
-    int gkb = 0, gq = 0, ui = 0;
+    const uint32_t kbfull_l = ptx::mapa(ptx::smem_u32(&bars.kb_full[0]), 0);
+    int gkb = 0, ui = 0;
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
       const FusedUnit f = fused_decode(sc, u);
-      float racc[C::HALF_COLS];
-#pragma unroll
-      for (int i = 0; i < C::HALF_COLS; ++i) racc[i] = 0.f;
-      float chk = 0.f;            // G: NaN iff this row holds a non-finite value
       float cs = 0.f, cc = 0.f;   // H: column sum (fp32 Kahan over the unit)
-      const int nq = (f.nk + kPromote - 1) / kPromote;
-      int promoted = 0;
       if (ct == 0) SPCA_TRACE(ui, 0);
-      // fold accumulator period qg into racc, hand the accumulator back to the MMAs
-      auto promote = [&](int qg) {
-        const int buf = qg & 1;
-        ptx::mbar_wait(&bars.acc_full[buf], (qg >> 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t base = lane_base + buf * C::ACC_COLS + half * C::HALF_COLS;
-#pragma unroll
-        for (int c0 = 0; c0 < C::HALF_COLS; c0 += 16) {
-          float v[16];
-          ptx::tmem_ld16(base + c0, v);
-          if constexpr (C::FOUR) {  // the A * W_lo half of the accumulator
-            float w[16];
-            ptx::tmem_ld16(base + LPAD + c0, w);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += w[i];
-          }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) racc[c0 + i] += v[i];
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(accempty_l + 8 * buf);
-      };
-      // The two converter groups take alternate K blocks (group `half` the blocks
-      // of its parity, all 32 K values of its row / column), so each warp has two
-      // MMA periods of time per block; promotion still splits the output columns.
 #pragma unroll 1
-      for (int kb = half; kb < f.nk; kb += 2) {
+      for (int kb = grp; kb < f.nk; kb += kGroups) {
         const int gk = gkb + kb;
-        const int s = gk % C::NA, ts = gk % C::NT;
+        const int s = gk % C::NA, ts = gk % C::NS;
+#ifdef SPCA_FINE_TRACE
+        unsigned long long *ctr = (trace && blockIdx.x == 0 && ct == 0 && (gk >> 1) < kTraceConv)
+                                      ? args.trace + 256 * kTraceStride + 4 * kTraceMma + 6 * (gk >> 1) : nullptr;
+#else
+        constexpr unsigned long long *ctr = nullptr;
+#endif
+        if (ctr) ctr[0] = clock64();
         ptx::mbar_wait(&bars.a_full[s], (gk / C::NA) & 1);
-        // the TMEM stage must be free before the first store
-        if (gk >= C::NT) ptx::mbar_wait(&bars.t_empty[ts], ((gk / C::NT) - 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t tst = lane_base + C::A_TMEM + 64 * ts;
-        if (args.dbg & 1) {
-          __syncwarp();
-        } else if (f.kind == 0) {
-          const uint32_t row = ptx::smem_u32(smem + s * C::A_BYTES + t * 128);
+        if (ctr) ctr[1] = clock64();
+        // Load and split first, then wait for the TMEM stage: the stage is held
+        // only for the two stores, which keeps the stage round trip (converters
+        // -> MMA -> commit -> converters) short; the TMEM ring is shallow.
+        // All 32 K values of this row (G) / column (H): hi = v with its low 13
+        // mantissa bits cleared, lo = v - hi (exact); the tensor core reads lo as
+        // tf32 (low 13 bits dropped): the operand keeps ~21 significant bits.
+        // Non-finite inputs are found from their G rows in the epilogue.
+        float v[32], hi[32];
+        if (!(args.dbg & 1)) {
+          if (f.kind == 0) {
+            const uint32_t row = ptx::smem_u32(smem + s * C::A_BYTES + t * 128);
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            float4 v[4];
-            float hi[16], lo[16];
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) v[q4] = ptx::lds128(row + (((4 * hh + q4) ^ (t & 7)) << 4));
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              chk = fmaf(v[q4].x, 0.f, fmaf(v[q4].y, 0.f, fmaf(v[q4].z, 0.f, fmaf(v[q4].w, 0.f, chk))));
-              split3(v[q4].x, hi[4 * q4 + 0], lo[4 * q4 + 0]);
-              split3(v[q4].y, hi[4 * q4 + 1], lo[4 * q4 + 1]);
-              split3(v[q4].z, hi[4 * q4 + 2], lo[4 * q4 + 2]);
-              split3(v[q4].w, hi[4 * q4 + 3], lo[4 * q4 + 3]);
+            for (int q4 = 0; q4 < 8; ++q4) {
+              const float4 x = ptx::lds128(row + ((q4 ^ (t & 7)) << 4));
+              v[4 * q4] = x.x; v[4 * q4 + 1] = x.y; v[4 * q4 + 2] = x.z; v[4 * q4 + 3] = x.w;
             }
-            ptx::tmem_st16(tst + 16 * hh, hi);
-            ptx::tmem_st16(tst + 32 + 16 * hh, lo);
-          }
-        } else {
-          const uint32_t raw = ptx::smem_u32(smem + s * C::A_BYTES + t * 4);  // column t
+          } else {
+            const uint32_t raw = ptx::smem_u32(smem + s * C::A_BYTES + t * 4);  // column t
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            float v[16], hi[16], lo[16];
+            for (int kq = 0; kq < 32; ++kq) v[kq] = ptx::lds32(raw + kq * 512);
+            float p16[16];  // pairwise sum of the 32 values, then one Kahan step
 #pragma unroll
-            for (int kq = 0; kq < 16; ++kq) v[kq] = ptx::lds32(raw + (16 * hh + kq) * 512);
+            for (int i = 0; i < 16; ++i) p16[i] = v[2 * i] + v[2 * i + 1];
 #pragma unroll
-            for (int kq = 0; kq < 16; ++kq) split3(v[kq], hi[kq], lo[kq]);
-            float p8[8];  // pairwise sum of the 16 values, then one Kahan step
+            for (int w = 8; w >= 1; w >>= 1)
 #pragma unroll
-            for (int i = 0; i < 8; ++i) p8[i] = v[2 * i] + v[2 * i + 1];
-            const float blk = ((p8[0] + p8[1]) + (p8[2] + p8[3])) + ((p8[4] + p8[5]) + (p8[6] + p8[7]));
-            const float y = blk - cc;
+              for (int i = 0; i < w; ++i) p16[i] = p16[i] + p16[i + w];
+            const float y = p16[0] - cc;
             const float tt = cs + y;
             cc = (tt - cs) - y;
             cs = tt;
-            ptx::tmem_st16(tst + 16 * hh, hi);
-            ptx::tmem_st16(tst + 32 + 16 * hh, lo);
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            hi[i] = trunc_tf32(v[i]);
+            v[i] -= hi[i];
           }
         }
         // every lane's loads were consumed by the split above: the landing slot
@@ -441,34 +446,84 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         // outstanding shared loads against the next TMA write)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&bars.a_empty[s]);
+        if (gk >= C::NS) ptx::mbar_wait(&bars.kb_empty[ts], ((gk / C::NS) - 1) & 1);
+        if (ctr) ctr[2] = clock64();
+        ptx::tc_fence_after();
+        const uint32_t tst = lane_base + C::A_TMEM + 64 * ts;
+        if (!(args.dbg & 1)) {
+          ptx::tmem_st32(tst, hi);
+          ptx::tmem_st32(tst + 32, v);
+        }
+        if (ctr) ctr[3] = clock64();
         ptx::tmem_wait_st();
+        if (ctr) ctr[4] = clock64();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(tfull_l + 8 * ts);
-        // fold the period before the one this block closes (the MMAs run ahead)
-        if ((kb % kPromote) == kPromote - 2 + half && kb >= kPromote) promote(gq + promoted++);
+        if (lane == 0) ptx::mbar_arrive_cluster(kbfull_l + 8 * ts);
+        if (ctr) ctr[5] = clock64();
       }
       gkb += f.nk;
-      for (; promoted < nq; ++promoted) promote(gq + promoted);
-      gq += nq;
       if (ct == 0) SPCA_TRACE(ui, 1);
+      // hand the column-sum partial to the epilogue with the unit's staging
+      if (ui >= 1) ptx::mbar_wait(&bars.epi_empty, (ui - 1) & 1);
+      if (f.kind == 1) stg_cs[grp * 128 + t] = (double)cs - (double)cc;
+      ptx::mbar_arrive(&bars.epi_full);
+    }
+  } else if (warp >= C::PROMO_BASE / 32 && warp < C::EPI_BASE / 32) {  // ----- promoters
+    const int pt = threadIdx.x - C::PROMO_BASE;
+    const int t = pt & 127;              // TMEM lane: G row / H column within the tile
+    const int c0 = (pt >> 7) * 64;       // this thread's 64 output columns
+    const uint32_t lane_base = tmem + ((uint32_t)(t & ~31) << 16);
+    const uint32_t accempty_l = ptx::mapa(ptx::smem_u32(&bars.acc_empty[0]), 0);
+    const uint32_t stg_row = ptx::smem_u32(smem + C::STG_OFF + t * LPAD * 4);
+    int gq = 0, ui = 0;
+#pragma unroll 1
+    for (int u = cid; u < sc.total; u += ncl, ++ui) {
+      const FusedUnit f = fused_decode(sc, u);
+      const int nq = (f.nk + kPromote - 1) / kPromote;
+      float racc[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) racc[i] = 0.f;
+      // fold each accumulator period into fp32 registers (round-to-nearest adds:
+      // the tensor core's own accumulation truncates) and hand it back
+#pragma unroll 1
+      for (int qq = 0; qq < nq; ++qq, ++gq) {
+        const int buf = gq & 1;
+        ptx::mbar_wait(&bars.acc_full[buf], (gq >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t base = lane_base + buf * C::ACC_COLS + c0;
+        if (!(args.dbg & 512))
+#pragma unroll
+        for (int c = 0; c < 64; c += 8) {
+          float v[8];
+          ptx::tmem_ld8(base + c, v);
+          if constexpr (C::STACKED) {  // + the A_hi W_lo half of the accumulator
+            float w[8];
+            ptx::tmem_ld8(base + LPAD + c, w);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] += w[i];
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) racc[c + i] += v[i];
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(accempty_l + 8 * buf);
+      }
+      if (pt == 0) SPCA_TRACE(ui, 6);
       // stage the result for the epilogue warps (16-byte chunks XOR-swizzled by row)
       if (ui >= 1) ptx::mbar_wait(&bars.epi_empty, (ui - 1) & 1);
-      if (ct == 0) SPCA_TRACE(ui, 2);
+      if (pt == 0) SPCA_TRACE(ui, 2);
 #pragma unroll
-      for (int i = 0; i < C::HALF_COLS / 4; ++i) {
-        const int q = half * (C::HALF_COLS / 4) + i;
+      for (int i = 0; i < 16; ++i) {
+        const int q = c0 / 4 + i;
         ptx::st_shared_v4(stg_row + ((q ^ (t & 7)) << 4),
                           make_float4(racc[4 * i], racc[4 * i + 1], racc[4 * i + 2], racc[4 * i + 3]));
       }
-      if (f.kind == 0)
-        stg_chk[half * 128 + t] = chk;
-      else
-        stg_cs[half * 128 + t] = (double)cs - (double)cc;
       ptx::mbar_arrive(&bars.epi_full);
     }
-  } else if (warp >= 12) {  // ------------------------------------ epilogue
-    const int e = threadIdx.x - kTcEpiBase;  // row (G) / column (H) of the tile
+  } else if (warp >= C::EPI_BASE / 32) {  // --------------------------------- epilogue
+    const int e = threadIdx.x - C::EPI_BASE;  // row (G) / column (H) of the tile
     constexpr int NQ = LPAD / 4;             // 16-byte chunks per row
     const uint32_t srow = ptx::smem_u32(smem + C::STG_OFF + e * LPAD * 4);
     const int twoT = 2 * sc.T;
@@ -491,13 +546,25 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           float4 *gp = reinterpret_cast<float4 *>(
               args.gpart + ((((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 + e) * LPAD);
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) gp[q] = ptx::lds128(srow + ((q ^ (e & 7)) << 4));
-          chk = stg_chk[e] + stg_chk[128 + e];
+          for (int q = 0; q < NQ; ++q) {
+            const float4 x = ptx::lds128(srow + ((q ^ (e & 7)) << 4));
+            chk = fmaf(x.x, 0.f, fmaf(x.y, 0.f, fmaf(x.z, 0.f, fmaf(x.w, 0.f, chk))));
+            gp[q] = x;
+          }
         }
         ptx::mbar_arrive(&bars.epi_empty);
         if (real) {
-          if (!(chk == 0.f) && row < f.rows)
-            report_bad_row(args.bad_row, args.first_row + (int64_t)f.c * sc.R0 + row);
+          // a non-finite input makes its G row non-finite: confirm on the raw row
+          // segment (a huge finite row may also overflow G; the reference only
+          // rejects non-finite values)
+          if (!(chk == 0.f) && row < f.rows) {
+            const int64_t grow = (int64_t)f.c * sc.R0 + row;
+            const float *ar = args.a + grow * args.lda;
+            const int k1 = min(args.n, (f.k0 + f.nk) * 32);
+            bool bad = false;
+            for (int k = f.k0 * 32; k < k1 && !bad; ++k) bad = !isfinite(ar[k]);
+            if (bad) report_bad_row(args.bad_row, args.first_row + grow);
+          }
           // every writer fences its own stores before the count (a fence by one
           // thread does not drain the other warps' outstanding stores)
           __threadfence();

@@ -38,11 +38,13 @@
 namespace spca {
 
 // Warps: 0 A producer, 1 TMEM allocator + MMA issuer (leader CTA), 2 B
-// producer, 3 idle, 4..11 converters / promoters, 12..15 epilogue.
-constexpr int kTcThreads = 512;
-constexpr int kTcConv = 256;    // converter threads (warps 4..11)
-constexpr int kTcEpi = 128;     // epilogue threads (warps 12..15)
-constexpr int kTcEpiBase = 384; // first epilogue thread
+// producer, 3 idle, 4..11 converters (two groups of four warps, one warp per
+// TMEM lane quarter; group g takes the K blocks kb = g mod 2), then the
+// promoter warps (fold each accumulator period into fp32 registers and stage
+// the unit's result; 64 output columns per warp) and 4 epilogue warps.
+constexpr int kGroups = 2;      // converter groups
+constexpr int kTcConv = 128 * kGroups;  // converter threads
+constexpr int kTcEpi = 128;     // epilogue threads
 constexpr uint32_t kTmemCols = 512;
 constexpr int kPromote = 4;     // K blocks per accumulator period
 
@@ -50,27 +52,39 @@ constexpr int kPromote = 4;     // K blocks per accumulator period
 // K=8 MMA takes 64 cycles per SM at N = 128 (the full tf32 rate), 44 at N = 64
 // and 128 at N = 256, with A from TMEM or SMEM, for one CTA (M = 128) and for
 // a CTA pair (cta_group::2, M = 256). The pass runs on CTA pairs: each CTA
-// keeps its own 128 rows of the A operand in TMEM and HALF of the N = 128 B
-// operand in SMEM, which halves B's shared-memory and L2->SM traffic per SM
-// (the SM ingress, ~94 GB/s per SM measured with tools/l2_bench.cu, is what
-// bounds a single-CTA version).
-//   l_pad = 64:  B = [W_hi | W_lo] (N = 128; rank 0 holds W_hi, rank 1 W_lo);
-//                two MMAs per K step: A_hi B + A_lo B (all four products);
-//                promotion adds the two column halves of the accumulator.
-//   l_pad = 128: B = W_hi and B = W_lo (N = 128 each; rank r holds rows
-//                64r..64r+63 of both); three MMAs: A_hi W_hi + A_hi W_lo + A_lo W_hi.
+// keeps its own 128 rows of the A operand in TMEM and HALF of every B operand
+// in shared memory, which halves B's shared-memory and L2->SM traffic per SM
+// (the per-SM ingress, ~90 GB/s measured with tools/l2_bench.cu and
+// tools/tma_bench.cu, is what bounds a single-CTA version).
+// Three products per K step into one accumulator of N = l_pad columns:
+// A_hi W_hi + A_hi W_lo + A_lo W_hi (the dropped A_lo W_lo is ~2^-22 of a
+// product). B stage per CTA: rows [r * l_pad/2, (r+1) * l_pad/2) of W_hi, then
+// the same rows of W_lo (rank r). l_pad = 64 keeps the accumulators at 64
+// columns, leaving TMEM for six A operand stages: the MMA completion latency
+// needs that depth when every K block's operand is produced on chip.
 template <int LPAD>
 struct TcCfg {
   static_assert(LPAD == 64 || LPAD == 128, "tensor-core path covers l <= 128");
-  static constexpr bool FOUR = LPAD == 64;
-  static constexpr int ACC_COLS = 128;                // one accumulator
-  static constexpr int NA = LPAD == 64 ? 8 : 5;       // raw A ring
-  static constexpr int NB = 4;                        // B operand ring
-  static constexpr int NT = (kTmemCols - 2 * ACC_COLS) / 64;  // TMEM operand ring (4)
-  static constexpr int HALF_COLS = LPAD / 2;          // output columns per converter thread
+  // l_pad = 64: "stacked" form, two MMAs per 8-deep step: A_hi [W_hi | W_lo]
+  // (N = 128) and A_lo W_hi (N = 64) into the first half; the accumulator is
+  // 128 columns and promotion adds its halves. l_pad = 128: three N = 128 MMAs.
+  static constexpr bool STACKED = LPAD == 64;
+  static constexpr int ACC_COLS = STACKED ? 128 : LPAD;  // one accumulator
+  static constexpr int NS = (kTmemCols - 2 * ACC_COLS) / 64;  // TMEM A operand stages
+  // B ring: deep enough to cover an L2 round trip (~1-2 us) at the MMA rate
+  static constexpr int PROMO_WARPS = 4 * (LPAD / 64);  // promoters: 64 output columns per thread
+  static constexpr int PROMO_BASE = 128 + kTcConv;     // first promoter thread
+  static constexpr int EPI_BASE = PROMO_BASE + 32 * PROMO_WARPS;  // first epilogue thread
+  static constexpr int THREADS = EPI_BASE + kTcEpi;
   static constexpr uint32_t A_BYTES = 128 * 32 * 4;   // raw A tile (16 KB)
-  static constexpr uint32_t BH_BYTES = 64 * 32 * 4;   // this CTA's half of one B matrix tile (8 KB)
-  static constexpr uint32_t B_STAGE = FOUR ? BH_BYTES : 2 * BH_BYTES;
+  static constexpr uint32_t BH_BYTES = (LPAD / 2) * 32 * 4;  // l_pad/2 rows of one B matrix tile
+  // B stage per CTA (rank r). Stacked: [R0 | R1 | R2] of 32 rows each:
+  //   rank 0: W_hi[0:32], W_hi[32:64], W_hi[0:32];  rank 1: W_lo[0:32], W_lo[32:64], W_hi[32:64]
+  // (R0..R1 = this CTA's 64 rows of [W_hi | W_lo], R2 = its 32 rows of W_hi).
+  // Otherwise: W_hi rows [r*l_pad/2, (r+1)*l_pad/2) then the same rows of W_lo.
+  static constexpr uint32_t B_STAGE = STACKED ? 3 * BH_BYTES : 2 * BH_BYTES;
+  static constexpr int NB = STACKED ? 7 : 4;          // B ring (12 KB | 16 KB stages)
+  static constexpr int NA = STACKED ? 6 : 5;          // raw A ring (16 KB stages)
   static constexpr uint32_t STG_BYTES = 128 * LPAD * 4;  // epilogue staging tile
   static constexpr uint32_t B_OFF = NA * A_BYTES;
   static constexpr uint32_t STG_OFF = B_OFF + NB * B_STAGE;
@@ -86,34 +100,42 @@ __device__ __forceinline__ float rna_tf32_fast(float v) {
   return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u);
 }
 
+// tf32 by truncation (the low 13 mantissa bits cleared): v - trunc(v) is exact
+__device__ __forceinline__ float trunc_tf32(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
+
 // tf32 split of v: hi = rna(v), lo = rna(v - hi); v - hi is exact in fp32
 __device__ __forceinline__ void split3(float v, float &hi, float &lo) {
   hi = rna_tf32_fast(v);
   lo = rna_tf32_fast(v - hi);
 }
 
-// The pair MMAs (M = 256) of one 32-deep K block into accumulator `acc`;
-// `bstage` is the B stage address (same offset in both CTAs).
+// The pair MMAs (M = 256) of one 32-deep K block into accumulator `acc`.
+// `db` is the shared-memory descriptor of the B stage (hi half at +0, lo half
+// at +BH_BYTES; same offset in both CTAs): the per-MMA descriptors differ
+// only in the 14-bit start-address field (16-byte units), so they are formed
+// by small adds instead of re-encoding (the issuing warp's per-block
+// bookkeeping must stay well under the 384 tensor cycles of a block).
 template <int LPAD>
-__device__ __forceinline__ void tc_mma_stage2(uint32_t tmem, uint32_t acc, int ts, uint32_t bstage,
-                                              bool first) {
+__device__ __forceinline__ void tc_mma_stage2(uint32_t a_hi, uint32_t acc, uint64_t db, bool first) {
   using C = TcCfg<LPAD>;
-  const uint32_t a_hi = tmem + C::A_TMEM + 64 * ts;
-  const uint32_t a_lo = a_hi + 32;
-  constexpr uint32_t idesc = ptx::idesc_tf32(256, 128, 0, 0);
+  if constexpr (C::STACKED) {
+    constexpr uint32_t idesc1 = ptx::idesc_tf32(256, 2 * LPAD, 0, 0);
+    constexpr uint32_t idesc2 = ptx::idesc_tf32(256, LPAD, 0, 0);
+    constexpr uint64_t R2 = (2 * C::BH_BYTES) >> 4;
 #pragma unroll
-  for (int kk = 0; kk < 4; ++kk) {
-    const uint32_t acc_flag = (first && kk == 0) ? 0u : 1u;
-    if constexpr (C::FOUR) {
-      const uint64_t db = ptx::sdesc_sw128(bstage + kk * 32, 16, 1024);
-      ptx::mma2_tf32_ts(acc, a_hi + kk * 8, db, idesc, acc_flag);
-      ptx::mma2_tf32_ts(acc, a_lo + kk * 8, db, idesc, 1u);
-    } else {
-      const uint64_t dh = ptx::sdesc_sw128(bstage + kk * 32, 16, 1024);
-      const uint64_t dl = ptx::sdesc_sw128(bstage + C::BH_BYTES + kk * 32, 16, 1024);
-      ptx::mma2_tf32_ts(acc, a_hi + kk * 8, dh, idesc, acc_flag);
+    for (int kk = 0; kk < 4; ++kk) {  // +32 bytes per 8-deep step
+      ptx::mma2_tf32_ts(acc, a_hi + kk * 8, db + 2 * kk, idesc1, (first && kk == 0) ? 0u : 1u);
+      ptx::mma2_tf32_ts(acc, a_hi + 32 + kk * 8, db + R2 + 2 * kk, idesc2, 1u);
+    }
+  } else {
+    constexpr uint32_t idesc = ptx::idesc_tf32(256, LPAD, 0, 0);
+    constexpr uint64_t LO = C::BH_BYTES >> 4;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const uint64_t dh = db + 2 * kk, dl = db + LO + 2 * kk;
+      ptx::mma2_tf32_ts(acc, a_hi + kk * 8, dh, idesc, (first && kk == 0) ? 0u : 1u);
       ptx::mma2_tf32_ts(acc, a_hi + kk * 8, dl, idesc, 1u);
-      ptx::mma2_tf32_ts(acc, a_lo + kk * 8, dh, idesc, 1u);
+      ptx::mma2_tf32_ts(acc, a_hi + 32 + kk * 8, dh, idesc, 1u);
     }
   }
 }

@@ -76,6 +76,8 @@ FusedSched tc_base_sched(const spca_sketch *h) {
   s.RS = (int)ceil_div(rkb, U);
   s.hseg = (int)ceil_div(rkb, s.RS);
   s.RS = (int)ceil_div(rkb, s.hseg);
+  s.D = 2;  // measured: one extra stage of slack removes the H units' waits for G^T
+  if (const char *e = getenv("SPCA_TC_LAG")) s.D = std::max(1, std::min(kMaxLag, atoi(e)));  // tuning knob
   return s;
 }
 
@@ -115,7 +117,7 @@ template <int LPAD>
 int tc_max_pairs() {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2, 1, 1);
-  cfg.blockDim = dim3(kTcThreads, 1, 1);
+  cfg.blockDim = dim3(TcCfg<LPAD>::THREADS, 1, 1);
   cfg.dynamicSmemBytes = TcCfg<LPAD>::SMEM;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -154,17 +156,18 @@ int tc_setup(spca_sketch *h) {
   tc_omega_prepare<<<grid_for((int64_t)h->lpad * h->n), 256, 0, h->stream>>>(
       h->omega64_dev, (int)h->n, (int)h->l, (int)h->lpad, whi, wlo);
   CK_LAUNCH(h);
-  // B tiles are loaded as 64-row halves (one per CTA of a pair)
-  int rc = encode_2d(h, &h->tm_whi, whi, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, 64);
+  // B tiles are loaded as l_pad/2-row halves (one per CTA of a pair)
+  const uint32_t hr = (uint32_t)(h->lpad / 2);
+  int rc = encode_2d(h, &h->tm_whi, whi, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, hr);
   if (rc) return rc;
-  rc = encode_2d(h, &h->tm_wlo, wlo, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, 64);
+  rc = encode_2d(h, &h->tm_wlo, wlo, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, hr);
   if (rc) return rc;
   const FusedSched s = tc_base_sched(h);
   // G^T hi / lo of kSlots chunks: [kSlots][2][lpad][R0], one TMA map
   h->tc_ws_bytes = (size_t)kSlots * 2 * h->lpad * s.R0 * 4;
   CK(h, cudaMalloc(&h->tc_ws, h->tc_ws_bytes));
   rc = encode_2d(h, &h->tm_gT, h->tc_ws, (uint64_t)s.R0, (uint64_t)kSlots * 2 * h->lpad, (uint64_t)s.R0 * 4,
-                 32, 64);
+                 32, hr);
   if (rc) return rc;
   h->gpart_elems = (int64_t)kSlots * 2 * s.T * s.S * 128 * h->lpad;
   CK(h, cudaMalloc(&h->gpart, (size_t)h->gpart_elems * 4));
@@ -247,15 +250,17 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   args.hseq = args.hdone + s.C;
   args.accumulate = h->chunks_since_flush > 0 ? 1 : 0;
   args.first_row = h->rows_done;
+  args.a = (const float *)a;
+  args.lda = lda;
   args.bad_row = h->bad_dev;
   args.trace = h->trace;
   args.dbg = h->tc_debug;
   const int grid = 2 * std::max(1, std::min(h->max_pairs, s.total));
   if (h->lpad == 64)
-    tc_pass_kernel<64><<<grid, kTcThreads, TcCfg<64>::SMEM, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo,
+    tc_pass_kernel<64><<<grid, TcCfg<64>::THREADS, TcCfg<64>::SMEM, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo,
                                                                          h->tm_gT, args);
   else
-    tc_pass_kernel<128><<<grid, kTcThreads, TcCfg<128>::SMEM, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo,
+    tc_pass_kernel<128><<<grid, TcCfg<128>::THREADS, TcCfg<128>::SMEM, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo,
                                                                            h->tm_gT, args);
   CK_LAUNCH(h);
   h->chunks_since_flush += s.C;

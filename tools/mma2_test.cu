@@ -142,6 +142,7 @@ void run(int iters) {
 }
 
 int main() {
+  run<64>(4096);
   run<128>(8);
   run<128>(4096);
   run<256>(4096);

@@ -21,9 +21,9 @@ lib.spca_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
 for rep in range(3):
     sk.reset(); sk.push(a, 0); sk.finish()
 STRIDE, UNITS = 1024, 127
-buf = np.zeros(256 * STRIDE, dtype=np.uint64)
+buf = np.zeros(256 * STRIDE + 4 * 2048, dtype=np.uint64)
 _lib.check(lib.spca_debug_trace(sk.h, 0, buf.ctypes.data, buf.size), sk.h)
-t = buf.reshape(256, STRIDE).astype(np.int64)
+t = buf[:256 * STRIDE].reshape(256, STRIDE).astype(np.int64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 end = (t[:, 1] - t0) / 1e3
@@ -47,3 +47,112 @@ stat("epilogue duration", np.where(valid, u[:, :, 4] - u[:, :, 3], np.nan).ravel
 mm = (u[:, :, 5] > 0) & (u[:, :, 6] > 0)
 stat("MMA issue span (leader)", np.where(mm, u[:, :, 6] - u[:, :, 5], np.nan).ravel())
 stat("B producer dep-wait end - conv start", np.where(valid & (u[:, :, 7] > 0), u[:, :, 7] - u[:, :, 0], np.nan).ravel())
+
+# per unit kind (replicates fused_decode for the single launch of this run)
+def sched(m, n, R0, U=32):
+    nkb = -(-n // 32); S = -(-nkb // U); kseg = -(-nkb // S); S = -(-nkb // kseg)
+    nt = R0 // 128; T = nt // 2; nx = -(-n // 128); X = -(-nx // 2)
+    rkb = R0 // 32; RS = -(-rkb // U); hseg = -(-rkb // RS); RS = -(-rkb // hseg)
+    C = -(-m // R0); rows_last = m - (C - 1) * R0; ntl = -(-rows_last // 128); Tl = -(-ntl // 2)
+    return dict(C=C, T=T, Tl=Tl, S=S, X=X, RS=RS)
+
+
+def kind_of(s, u):
+    TS, XR = s["T"] * s["S"], s["X"] * s["RS"]
+    g0 = (s["Tl"] if s["C"] == 1 else s["T"]) * s["S"]
+    if u < g0:
+        return 0, 0
+    u -= g0
+    F = TS + XR
+    nmid = max(0, s["C"] - 2)
+    if u < nmid * F:
+        st = 1 + u // F
+        r = u - (st - 1) * F
+        return (0, st) if r < TS else (1, st - 1)
+    u -= nmid * F
+    TlS = s["Tl"] * s["S"]
+    if s["C"] >= 2 and u < TlS + XR:
+        return (0, s["C"] - 1) if u < TlS else (1, s["C"] - 2)
+    return 1, s["C"] - 1
+
+
+R0 = sk.chunk_rows()
+sc = sched(rows, n, R0)
+ncl = len(t) // 2
+kinds = np.full(u.shape[:2], -1)
+for cta in range(len(t)):
+    for i in range(UNITS):
+        uu = (cta // 2) + i * ncl
+        kinds[cta, i] = kind_of(sc, uu)[0]
+for k, nm in ((0, "G"), (1, "H")):
+    sel = valid & (kinds == k)
+    stat(f"{nm} units: converter main loop", np.where(sel, u[:, :, 1] - u[:, :, 0], np.nan).ravel())
+    stat(f"{nm} units: B producer ready - conv start", np.where(sel & (u[:, :, 7] > 0), u[:, :, 7] - u[:, :, 0], np.nan).ravel())
+
+# leader of pair 0: per K block, time spent in each MMA-warp wait
+mt = buf[256 * STRIDE:256 * STRIDE + 4 * 2048].reshape(2048, 4).astype(np.int64)
+mt = mt[mt[:, 0] > 0]
+if len(mt) > 2:
+    nxt = np.roll(mt[:, 0], -1)
+    d = np.diff(mt, axis=1) / 1e3
+    issue = (nxt - mt[:, 3])[:-1] / 1e3
+    per = (nxt - mt[:, 0])[:-1] / 1e3
+    ok = (per > 0) & (per < 9)  # drop unit boundaries
+    med = lambda x: np.median(x[:-1][ok]) if x.ndim == 1 and len(x) > len(ok) else np.median(x[ok])
+    print(f"MMA warp (x1000 cycles), {ok.sum()} K blocks: per block med {np.median(per[ok]):.3f}; waits med "
+          f"acc_empty {np.median(d[:-1, 0][ok]):.3f} t_full {np.median(d[:-1, 1][ok]):.3f} "
+          f"b_full {np.median(d[:-1, 2][ok]):.3f}; issue+commit {np.median(issue[ok]):.3f} us; "
+          f"sum of means: waits {d[:-1][ok].sum(axis=0).round(0)} issue {issue[ok].sum():.0f} us")
+
+# converter thread 0 of CTA 0 (group 0): per K block of its own
+off = 256 * STRIDE + 4 * 2048
+cb = np.zeros(6 * 1024, dtype=np.uint64)
+full = np.zeros(off + 6 * 1024, dtype=np.uint64)
+_lib.check(lib.spca_debug_trace(sk.h, 0, full.ctypes.data, full.size), sk.h)
+ct = full[off:].reshape(1024, 6).astype(np.int64)
+ct = ct[ct[:, 0] > 0]
+if len(ct) > 2:
+    d = np.diff(ct, axis=1)
+    per = np.diff(ct[:, 0])
+    ok = (per > 0) & (per < 20000)
+    names = ["a_full wait", "load+split+kb_empty wait", "tmem st", "wait::st", "arrive"]
+    print("converter (cycles, median): per own block %d; " % np.median(per[ok]) +
+          ", ".join(f"{nm} {np.median(d[:-1, i][ok]):.0f}" for i, nm in enumerate(names)) +
+          "; loop rest %d" % np.median((np.roll(ct[:, 0], -1) - ct[:, 5])[:-1][ok]))
+
+# MMA completion times (pair 0 leader), against the MMA warp's issue times
+off2 = 256 * STRIDE + 4 * 2048 + 6 * 1024
+full2 = np.zeros(off2 + 2048, dtype=np.uint64)
+_lib.check(lib.spca_debug_trace(sk.h, 0, full2.ctypes.data, full2.size), sk.h)
+done = full2[off2:].astype(np.int64)
+iss = full2[256 * STRIDE:256 * STRIDE + 4 * 2048].reshape(2048, 4).astype(np.int64)[:, 3]
+n_ = min((done > 0).sum(), (iss > 0).sum())
+if n_ > 10:
+    done, iss = done[:n_], iss[:n_]
+    gap = np.diff(done)
+    ok = (gap > 0) & (gap < 20000)
+    lat = done - iss
+    print(f"MMA completions: per block med {np.median(gap[ok]):.0f} cycles (p10 {np.percentile(gap[ok], 10):.0f}); "
+          f"issue->completion med {np.median(lat):.0f} p90 {np.percentile(lat, 90):.0f} cycles")
+
+# block-level chain for even blocks (converter group 0, thread 0 of CTA 0):
+# converter arrive(k) -> MMA issue(k) -> MMA complete(k) -> converter arrive(k + NS) (stage reuse)
+conv = full[off:off + 6 * 1024].reshape(1024, 6).astype(np.int64)  # own blocks 0,2,4,... (index gk>>1)
+arr = conv[:, 5]
+issue_t = full2[256 * STRIDE:256 * STRIDE + 4 * 2048].reshape(2048, 4).astype(np.int64)[:, 3]
+comp = full2[off2:off2 + 2048].astype(np.int64)
+rows = []
+NS = 4
+for j in range(8, 1000):
+    k = 2 * j
+    if k + NS >= 2048 or arr[j] == 0 or issue_t[k] == 0 or comp[k] == 0:
+        continue
+    jr = (k + NS) // 2
+    if arr[jr] == 0:
+        continue
+    rows.append((issue_t[k] - arr[j], comp[k] - issue_t[k], arr[jr] - comp[k]))
+if rows:
+    r = np.array(rows)
+    ok = np.all((r > -5000) & (r < 20000), axis=1)
+    print("stage chain (cycles, median): conv arrive->MMA issue %d, issue->complete %d, complete->conv arrive(k+NS) %d"
+          % tuple(np.median(r[ok], axis=0)))
