@@ -180,12 +180,12 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def profile_traffic(rows_per_chunk: float):
-    """dram read+write bytes of one chunk's G/H kernels, scaled from the
+def profile_traffic(rows: float):
+    """dram read+write bytes of the pass kernel over `rows` rows, scaled from the
     committed ncu --set full capture (profiles/ncu_summary.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
-            return json.load(fh)["dram_bytes_per_row"] * rows_per_chunk
+            return json.load(fh)["dram_bytes_per_row"] * rows
     except Exception:
         return None
 
@@ -254,15 +254,13 @@ def run_ours(args):
     ms_step = ms / args.steps
     value = world * bytes_per_rank / (ms_step * 1e-3) / 1e9
 
-    # Roofline of the dominant kernel group: one canonical chunk of the pass
-    # (G and H contractions + finalize + column sums), timed with CUDA events on
-    # the library's streams over the timed region (window per pass / chunks).
+    # Roofline of the dominant kernel: the pass kernel (tc_pass_kernel, one
+    # persistent launch per push) timed with CUDA events around its launches on
+    # the library's stream over the timed region (spca_kernel_time_ms).
     chunk_rows = sk.chunk_rows()
-    chunks_per_pass = -(-m // chunk_rows)
-    chunk_ms = kern_ms / max(1, kern_chunks)
-    avg_rows = m / chunks_per_pass
-    chunk_bytes = avg_rows * n * 4
-    flops = 4.0 * avg_rows * n * l
+    pass_ms = kern_ms / max(1, args.steps)
+    pass_bytes = m * n * 4
+    flops = 4.0 * m * n * l
     used_tc = (args.precision in ("auto", "tc")) and l <= 128
     if used_tc:
         peak_tf = bf16_peak / 2.0 / 3.0   # 3xTF32: tf32 = bf16/2, three products
@@ -270,10 +268,10 @@ def run_ours(args):
     else:
         peak_tf = 148 * 128 * 2 * 1.965e9 / 1e12  # FFMA nominal
         peak_desc = "FFMA nominal (148 SMs x 128 lanes x 2 x 1965 MHz)"
-    hbm_floor = chunk_bytes / (hbm_peak * 1e9)
+    hbm_floor = pass_bytes / (hbm_peak * 1e9)
     tc_floor = flops / (peak_tf * 1e12)
-    achieved_tf = flops / (chunk_ms * 1e-3) / 1e12
-    achieved_gbs = chunk_bytes / (chunk_ms * 1e-3) / 1e9
+    achieved_tf = flops / (pass_ms * 1e-3) / 1e12
+    achieved_gbs = pass_bytes / (pass_ms * 1e-3) / 1e9
     if tc_floor >= hbm_floor:
         roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": achieved_tf / peak_tf}
@@ -281,15 +279,15 @@ def run_ours(args):
         roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": achieved_gbs / hbm_peak}
     roofline.update({
-        "traffic": profile_traffic(avg_rows) if used_tc else None,
+        "traffic": profile_traffic(m) if used_tc else None,
         "peak_kind": peak_kind, "peak_desc": peak_desc,
-        "kernel": "sketch chunk: tc_g_kernel + tc_g_finalize + tc_h_kernel + colsum" if used_tc
+        "kernel": "tc_pass_kernel (persistent, CTA pairs; G + H + column sums of all chunks)" if used_tc
                   else "sketch chunk: simt_g_kernel + simt_h_kernel + colsum",
-        "chunk_rows": chunk_rows, "chunk_ms": chunk_ms,
+        "kernel_ms_per_pass": pass_ms, "chunk_rows": chunk_rows,
         "hbm": {"achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved_gbs / hbm_peak},
-        "algorithmic_bytes_per_chunk": chunk_bytes, "flops_per_chunk": flops,
-        "floors_ms_per_chunk": {"hbm": hbm_floor * 1e3, "tensor": tc_floor * 1e3},
+        "algorithmic_bytes_per_pass": pass_bytes, "flops_per_pass": flops,
+        "floors_ms_per_pass": {"hbm": hbm_floor * 1e3, "tensor": tc_floor * 1e3},
     })
 
     out = {}

@@ -251,7 +251,10 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
   const uint32_t tmem = bars.tmem_base;
 
   if (warp == 0) {  // ---------------------------------------------- A producer
-    const uint64_t keep = ptx::policy_evict_last(), drop = ptx::policy_evict_first();
+    // L2 policy of A: the G units' loads (from HBM) must survive until the H
+    // units re-read the chunk D stages later; the H units' loads are the last use
+    const uint64_t keep = (args.dbg & 4096) ? ptx::policy_evict_normal() : ptx::policy_evict_last();
+    const uint64_t drop = (args.dbg & 8192) ? ptx::policy_evict_normal() : ptx::policy_evict_first();
     int gkb = 0;
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl) {
@@ -268,10 +271,12 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             ptx::mbar_arrive(&bars.a_full[s]);
           } else {
             ptx::mbar_arrive_expect_tx(&bars.a_full[s], C::A_BYTES);
+            const int kx = (args.dbg & 2048) ? 0 : (f.k0 + kb) * 32;  // profiling knob: L2-resident A
+            const int ry = (args.dbg & 2048) ? 0 : rbase;
             if (f.kind == 0) {  // 128 rows x 32 k, row-major (swizzled)
-              ptx::tma_load_2d_hint(st, &tAg, &bars.a_full[s], (f.k0 + kb) * 32, rbase + tile * 128, keep);
+              ptx::tma_load_2d_hint(st, &tAg, &bars.a_full[s], kx, ry + tile * 128, keep);
             } else {            // 32 rows x 128 columns, one unswizzled box
-              ptx::tma_load_2d_hint(st, &tAh, &bars.a_full[s], tile * 128, rbase + (f.k0 + kb) * 32, drop);
+              ptx::tma_load_2d_hint(st, &tAh, &bars.a_full[s], tile * 128, ry + ((args.dbg & 2048) ? 0 : (f.k0 + kb) * 32), drop);
             }
           }
         }

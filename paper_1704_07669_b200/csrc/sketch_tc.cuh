@@ -68,7 +68,10 @@ struct TcCfg {
   // l_pad = 64: "stacked" form, two MMAs per 8-deep step: A_hi [W_hi | W_lo]
   // (N = 128) and A_lo W_hi (N = 64) into the first half; the accumulator is
   // 128 columns and promotion adds its halves. l_pad = 128: three N = 128 MMAs.
-  static constexpr bool STACKED = LPAD == 64;
+#ifndef SPCA_STACKED_64
+#define SPCA_STACKED_64 1
+#endif
+  static constexpr bool STACKED = LPAD == 64 && SPCA_STACKED_64;
   static constexpr int ACC_COLS = STACKED ? 128 : LPAD;  // one accumulator
   static constexpr int NS = (kTmemCols - 2 * ACC_COLS) / 64;  // TMEM A operand stages
   // B ring: deep enough to cover an L2 round trip (~1-2 us) at the MMA rate
@@ -83,8 +86,8 @@ struct TcCfg {
   // (R0..R1 = this CTA's 64 rows of [W_hi | W_lo], R2 = its 32 rows of W_hi).
   // Otherwise: W_hi rows [r*l_pad/2, (r+1)*l_pad/2) then the same rows of W_lo.
   static constexpr uint32_t B_STAGE = STACKED ? 3 * BH_BYTES : 2 * BH_BYTES;
-  static constexpr int NB = STACKED ? 7 : 4;          // B ring (12 KB | 16 KB stages)
-  static constexpr int NA = STACKED ? 6 : 5;          // raw A ring (16 KB stages)
+  static constexpr int NB = STACKED ? 7 : (LPAD == 64 ? 8 : 4);  // B ring (12 | 8 | 16 KB stages)
+  static constexpr int NA = STACKED ? 6 : (LPAD == 64 ? 7 : 5);  // raw A ring (16 KB stages)
   static constexpr uint32_t STG_BYTES = 128 * LPAD * 4;  // epilogue staging tile
   static constexpr uint32_t B_OFF = NA * A_BYTES;
   static constexpr uint32_t STG_OFF = B_OFF + NB * B_STAGE;

@@ -13,14 +13,14 @@
 using namespace spca;
 __device__ __forceinline__ bool lane0() { return (threadIdx.x & 31) == 0; }
 
-template <int V, int BUSY = 0, int RND = 0, int MEM = 0>
+template <int V, int BUSY = 0, int RND = 0, int MEM = 0, int STORES = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) kb(int nkb, unsigned long long *out,
                                                                     const char *gsrc = nullptr) {
   using C = TcCfg<64>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint32_t tbase;
-  __shared__ uint64_t kb_empty[6], acc_full[2], ready;
+  __shared__ uint64_t kb_empty[6], acc_full[2], ready, b_empty[8];
   const uint32_t rank = ptx::cluster_rank();
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < (RND ? 12 : 6) * 8192 / 4; i += blockDim.x) {
@@ -35,6 +35,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) kb(int nkb, 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 6; ++i) ptx::mbar_init(&kb_empty[i], 1);
     for (int i = 0; i < 2; ++i) ptx::mbar_init(&acc_full[i], 1);
+    for (int i = 0; i < 8; ++i) ptx::mbar_init(&b_empty[i], 1);
     ptx::mbar_init(&ready, 1);
     ptx::mbar_arrive(&ready);  // phase 0 complete: waits on it return at once
     ptx::fence_mbar_init();
@@ -84,6 +85,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) kb(int nkb, 
     for (int k = it; k < it + 4; ++k)
       if (k >= 4) ptx::mbar_wait(&tbar[k & 3], ((k >> 2) - 1) & 1);
   }
+  if (STORES && warp >= 4 && warp < 12) {  // converter-like TMEM stores into the A stages
+    float v[32];
+    for (int i = 0; i < 32; ++i) v[i] = 0.5f + i;
+    const uint32_t lb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    int it = 0;
+    while (!stop) {
+      const uint32_t col = 256 + ((it + (warp >> 2)) & 3) * 64;
+      ptx::tmem_st32(lb + col, v);
+      ptx::tmem_st32(lb + col + 32, v);
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ++it;
+    }
+  }
   if (BUSY && warp >= 4 && warp < 4 + BUSY) {  // ALU-bound warps sharing the schedulers
     float x = threadIdx.x, y = 1.0001f;
     while (!stop) {
@@ -105,6 +120,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) kb(int nkb, 
         tc_mma_stage2<64>(tmem + C::A_TMEM + 64 * ks, tmem + buf * C::ACC_COLS,
                           bdesc0 + (uint64_t)((ks * C::B_STAGE) >> 4), kb == 0);
         ptx::mma2_commit_both(&kb_empty[ks]);
+        if (V & 4) ptx::mma2_commit_both(&b_empty[gkb % 7]);
         if (kb == 3) ptx::mma2_commit_both(&acc_full[buf]);
       }
       __syncwarp();
@@ -138,13 +154,18 @@ int main() {
   cudaMemset(g, 1, (size_t)65536 * 16384);
   cudaFuncSetAttribute(kb<3, 8, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024);
   kb<3, 8, 1, 1><<<148, 512, 180 * 1024>>>(16384, d + 6, g);
+  cudaFuncSetAttribute(kb<3, 0, 1, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  kb<3, 0, 1, 0, 1><<<148, 512, 100 * 1024>>>(8192, d + 7);
+  cudaFuncSetAttribute(kb<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 60 * 1024);
+  kb<7><<<2, 128, 60 * 1024>>>(2048, d + 1);
   kb<3, 12><<<2, 512, 60 * 1024>>>(2048, d + 4);
   kb<1><<<2, 128, 60 * 1024>>>(2048, d);
   kb<3><<<2, 128, 60 * 1024>>>(2048, d);
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(h, d, 128, cudaMemcpyDeviceToHost);
   printf("%s: cycles per K block (ideal 384): no waits %llu, 1 wait %llu, 2 waits %llu, all SMs %llu,"
-         " +4 busy warps %llu, +12 busy warps %llu, random data all SMs %llu, + HBM copies + ALU all SMs %llu\n",
-         cudaGetErrorString(e), h[0], h[1], h[3], h[2 + 3], h[3 + 3], h[4 + 3], h[5 + 3], h[6 + 3]);
+         " +4 busy warps %llu, +12 busy warps %llu, random data all SMs %llu, + HBM copies + ALU all SMs %llu,"
+         " + TMEM stores into the A stages %llu, 3 commits %llu\n",
+         cudaGetErrorString(e), h[0], h[1], h[3], h[2 + 3], h[3 + 3], h[4 + 3], h[5 + 3], h[6 + 3], h[7 + 3], h[1 + 7]);
   return 0;
 }

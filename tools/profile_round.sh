@@ -1,12 +1,12 @@
 # Round profiling recipe (run on the GPU box via gpurun):
 #   bash tools/profile_round.sh TAG
-# 1. plain bench (exit 0 required before ncu), 2. ncu launch list,
-# 3. ncu --set full on the G and H contraction kernels.
+# 1. plain bench (exit 0 required before ncu), 2. ncu launch list of the same
+# command, 3. ncu --set full on the pass kernel (one launch = one cfg2 pass).
 TAG=${1:-r1}
-CMD="python bench.py --steps 3 --warmup 2 --rows 32768 --no-e2e --no-pca --no-cpu"
+CMD="python bench.py --steps 3 --warmup 2 --no-e2e --no-pca --no-cpu"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 || { echo "plain run failed"; tail -20 gpurun_out/${TAG}_plain.log; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"tc_(g|h)_kernel" -s 4 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:"tc_pass_kernel" -s 2 -c 1 \
     -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "profile done: $(ls gpurun_out | grep ${TAG}_ | tr '\n' ' ')"
