@@ -219,7 +219,7 @@ def run_ours(args):
 
     def step():
         sk.reset()
-        sk.push(a, 0)
+        sk.push(a, 0, final=True)
         g, h, c, rows = sk.finish(on_device=True)
         if pg is not None:
             allreduce_sketch(h, c, pg, rows=rows)
@@ -344,7 +344,7 @@ def e2e_leg(args, a_dev, omega, dev, steps=3):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         sk.reset()
-        sk.push(host, 0)
+        sk.push(host, 0, final=True)
         g, h, c, rows = sk.finish(on_device=False)
         dt = time.perf_counter() - t0
         d2h = g.nbytes + h.nbytes + c.nbytes

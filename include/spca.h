@@ -106,6 +106,15 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype,
 int spca_sketch_push(spca_handle_t h, const void *a, int64_t rows, int64_t ld,
                      int64_t first_row, int where);
 
+/* spca_sketch_push for the last block of the stream (the final iteration of
+ * `for block in stream.blocks(...)`, sketch.py:85-113): the trailing partial
+ * chunk is processed with the rest of the block instead of waiting in the
+ * staging buffer for spca_sketch_finish. Results are bitwise identical to
+ * push + finish (the canonical chunk boundaries do not move); pushes after a
+ * final push fail with SPCA_ERR_STATE until spca_sketch_reset. */
+int spca_sketch_push_final(spca_handle_t h, const void *a, int64_t rows, int64_t ld,
+                           int64_t first_row, int where);
+
 /* Start a new pass on the same handle (same n, l, Omega): zero the
  * accumulators and the row counter, keep every allocation. Lets a caller
  * run repeated passes (or a second pass of power_refine with the same Omega)

@@ -51,6 +51,7 @@ struct spca_sketch {
   int num_sms = 148;
   int max_pairs = 74;             // co-resident CTA pairs of the pass kernel
   unsigned long long *bad_dev = nullptr;
+  unsigned long long *bad_host = nullptr;  // pinned copy read at finish
 
   int64_t chunk_rows = 0;        // canonical chunk (R0)
   void *tail = nullptr;          // R0 x n staging for the partial chunk
@@ -62,6 +63,7 @@ struct spca_sketch {
   int tc_debug = 0;              // SPCA_TC_DEBUG bitmask (profiling experiments only)
   unsigned long long *trace = nullptr;  // SPCA_TC_TRACE per-CTA timeline
   bool finished = false;
+  bool final_pushed = false;     // spca_sketch_push_final was called (no more rows)
 
   // host staging (pinned double buffer)
   void *pinned[2] = {nullptr, nullptr};

@@ -268,7 +268,7 @@ int process_rows_tc(spca_sketch *h, const char *a, int64_t lda, int64_t rows) {
 }
 
 // Rows already on the device: feed canonical chunks, keep the remainder in `tail`.
-int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda) {
+int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, bool final = false) {
   const int64_t R0 = h->chunk_rows;
   const size_t row_bytes = (size_t)h->n * h->ds;
   int64_t off = 0;
@@ -290,18 +290,23 @@ int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda) {
       h->tail_rows = 0;
     }
   }
-  if (h->precision == SPCA_PREC_TC) {  // all whole chunks in one go
-    const int64_t whole = ((rows - off) / R0) * R0;
-    if (whole > 0) {
-      int rc = process_rows_tc(h, a + (size_t)off * lda * h->ds, lda, whole);
+  if (h->precision == SPCA_PREC_TC) {  // all whole chunks (and a final partial one) in one go
+    const int64_t take = final ? rows - off : ((rows - off) / R0) * R0;
+    if (take > 0) {
+      int rc = process_rows_tc(h, a + (size_t)off * lda * h->ds, lda, take);
       if (rc) return rc;
-      off += whole;
+      off += take;
     }
   }
   while (rows - off >= R0) {
     int rc = process_chunk(h, a + (size_t)off * lda * h->ds, lda, R0);
     if (rc) return rc;
     off += R0;
+  }
+  if (off < rows && final) {  // SIMT path: the last partial chunk straight from the source
+    int rc = process_chunk(h, a + (size_t)off * lda * h->ds, lda, rows - off);
+    if (rc) return rc;
+    off = rows;
   }
   if (off < rows) {
     int64_t rem = rows - off;
@@ -325,7 +330,7 @@ int ensure_staging(spca_sketch *h, bool need_pinned) {
   return SPCA_OK;
 }
 
-int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, bool pageable) {
+int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, bool pageable, bool final = false) {
   int rc = ensure_staging(h, pageable);
   if (rc) return rc;
   const size_t row_bytes = (size_t)h->n * h->ds;
@@ -355,7 +360,7 @@ int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, boo
     }
     CK(h, cudaEventRecord(h->copy_done[i], h->copy_stream));
     CK(h, cudaStreamWaitEvent(h->stream, h->copy_done[i], 0));
-    rc = push_device_rows(h, (const char *)h->dstage[i], take, h->n);
+    rc = push_device_rows(h, (const char *)h->dstage[i], take, h->n, final && off + take == rows);
     if (rc) return rc;
     CK(h, cudaEventRecord(h->comp_done[i], h->stream));
     h->stage_used[i] = true;
@@ -521,29 +526,60 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
   return SPCA_OK;
 }
 
-int spca_sketch_push(spca_handle_t h, const void *a, int64_t rows, int64_t ld, int64_t first_row,
-                     int where) {
+}  // extern "C"
+
+namespace {
+int push_impl(spca_handle_t h, const void *a, int64_t rows, int64_t ld, int64_t first_row, int where,
+              bool final) {
   if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
   if (h->finished) return set_err(h, SPCA_ERR_STATE, -1, "push after finish");
+  if (h->final_pushed) return set_err(h, SPCA_ERR_STATE, -1, "push after the final push");
   if (rows < 0) return set_err(h, SPCA_ERR_FORMAT, first_row, "negative row count");
   if (first_row != h->rows_seen)
     return set_err(h, SPCA_ERR_FORMAT, first_row,
                    "block starts at row %lld but %lld rows were consumed (blocks must be consecutive)",
                    (long long)first_row, (long long)h->rows_seen);
-  if (rows == 0) return SPCA_OK;
-  if (!a) return set_err(h, SPCA_ERR_FORMAT, first_row, "null block pointer");
-  if (ld < h->n)
+  if (rows == 0 && !final) return SPCA_OK;
+  if (rows > 0 && !a) return set_err(h, SPCA_ERR_FORMAT, first_row, "null block pointer");
+  if (rows > 0 && ld < h->n)
     return set_err(h, SPCA_ERR_FORMAT, first_row, "block at row %lld has row stride %lld < n=%lld",
                    (long long)first_row, (long long)ld, (long long)h->n);
   DeviceGuard dg(h->device);
-  int rc;
-  if (where == SPCA_MEM_DEVICE) rc = push_device_rows(h, (const char *)a, rows, ld);
-  else if (where == SPCA_MEM_PINNED) rc = push_host_rows(h, (const char *)a, rows, ld, false);
-  else if (where == SPCA_MEM_PAGEABLE) rc = push_host_rows(h, (const char *)a, rows, ld, true);
-  else return set_err(h, SPCA_ERR_CONFIG, -1, "bad memory kind %d", where);
+  int rc = SPCA_OK;
+  if (rows == 0) {
+    // final push of nothing: still flush the staged tail now
+  } else if (where == SPCA_MEM_DEVICE) {
+    rc = push_device_rows(h, (const char *)a, rows, ld, final);
+  } else if (where == SPCA_MEM_PINNED) {
+    rc = push_host_rows(h, (const char *)a, rows, ld, false, final);
+  } else if (where == SPCA_MEM_PAGEABLE) {
+    rc = push_host_rows(h, (const char *)a, rows, ld, true, final);
+  } else {
+    return set_err(h, SPCA_ERR_CONFIG, -1, "bad memory kind %d", where);
+  }
   if (rc) return rc;
+  if (final && h->tail_rows > 0) {  // rows == 0, or a tail left by earlier pushes
+    rc = h->precision == SPCA_PREC_TC ? process_rows_tc(h, (const char *)h->tail, h->n, h->tail_rows)
+                                      : process_chunk(h, h->tail, h->n, h->tail_rows);
+    if (rc) return rc;
+    h->tail_rows = 0;
+  }
   h->rows_seen += rows;
+  if (final) h->final_pushed = true;
   return SPCA_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int spca_sketch_push(spca_handle_t h, const void *a, int64_t rows, int64_t ld, int64_t first_row,
+                     int where) {
+  return push_impl(h, a, rows, ld, first_row, where, false);
+}
+
+int spca_sketch_push_final(spca_handle_t h, const void *a, int64_t rows, int64_t ld, int64_t first_row,
+                           int where) {
+  return push_impl(h, a, rows, ld, first_row, where, true);
 }
 
 int spca_sketch_reset(spca_handle_t h) {
@@ -560,6 +596,7 @@ int spca_sketch_reset(spca_handle_t h) {
   h->rows_done = 0;
   h->chunks_since_flush = 0;
   h->finished = false;
+  h->final_pushed = false;
   h->last_code = SPCA_OK;
   h->last_bad_row = -1;
   h->last_msg[0] = 0;
@@ -613,13 +650,11 @@ int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out, double *co
                                                                 h->rows_seen, (int)h->l, h->g64_dev);
       CK_LAUNCH(h);
     }
-    CK(h, cudaStreamSynchronize(h->stream));
-    rc = collect_timers(h);
-    if (rc) return rc;
-    rc = check_bad_row(h);
-    if (rc) return rc;
-    h->finished = true;
+    // the first non-finite row comes back with the outputs: one synchronization
+    if (!h->bad_host) CK(h, cudaHostAlloc((void **)&h->bad_host, sizeof(unsigned long long), cudaHostAllocDefault));
+    CK(h, cudaMemcpyAsync(h->bad_host, h->bad_dev, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
   }
+  const bool first_finish = !h->finished;
   cudaMemcpyKind kind = out_where == SPCA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   if (g_out && h->rows_seen > 0)
     CK(h, cudaMemcpyAsync(g_out, h->g64_dev, (size_t)h->rows_seen * h->l * 8, kind, h->stream));
@@ -628,6 +663,14 @@ int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out, double *co
     CK(h, cudaMemcpyAsync(colsum_out, h->hcs_dev + h->n * h->l, (size_t)h->n * 8, kind, h->stream));
   if (rows_seen) *rows_seen = h->rows_seen;
   CK(h, cudaStreamSynchronize(h->stream));
+  if (first_finish) {
+    rc = collect_timers(h);
+    if (rc) return rc;
+    if (*h->bad_host != (unsigned long long)kNoBadRow)
+      return set_err(h, SPCA_ERR_DATA, (int64_t)*h->bad_host, "non-finite value in row %lld",
+                     (long long)*h->bad_host);
+    h->finished = true;
+  }
   return SPCA_OK;
 }
 
@@ -771,6 +814,7 @@ void spca_sketch_destroy(spca_handle_t h) {
     if (p) cudaFree(p);
   for (int i = 0; i < 2; ++i) {
     if (h->pinned[i]) cudaFreeHost(h->pinned[i]);
+    if (i == 0 && h->bad_host) cudaFreeHost(h->bad_host);
     if (h->copy_done[i]) cudaEventDestroy(h->copy_done[i]);
     if (h->comp_done[i]) cudaEventDestroy(h->comp_done[i]);
   }

@@ -218,9 +218,12 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   int row_base = 0;
   const char *base = (const char *)h->src_ptr;
   const int64_t row_bytes = lda * 4;
-  if (s.rows_last == s.R0 && base && lda == h->src_lda && (const char *)a >= base &&
-      ((const char *)a - base) % row_bytes == 0 &&
-      ((const char *)a - base) / row_bytes + rows <= h->src_rows) {
+  // cached maps over the pushed buffer: whole chunks, or a partial last chunk
+  // that ends exactly where the buffer ends (rows beyond it read as zeros)
+  const int64_t rb = base && (const char *)a >= base && ((const char *)a - base) % row_bytes == 0
+                         ? ((const char *)a - base) / row_bytes : -1;
+  if (base && lda == h->src_lda && rb >= 0 &&
+      (s.rows_last == s.R0 ? rb + rows <= h->src_rows : rb + rows == h->src_rows)) {
     row_base = (int)(((const char *)a - base) / row_bytes);
     ta_g = &h->src_tg;
     ta_h = &h->src_th;

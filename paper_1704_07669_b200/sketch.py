@@ -85,8 +85,10 @@ class GpuSketch:
         self._finished = False
 
     # -- pushing ------------------------------------------------------------
-    def push(self, values, first_row: int) -> int:
-        """Append one block; numpy (pageable host), pinned host tensor or CUDA tensor."""
+    def push(self, values, first_row: int, final: bool = False) -> int:
+        """Append one block; numpy (pageable host), pinned host tensor or CUDA tensor.
+        ``final=True`` marks the last block of the stream: its trailing partial
+        chunk is processed now instead of at finish (spca_sketch_push_final)."""
         torch = torch_mod()
         if is_torch(values):
             t = values
@@ -117,10 +119,11 @@ class GpuSketch:
             ld = a.strides[0] // a.itemsize if rows > 1 else self.n
             ptr = a.ctypes.data
             where = _lib.MEM_PAGEABLE
-        if rows == 0:
+        if rows == 0 and not final:
             return 0
-        _lib.check(self.lib.spca_sketch_push(self.h, ctypes.c_void_p(ptr), rows, max(ld, self.n),
-                                             int(first_row), where), self.h)
+        fn = self.lib.spca_sketch_push_final if final else self.lib.spca_sketch_push
+        _lib.check(fn(self.h, ctypes.c_void_p(ptr) if rows else None, rows, max(ld, self.n),
+                      int(first_row), where), self.h)
         return rows
 
     def reset(self) -> None:
@@ -206,11 +209,12 @@ def run_pass(stream, omega, block_rows=None, compensated=False, precision="auto"
     if has_whole(stream):
         kind, mat = stream.whole()
         if mat.shape[0]:
-            sk.push(mat, 0)
+            sk.push(mat, 0, final=True)
     else:
         if block_rows is None:
             block_rows = l
-        seen = 0
+        # blocks are pushed as they come (a stream may reuse its block buffer,
+        # so no look-ahead); the trailing partial chunk is flushed at finish
         for block in stream.blocks(block_rows):
             vals = block.values
             if getattr(vals, "ndim", None) != 2 or vals.shape[1] != n:
@@ -218,7 +222,6 @@ def run_pass(stream, omega, block_rows=None, compensated=False, precision="auto"
                     f"block at row {block.first_row_index} has shape {tuple(vals.shape)}, "
                     f"expected (*, {n})")
             sk.push(vals, block.first_row_index)
-            seen += vals.shape[0]
     return sk
 
 

@@ -374,3 +374,28 @@ def test_config2_full_size_properties():
     assert float(torch.linalg.norm(cross - cross.T) / torch.linalg.norm(cross)) < 1e-5
     st2 = P.sketch_pass(P.DeviceRowStream(a), om, keep_on_device=True)
     assert torch.equal(st.h, st2.h) and torch.equal(st.g, st2.g)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["simt", "tc"])
+def test_final_push_matches_push_then_finish(precision):
+    """spca_sketch_push_final processes the trailing partial chunk with the
+    block: bitwise identical to push + finish, and later pushes are refused."""
+    if precision == "tc" and not _tc_ok():
+        pytest.skip("tensor-core path unavailable")
+    a = torch.from_numpy(O.gaussian(5000, 1200, seed=41).astype(np.float32)).cuda()
+    om = O.gaussian(1200, 60, seed=42)
+    out = []
+    for final in (False, True):
+        sk = P.GpuSketch(1200, om, np.float32, precision=precision, rows_hint=5000)
+        sk.push(a[:3000], 0)
+        sk.push(a[3000:], 3000, final=final)
+        if final:
+            with pytest.raises(P.DeviceError):
+                sk.push(a[:10], 5000)
+        g, h, c, rows = sk.finish(on_device=False)
+        sk.close()
+        out.append((g, h, c, rows))
+    assert out[0][3] == out[1][3] == 5000
+    for x, y in zip(out[0][:3], out[1][:3]):
+        assert np.array_equal(x, y)

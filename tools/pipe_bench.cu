@@ -22,7 +22,7 @@ pipe(const __grid_constant__ CUtensorMap tW, const __grid_constant__ CUtensorMap
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint32_t tbase;
-  __shared__ uint64_t b_full[NB], b_empty[NB], done, kb_full[4], kb_empty[4], acc_full[2], acc_empty[2];
+  __shared__ uint64_t b_full[NB], b_empty[NB], done, kb_full[8], kb_empty[8], acc_full[2], acc_empty[2];
   __shared__ uint64_t a_full[6], a_empty[6];
   const uint32_t rank = ptx::cluster_rank();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -32,7 +32,7 @@ pipe(const __grid_constant__ CUtensorMap tW, const __grid_constant__ CUtensorMap
       ptx::mbar_init(&b_empty[i], 1);
     }
     ptx::mbar_init(&done, 1);
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < C::NS; ++i) {
       ptx::mbar_init(&kb_full[i], 8);
       ptx::mbar_init(&kb_empty[i], 1);
     }
@@ -59,7 +59,8 @@ pipe(const __grid_constant__ CUtensorMap tW, const __grid_constant__ CUtensorMap
       if (kb >= 6) ptx::mbar_wait(&a_empty[s], ((kb / 6) - 1) & 1);
       if (ptx::elect_one()) {
         ptx::mbar_arrive_expect_tx(&a_full[s], 16384);
-        const int tile = (blockIdx.x + (kb / (n / 32)) * gridDim.x) % 780, kk = kb % (n / 32);
+        const int tile = MODE == 7 ? (blockIdx.x % 8) : (blockIdx.x + (kb / (n / 32)) * gridDim.x) % 780;
+        const int kk = kb % (n / 32);
         ptx::tma_load_2d(aring + s * 16384, &tA, &a_full[s], kk * 32, tile * 128);
       }
       __syncwarp();
@@ -77,7 +78,7 @@ pipe(const __grid_constant__ CUtensorMap tW, const __grid_constant__ CUtensorMap
           if (rank == 0) ptx::mbar_arrive_expect_tx(&b_full[s], 2 * C::B_STAGE);
           ptx::tma_load_2d_pair(st, &tW, bar, k, 0, 0);
           ptx::tma_load_2d_pair(st + C::BH_BYTES, &tW, bar, k, 32, 0);
-          ptx::tma_load_2d_pair(st + 2 * C::BH_BYTES, &tW, bar, k, 32 * (int)rank, 0);
+          if (C::STACKED) ptx::tma_load_2d_pair(st + 2 * C::BH_BYTES, &tW, bar, k, 32 * (int)rank, 0);
         } else {
           if (rank == 0) ptx::mbar_arrive(&b_full[s]);
         }
@@ -97,7 +98,8 @@ pipe(const __grid_constant__ CUtensorMap tW, const __grid_constant__ CUtensorMap
       for (int c = 0; c < 64; c += 8) {
         float v8[8], w8[8];
         ptx::tmem_ld8(lane_base + buf * C::ACC_COLS + c, v8);
-        ptx::tmem_ld8(lane_base + buf * C::ACC_COLS + 64 + c, w8);
+        if (C::STACKED) ptx::tmem_ld8(lane_base + buf * C::ACC_COLS + 64 + c, w8);
+        else for (int i = 0; i < 8; ++i) w8[i] = 0.f;
         for (int i = 0; i < 8; ++i) racc[c + i] += v8[i] + w8[i];
       }
       ptx::tc_fence_before();
@@ -113,11 +115,20 @@ pipe(const __grid_constant__ CUtensorMap tW, const __grid_constant__ CUtensorMap
     for (int i = 0; i < 32; ++i) { v[i] = 0.25f * i; hi[i] = 1.f; }
     const uint32_t arow = ptx::smem_u32(smem + NB * C::B_STAGE + t * 128);  // static A landing tile (16 KB)
     for (int kb = grp; kb < nkb; kb += 2) {
-      const int ts = kb & 3;
+      const int ts = kb % C::NS;
       const int as = kb % 6;
       if (MODE >= 5) ptx::mbar_wait(&a_full[as], (kb / 6) & 1);
       const uint32_t srcrow = MODE >= 5 ? ptx::smem_u32(aring + as * 16384 + t * 128) : arow;
-      if (MODE >= 4) {  // converter work: 8 x LDS.128 + split, like the pass kernel
+      if (MODE == 6) {  // H-style converter loads: column t, 32 x LDS.32 (A from HBM)
+        const uint32_t raw = ptx::smem_u32(aring + as * 16384 + t * 4);
+#pragma unroll
+        for (int kq = 0; kq < 32; ++kq) v[kq] = ptx::lds32(raw + kq * 512);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          hi[i] = trunc_tf32(v[i]);
+          v[i] -= hi[i];
+        }
+      } else if (MODE >= 4) {  // converter work: 8 x LDS.128 + split, like the pass kernel
 #pragma unroll
         for (int q4 = 0; q4 < 8; ++q4) {
           const float4 x = ptx::lds128(srcrow + ((q4 ^ (t & 7)) << 4));
@@ -133,7 +144,7 @@ pipe(const __grid_constant__ CUtensorMap tW, const __grid_constant__ CUtensorMap
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&a_empty[as]);
       }
-      if (kb >= 4) ptx::mbar_wait(&kb_empty[ts], ((kb / 4) - 1) & 1);
+      if (kb >= C::NS) ptx::mbar_wait(&kb_empty[ts], ((kb / C::NS) - 1) & 1);
       ptx::tc_fence_after();
       ptx::tmem_st32(lane_base + C::A_TMEM + 64 * ts, hi);
       ptx::tmem_st32(lane_base + C::A_TMEM + 64 * ts + 32, v);
@@ -147,15 +158,15 @@ pipe(const __grid_constant__ CUtensorMap tW, const __grid_constant__ CUtensorMap
     long long t0 = clock64();
     for (int kb = 0; kb < nkb; ++kb) {
       const int bs = kb % NB, q = kb >> 2, buf = q & 1;
-      if (MODE >= 2) ptx::mbar_wait(&kb_full[kb & 3], (kb / 4) & 1);
+      if (MODE >= 2) ptx::mbar_wait(&kb_full[kb % C::NS], (kb / C::NS) & 1);
       if (MODE >= 3 && (kb & 3) == 0 && q >= 2) ptx::mbar_wait(&acc_empty[buf], ((q >> 1) - 1) & 1);
       ptx::mbar_wait(&b_full[bs], (kb / NB) & 1);
       ptx::tc_fence_after();
       if (ptx::elect_one()) {
-        tc_mma_stage2<64>(tmem + C::A_TMEM + 64 * (kb & 3), tmem + buf * C::ACC_COLS,
+        tc_mma_stage2<64>(tmem + C::A_TMEM + 64 * (kb % C::NS), tmem + buf * C::ACC_COLS,
                           bdesc0 + (uint64_t)((bs * C::B_STAGE) >> 4), (kb & 3) == 0);
         ptx::mma2_commit_both(&b_empty[bs]);
-        if (MODE >= 2) ptx::mma2_commit_both(&kb_empty[kb & 3]);
+        if (MODE >= 2) ptx::mma2_commit_both(&kb_empty[kb % C::NS]);
         if (MODE >= 3 && (kb & 3) == 3) ptx::mma2_commit_both(&acc_full[buf]);
       }
       __syncwarp();
@@ -208,16 +219,21 @@ int main() {
   cudaFuncSetAttribute(pipe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(pipe<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pipe<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pipe<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   pipe<0><<<148, 512, smem>>>(map, amap, 4096, n, d);
   pipe<1><<<148, 512, smem>>>(map, amap, 4096, n, d);
   pipe<2><<<148, 512, smem>>>(map, amap, 4096, n, d);
   pipe<3><<<148, 512, smem>>>(map, amap, 4096, n, d);
   pipe<4><<<148, 512, smem>>>(map, amap, 4096, n, d);
   pipe<5><<<148, 512, smem>>>(map, amap, 4096, n, d);
+  pipe<6><<<148, 512, smem>>>(map, amap, 4096, n, d);
+  pipe<7><<<148, 512, smem>>>(map, amap, 4096, n, d);
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(h, d, 64, cudaMemcpyDeviceToHost);
   printf("%s: MMA cycles per K block: with pair-TMA B stream %llu, without B loads %llu, B stream + converter"
-         " TMEM stages %llu, + promoters %llu, + converter loads/split %llu, + A TMA ring from HBM %llu (ideal 384)\n",
-         cudaGetErrorString(e), h[0], h[1], h[2], h[3], h[4], h[5]);
+         " TMEM stages %llu, + promoters %llu, + converter loads/split %llu, + A TMA ring from HBM %llu,"
+         " H-style column loads %llu, A TMA ring from L2 %llu (ideal 384)\n",
+         cudaGetErrorString(e), h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
   return 0;
 }
