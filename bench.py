@@ -180,12 +180,15 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def profile_traffic(rows: float):
+def profile_traffic(rows: float, config: str):
     """dram read+write bytes of the pass kernel over `rows` rows, scaled from the
-    committed ncu --set full capture (profiles/ncu_summary.json)."""
+    committed ncu --set full capture (profiles/ncu_summary.json) of the same config."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
-            return json.load(fh)["dram_bytes_per_row"] * rows
+            prof = json.load(fh)
+        if prof.get("config", "cfg2") != config:
+            return None
+        return prof["dram_bytes_per_row"] * rows
     except Exception:
         return None
 
@@ -261,7 +264,7 @@ def run_ours(args):
     pass_ms = kern_ms / max(1, args.steps)
     pass_bytes = m * n * 4
     flops = 4.0 * m * n * l
-    used_tc = (args.precision in ("auto", "tc")) and l <= 128
+    used_tc = sk.precision == "tc"
     if used_tc:
         peak_tf = bf16_peak / 2.0 / 3.0   # 3xTF32: tf32 = bf16/2, three products
         peak_desc = "3xTF32 effective = measured bf16 burst / 2 (tf32) / 3 (products)"
@@ -279,7 +282,7 @@ def run_ours(args):
         roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": achieved_gbs / hbm_peak}
     roofline.update({
-        "traffic": profile_traffic(m) if used_tc else None,
+        "traffic": profile_traffic(m, args.config) if used_tc else None,
         "peak_kind": peak_kind, "peak_desc": peak_desc,
         "kernel": "tc_pass_kernel (persistent, CTA pairs; G + H + column sums of all chunks)" if used_tc
                   else "sketch chunk: simt_g_kernel + simt_h_kernel + colsum",

@@ -115,6 +115,10 @@ int spca_sketch_push(spca_handle_t h, const void *a, int64_t rows, int64_t ld,
 int spca_sketch_push_final(spca_handle_t h, const void *a, int64_t rows, int64_t ld,
                            int64_t first_row, int where);
 
+/* The arithmetic the handle runs: SPCA_PREC_SIMT or SPCA_PREC_TC (what
+ * SPCA_PREC_AUTO resolved to for this dtype, shape and device); -1 on a null handle. */
+int spca_sketch_precision(spca_handle_t h);
+
 /* Start a new pass on the same handle (same n, l, Omega): zero the
  * accumulators and the row counter, keep every allocation. Lets a caller
  * run repeated passes (or a second pass of power_refine with the same Omega)

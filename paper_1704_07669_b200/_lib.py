@@ -38,6 +38,7 @@ SIGNATURES = {
                                    c_int, c_int, c_void_p, c_int64, c_int]),
     "spca_sketch_push": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int]),
     "spca_sketch_push_final": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int]),
+    "spca_sketch_precision": (c_int, [c_void_p]),
     "spca_sketch_reset": (c_int, [c_void_p]),
     "spca_sketch_sync": (c_int, [c_void_p]),
     "spca_sketch_rows": (c_int, [c_void_p, POINTER(c_int64)]),

@@ -412,7 +412,9 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
   if (n > INT32_MAX / 2) return set_err(nullptr, SPCA_ERR_CONFIG, -1, "n too large");
   if (dtype != SPCA_F32 && dtype != SPCA_F64) return set_err(nullptr, SPCA_ERR_CONFIG, -1, "bad dtype %d", dtype);
   if (!omega) return set_err(nullptr, SPCA_ERR_FORMAT, -1, "omega is null");
-  if (precision == SPCA_PREC_AUTO) precision = (dtype == SPCA_F32 && tc_available(device)) ? SPCA_PREC_TC : SPCA_PREC_SIMT;
+  if (precision == SPCA_PREC_AUTO)
+    precision = (dtype == SPCA_F32 && tc_supported_shape(n, l) && tc_available(device)) ? SPCA_PREC_TC
+                                                                                       : SPCA_PREC_SIMT;
   if (precision == SPCA_PREC_TC && dtype != SPCA_F32)
     return set_err(nullptr, SPCA_ERR_CONFIG, -1, "tensor-core path is f32 only (fp64 uses DFMA)");
   if (precision == SPCA_PREC_TC && !tc_supported_shape(n, l))
@@ -619,6 +621,8 @@ int spca_sketch_rows(spca_handle_t h, int64_t *rows_seen) {
 }
 
 int64_t spca_sketch_chunk_rows(spca_handle_t h) { return h ? h->chunk_rows : -1; }
+
+int spca_sketch_precision(spca_handle_t h) { return h ? h->precision : -1; }
 
 int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out, double *colsum_out,
                        int64_t *rows_seen, int out_where) {

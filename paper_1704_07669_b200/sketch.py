@@ -83,6 +83,8 @@ class GpuSketch:
         self.h = handle
         self._keep = []          # host/device sources that must outlive async copies
         self._finished = False
+        # what "auto" resolved to: "tc" (tcgen05 3xTF32) or "simt" (FFMA / DFMA)
+        self.precision = "tc" if self.lib.spca_sketch_precision(self.h) == _PRECISIONS["tc"] else "simt"
 
     # -- pushing ------------------------------------------------------------
     def push(self, values, first_row: int, final: bool = False) -> int:

@@ -59,7 +59,7 @@ pipe(const __grid_constant__ CUtensorMap tW, const __grid_constant__ CUtensorMap
       if (kb >= 6) ptx::mbar_wait(&a_empty[s], ((kb / 6) - 1) & 1);
       if (ptx::elect_one()) {
         ptx::mbar_arrive_expect_tx(&a_full[s], 16384);
-        const int tile = MODE == 7 ? (blockIdx.x % 8) : (blockIdx.x + (kb / (n / 32)) * gridDim.x) % 780;
+        const int tile = MODE >= 7 ? (blockIdx.x % 8) : (blockIdx.x + (kb / (n / 32)) * gridDim.x) % 780;
         const int kk = kb % (n / 32);
         ptx::tma_load_2d(aring + s * 16384, &tA, &a_full[s], kk * 32, tile * 128);
       }
@@ -128,7 +128,7 @@ pipe(const __grid_constant__ CUtensorMap tW, const __grid_constant__ CUtensorMap
           hi[i] = trunc_tf32(v[i]);
           v[i] -= hi[i];
         }
-      } else if (MODE >= 4) {  // converter work: 8 x LDS.128 + split, like the pass kernel
+      } else if (MODE >= 4 && MODE != 8) {  // converter work: 8 x LDS.128 + split, like the pass kernel
 #pragma unroll
         for (int q4 = 0; q4 < 8; ++q4) {
           const float4 x = ptx::lds128(srcrow + ((q4 ^ (t & 7)) << 4));
@@ -158,12 +158,17 @@ pipe(const __grid_constant__ CUtensorMap tW, const __grid_constant__ CUtensorMap
     long long t0 = clock64();
     for (int kb = 0; kb < nkb; ++kb) {
       const int bs = kb % NB, q = kb >> 2, buf = q & 1;
+      unsigned long long *mt = (MODE == 8 && lane == 0) ? out + 16 + 4 * (kb & 1023) : nullptr;
+      if (mt) mt[0] = clock64();
+      if (mt) mt[1] = clock64();
       if (MODE >= 2) ptx::mbar_wait(&kb_full[kb % C::NS], (kb / C::NS) & 1);
+      if (mt) mt[2] = clock64();
       if (MODE >= 3 && (kb & 3) == 0 && q >= 2) ptx::mbar_wait(&acc_empty[buf], ((q >> 1) - 1) & 1);
       ptx::mbar_wait(&b_full[bs], (kb / NB) & 1);
+      if (mt) mt[3] = clock64();
       ptx::tc_fence_after();
       if (ptx::elect_one()) {
-        tc_mma_stage2<64>(tmem + C::A_TMEM + 64 * (kb % C::NS), tmem + buf * C::ACC_COLS,
+        tc_mma_stage2<64>(tmem + C::A_TMEM + 64 * (MODE == 9 ? 0 : kb % C::NS), tmem + buf * C::ACC_COLS,
                           bdesc0 + (uint64_t)((bs * C::B_STAGE) >> 4), (kb & 3) == 0);
         ptx::mma2_commit_both(&b_empty[bs]);
         if (MODE >= 2) ptx::mma2_commit_both(&kb_empty[kb % C::NS]);
@@ -210,8 +215,8 @@ int main() {
   cuuint32_t abox[2] = {32, 128};
   ((EncodeFn)fn)(&amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, abuf, adims, strides, abox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  unsigned long long *d, h[8] = {0};
-  cudaMalloc(&d, 64);
+  unsigned long long *d, h[10] = {0};
+  cudaMalloc(&d, (16 + 4 * 1024) * 8);
   const int smem = NB * TcCfg<64>::B_STAGE + 16384 + 6 * 16384 + 1024;
   cudaFuncSetAttribute(pipe<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(pipe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -221,6 +226,8 @@ int main() {
   cudaFuncSetAttribute(pipe<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(pipe<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(pipe<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pipe<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pipe<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   pipe<0><<<148, 512, smem>>>(map, amap, 4096, n, d);
   pipe<1><<<148, 512, smem>>>(map, amap, 4096, n, d);
   pipe<2><<<148, 512, smem>>>(map, amap, 4096, n, d);
@@ -229,11 +236,14 @@ int main() {
   pipe<5><<<148, 512, smem>>>(map, amap, 4096, n, d);
   pipe<6><<<148, 512, smem>>>(map, amap, 4096, n, d);
   pipe<7><<<148, 512, smem>>>(map, amap, 4096, n, d);
+  pipe<8><<<148, 512, smem>>>(map, amap, 4096, n, d);
+  pipe<9><<<148, 512, smem>>>(map, amap, 4096, n, d);
   cudaError_t e = cudaDeviceSynchronize();
-  cudaMemcpy(h, d, 64, cudaMemcpyDeviceToHost);
+  cudaMemcpy(h, d, 80, cudaMemcpyDeviceToHost);
   printf("%s: MMA cycles per K block: with pair-TMA B stream %llu, without B loads %llu, B stream + converter"
          " TMEM stages %llu, + promoters %llu, + converter loads/split %llu, + A TMA ring from HBM %llu,"
-         " H-style column loads %llu, A TMA ring from L2 %llu (ideal 384)\n",
-         cudaGetErrorString(e), h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
+         " H-style column loads %llu, A TMA ring from L2 %llu, + per-block clock/STG trace %llu,"
+         " MMA reads a fixed A stage %llu (ideal 384)\n",
+         cudaGetErrorString(e), h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
   return 0;
 }

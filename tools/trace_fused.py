@@ -156,3 +156,28 @@ if rows:
     ok = np.all((r > -5000) & (r < 20000), axis=1)
     print("stage chain (cycles, median): conv arrive->MMA issue %d, issue->complete %d, complete->conv arrive(k+NS) %d"
           % tuple(np.median(r[ok], axis=0)))
+
+# MMA waits by block position inside its unit (pair 0): where do the stalls sit?
+def unit_nk(s, n_, R0_, u_):
+    kind, c = kind_of(s, u_)
+    nkb_ = -(-n_ // 32); U = 32
+    S_ = -(-nkb_ // U); kseg_ = -(-nkb_ // S_)
+    if kind == 0:
+        TS = s["T"] * s["S"]
+        # recover segment index b from the unit's position (approximation: full chunks)
+        return kind, None
+    return kind, None
+
+mtall = full2[256 * STRIDE:256 * STRIDE + 4 * 2048].reshape(2048, 4).astype(np.int64)
+valid_m = mtall[:, 0] > 0
+if valid_m.sum() > 100:
+    # unit boundaries: the SPCA_TRACE(ui, 5) stamp is at kb == 0 of each unit; use the gap
+    # structure instead: acc_empty waits happen at kb % 4 == 0; report by (gkb mod 32)
+    waits = np.diff(mtall[:, :4], axis=1)
+    pos = np.arange(2048) % 32
+    for p_ in (0, 1, 2, 3, 4, 8, 16, 31):
+        sel = valid_m & (pos == p_)
+        if sel.sum():
+            w = waits[sel]
+            print(f"  block pos {p_:2d}: mean acc_empty {w[:, 0].mean():6.0f} kb_full {w[:, 1].mean():6.0f} "
+                  f"b_full {w[:, 2].mean():6.0f} cycles")
