@@ -22,7 +22,8 @@ from .errors import (
 )
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspca.so")
+# SPCA_LIB: load a differently-built copy (A/B timing of build variants)
+LIB_PATH = os.environ.get("SPCA_LIB") or os.path.join(HERE, "libspca.so")
 
 SPCA_F32, SPCA_F64 = 0, 1
 PREC_AUTO, PREC_SIMT, PREC_TC = 0, 1, 2

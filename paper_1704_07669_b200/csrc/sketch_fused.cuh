@@ -209,6 +209,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ PairBars<LPAD> bars;
   __shared__ double stg_cs[kGroups * 128];  // H: per converter group, column-sum partial
+  __shared__ int stg_bad[128];              // G epilogue: row of the tile has a non-finite partial
   const FusedSched &sc = args.s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -243,6 +244,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     ptx::tma_prefetch(&tWlo);
     ptx::tma_prefetch(&tGT);
   }
+  if (threadIdx.x < 128) stg_bad[threadIdx.x] = 0;
   if (warp == 1) ptx::tmem_alloc2(&bars.tmem_base, kTmemCols);
   ptx::tc_fence_before();
   __syncthreads();
@@ -367,7 +369,9 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           if (mt) mt[1] = clock64();
           ptx::mbar_wait(&bars.kb_full[ks], (gkb / C::NS) & 1);
           if (mt) mt[2] = clock64();
+#if !SPCA_RELAY
           ptx::mbar_wait(&bars.b_full[bs], (gkb / C::NB) & 1);
+#endif
           if (mt) mt[3] = clock64();
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
@@ -375,7 +379,9 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
               tc_mma_stage2<LPAD>(tmem + C::A_TMEM + 64 * ks, tmem + buf * C::ACC_COLS,
                                   bdesc0 + (uint64_t)((bs * C::B_STAGE) >> 4), first);
             ptx::mma2_commit_both(&bars.kb_empty[ks]);
+#if !SPCA_RELAY
             ptx::mma2_commit_both(&bars.b_empty[bs]);
+#endif
             if ((kb % kPromote) == kPromote - 1 || kb == f.nk - 1) ptx::mma2_commit_both(&bars.acc_full[buf]);
           }
           __syncwarp();
@@ -451,7 +457,14 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         // outstanding shared loads against the next TMA write)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&bars.a_empty[s]);
-        if (gk >= C::NS) ptx::mbar_wait(&bars.kb_empty[ts], ((gk / C::NS) - 1) & 1);
+        if (gk >= C::NS) {
+          ptx::mbar_wait(&bars.kb_empty[ts], ((gk / C::NS) - 1) & 1);
+#if SPCA_RELAY
+          // block gk - NS is done: its B stage goes back to this CTA's B producer
+          // (one arrival per block: lane 0 of the group's first warp)
+          if (t == 0) ptx::mbar_arrive(&bars.b_empty[(gk - C::NS) % C::NB]);
+#endif
+        }
         if (ctr) ctr[2] = clock64();
         ptx::tc_fence_after();
         const uint32_t tst = lane_base + C::A_TMEM + 64 * ts;
@@ -462,6 +475,11 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         if (ctr) ctr[3] = clock64();
         ptx::tmem_wait_st();
         if (ctr) ctr[4] = clock64();
+#if SPCA_RELAY
+        // the leader's converters also vouch for the block's B stage (both CTAs'
+        // halves complete on the leader's barrier): the MMA warp waits on kb_full only
+        if (rank == 0) ptx::mbar_wait(&bars.b_full[gk % C::NB], (gk / C::NB) & 1);
+#endif
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(kbfull_l + 8 * ts);
@@ -530,7 +548,6 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
   } else if (warp >= C::EPI_BASE / 32) {  // --------------------------------- epilogue
     const int e = threadIdx.x - C::EPI_BASE;  // row (G) / column (H) of the tile
     constexpr int NQ = LPAD / 4;             // 16-byte chunks per row
-    const uint32_t srow = ptx::smem_u32(smem + C::STG_OFF + e * LPAD * 4);
     const int twoT = 2 * sc.T;
     int ui = 0;
 #pragma unroll 1
@@ -547,26 +564,34 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         const int gslot = f.c % kSlots;
         const bool real = tile < fused_real_tiles(sc, f.c);
         const int row = tile * 128 + e;
-        float chk = 0.f;
+        bool flagged = false;
         if (real) {
           // the partial slot was last used kSlots chunks ago: its slices must be reduced
           if (f.c >= kSlots && e == 0) ptx::spin_until_geq(&args.ready[f.c - kSlots], sc.nt * sc.S);
           ptx::named_bar(2, kTcEpi);
+          // copy the staged tile to its partial slot, NQ consecutive lanes per row
+          // (each warp store covers whole rows: coalesced)
           float4 *gp = reinterpret_cast<float4 *>(
-              args.gpart + ((((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 + e) * LPAD);
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-            const float4 x = ptx::lds128(srow + ((q ^ (e & 7)) << 4));
-            chk = fmaf(x.x, 0.f, fmaf(x.y, 0.f, fmaf(x.z, 0.f, fmaf(x.w, 0.f, chk))));
-            gp[q] = x;
+              args.gpart + (((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 * LPAD);
+          const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF);
+#pragma unroll 4
+          for (int it = e; it < 128 * NQ; it += kTcEpi) {
+            const int r = it / NQ, q = it % NQ;
+            const float4 x = ptx::lds128(stg0 + r * LPAD * 4 + ((q ^ (r & 7)) << 4));
+            const float chk = fmaf(x.x, 0.f, fmaf(x.y, 0.f, fmaf(x.z, 0.f, x.w * 0.f)));
+            if (!(chk == 0.f)) stg_bad[r] = 1;
+            gp[it] = x;
           }
+          ptx::named_bar(2, kTcEpi);
+          flagged = stg_bad[e] != 0;
+          stg_bad[e] = 0;
         }
         ptx::mbar_arrive(&bars.epi_empty);
         if (real) {
           // a non-finite input makes its G row non-finite: confirm on the raw row
           // segment (a huge finite row may also overflow G; the reference only
           // rejects non-finite values)
-          if (!(chk == 0.f) && row < f.rows) {
+          if (flagged && row < f.rows) {
             const int64_t grow = (int64_t)f.c * sc.R0 + row;
             const float *ar = args.a + grow * args.lda;
             const int k1 = min(args.n, (f.k0 + f.nk) * 32);
@@ -626,17 +651,20 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         if (real) {
           if (e == 0) ptx::spin_until_geq(&args.hseq[tile], seq);
           ptx::named_bar(2, kTcEpi);
-          if (col < args.n) {
-            float4 *hp = reinterpret_cast<float4 *>(args.hpart + (int64_t)col * LPAD);
+          {  // H rows of the tile's columns, NQ consecutive lanes per column (coalesced)
+            float4 *hp = reinterpret_cast<float4 *>(args.hpart + (int64_t)tile * 128 * LPAD);
             const bool overwrite = !args.accumulate && seq == 0;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-              float4 w = ptx::lds128(srow + ((q ^ (e & 7)) << 4));
+            const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF);
+            const int items = min(128, args.n - tile * 128) * NQ;
+#pragma unroll 4
+            for (int it = e; it < items; it += kTcEpi) {
+              const int r = it / NQ, q = it % NQ;
+              float4 w = ptx::lds128(stg0 + r * LPAD * 4 + ((q ^ (r & 7)) << 4));
               if (!overwrite) {
-                const float4 o = __ldcg(hp + q);
+                const float4 o = __ldcg(hp + it);
                 w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
               }
-              hp[q] = w;
+              hp[it] = w;
             }
           }
           csv = stg_cs[e] + stg_cs[128 + e];

@@ -68,8 +68,13 @@ struct TcCfg {
   // l_pad = 64: "stacked" form, two MMAs per 8-deep step: A_hi [W_hi | W_lo]
   // (N = 128) and A_lo W_hi (N = 64) into the first half; the accumulator is
   // 128 columns and promotion adds its halves. l_pad = 128: three N = 128 MMAs.
+// converters relay the B ring (wait b_full before arriving, release b_empty
+// after the block's MMAs): the MMA warp waits and commits once per K block
+#ifndef SPCA_RELAY
+#define SPCA_RELAY 1
+#endif
 #ifndef SPCA_STACKED_64
-#define SPCA_STACKED_64 1
+#define SPCA_STACKED_64 0
 #endif
   static constexpr bool STACKED = LPAD == 64 && SPCA_STACKED_64;
   static constexpr int ACC_COLS = STACKED ? 128 : LPAD;  // one accumulator

@@ -31,7 +31,7 @@ template <int G, int WITH_B, int STAGES, int ABOX>
 __global__ void __launch_bounds__(32, 1)
 bench(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, int atiles, int nkb,
       int iters, unsigned long long *out) {
-  constexpr int A_BYTES = 16384 * ABOX, STAGE = A_BYTES + (WITH_B ? B_BYTES : 0);
+  constexpr int A_BYTES = 16384 * (ABOX == 1 ? 1 : 2), STAGE = A_BYTES + (WITH_B ? B_BYTES : 0);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[STAGES], empty[STAGES];
@@ -60,6 +60,13 @@ bench(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensor
     const int kb = k % nkb, tile = (blockIdx.x + (k / nkb) * gridDim.x) % atiles;
     if (ABOX == 1)
       ptx::tma_load_2d(dst, &amap, &full[s], kb * 32, tile * 128);
+    else if (ABOX == 4)
+      ptx::tma_load_2d(dst, &amap, &full[s], kb * 32, (tile * 128) % (atiles * 128 - 128));
+    else if (ABOX == 3)
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+          ::"r"(ptx::smem_u32(dst)), "l"(&amap), "r"(ptx::smem_u32(&full[s])), "r"(0), "r"(tile * 128),
+          "r"((kb * 2) % (nkb - 2)) : "memory");
     else
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
@@ -96,7 +103,7 @@ typedef CUresult (*EncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, voi
 
 template <int G, int WITH_B, int STAGES, int ABOX>
 void run(EncodeFn enc, float *a, float *b, int n, int arows) {
-  constexpr int A_BYTES = 16384 * ABOX, STAGE = A_BYTES + (WITH_B ? B_BYTES : 0);
+  constexpr int A_BYTES = 16384 * (ABOX == 1 ? 1 : 2), STAGE = A_BYTES + (WITH_B ? B_BYTES : 0);
   CUtensorMap amap, bmap;
   cuuint32_t es[3] = {1, 1, 1};
   if (ABOX == 1) {
@@ -104,6 +111,17 @@ void run(EncodeFn enc, float *a, float *b, int n, int arows) {
     cuuint32_t abox[2] = {32, 128};
     enc(&amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, a, adims, astr, abox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (ABOX == 4) {
+    cuuint64_t adims[2] = {(cuuint64_t)n, (cuuint64_t)arows}, astr[1] = {(cuuint64_t)n * 4};
+    cuuint32_t abox[2] = {32, 256};
+    enc(&amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, a, adims, astr, abox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (ABOX == 3) {
+    cuuint64_t adims[3] = {32, (cuuint64_t)arows, (cuuint64_t)n / 32}, astr[2] = {(cuuint64_t)n * 4, 128};
+    cuuint32_t abox[3] = {32, 128, 2};
+    CUresult r = enc(&amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a, adims, astr, abox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r) printf("encode 3d (k-block outer) failed %d\n", (int)r);
   } else {
     cuuint64_t adims[3] = {32, (cuuint64_t)n / 32, (cuuint64_t)arows}, astr[2] = {128, (cuuint64_t)n * 4};
     cuuint32_t abox[3] = {32, ABOX, 128};
@@ -180,5 +198,10 @@ int main(int argc, char **argv) {
   if (which < 0 || which == 10) run<1, 0, 6, 1>(enc, a, b, n, hrows);
   if (which < 0 || which == 11) run<1, 0, 6, 2>(enc, a, b, n, hrows);
   if (which < 0 || which == 12) run<1, 1, 6, 1>(enc, a, b, n, hrows);
+  if (which < 0 || which == 13) run<1, 0, 6, 3>(enc, a, b, n, arows);
+  if (which < 0 || which == 14) run<1, 0, 6, 4>(enc, a, b, n, arows);
+  if (which < 0 || which == 15) run<1, 1, 5, 2>(enc, a, b, n, arows);
+  if (which < 0 || which == 16) run<1, 1, 5, 3>(enc, a, b, n, arows);
+  if (which < 0 || which == 17) run<1, 0, 6, 3>(enc, a, b, n, hrows);
   return 0;
 }

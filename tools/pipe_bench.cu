@@ -192,11 +192,21 @@ typedef CUresult (*EncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, voi
                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int main() {
+__global__ void fill_rand(float *p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t x = (uint32_t)(i * 2654435761u) ^ (uint32_t)(i >> 32) ^ 0x9e3779b9u;
+    x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+    p[i] = ((float)(x & 0xffffff) / 16777216.f - 0.5f) * 3.4f;
+  }
+}
+
+int main(int argc, char **argv) {
+  const bool rnd = argc > 1;
   const int n = 10000;
   float *w;
   cudaMalloc(&w, (size_t)64 * n * 4);
   cudaMemset(w, 0, (size_t)64 * n * 4);
+  if (rnd) fill_rand<<<1184, 256>>>(w, (size_t)64 * n);
   void *fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
@@ -210,6 +220,7 @@ int main() {
   float *abuf;
   cudaMalloc(&abuf, (size_t)100000 * n * 4);
   cudaMemset(abuf, 0, (size_t)100000 * n * 4);
+  if (rnd) fill_rand<<<1184, 256>>>(abuf, (size_t)100000 * n);
   CUtensorMap amap;
   cuuint64_t adims[2] = {(cuuint64_t)n, 100000};
   cuuint32_t abox[2] = {32, 128};
@@ -240,10 +251,10 @@ int main() {
   pipe<9><<<148, 512, smem>>>(map, amap, 4096, n, d);
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(h, d, 80, cudaMemcpyDeviceToHost);
-  printf("%s: MMA cycles per K block: with pair-TMA B stream %llu, without B loads %llu, B stream + converter"
+  printf("%s data %s: MMA cycles per K block: with pair-TMA B stream %llu, without B loads %llu, B stream + converter"
          " TMEM stages %llu, + promoters %llu, + converter loads/split %llu, + A TMA ring from HBM %llu,"
          " H-style column loads %llu, A TMA ring from L2 %llu, + per-block clock/STG trace %llu,"
          " MMA reads a fixed A stage %llu (ideal 384)\n",
-         cudaGetErrorString(e), h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
+         cudaGetErrorString(e), rnd ? "random" : "zero", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
   return 0;
 }
