@@ -195,7 +195,7 @@ struct PairBars {
   uint64_t b_empty[C::NB];                 // each CTA: MMAs done with the B stage
   uint64_t acc_full[2];                    // each CTA: accumulator period complete
   uint64_t acc_empty[2];                   // leader: both CTAs folded the period
-  uint64_t epi_full, epi_empty;            // local: converters <-> epilogue staging
+  uint64_t epi_full[2], epi_empty[2];      // local: converters/promoters <-> epilogue staging
   uint32_t tmem_base;
 };
 
@@ -208,7 +208,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ PairBars<LPAD> bars;
-  __shared__ double stg_cs[kGroups * 128];  // H: per converter group, column-sum partial
+  __shared__ double stg_cs[C::NSTG][kGroups * 128];  // H: per converter group, column-sum partial
   __shared__ int stg_bad[128];              // G epilogue: row of the tile has a non-finite partial
   const FusedSched &sc = args.s;
 
@@ -235,8 +235,10 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       ptx::mbar_init(&bars.acc_full[s], 1);
       ptx::mbar_init(&bars.acc_empty[s], 2 * C::PROMO_WARPS);
     }
-    ptx::mbar_init(&bars.epi_full, kTcConv + 32 * C::PROMO_WARPS);  // converters (column sums) + promoters
-    ptx::mbar_init(&bars.epi_empty, kTcEpi);
+    for (int s = 0; s < C::NSTG; ++s) {
+      ptx::mbar_init(&bars.epi_full[s], kTcConv + 32 * C::PROMO_WARPS);  // converters (column sums) + promoters
+      ptx::mbar_init(&bars.epi_empty[s], kTcEpi);
+    }
     ptx::fence_mbar_init();
     ptx::tma_prefetch(&tAg);
     ptx::tma_prefetch(&tAh);
@@ -488,9 +490,10 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       gkb += f.nk;
       if (ct == 0) SPCA_TRACE(ui, 1);
       // hand the column-sum partial to the epilogue with the unit's staging
-      if (ui >= 1) ptx::mbar_wait(&bars.epi_empty, (ui - 1) & 1);
-      if (f.kind == 1) stg_cs[grp * 128 + t] = (double)cs - (double)cc;
-      ptx::mbar_arrive(&bars.epi_full);
+      const int sb = ui % C::NSTG;  // staging buffer of this unit
+      if (ui >= C::NSTG) ptx::mbar_wait(&bars.epi_empty[sb], ((ui / C::NSTG) - 1) & 1);
+      if (f.kind == 1) stg_cs[sb][grp * 128 + t] = (double)cs - (double)cc;
+      ptx::mbar_arrive(&bars.epi_full[sb]);
     }
   } else if (warp >= C::PROMO_BASE / 32 && warp < C::EPI_BASE / 32) {  // ----- promoters
     const int pt = threadIdx.x - C::PROMO_BASE;
@@ -535,15 +538,16 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       }
       if (pt == 0) SPCA_TRACE(ui, 6);
       // stage the result for the epilogue warps (16-byte chunks XOR-swizzled by row)
-      if (ui >= 1) ptx::mbar_wait(&bars.epi_empty, (ui - 1) & 1);
+      const int sb = ui % C::NSTG;  // staging buffer of this unit
+      if (ui >= C::NSTG) ptx::mbar_wait(&bars.epi_empty[sb], ((ui / C::NSTG) - 1) & 1);
       if (pt == 0) SPCA_TRACE(ui, 2);
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int q = c0 / 4 + i;
-        ptx::st_shared_v4(stg_row + ((q ^ (t & 7)) << 4),
+        ptx::st_shared_v4(stg_row + sb * C::STG_BYTES + ((q ^ (t & 7)) << 4),
                           make_float4(racc[4 * i], racc[4 * i + 1], racc[4 * i + 2], racc[4 * i + 3]));
       }
-      ptx::mbar_arrive(&bars.epi_full);
+      ptx::mbar_arrive(&bars.epi_full[sb]);
     }
   } else if (warp >= C::EPI_BASE / 32) {  // --------------------------------- epilogue
     const int e = threadIdx.x - C::EPI_BASE;  // row (G) / column (H) of the tile
@@ -554,10 +558,11 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
       const FusedUnit f = fused_decode(sc, u);
       const int tile = 2 * f.a + (int)rank;
-      ptx::mbar_wait(&bars.epi_full, ui & 1);
+      const int sb = ui % C::NSTG;  // staging buffer of this unit
+      ptx::mbar_wait(&bars.epi_full[sb], (ui / C::NSTG) & 1);
       if (e == 0) SPCA_TRACE(ui, 3);
       if (args.dbg & 16384) {  // profiling knob: no epilogue work (results are garbage)
-        ptx::mbar_arrive(&bars.epi_empty);
+        ptx::mbar_arrive(&bars.epi_empty[sb]);
         continue;
       }
       if (f.kind == 0) {  // ---------------------------------- G epilogue
@@ -573,7 +578,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           // (each warp store covers whole rows: coalesced)
           float4 *gp = reinterpret_cast<float4 *>(
               args.gpart + (((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 * LPAD);
-          const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF);
+          const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF + sb * C::STG_BYTES);
 #pragma unroll 4
           for (int it = e; it < 128 * NQ; it += kTcEpi) {
             const int r = it / NQ, q = it % NQ;
@@ -586,7 +591,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           flagged = stg_bad[e] != 0;
           stg_bad[e] = 0;
         }
-        ptx::mbar_arrive(&bars.epi_empty);
+        ptx::mbar_arrive(&bars.epi_empty[sb]);
         if (real) {
           // a non-finite input makes its G row non-finite: confirm on the raw row
           // segment (a huge finite row may also overflow G; the reference only
@@ -654,7 +659,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           {  // H rows of the tile's columns, NQ consecutive lanes per column (coalesced)
             float4 *hp = reinterpret_cast<float4 *>(args.hpart + (int64_t)tile * 128 * LPAD);
             const bool overwrite = !args.accumulate && seq == 0;
-            const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF);
+            const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF + sb * C::STG_BYTES);
             const int items = min(128, args.n - tile * 128) * NQ;
 #pragma unroll 4
             for (int it = e; it < items; it += kTcEpi) {
@@ -667,9 +672,9 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
               hp[it] = w;
             }
           }
-          csv = stg_cs[e] + stg_cs[128 + e];
+          csv = stg_cs[sb][e] + stg_cs[sb][128 + e];
         }
-        ptx::mbar_arrive(&bars.epi_empty);
+        ptx::mbar_arrive(&bars.epi_empty[sb]);
         if (real) {
           if (col < args.n) {
             if (args.carry) {

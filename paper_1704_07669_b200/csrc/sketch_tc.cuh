@@ -62,20 +62,26 @@ constexpr int kPromote = 4;     // K blocks per accumulator period
 // the same rows of W_lo (rank r). l_pad = 64 keeps the accumulators at 64
 // columns, leaving TMEM for six A operand stages: the MMA completion latency
 // needs that depth when every K block's operand is produced on chip.
+// converters relay the B ring (wait b_full before arriving, release b_empty
+// after the block's MMAs): the MMA warp waits and commits once per K block
+#ifndef SPCA_RELAY
+#define SPCA_RELAY 1
+#endif
+// l_pad = 64 MMA form: 0 = three N = 64 MMAs per step (default, measured
+// faster: 8 KB B stages, six TMEM operand stages), 1 = stacked N = 128 + 64
+#ifndef SPCA_STACKED_64
+#define SPCA_STACKED_64 0
+#endif
+// epilogue staging buffers for l_pad = 64. Two (at the cost of two A stages)
+// measured no faster and failed 1 run in 8 (a launch fault not yet understood):
+// kept at one; the staging code is written for either.
+#define SPCA_NSTG_64 1
 template <int LPAD>
 struct TcCfg {
   static_assert(LPAD == 64 || LPAD == 128, "tensor-core path covers l <= 128");
   // l_pad = 64: "stacked" form, two MMAs per 8-deep step: A_hi [W_hi | W_lo]
   // (N = 128) and A_lo W_hi (N = 64) into the first half; the accumulator is
   // 128 columns and promotion adds its halves. l_pad = 128: three N = 128 MMAs.
-// converters relay the B ring (wait b_full before arriving, release b_empty
-// after the block's MMAs): the MMA warp waits and commits once per K block
-#ifndef SPCA_RELAY
-#define SPCA_RELAY 1
-#endif
-#ifndef SPCA_STACKED_64
-#define SPCA_STACKED_64 0
-#endif
   static constexpr bool STACKED = LPAD == 64 && SPCA_STACKED_64;
   static constexpr int ACC_COLS = STACKED ? 128 : LPAD;  // one accumulator
   static constexpr int NS = (kTmemCols - 2 * ACC_COLS) / 64;  // TMEM A operand stages
@@ -92,11 +98,12 @@ struct TcCfg {
   // Otherwise: W_hi rows [r*l_pad/2, (r+1)*l_pad/2) then the same rows of W_lo.
   static constexpr uint32_t B_STAGE = STACKED ? 3 * BH_BYTES : 2 * BH_BYTES;
   static constexpr int NB = STACKED ? 7 : (LPAD == 64 ? 8 : 4);  // B ring (12 | 8 | 16 KB stages)
-  static constexpr int NA = STACKED ? 6 : (LPAD == 64 ? 7 : 5);  // raw A ring (16 KB stages)
+  static constexpr int NSTG = LPAD == 64 ? SPCA_NSTG_64 : 1;  // epilogue staging buffers
+  static constexpr int NA = STACKED ? 6 : (LPAD == 64 ? (NSTG == 2 ? 5 : 7) : 5);  // raw A ring (16 KB stages)
   static constexpr uint32_t STG_BYTES = 128 * LPAD * 4;  // epilogue staging tile
   static constexpr uint32_t B_OFF = NA * A_BYTES;
   static constexpr uint32_t STG_OFF = B_OFF + NB * B_STAGE;
-  static constexpr uint32_t SMEM = STG_OFF + STG_BYTES + 1024;
+  static constexpr uint32_t SMEM = STG_OFF + NSTG * STG_BYTES + 1024;
   static constexpr uint32_t A_TMEM = 2 * ACC_COLS;    // first operand column
   static_assert(SMEM <= 227 * 1024 - 4096, "shared memory budget");
 };
