@@ -32,12 +32,14 @@ from .errors import (
 from .streams import (
     ArrayRowStream,
     DeviceRowStream,
+    FileRowStream,
     GeneratorRowStream,
     PassCounter,
     PinnedRowStream,
     RowBlock,
     RowStream,
 )
+from . import matfile
 from .sketch import GpuSketch, SketchState, center_correct, sketch_pass
 from .qb import QbFactor, blocked_qb
 from .linalg import dense_svd, gaussian_matrix, qr_unpivoted, sign_align, solve_rt
@@ -55,7 +57,7 @@ __version__ = "0.1.0"
 __all__ = [
     "ArrayRowStream", "CapabilityError", "ConditioningWarning", "ConfigError", "DataError",
     "DeviceError", "DeviceMemoryError", "DeviceRowStream", "DimensionError", "EmptyStreamError",
-    "FormatError", "GeneratorRowStream", "GpuSketch", "PassCounter", "PcaConfig",
+    "FileRowStream", "FormatError", "GeneratorRowStream", "GpuSketch", "PassCounter", "PcaConfig",
     "PinnedRowStream", "QbFactor", "RankDeficiencyError", "RowBlock", "RowStream", "ScaleError",
     "SingularMatrixError", "SketchState", "StreamFormatError", "StreamPcaError", "TruncatedSvd",
     "as_row_stream", "blocked_qb", "center_correct", "dense_svd", "gaussian_matrix",

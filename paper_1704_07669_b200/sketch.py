@@ -21,6 +21,9 @@ sketch actually used so the post-pass stays consistent with it.
 from __future__ import annotations
 
 import ctypes
+import queue
+import threading
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, replace
 from typing import Optional
 
@@ -29,7 +32,7 @@ import numpy as np
 from . import _lib
 from .device import default_device, is_torch, to_device64, torch_mod
 from .errors import DeviceError, EmptyStreamError, StreamFormatError
-from .streams import PassCounter, has_whole
+from .streams import FileRowStream, PassCounter, has_whole
 
 _PRECISIONS = {"auto": _lib.PREC_AUTO, "simt": _lib.PREC_SIMT, "tc": _lib.PREC_TC}
 
@@ -208,7 +211,14 @@ def run_pass(stream, omega, block_rows=None, compensated=False, precision="auto"
     n, l = om.shape
     sk = GpuSketch(n, om, dtype, precision=precision, device=device,
                    rows_hint=stream.n_rows or 0, compensated=compensated)
-    if has_whole(stream):
+    fs = _file_source(stream)
+    if fs is not None:
+        _push_file(sk, fs)
+        if isinstance(stream, PassCounter):
+            stream.rows_read += fs.n_rows
+            stream.passes_completed += 1
+            stream.pass_in_progress = False
+    elif has_whole(stream):
         kind, mat = stream.whole()
         if mat.shape[0]:
             sk.push(mat, 0, final=True)
@@ -225,6 +235,69 @@ def run_pass(stream, omega, block_rows=None, compensated=False, precision="auto"
                     f"expected (*, {n})")
             sk.push(vals, block.first_row_index)
     return sk
+
+
+def _file_source(stream) -> Optional[FileRowStream]:
+    inner = stream.wrapped if isinstance(stream, PassCounter) else stream
+    return inner if isinstance(inner, FileRowStream) else None
+
+
+def _push_file(sk: GpuSketch, fs: FileRowStream, nbuf: int = 3) -> None:
+    """Stream a matrix file through page-locked buffers: a reader thread fills
+    buffer j % nbuf with parallel positional reads (no host-side copy, the
+    file's element type kept) while the library copies and sketches the
+    previous ones; a buffer is refilled only after the event recorded behind
+    its push on the sketch stream has completed."""
+    torch = torch_mod()
+    lay = fs.layout
+    m, n = lay.rows, lay.cols
+    tdt = torch.float32 if fs.dtype == np.float32 else torch.float64
+    buf_rows = max(1, min(m, fs.buffer_bytes // lay.row_bytes))
+    starts = list(range(0, m, buf_rows))
+    nb = max(1, min(nbuf, len(starts)))
+    bufs = [torch.empty((buf_rows, n), dtype=tdt, pin_memory=True) for _ in range(nb)]
+    views = [b.numpy() for b in bufs]
+    full: queue.Queue = queue.Queue()
+    released: queue.Queue = queue.Queue()
+
+    def reader():
+        try:
+            with ThreadPoolExecutor(fs.read_threads) as pool:
+                for j, start in enumerate(starts):
+                    i = j % nb
+                    if j >= nb:
+                        ri, ev = released.get()
+                        if ri is None:  # the consumer gave up
+                            return
+                        ev.synchronize()
+                    rows = min(buf_rows, m - start)
+                    fs.read_rows_into(views[i], start, rows, pool)
+                    full.put((i, start, rows))
+            full.put(None)
+        except BaseException as exc:  # handed to the consumer
+            full.put(exc)
+
+    th = threading.Thread(target=reader, name="spca-file-reader", daemon=True)
+    th.start()
+    try:
+        while True:
+            item = full.get()
+            if item is None:
+                break
+            if isinstance(item, BaseException):
+                raise item
+            i, start, rows = item
+            sk.push(bufs[i][:rows], start, final=start + rows == m)
+            ev = torch.cuda.Event()
+            ev.record(sk.stream)
+            released.put((i, ev))
+    except BaseException:
+        released.put((None, None))
+        raise
+    finally:
+        th.join(timeout=60)
+    if m == 0:
+        sk.push(np.empty((0, n), dtype=fs.dtype), 0, final=True)
 
 
 def sketch_pass(

@@ -399,3 +399,48 @@ def test_final_push_matches_push_then_finish(precision):
     assert out[0][3] == out[1][3] == 5000
     for x, y in zip(out[0][:3], out[1][:3]):
         assert np.array_equal(x, y)
+
+
+# ------------------------------------------------------- disk streaming (§8 f)
+@pytest.mark.parametrize("dtype,precision", [("float64", "auto"), ("float32", "simt"), ("float32", "tc")])
+@pytest.mark.parametrize("header", [True, False])
+def test_file_stream_matches_array(tmp_path, dtype, precision, header):
+    """FileRowStream through page-locked buffers == the same rows handed over
+    in memory, bitwise (canonical chunking), for several buffer sizes."""
+    if precision == "tc" and not _tc_ok():
+        pytest.skip("no tensor-core path")
+    m, n, l = 5000, 300, 24
+    a = O.gaussian(m, n, seed=21).astype(dtype)
+    om = O.gaussian(n, l, seed=22)
+    p = tmp_path / "a.mat"
+    P.matfile.write_matrix(p, a, dtype=dtype, header=header)
+    want = P.sketch_pass(P.ArrayRowStream(a), om, precision=precision)
+    kw = {} if header else dict(rows=m, cols=n, dtype=dtype)
+    for buf in (1 << 20, 333 * n * a.itemsize, 64 << 20):
+        fs = P.FileRowStream(p, buffer_bytes=buf, **kw)
+        got = P.sketch_pass(fs, om, precision=precision)
+        assert got.rows_seen == m
+        for x, y in ((got.g, want.g), (got.h, want.h), (got.col_sums, want.col_sums)):
+            assert np.array_equal(x, y)
+        assert fs.bytes_read == m * n * a.itemsize
+
+
+def test_file_stream_nonfinite_row_and_pca(tmp_path):
+    m, n = 3000, 64
+    a = O.gaussian(m, n, seed=23).astype(np.float32)
+    a[2222, 5] = np.inf
+    p = tmp_path / "bad.spca"
+    P.matfile.write_matrix(p, a, dtype="float32")
+    with pytest.raises(P.DataError) as ei:
+        P.sketch_pass(P.FileRowStream(p, buffer_bytes=200 * n * 4), O.gaussian(n, 8, seed=1))
+    assert ei.value.row == 2222
+    # end to end through single_pass_pca and the pass counter
+    a[2222, 5] = 0.0
+    P.matfile.write_matrix(p, a, dtype="float32")
+    cfg = P.PcaConfig(k=5, oversample=5, block_size=5, seed=3)
+    res_f = P.single_pass_pca(P.FileRowStream(p, buffer_bytes=1 << 20), cfg)
+    res_a = P.single_pass_pca(a, cfg)
+    assert np.array_equal(res_f.s, res_a.s)
+    pc = P.PassCounter(P.FileRowStream(p))
+    P.sketch_pass(pc, O.gaussian(n, 8, seed=1))
+    assert pc.passes_completed == 1 and pc.rows_read == m
