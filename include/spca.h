@@ -158,6 +158,15 @@ int spca_center_correct(spca_handle_t h, int64_t m_total, const double *gsum,
 /* Column sums of the finished G (l values, float64) — for center_correct. */
 int spca_g_colsum(spca_handle_t h, double *out, int out_where);
 
+/* normalize_rows (sketch.py:142-153) on device rows: each row minus its
+ * mean, divided by its Euclidean norm (a constant row becomes zero), fp64
+ * arithmetic; dtype SPCA_F32 / SPCA_F64 for both src and dst (device
+ * pointers, row strides in elements; dst may equal src). Enqueued on
+ * `stream` (a cudaStream_t, NULL = legacy default); errors are reported
+ * through spca_last_error(NULL, ...). */
+int spca_normalize_rows(const void *src, int64_t rows, int64_t n, int64_t ld_src, void *dst,
+                        int64_t ld_dst, int dtype, void *stream);
+
 /* Last error of the handle (or of the calling thread when h == NULL):
  * code, offending absolute row (or -1) and a message. */
 int spca_last_error(spca_handle_t h, int *code, int64_t *bad_row, char *msg,

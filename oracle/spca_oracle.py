@@ -25,7 +25,7 @@ __all__ = [
     "RANK_TOL", "STREAM_SKETCH", "STREAM_FACTOR_U", "STREAM_FACTOR_V", "STREAM_REPAIR",
     "OracleError", "OracleDataError", "OracleFormatError", "OracleEmptyError",
     "OracleDeficiencyError", "OracleSingularError",
-    "sketch_width", "gaussian", "row_blocks", "oracle_sketch", "oracle_center",
+    "sketch_width", "gaussian", "row_blocks", "oracle_sketch", "oracle_center", "oracle_normalize_rows",
     "qr_pos", "solve_upper_t", "thin_svd", "align_signs", "oracle_qb",
     "oracle_single_pass", "OracleSketch", "OracleQb", "OracleSvd",
     "synth_lowrank_plus_noise", "reference_synth_matrix", "subspace_angle",
@@ -162,6 +162,15 @@ def oracle_sketch(
         seen += vals.shape[0]
     g = np.vstack(pieces) if pieces else np.zeros((0, l))
     return OracleSketch(g=g, h=h, col_sums=cs, rows_seen=seen)
+
+
+def oracle_normalize_rows(vals: np.ndarray) -> np.ndarray:
+    """sketch.py:142-153: subtract each row's mean, divide by the centered
+    row's Euclidean norm; a zero norm divides by 1 (constant rows -> 0)."""
+    x = np.asarray(vals, dtype=np.float64)
+    c = x - x.mean(axis=1, keepdims=True)
+    nrm = np.sqrt((c * c).sum(axis=1, keepdims=True))
+    return c / np.where(nrm == 0.0, 1.0, nrm)
 
 
 def oracle_center(st: OracleSketch, omega: np.ndarray) -> OracleSketch:

@@ -40,7 +40,14 @@ from .streams import (
     RowStream,
 )
 from . import matfile
-from .sketch import GpuSketch, SketchState, center_correct, sketch_pass
+from .sketch import (
+    GpuSketch,
+    NormalizedRowStream,
+    SketchState,
+    center_correct,
+    normalize_rows,
+    sketch_pass,
+)
 from .qb import QbFactor, blocked_qb
 from .linalg import dense_svd, gaussian_matrix, qr_unpivoted, sign_align, solve_rt
 from .algorithms import (
@@ -54,12 +61,20 @@ from .algorithms import (
 
 __version__ = "0.1.0"
 
+
+def __getattr__(name):
+    # the scikit-learn front end is imported on first use (sklearn is slow to import)
+    if name == "SinglePassPCA":
+        from .estimator import SinglePassPCA
+        return SinglePassPCA
+    raise AttributeError(name)
+
 __all__ = [
     "ArrayRowStream", "CapabilityError", "ConditioningWarning", "ConfigError", "DataError",
     "DeviceError", "DeviceMemoryError", "DeviceRowStream", "DimensionError", "EmptyStreamError",
-    "FileRowStream", "FormatError", "GeneratorRowStream", "GpuSketch", "PassCounter", "PcaConfig",
+    "FileRowStream", "FormatError", "GeneratorRowStream", "NormalizedRowStream", "normalize_rows", "GpuSketch", "PassCounter", "PcaConfig",
     "PinnedRowStream", "QbFactor", "RankDeficiencyError", "RowBlock", "RowStream", "ScaleError",
-    "SingularMatrixError", "SketchState", "StreamFormatError", "StreamPcaError", "TruncatedSvd",
+    "SinglePassPCA", "SingularMatrixError", "SketchState", "StreamFormatError", "StreamPcaError", "TruncatedSvd",
     "as_row_stream", "blocked_qb", "center_correct", "dense_svd", "gaussian_matrix",
     "power_refine", "principal_components", "qr_unpivoted", "sign_align", "single_pass_pca",
     "sketch_pass", "solve_rt", "__version__",

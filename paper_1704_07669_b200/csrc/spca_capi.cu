@@ -103,6 +103,7 @@ int ensure_g(spca_sketch *h, int64_t rows_needed) {
 
 // tensor-core path (uses set_err / CK / grid_for above)
 #include "sketch_fused.cuh"
+#include "normalize.cuh"
 #include "tc_host.cuh"
 
 namespace {
@@ -699,6 +700,29 @@ int spca_g_colsum(spca_handle_t h, double *out, int out_where) {
                         h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   cudaFree(d);
+  return SPCA_OK;
+}
+
+int spca_normalize_rows(const void *src, int64_t rows, int64_t n, int64_t ld_src, void *dst, int64_t ld_dst,
+                        int dtype, void *stream) {
+  if (rows < 0 || n < 1 || ld_src < n || ld_dst < n)
+    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "normalize_rows: bad shape %lld x %lld (ld %lld, %lld)",
+                   (long long)rows, (long long)n, (long long)ld_src, (long long)ld_dst);
+  if (rows == 0) return SPCA_OK;
+  if (!src || !dst) return set_err(nullptr, SPCA_ERR_STATE, -1, "normalize_rows: null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)std::min<int64_t>(rows, 148 * 8);
+  if (dtype == SPCA_F32) {
+    normalize_rows_kernel<float><<<grid, kNormThreads, 0, st>>>((const float *)src, rows, n, ld_src,
+                                                                 (float *)dst, ld_dst);
+  } else if (dtype == SPCA_F64) {
+    normalize_rows_kernel<double><<<grid, kNormThreads, 0, st>>>((const double *)src, rows, n, ld_src,
+                                                                  (double *)dst, ld_dst);
+  } else {
+    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "normalize_rows: bad dtype %d", dtype);
+  }
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(nullptr, SPCA_ERR_CUDA, -1, "normalize_rows launch: %s", cudaGetErrorString(e));
   return SPCA_OK;
 }
 

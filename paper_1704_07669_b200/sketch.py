@@ -32,7 +32,7 @@ import numpy as np
 from . import _lib
 from .device import default_device, is_torch, to_device64, torch_mod
 from .errors import DeviceError, EmptyStreamError, StreamFormatError
-from .streams import FileRowStream, PassCounter, has_whole
+from .streams import FileRowStream, PassCounter, RowBlock, RowStream, has_whole
 
 _PRECISIONS = {"auto": _lib.PREC_AUTO, "simt": _lib.PREC_SIMT, "tc": _lib.PREC_TC}
 
@@ -168,6 +168,12 @@ class GpuSketch:
         self._finished = True
         return g, hh, cs, m
 
+    def rows(self) -> int:
+        """Rows pushed so far (spca_sketch_rows)."""
+        r = ctypes.c_int64(0)
+        _lib.check(self.lib.spca_sketch_rows(self.h, ctypes.byref(r)), self.h)
+        return r.value
+
     def kernel_launches(self) -> int:
         return int(self.lib.spca_kernel_launches(self.h))
 
@@ -211,11 +217,15 @@ def run_pass(stream, omega, block_rows=None, compensated=False, precision="auto"
     n, l = om.shape
     sk = GpuSketch(n, om, dtype, precision=precision, device=device,
                    rows_hint=stream.n_rows or 0, compensated=compensated)
+    inner = stream.wrapped if isinstance(stream, PassCounter) else stream
     fs = _file_source(stream)
-    if fs is not None:
-        _push_file(sk, fs)
+    if fs is not None or isinstance(inner, NormalizedRowStream):
+        if fs is not None:
+            _push_file(sk, fs)
+        else:
+            _push_normalized(sk, inner, block_rows)
         if isinstance(stream, PassCounter):
-            stream.rows_read += fs.n_rows
+            stream.rows_read += int(sk.rows())
             stream.passes_completed += 1
             stream.pass_in_progress = False
     elif has_whole(stream):
@@ -242,7 +252,7 @@ def _file_source(stream) -> Optional[FileRowStream]:
     return inner if isinstance(inner, FileRowStream) else None
 
 
-def _push_file(sk: GpuSketch, fs: FileRowStream, nbuf: int = 3) -> None:
+def _push_file(sk: GpuSketch, fs: FileRowStream, nbuf: int = 3, transform=None) -> None:
     """Stream a matrix file through page-locked buffers: a reader thread fills
     buffer j % nbuf with parallel positional reads (no host-side copy, the
     file's element type kept) while the library copies and sketches the
@@ -287,7 +297,11 @@ def _push_file(sk: GpuSketch, fs: FileRowStream, nbuf: int = 3) -> None:
             if isinstance(item, BaseException):
                 raise item
             i, start, rows = item
-            sk.push(bufs[i][:rows], start, final=start + rows == m)
+            block = bufs[i][:rows]
+            if transform is not None:  # copy to the device, transform there, push device rows
+                with torch.cuda.stream(sk.stream):
+                    block = transform(block.to(sk.device, non_blocking=True))
+            sk.push(block, start, final=start + rows == m)
             ev = torch.cuda.Event()
             ev.record(sk.stream)
             released.put((i, ev))
@@ -298,6 +312,142 @@ def _push_file(sk: GpuSketch, fs: FileRowStream, nbuf: int = 3) -> None:
         th.join(timeout=60)
     if m == 0:
         sk.push(np.empty((0, n), dtype=fs.dtype), 0, final=True)
+
+
+def normalize_rows_device(t, out=None):
+    """Rows of a CUDA tensor (float32/float64) to zero mean and unit norm with
+    the libspca kernel (spca_normalize_rows), on torch's current stream.
+    ``out`` (same shape and dtype, may be ``t``) receives the result."""
+    torch = torch_mod()
+    lib = _lib.load()
+    if t.dim() != 2 or t.dtype not in (torch.float32, torch.float64) or not t.is_cuda:
+        raise StreamFormatError("normalize_rows_device needs a 2-d float32/float64 CUDA tensor")
+    if t.stride(1) != 1:
+        t = t.contiguous()
+    if out is None:
+        out = torch.empty(t.shape, dtype=t.dtype, device=t.device)
+    rows, n = int(t.shape[0]), int(t.shape[1])
+    code = _lib.SPCA_F32 if t.dtype == torch.float32 else _lib.SPCA_F64
+    st = torch.cuda.current_stream(t.device).cuda_stream
+    with torch.cuda.device(t.device):
+        rc = lib.spca_normalize_rows(ctypes.c_void_p(t.data_ptr()), rows, n, max(int(t.stride(0)), n),
+                                     ctypes.c_void_p(out.data_ptr()), max(int(out.stride(0)), n), code,
+                                     ctypes.c_void_p(st))
+    _lib.check(rc)
+    return out
+
+
+def normalize_rows(block, device=None):
+    """Shift each row to zero mean, then scale it to unit Euclidean norm; a
+    constant row becomes the zero row (sketch.py:142-153). RowBlock or bare
+    2-d array in, the same kind out; host input gives float64 numpy (as the
+    reference), CUDA tensors stay on the device in their dtype. The
+    arithmetic runs on the GPU (fp64)."""
+    torch = torch_mod()
+    bare = not isinstance(block, RowBlock)
+    vals = block if bare else block.values
+    if is_torch(vals) and vals.is_cuda:
+        out = normalize_rows_device(vals)
+    else:
+        arr = np.ascontiguousarray(np.asarray(vals.cpu().numpy() if is_torch(vals) else vals,
+                                              dtype=np.float64))
+        if arr.ndim != 2:
+            raise StreamFormatError("normalize_rows expects a 2-d block")
+        if arr.shape[0] == 0 or arr.shape[1] == 0:
+            out = arr.copy()
+        else:
+            dev = default_device(device)
+            out = normalize_rows_device(torch.from_numpy(arr).to(dev)).cpu().numpy()
+    return out if bare else RowBlock(block.first_row_index, out)
+
+
+class NormalizedRowStream(RowStream):
+    """View of a stream with normalize_rows applied to every block
+    (sketch.py:156-182). ``blocks`` yields float64 numpy blocks like the
+    reference; the device pass instead normalizes each chunk in HBM right
+    before sketching it (``_push_normalized``), in the wrapped stream's
+    element type."""
+
+    def __init__(self, wrapped):
+        self._wrapped = wrapped
+
+    @property
+    def wrapped(self):
+        return self._wrapped
+
+    @property
+    def n_rows(self):
+        return self._wrapped.n_rows
+
+    @property
+    def n_cols(self) -> int:
+        return self._wrapped.n_cols
+
+    @property
+    def resettable(self) -> bool:
+        return self._wrapped.resettable
+
+    @property
+    def dtype(self) -> np.dtype:
+        return np.dtype(getattr(self._wrapped, "dtype", np.float64))
+
+    def blocks(self, block_rows: int):
+        for block in self._wrapped.blocks(block_rows):
+            yield normalize_rows(block)
+
+
+def _push_normalized(sk: GpuSketch, ns: NormalizedRowStream, block_rows, chunk_bytes: int = 256 << 20) -> None:
+    """Device pass over a NormalizedRowStream: every chunk lands in HBM,
+    spca_normalize_rows writes it into one of two workspaces on the sketch
+    stream, and the library sketches the workspace (same stream: the next
+    normalisation into a workspace queues behind the kernels that read it)."""
+    torch = torch_mod()
+    inner = ns.wrapped
+    n = sk.n
+    tdt = torch.float32 if sk.dtype == np.float32 else torch.float64
+    esz = 4 if tdt == torch.float32 else 8
+    step = max(1, chunk_bytes // (n * esz))
+    ws = []
+
+    def norm(dev_rows):
+        if not ws:
+            ws.extend(torch.empty((step, n), dtype=tdt, device=sk.device) for _ in range(2))
+        k = norm.count % 2
+        norm.count += 1
+        if dev_rows.shape[0] > step:  # one-off larger block
+            return normalize_rows_device(dev_rows.to(tdt))
+        out = ws[k][:dev_rows.shape[0]]
+        return normalize_rows_device(dev_rows.to(tdt), out)
+    norm.count = 0
+
+    with torch.cuda.stream(sk.stream):
+        fs = inner if isinstance(inner, FileRowStream) else None
+        if fs is not None:
+            _push_file(sk, fs, transform=norm)
+            return
+        if has_whole(inner):
+            kind, mat = inner.whole()
+            m = int(mat.shape[0])
+            for start in range(0, m, step):
+                part = mat[start:start + step]
+                dev_rows = part if (is_torch(part) and part.is_cuda) else (
+                    part.to(sk.device, non_blocking=True) if is_torch(part) else torch.from_numpy(
+                        np.ascontiguousarray(part)).to(sk.device))
+                sk.push(norm(dev_rows), start, final=start + step >= m)
+            if m == 0:
+                sk.push(np.empty((0, n), dtype=sk.dtype), 0, final=True)
+            return
+        if block_rows is None:
+            block_rows = sk.l
+        for block in inner.blocks(block_rows):
+            vals = block.values
+            if getattr(vals, "ndim", None) != 2 or vals.shape[1] != n:
+                raise StreamFormatError(
+                    f"block at row {block.first_row_index} has shape {tuple(vals.shape)}, expected (*, {n})")
+            dev_rows = vals.to(sk.device) if is_torch(vals) else torch.from_numpy(
+                np.ascontiguousarray(vals)).to(sk.device)
+            if dev_rows.shape[0]:
+                sk.push(norm(dev_rows), block.first_row_index)
 
 
 def sketch_pass(

@@ -10,6 +10,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden", "golden.npz")
+GOLDEN_F = os.path.join(ROOT, "tests", "golden", "golden_f.npz")
 
 
 def pytest_configure(config):
@@ -29,6 +30,12 @@ def golden():
     g = np.load(GOLDEN)
     meta = dict(zip(g["meta_keys"].tolist(), g["meta_vals"].tolist()))
     return g, meta
+
+
+@pytest.fixture(scope="session")
+def golden_f():
+    """Reference outputs for the §8 (f) rows (tests/golden/make_golden_f.py)."""
+    return np.load(GOLDEN_F)
 
 
 def has_cuda() -> bool:

@@ -444,3 +444,95 @@ def test_file_stream_nonfinite_row_and_pca(tmp_path):
     pc = P.PassCounter(P.FileRowStream(p))
     P.sketch_pass(pc, O.gaussian(n, 8, seed=1))
     assert pc.passes_completed == 1 and pc.rows_read == m
+
+
+# ------------------------------------- row normalisation + estimator (§8 f)
+def test_normalize_rows_kernel(golden_f):
+    x = golden_f["norm_in"]
+    got = P.normalize_rows(x)
+    assert got.dtype == np.float64
+    # fp64 with a different summation order than numpy's pairwise sum: ~1 ulp,
+    # except row 7 (1e6 offset: the mean's rounding, 1e6 * 2^-52, survives centering)
+    err = np.abs(got - golden_f["norm_out"]).max(axis=1)
+    assert np.all(np.delete(err, 7) <= 1e-15) and err[7] <= 1e-11
+    assert np.array_equal(got[2], np.zeros(13)) and np.array_equal(got[4], np.zeros(13))
+    blk = P.normalize_rows(P.RowBlock(17, x))
+    assert blk.first_row_index == 17 and np.array_equal(blk.values, got)
+    # device tensors stay on the device in their dtype; in place works
+    t = torch.from_numpy(x.astype(np.float32)).cuda()
+    d = P.normalize_rows(t)
+    assert d.is_cuda and d.dtype == torch.float32
+    want32 = O.oracle_normalize_rows(x.astype(np.float32).astype(np.float64))
+    assert np.abs(d.cpu().numpy() - want32).max() <= 1.2e-7  # fp64 arithmetic, fp32 output
+    from paper_1704_07669_b200.sketch import normalize_rows_device
+    normalize_rows_device(t, t)
+    assert torch.equal(t, d)
+    # wide rows (several strides per thread) vs the oracle
+    w = O.gaussian(33, 70001, seed=9) + 5.0
+    assert np.allclose(P.normalize_rows(w), O.oracle_normalize_rows(w), rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("source", ["array", "device", "generator", "file"])
+def test_normalized_stream_pca(golden_f, tmp_path, source):
+    a = golden_f["ns_a"].astype(np.float64)  # fp32 values; the reference widened them
+    cfg = P.PcaConfig(k=8, oversample=6, block_size=7, seed=2)
+    if source == "array":
+        st = P.ArrayRowStream(a)
+    elif source == "device":
+        st = P.DeviceRowStream(torch.from_numpy(a).cuda())
+    elif source == "generator":
+        st = P.GeneratorRowStream(iter([a[:150], a[150:]]), n_cols=a.shape[1])
+    else:
+        p = tmp_path / "a.spca"
+        P.matfile.write_matrix(p, a, dtype="float64")
+        st = P.FileRowStream(p, buffer_bytes=100 * a.shape[1] * 8)
+    res = P.single_pass_pca(P.NormalizedRowStream(st), cfg, block_rows=64)
+    assert rel(res.s, golden_f["ns_s"]) <= 1e-10
+    assert O.subspace_angle(res.u, golden_f["ns_u"]) <= 1e-10
+    assert O.subspace_angle(res.v, golden_f["ns_v"]) <= 1e-10
+
+
+@pytest.mark.parametrize("precision", PRECISIONS_F32)
+def test_normalized_stream_fp32_file(golden_f, tmp_path, precision):
+    if precision == "tc" and not _tc_ok():
+        pytest.skip("no tensor-core path")
+    a = golden_f["ns_a"]
+    p = tmp_path / "a32.spca"
+    P.matfile.write_matrix(p, a, dtype="float32")
+    cfg = P.PcaConfig(k=8, oversample=6, block_size=7, seed=2)
+    res = P.single_pass_pca(P.NormalizedRowStream(P.FileRowStream(p)), cfg, precision=precision)
+    assert rel(res.s, golden_f["ns32_s"]) <= 1e-4
+    assert O.subspace_angle(res.u, golden_f["ns32_u"]) <= 1e-4
+    assert O.subspace_angle(res.v, golden_f["ns32_v"]) <= 1e-4
+
+
+@pytest.mark.parametrize("tag,kw", [("c", {}), ("n", {"normalize": True}), ("p", {"power": 1}),
+                                    ("nc", {"center": False})])
+def test_estimator_matches_reference(golden_f, tag, kw):
+    from sklearn.base import clone
+    a = golden_f["ns_a"]
+    est = P.SinglePassPCA(n_components=8, oversample=6, block_size=7, seed=3, **kw)
+    est = clone(est).fit(a.astype(np.float64))
+    assert rel(est.singular_values_, golden_f[f"est_{tag}_sv"]) <= 1e-10
+    assert rel(est.explained_variance_, golden_f[f"est_{tag}_ev"]) <= 1e-10
+    assert np.allclose(est.mean_, golden_f[f"est_{tag}_mean"], rtol=1e-12, atol=1e-15)
+    assert O.subspace_angle(est.components_.T, golden_f[f"est_{tag}_components"].T) <= 1e-10
+    assert np.allclose(est.components_, golden_f[f"est_{tag}_components"], atol=1e-9)  # signs too
+    assert list(golden_f[f"est_{tag}_meta"]) == [est.n_samples_, est.n_passes_, est.retained_floats_]
+    assert np.allclose(est.transform(golden_f["est_x2"]), golden_f[f"est_{tag}_t"], rtol=1e-9, atol=1e-11)
+    assert np.allclose(est.inverse_transform(golden_f["est_z"]), golden_f[f"est_{tag}_it"], rtol=1e-9,
+                       atol=1e-11)
+
+
+def test_estimator_errors():
+    est = P.SinglePassPCA(n_components=2)
+    with pytest.raises(P.DimensionError):
+        est.fit(np.ones(5))
+    with pytest.raises(P.DataError):
+        est.fit(np.array([[1.0, np.nan], [0.0, 1.0]]))
+    from sklearn.exceptions import NotFittedError
+    with pytest.raises(NotFittedError):
+        est.transform(np.ones((2, 2)))
+    est.fit(O.gaussian(30, 24, seed=5))
+    with pytest.raises(P.DimensionError):
+        est.transform(np.ones((2, 5)))
