@@ -51,7 +51,7 @@ struct spca_sketch {
   int num_sms = 148;
   int max_pairs = 74;             // co-resident CTA pairs of the pass kernel
   unsigned long long *bad_dev = nullptr;
-  unsigned long long *bad_host = nullptr;  // pinned copy read at finish
+  unsigned long long bad_seen = 0;  // first non-finite row, read back at finish
 
   int64_t chunk_rows = 0;        // canonical chunk (R0)
   void *tail = nullptr;          // R0 x n staging for the partial chunk

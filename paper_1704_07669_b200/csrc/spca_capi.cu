@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -63,6 +64,37 @@ int set_err(spca_sketch *h, int code, int64_t row, const char *fmt, ...) {
     (h)->launches++;                                                                       \
   } while (0)
 
+// Device buffers of a handle come from the device's stream-ordered pool
+// (cudaMallocAsync / cudaFreeAsync on the handle's stream) whose release
+// threshold is raised once per device: creating and destroying a handle
+// then costs microseconds, where cudaMalloc / cudaFree (which synchronizes
+// the device) cost milliseconds per pass. Buffers also touched by the copy
+// stream (the host staging ring) keep plain cudaMalloc.
+std::mutex g_pool_mu;
+bool g_pool_ready[64];
+
+void ensure_pool(int dev) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (dev < 0 || dev >= 64 || g_pool_ready[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  g_pool_ready[dev] = true;
+}
+
+cudaError_t dalloc(spca_sketch *h, void **p, size_t bytes) {
+  return cudaMallocAsync(p, std::max<size_t>(bytes, 1), h->stream);
+}
+template <typename T>
+cudaError_t dalloc(spca_sketch *h, T **p, size_t bytes) {
+  return dalloc(h, reinterpret_cast<void **>(p), bytes);
+}
+void dfree(spca_sketch *h, void *p) {
+  if (p) cudaFreeAsync(p, h->stream);
+}
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -85,15 +117,12 @@ int ensure_g(spca_sketch *h, int64_t rows_needed) {
   if (rows_needed <= h->g_cap) return SPCA_OK;
   int64_t cap = std::max<int64_t>(rows_needed, std::max<int64_t>(h->g_cap * 2, 4096));
   void *nb = nullptr;
-  CK(h, cudaMalloc(&nb, (size_t)cap * h->lpad * h->ds));
+  CK(h, dalloc(h, &nb, (size_t)cap * h->lpad * h->ds));
   if (h->g_dev && h->rows_done > 0) {
     CK(h, cudaMemcpyAsync(nb, h->g_dev, (size_t)h->rows_done * h->lpad * h->ds,
                           cudaMemcpyDeviceToDevice, h->stream));
   }
-  if (h->g_dev) {
-    CK(h, cudaStreamSynchronize(h->stream));
-    cudaFree(h->g_dev);
-  }
+  dfree(h, h->g_dev);  // stream-ordered after the copy
   h->g_dev = nb;
   h->g_cap = cap;
   return SPCA_OK;
@@ -146,12 +175,9 @@ int simt_chunk(spca_sketch *h, const T *a, int64_t lda, int rows) {
   if (ksplit > 1) {
     int64_t need = (int64_t)ksplit * rows * h->lpad;
     if (need > h->gpart_elems) {
-      if (h->gpart) {
-        CK(h, cudaStreamSynchronize(h->stream));
-        cudaFree(h->gpart);
-      }
+      dfree(h, h->gpart);
       h->gpart = nullptr;
-      CK(h, cudaMalloc(&h->gpart, (size_t)need * h->ds));
+      CK(h, dalloc(h, &h->gpart, (size_t)need * h->ds));
       h->gpart_elems = need;
     }
     p1_out = (T *)h->gpart;
@@ -476,32 +502,33 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
       return fail(set_err(nullptr, _e == cudaErrorMemoryAllocation ? SPCA_ERR_OOM : SPCA_ERR_CUDA, -1, \
                           "%s: %s", #call, cudaGetErrorString(_e)));                   \
   } while (0)
-  TRY(cudaMalloc(&h->omega_dev, (size_t)n * h->lpad * ds));
-  TRY(cudaMalloc(&h->omega64_dev, (size_t)n * l * 8));
-  TRY(cudaMalloc(&h->hcs_dev, (size_t)n * (l + 1) * 8));
+  ensure_pool(device);
+  TRY(dalloc(h, &h->omega_dev, (size_t)n * h->lpad * ds));
+  TRY(dalloc(h, &h->omega64_dev, (size_t)n * l * 8));
+  TRY(dalloc(h, &h->hcs_dev, (size_t)n * (l + 1) * 8));
   TRY(cudaMemsetAsync(h->hcs_dev, 0, (size_t)n * (l + 1) * 8, h->stream));
   if (h->compensated) {
-    TRY(cudaMalloc(&h->carry_dev, (size_t)n * 8));
+    TRY(dalloc(h, &h->carry_dev, (size_t)n * 8));
     TRY(cudaMemsetAsync(h->carry_dev, 0, (size_t)n * 8, h->stream));
   }
-  TRY(cudaMalloc(&h->hpart, (size_t)h->hsplit * n * h->lpad * ds));
+  TRY(dalloc(h, &h->hpart, (size_t)h->hsplit * n * h->lpad * ds));
   TRY(cudaMemsetAsync(h->hpart, 0, (size_t)h->hsplit * n * h->lpad * ds, h->stream));
-  TRY(cudaMalloc(&h->cspart, (size_t)h->hsplit * n * 8));
+  TRY(dalloc(h, &h->cspart, (size_t)h->hsplit * n * 8));
   TRY(cudaMemsetAsync(h->cspart, 0, (size_t)h->hsplit * n * 8, h->stream));
-  TRY(cudaMalloc(&h->bad_dev, sizeof(unsigned long long)));
+  TRY(dalloc(h, &h->bad_dev, sizeof(unsigned long long)));
   {
     unsigned long long init = (unsigned long long)kNoBadRow;
     TRY(cudaMemcpyAsync(h->bad_dev, &init, sizeof init, cudaMemcpyHostToDevice, h->stream));
     TRY(cudaStreamSynchronize(h->stream));
   }
-  TRY(cudaMalloc(&h->tail, (size_t)h->chunk_rows * n * ds));
+  TRY(dalloc(h, &h->tail, (size_t)h->chunk_rows * n * ds));
   // Omega: upload fp64, derive the compute-precision copy
   {
     double *om_src = nullptr;
     if (omega_where == SPCA_MEM_DEVICE) {
       om_src = const_cast<double *>(omega);
     } else {
-      TRY(cudaMalloc(&om_src, (size_t)n * l * 8));
+      TRY(dalloc(h, &om_src, (size_t)n * l * 8));
       TRY(cudaMemcpyAsync(om_src, omega, (size_t)n * l * 8, cudaMemcpyHostToDevice, h->stream));
     }
     if (dtype == SPCA_F32)
@@ -513,8 +540,7 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
     cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) return fail(set_err(nullptr, SPCA_ERR_CUDA, -1, "omega_prepare: %s", cudaGetErrorString(le)));
     h->launches++;
-    TRY(cudaStreamSynchronize(h->stream));
-    if (omega_where != SPCA_MEM_DEVICE) cudaFree(om_src);
+    if (omega_where != SPCA_MEM_DEVICE) dfree(h, om_src);  // stream-ordered after omega_prepare
   }
   if (h->precision == SPCA_PREC_TC) {
     rc = tc_setup(h);
@@ -640,9 +666,9 @@ int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out, double *co
     rc = flush_h(h);
     if (rc) return rc;
     if (h->rows_seen > h->g64_cap) {
-      if (h->g64_dev) cudaFree(h->g64_dev);
+      dfree(h, h->g64_dev);
       h->g64_dev = nullptr;
-      CK(h, cudaMalloc(&h->g64_dev, (size_t)std::max<int64_t>(1, h->rows_seen) * h->l * 8));
+      CK(h, dalloc(h, &h->g64_dev, (size_t)std::max<int64_t>(1, h->rows_seen) * h->l * 8));
       h->g64_cap = h->rows_seen;
     }
     if (h->rows_seen > 0) {
@@ -655,9 +681,6 @@ int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out, double *co
                                                                 h->rows_seen, (int)h->l, h->g64_dev);
       CK_LAUNCH(h);
     }
-    // the first non-finite row comes back with the outputs: one synchronization
-    if (!h->bad_host) CK(h, cudaHostAlloc((void **)&h->bad_host, sizeof(unsigned long long), cudaHostAllocDefault));
-    CK(h, cudaMemcpyAsync(h->bad_host, h->bad_dev, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
   }
   const bool first_finish = !h->finished;
   cudaMemcpyKind kind = out_where == SPCA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
@@ -667,13 +690,19 @@ int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out, double *co
   if (colsum_out)
     CK(h, cudaMemcpyAsync(colsum_out, h->hcs_dev + h->n * h->l, (size_t)h->n * 8, kind, h->stream));
   if (rows_seen) *rows_seen = h->rows_seen;
+  // the first non-finite row comes back behind the outputs: a copy into
+  // pageable memory returns once the stream has drained (the one synchronization)
+  if (first_finish) {
+    CK(h, cudaMemcpyAsync(&h->bad_seen, h->bad_dev, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          h->stream));
+  }
   CK(h, cudaStreamSynchronize(h->stream));
   if (first_finish) {
     rc = collect_timers(h);
     if (rc) return rc;
-    if (*h->bad_host != (unsigned long long)kNoBadRow)
-      return set_err(h, SPCA_ERR_DATA, (int64_t)*h->bad_host, "non-finite value in row %lld",
-                     (long long)*h->bad_host);
+    if (h->bad_seen != (unsigned long long)kNoBadRow)
+      return set_err(h, SPCA_ERR_DATA, (int64_t)h->bad_seen, "non-finite value in row %lld",
+                     (long long)h->bad_seen);
     h->finished = true;
   }
   return SPCA_OK;
@@ -692,14 +721,14 @@ int spca_g_colsum(spca_handle_t h, double *out, int out_where) {
   if (!h->finished) return set_err(h, SPCA_ERR_STATE, -1, "g_colsum needs a finished sketch");
   DeviceGuard dg(h->device);
   double *d = nullptr;
-  CK(h, cudaMalloc(&d, (size_t)h->l * 8));
+  CK(h, dalloc(h, &d, (size_t)h->l * 8));
   column_sums64<<<(unsigned)h->l, 256, 0, h->stream>>>(h->g64_dev, h->rows_seen, (int)h->l, d);
   CK_LAUNCH(h);
   CK(h, cudaMemcpyAsync(out, d, (size_t)h->l * 8,
                         out_where == SPCA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                         h->stream));
+  dfree(h, d);
   CK(h, cudaStreamSynchronize(h->stream));
-  cudaFree(d);
   return SPCA_OK;
 }
 
@@ -734,9 +763,9 @@ int spca_center_correct(spca_handle_t h, int64_t m_total, const double *gsum, do
   DeviceGuard dg(h->device);
   const int64_t n = h->n, l = h->l;
   double *mu = nullptr, *w = nullptr, *gs = nullptr;
-  CK(h, cudaMalloc(&mu, (size_t)n * 8));
-  CK(h, cudaMalloc(&w, (size_t)l * 8));
-  CK(h, cudaMalloc(&gs, (size_t)l * 8));
+  CK(h, dalloc(h, &mu, (size_t)n * 8));
+  CK(h, dalloc(h, &w, (size_t)l * 8));
+  CK(h, dalloc(h, &gs, (size_t)l * 8));
   double *colsum = h->hcs_dev + n * l;
   mean_from_colsum<<<(unsigned)ceil_div(n, 256), 256, 0, h->stream>>>(colsum, (int)n, 1.0 / (double)m_total, mu);
   CK_LAUNCH(h);
@@ -758,10 +787,10 @@ int spca_center_correct(spca_handle_t h, int64_t m_total, const double *gsum, do
     CK(h, cudaMemcpyAsync(mean_out, mu, (size_t)n * 8,
                           mean_where == SPCA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                           h->stream));
+  dfree(h, mu);
+  dfree(h, w);
+  dfree(h, gs);
   CK(h, cudaStreamSynchronize(h->stream));
-  cudaFree(mu);
-  cudaFree(w);
-  cudaFree(gs);
   return SPCA_OK;
 }
 
@@ -824,7 +853,10 @@ int spca_debug_gpart(spca_handle_t h, float *out, int64_t count) {
 void spca_sketch_destroy(spca_handle_t h) {
   if (!h) return;
   DeviceGuard dg(h->device);
-  if (h->stream) cudaStreamSynchronize(h->stream);
+  // host staging (pinned buffers, copy stream) is released after the work
+  // that reads it; device buffers go back to the pool in stream order
+  const bool host_side = h->copy_stream || h->pinned[0] || h->pinned[1] || h->dstage[0] || h->dstage[1];
+  if (h->stream && host_side) cudaStreamSynchronize(h->stream);
   for (cudaEvent_t e : {h->t_start, h->t_stop})
     if (e) cudaEventDestroy(e);
   if (h->copy_stream) {
@@ -835,14 +867,16 @@ void spca_sketch_destroy(spca_handle_t h) {
     cudaEventDestroy(t.start);
     cudaEventDestroy(t.stop);
   }
-  void *bufs[] = {h->omega_dev, h->omega64_dev, h->tc_omega, h->g_dev, h->g64_dev, h->hcs_dev,
-                  h->carry_dev, h->hpart, h->cspart, h->gpart, h->tc_ws, h->bad_dev, h->tail,
-                  h->dstage[0], h->dstage[1], h->trace, h->tc_ctr};
-  for (void *p : bufs)
+  if (h->stream) {
+    void *pooled[] = {h->omega_dev, h->omega64_dev, h->tc_omega, h->g_dev, h->g64_dev, h->hcs_dev,
+                      h->carry_dev, h->hpart, h->cspart, h->gpart, h->tc_ws, h->bad_dev, h->tail,
+                      h->trace, h->tc_ctr};
+    for (void *p : pooled) dfree(h, p);
+  }
+  for (void *p : {h->dstage[0], h->dstage[1]})
     if (p) cudaFree(p);
   for (int i = 0; i < 2; ++i) {
     if (h->pinned[i]) cudaFreeHost(h->pinned[i]);
-    if (i == 0 && h->bad_host) cudaFreeHost(h->bad_host);
     if (h->copy_done[i]) cudaEventDestroy(h->copy_done[i]);
     if (h->comp_done[i]) cudaEventDestroy(h->comp_done[i]);
   }

@@ -126,8 +126,14 @@ int tc_max_pairs() {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // one query per process and device (it costs about a millisecond)
+  static int cached[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && cached[dev] > 0) return cached[dev];
   int nc = 0;
   if (cudaOccupancyMaxActiveClusters(&nc, tc_pass_kernel<LPAD>, &cfg) != cudaSuccess) return 0;
+  if (dev >= 0 && dev < 64) cached[dev] = nc;
   return nc;
 }
 
@@ -137,12 +143,12 @@ int tc_setup(spca_sketch *h) {
     // the SIMT layout padded l to 32/64; the tensor-core path needs 64/128
     h->lpad = lp;
     h->bl = 64;
-    cudaFree(h->omega_dev);
+    dfree(h, h->omega_dev);
     h->omega_dev = nullptr;
-    cudaFree(h->hpart);
+    dfree(h, h->hpart);
     h->hpart = nullptr;
-    CK(h, cudaMalloc(&h->omega_dev, (size_t)h->n * h->lpad * 4));
-    CK(h, cudaMalloc(&h->hpart, (size_t)h->n * h->lpad * 4));
+    CK(h, dalloc(h, &h->omega_dev, (size_t)h->n * h->lpad * 4));
+    CK(h, dalloc(h, &h->hpart, (size_t)h->n * h->lpad * 4));
     CK(h, cudaMemsetAsync(h->hpart, 0, (size_t)h->n * h->lpad * 4, h->stream));
   }
   int bad = lp == 64 ? tc_set_smem_attrs<64>() : tc_set_smem_attrs<128>();
@@ -150,7 +156,7 @@ int tc_setup(spca_sketch *h) {
   CK(h, cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
   h->max_pairs = lp == 64 ? tc_max_pairs<64>() : tc_max_pairs<128>();
   if (h->max_pairs < 1) return set_err(h, SPCA_ERR_CUDA, -1, "no CTA pair of the pass kernel fits an SM pair");
-  CK(h, cudaMalloc(&h->tc_omega, (size_t)2 * h->lpad * h->n * 4));
+  CK(h, dalloc(h, &h->tc_omega, (size_t)2 * h->lpad * h->n * 4));
   float *whi = (float *)h->tc_omega;
   float *wlo = whi + (size_t)h->lpad * h->n;
   tc_omega_prepare<<<grid_for((int64_t)h->lpad * h->n), 256, 0, h->stream>>>(
@@ -165,20 +171,19 @@ int tc_setup(spca_sketch *h) {
   const FusedSched s = tc_base_sched(h);
   // G^T hi / lo of kSlots chunks: [kSlots][2][lpad][R0], one TMA map
   h->tc_ws_bytes = (size_t)kSlots * 2 * h->lpad * s.R0 * 4;
-  CK(h, cudaMalloc(&h->tc_ws, h->tc_ws_bytes));
+  CK(h, dalloc(h, &h->tc_ws, h->tc_ws_bytes));
   rc = encode_2d(h, &h->tm_gT, h->tc_ws, (uint64_t)s.R0, (uint64_t)kSlots * 2 * h->lpad, (uint64_t)s.R0 * 4,
                  32, hr);
   if (rc) return rc;
   h->gpart_elems = (int64_t)kSlots * 2 * s.T * s.S * 128 * h->lpad;
-  CK(h, cudaMalloc(&h->gpart, (size_t)h->gpart_elems * 4));
+  CK(h, dalloc(h, &h->gpart, (size_t)h->gpart_elems * 4));
   // ordering counters of one launch (at most flush_every chunks)
   h->tc_ctr_chunks = h->flush_every;
-  CK(h, cudaMalloc(&h->tc_ctr, (size_t)(h->tc_ctr_chunks * (2 * s.T + 2) + 2 * s.X) * 4));
+  CK(h, dalloc(h, &h->tc_ctr, (size_t)(h->tc_ctr_chunks * (2 * s.T + 2) + 2 * s.X) * 4));
   if (getenv("SPCA_TC_TRACE")) {
-    CK(h, cudaMalloc(&h->trace, (size_t)kTraceWords * 8));
+    CK(h, dalloc(h, &h->trace, (size_t)kTraceWords * 8));
     CK(h, cudaMemsetAsync(h->trace, 0, (size_t)kTraceWords * 8, h->stream));
   }
-  CK(h, cudaStreamSynchronize(h->stream));
   return SPCA_OK;
 }
 

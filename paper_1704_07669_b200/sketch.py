@@ -80,7 +80,10 @@ class GpuSketch:
             rc = self.lib.spca_sketch_create(
                 ctypes.byref(handle), self.n, self.l, code, prec,
                 om.ctypes.data_as(ctypes.c_void_p), _lib.MEM_PAGEABLE,
-                self.device.index, ctypes.c_void_p(stream.cuda_stream), int(rows_hint),
+                # torch's default stream is the legacy NULL stream: hand the library
+                # cudaStreamLegacy (0x1) so both order on it (NULL would mean a
+                # private stream that does not synchronize with torch's work)
+                self.device.index, ctypes.c_void_p(stream.cuda_stream or 1), int(rows_hint),
                 1 if compensated else 0)
         _lib.check(rc)
         self.h = handle
