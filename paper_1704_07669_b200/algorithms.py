@@ -17,7 +17,7 @@ from typing import Optional, Union
 
 import numpy as np
 
-from .device import default_device, to_device64, torch_mod
+from .device import default_device, host_copy, to_device64, torch_mod
 from .errors import ConfigError, EmptyStreamError
 from .linalg import STREAM_SKETCH, dense_svd, gaussian_matrix, qr_unpivoted, sign_align
 from .qb import QbFactor, blocked_qb
@@ -159,8 +159,8 @@ def _post_pass(state: SketchState, cfg: PcaConfig, stream, on_deficiency, return
     u, s, v = finish_svd(factor, cfg.k)
     retained = state.retained_floats + int(state.omega.numel())
     if not return_device:
-        u, s, v = u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
-        mean = mean.cpu().numpy() if mean is not None else None
+        u, s, v = host_copy(u), host_copy(s), host_copy(v)
+        mean = host_copy(mean) if mean is not None else None
     return TruncatedSvd(u=u, s=s, v=v, mean=mean,
                         passes=_measured_passes(stream, passes_fallback),
                         retained_floats=retained)
@@ -210,8 +210,8 @@ def power_refine(
     u, s, v = finish_svd(factor, cfg.k)
     retained = second.retained_floats + int(second.omega.numel())
     if not return_device:
-        u, s, v = u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
-        mean = mean.cpu().numpy() if mean is not None else None
+        u, s, v = host_copy(u), host_copy(s), host_copy(v)
+        mean = host_copy(mean) if mean is not None else None
     return TruncatedSvd(u=u, s=s, v=v, mean=mean, passes=_measured_passes(stream, 2),
                         retained_floats=retained)
 

@@ -18,7 +18,7 @@ from typing import Optional
 
 import numpy as np
 
-from .device import torch_mod
+from .device import host_copy, torch_mod
 
 
 def allreduce_sketch(h, col_sums, dist, rows: Optional[int] = None, group=None):
@@ -105,6 +105,6 @@ def sharded_single_pass_pca(local_rows, cfg, dist, group=None, precision: str = 
                         repair_seed=cfg.seed)
     u, s, v = finish_svd(factor, cfg.k)
     retained = int(g_full.numel() + h.numel() + cs.numel() + st.omega.numel())
-    return TruncatedSvd(u=u.cpu().numpy(), s=s.cpu().numpy(), v=v.cpu().numpy(),
-                        mean=None if mean is None else mean.cpu().numpy(), passes=1,
+    return TruncatedSvd(u=host_copy(u), s=host_copy(s), v=host_copy(v),
+                        mean=None if mean is None else host_copy(mean), passes=1,
                         retained_floats=retained)

@@ -30,7 +30,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from .device import default_device, is_torch, to_device64, torch_mod
+from .device import default_device, host_copy, is_torch, to_device64, torch_mod
 from .errors import DeviceError, EmptyStreamError, StreamFormatError
 from .streams import FileRowStream, PassCounter, RowBlock, RowStream, has_whole
 
@@ -146,8 +146,12 @@ class GpuSketch:
 
     # -- results ------------------------------------------------------------
     def finish(self, on_device: bool = True):
-        """(g, h, col_sums, rows_seen) as CUDA float64 tensors (or numpy)."""
+        """(g, h, col_sums, rows_seen) as CUDA float64 tensors (or numpy,
+        read back through page-locked staging)."""
         torch = torch_mod()
+        if not on_device:
+            g, hh, cs, m = self.finish(on_device=True)
+            return host_copy(g), host_copy(hh), host_copy(cs), m
         rows = ctypes.c_int64(0)
         _lib.check(self.lib.spca_sketch_rows(self.h, ctypes.byref(rows)), self.h)
         m = rows.value
@@ -508,5 +512,5 @@ def center_correct(state: SketchState, omega) -> SketchState:
     h_c = h - torch.outer(mu, g.sum(dim=0))
     z = torch.zeros_like(cs)
     if not on_dev:
-        g_c, h_c, z = g_c.cpu().numpy(), h_c.cpu().numpy(), z.cpu().numpy()
+        g_c, h_c, z = host_copy(g_c), host_copy(h_c), host_copy(z)
     return replace(state, g=g_c, h=h_c, col_sums=z)
