@@ -47,6 +47,10 @@ struct spca_sketch {
   void *tc_ws = nullptr;         // tensor-core G^T slots [kSlots][2][lpad][R0]
   size_t tc_ws_bytes = 0;
   int *tc_ctr = nullptr;         // per-launch ordering counters of the pass kernel
+  int *order_dev = nullptr;      // unit order table of the last launch shape (tc_unit_order)
+  int64_t order_cap = 0;
+  int order_C = -1, order_TS = -1, order_TlS = -1, order_XR = -1;
+  double order_lag = -1.0;
   int64_t tc_ctr_chunks = 0;     // chunks one launch may cover
   int num_sms = 148;
   int max_pairs = 74;             // co-resident CTA pairs of the pass kernel

@@ -72,6 +72,7 @@ struct FusedSched {
   int RS, hseg;   // H: row segments per chunk, K blocks per segment
   int D;          // stage lag of a chunk's H units behind its G units
   int total;      // pair units in this launch
+  const int *order;  // device: unit u -> kind << 30 | chunk << 15 | index (null: closed form, lag D)
 };
 
 struct FusedArgs {
@@ -118,6 +119,15 @@ __host__ __device__ inline int fused_total(const FusedSched &s) {
 __host__ __device__ __forceinline__ FusedUnit fused_decode(const FusedSched &s, int u) {
   const int TS = s.T * s.S, TlS = s.Tl * s.S, XR = s.X * s.RS, F = TS + XR, D = s.D;
   int kind = 0, c = 0, r = 0;
+#ifdef __CUDA_ARCH__
+  if (s.order) {  // host-built order (tc_unit_order): any lag, including fractional stages
+    const int e = __ldg(s.order + u);
+    kind = e >> 30;
+    c = (e >> 15) & 0x7fff;
+    r = e & 0x7fff;
+  } else
+#endif
+  {
   // region 1: stages 0 .. min(C, D) - 1, G units only
   const int size1 = s.C <= D ? (s.C - 1) * TS + TlS : D * TS;
   if (u < size1) {
@@ -162,6 +172,7 @@ __host__ __device__ __forceinline__ FusedUnit fused_decode(const FusedSched &s, 
       c = st - D;
       r = u % XR;
     }
+  }
   }
   FusedUnit f;
   f.kind = kind;

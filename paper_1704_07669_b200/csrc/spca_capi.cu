@@ -870,7 +870,7 @@ void spca_sketch_destroy(spca_handle_t h) {
   if (h->stream) {
     void *pooled[] = {h->omega_dev, h->omega64_dev, h->tc_omega, h->g_dev, h->g64_dev, h->hcs_dev,
                       h->carry_dev, h->hpart, h->cspart, h->gpart, h->tc_ws, h->bad_dev, h->tail,
-                      h->trace, h->tc_ctr};
+                      h->trace, h->tc_ctr, h->order_dev};
     for (void *p : pooled) dfree(h, p);
   }
   for (void *p : {h->dstage[0], h->dstage[1]})

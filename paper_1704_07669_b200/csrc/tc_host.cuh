@@ -206,6 +206,57 @@ int tc_register_source(spca_sketch *h, const void *a, int64_t rows, int64_t lda)
   return SPCA_OK;
 }
 
+// Unit order of a launch, built on the host: G units of chunk c sit at
+// virtual times c*P + r (P = units of a full stage), H units at
+// c*P + TS + lag*P + r; units are dealt in that order (G first on ties).
+// lag = 2 reproduces the closed-form stage layout with D = 2; a fractional
+// lag (SPCA_TC_LAGF) moves a chunk's H units closer to its G units, which
+// keeps the chunk's rows in L2 for the re-read at the price of less slack for
+// the G^T reduction. Every wait still points at a unit dealt earlier for
+// 0.5 <= lag <= 3 (H(c) after G(c); G(c)'s slot reuse after H(c - kSlots)).
+int tc_unit_order(spca_sketch *h, FusedSched &s) {
+  double lag = 2.0;
+  if (const char *e = getenv("SPCA_TC_LAGF")) lag = std::max(0.5, std::min((double)kMaxLag, atof(e)));
+  const int TS = s.T * s.S, TlS = s.Tl * s.S, XR = s.X * s.RS, P = TS + XR;
+  if (s.C >= 32768 || std::max(TS, XR) >= 32768) {  // outside the table encoding: closed form
+    s.order = nullptr;
+    return SPCA_OK;
+  }
+  const bool same = h->order_dev && h->order_C == s.C && h->order_TS == TS && h->order_TlS == TlS &&
+                    h->order_XR == XR && h->order_lag == lag;
+  if (!same) {
+    std::vector<std::pair<double, int>> keys;
+    keys.reserve(s.total);
+    for (int c = 0; c < s.C; ++c) {
+      const int g = c == s.C - 1 ? TlS : TS;
+      for (int r = 0; r < g; ++r) keys.push_back({(double)c * P + r, (c << 15) | r});
+      for (int r = 0; r < XR; ++r)
+        keys.push_back({(double)c * P + TS + lag * P + r + 0.25, (1 << 30) | (c << 15) | r});
+    }
+    std::stable_sort(keys.begin(), keys.end(),
+                     [](const std::pair<double, int> &x, const std::pair<double, int> &y) { return x.first < y.first; });
+    if ((int)keys.size() != s.total) return set_err(h, SPCA_ERR_STATE, -1, "unit order size mismatch");
+    std::vector<int> ord(keys.size());
+    for (size_t i = 0; i < keys.size(); ++i) ord[i] = keys[i].second;
+    if ((int64_t)ord.size() > h->order_cap) {
+      dfree(h, h->order_dev);
+      h->order_dev = nullptr;
+      CK(h, dalloc(h, &h->order_dev, ord.size() * sizeof(int)));
+      h->order_cap = (int64_t)ord.size();
+    }
+    // stream-ordered after every launch that read the previous table
+    CK(h, cudaMemcpyAsync(h->order_dev, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));  // ord is about to go out of scope
+    h->order_C = s.C;
+    h->order_TS = TS;
+    h->order_TlS = TlS;
+    h->order_XR = XR;
+    h->order_lag = lag;
+  }
+  s.order = h->order_dev;
+  return SPCA_OK;
+}
+
 // One launch of the pass kernel over `rows` rows at `a` (a whole number of
 // canonical chunks, or one partial chunk at the end of the stream).
 int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
@@ -217,7 +268,12 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   s.ntl = (int)ceil_div(s.rows_last, 128);
   s.Tl = (int)ceil_div(s.ntl, 2);
   s.total = fused_total(s);
+  s.order = nullptr;
   if (s.C > h->tc_ctr_chunks) return set_err(h, SPCA_ERR_STATE, -1, "tc launch exceeds its counters");
+  if (!getenv("SPCA_TC_CLOSED_FORM")) {
+    const int orc = tc_unit_order(h, s);
+    if (orc) return orc;
+  }
   CUtensorMap fa_g, fa_h;
   const CUtensorMap *ta_g, *ta_h;
   int row_base = 0;
