@@ -741,7 +741,19 @@ int spca_normalize_rows(const void *src, int64_t rows, int64_t n, int64_t ld_src
   if (!src || !dst) return set_err(nullptr, SPCA_ERR_STATE, -1, "normalize_rows: null pointer");
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned grid = (unsigned)std::min<int64_t>(rows, 148 * 8);
-  if (dtype == SPCA_F32) {
+  const int64_t es = dtype == SPCA_F32 ? 4 : 8, ev = 16 / es;
+  const bool vec = (dtype == SPCA_F32 || dtype == SPCA_F64) && n % ev == 0 && ld_src % ev == 0 &&
+                   ld_dst % ev == 0 && (reinterpret_cast<uintptr_t>(src) % 16) == 0 &&
+                   (reinterpret_cast<uintptr_t>(dst) % 16) == 0;
+  constexpr int kNV = 12;  // vectors per thread: rows up to 12288 fp32 / 6144 fp64 stay in registers
+  if (vec && n <= (int64_t)kNormThreads * kNV * ev) {
+    if (dtype == SPCA_F32)
+      normalize_rows_vec_kernel<float, kNV><<<grid, kNormThreads, 0, st>>>((const float *)src, rows, n, ld_src,
+                                                                           (float *)dst, ld_dst);
+    else
+      normalize_rows_vec_kernel<double, kNV><<<grid, kNormThreads, 0, st>>>((const double *)src, rows, n, ld_src,
+                                                                            (double *)dst, ld_dst);
+  } else if (dtype == SPCA_F32) {
     normalize_rows_kernel<float><<<grid, kNormThreads, 0, st>>>((const float *)src, rows, n, ld_src,
                                                                  (float *)dst, ld_dst);
   } else if (dtype == SPCA_F64) {

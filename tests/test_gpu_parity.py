@@ -470,6 +470,20 @@ def test_normalize_rows_kernel(golden_f):
     # wide rows (several strides per thread) vs the oracle
     w = O.gaussian(33, 70001, seed=9) + 5.0
     assert np.allclose(P.normalize_rows(w), O.oracle_normalize_rows(w), rtol=0, atol=1e-15)
+    # register-resident vector path (n a multiple of the vector width, up to
+    # 12288 fp32 / 6144 fp64), with constant and zero rows, out of place and in place
+    for dt, width in ((np.float32, 10000), (np.float64, 6144), (np.float32, 12288), (np.float64, 6146)):
+        z = O.gaussian(70, width, seed=11) * 2.0 + 3.0
+        z[3] = 1.25
+        z[5] = 0.0
+        zd = torch.from_numpy(z.astype(dt)).cuda()
+        want = O.oracle_normalize_rows(z.astype(dt).astype(np.float64))
+        got = normalize_rows_device(zd).cpu().numpy().astype(np.float64)
+        tol = 1.2e-7 if dt == np.float32 else 1e-15
+        assert np.abs(got - want).max() <= tol, (dt, width)
+        assert not got[3].any() and not got[5].any()
+        normalize_rows_device(zd, zd)
+        assert np.array_equal(zd.cpu().numpy().astype(np.float64), got)
 
 
 @pytest.mark.parametrize("source", ["array", "device", "generator", "file"])
