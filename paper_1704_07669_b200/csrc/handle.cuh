@@ -47,6 +47,8 @@ struct spca_sketch {
   void *tc_ws = nullptr;         // tensor-core G^T slots [kSlots][2][lpad][R0]
   size_t tc_ws_bytes = 0;
   int *tc_ctr = nullptr;         // per-launch ordering counters of the pass kernel
+  int tc_lp = 64;                // l_pad of one pass-kernel launch (64 or 128)
+  int tc_groups = 1;             // column groups of 128 (l > 128): one launch each
   int *order_dev = nullptr;      // unit order table of the last launch shape (tc_unit_order)
   int64_t order_cap = 0;
   int order_C = -1, order_TS = -1, order_TlS = -1, order_XR = -1;

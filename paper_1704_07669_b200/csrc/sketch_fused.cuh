@@ -95,6 +95,9 @@ struct FusedArgs {
   int64_t lda;              //   exact non-finite re-check of a flagged row
   unsigned long long *bad_row;
   unsigned long long *trace;  // null unless profiling
+  int wy0;                    // first Omega^T row of this launch's column group
+  int gld;                    // row stride (floats) of g_out and hpart (all column groups)
+  int colsum_on;              // this launch also accumulates the column sums (group 0)
   int dbg;                    // profiling knobs (SPCA_TC_DEBUG), 0 in production:
                               // 1 converters skip the split, 2 no MMAs, 4 no B loads, 8 no A loads
 
@@ -328,7 +331,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           constexpr int HR = LPAD / 2;  // rows per B box
           // rows of W_hi / W_lo in the maps: Omega^T (G units) or G^T slot (H units)
           const CUtensorMap *mh = f.kind == 0 ? &tWhi : &tGT, *ml = f.kind == 0 ? &tWlo : &tGT;
-          const int yh = f.kind == 0 ? 0 : 2 * gslot * LPAD, yl = f.kind == 0 ? 0 : (2 * gslot + 1) * LPAD;
+          const int yh = f.kind == 0 ? args.wy0 : 2 * gslot * LPAD,
+                    yl = f.kind == 0 ? args.wy0 : (2 * gslot + 1) * LPAD;
           if constexpr (C::STACKED) {
             const CUtensorMap *m01 = rank == 0 ? mh : ml;
             const int y01 = rank == 0 ? yh : yl;
@@ -644,7 +648,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             }
             const int rc = tile * 128 + r;  // row within the chunk
             const bool valid = rc < f.rows;
-            if (valid) reinterpret_cast<float4 *>(args.g_out + ((int64_t)f.c * sc.R0 + rc) * LPAD)[q] = acc;
+            if (valid) reinterpret_cast<float4 *>(args.g_out + ((int64_t)f.c * sc.R0 + rc) * args.gld)[q] = acc;
             const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -668,7 +672,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           if (e == 0) ptx::spin_until_geq(&args.hseq[tile], seq);
           ptx::named_bar(2, kTcEpi);
           {  // H rows of the tile's columns, NQ consecutive lanes per column (coalesced)
-            float4 *hp = reinterpret_cast<float4 *>(args.hpart + (int64_t)tile * 128 * LPAD);
+            float *hp0 = args.hpart + (int64_t)tile * 128 * args.gld;
             const bool overwrite = !args.accumulate && seq == 0;
             const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF + sb * C::STG_BYTES);
             const int items = min(128, args.n - tile * 128) * NQ;
@@ -676,18 +680,19 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             for (int it = e; it < items; it += kTcEpi) {
               const int r = it / NQ, q = it % NQ;
               float4 w = ptx::lds128(stg0 + r * LPAD * 4 + ((q ^ (r & 7)) << 4));
+              float4 *hp = reinterpret_cast<float4 *>(hp0 + (int64_t)r * args.gld) + q;
               if (!overwrite) {
-                const float4 o = __ldcg(hp + it);
+                const float4 o = __ldcg(hp);
                 w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
               }
-              hp[it] = w;
+              *hp = w;
             }
           }
           csv = stg_cs[sb][e] + stg_cs[sb][128 + e];
         }
         ptx::mbar_arrive(&bars.epi_empty[sb]);
         if (real) {
-          if (col < args.n) {
+          if (col < args.n && args.colsum_on) {
             if (args.carry) {
               const double y = csv - __ldcg(args.carry + col);
               const double s0 = __ldcg(args.colsum + col);

@@ -36,9 +36,14 @@ bool tc_available(int device) {
 
 // l <= 128: wider sketches (config 5's l = 250) use the SIMT kernels until the
 // promoted accumulators of an N = 256 tile fit the register budget.
-bool tc_supported_shape(int64_t n, int64_t l) { return n >= 32 && n % 4 == 0 && l >= 1 && l <= 128; }
+// l > 128 runs as column groups of 128 (one launch per group over the same
+// rows): H[:, J] = A^T (A Omega[:, J]) needs only G[:, J].
+constexpr int kTcMaxL = 512;
+bool tc_supported_shape(int64_t n, int64_t l) { return n >= 32 && n % 4 == 0 && l >= 1 && l <= kTcMaxL; }
 
-int tc_lpad(int64_t l) { return l <= 64 ? 64 : 128; }
+// l_pad of the whole sketch (accumulator layouts) and of one launch
+int tc_lpad(int64_t l) { return l <= 64 ? 64 : (int)(128 * ceil_div(l, 128)); }
+int tc_launch_lpad(int64_t l) { return l <= 64 ? 64 : 128; }
 
 // Canonical chunk of the single-read pass: A_c is read from HBM by the G
 // units and again from L2 by the H units one stage later, so about two
@@ -48,7 +53,10 @@ int64_t tc_chunk_rows(int64_t n, int64_t /*l*/) {
   int64_t mb = 40;
   if (const char *e = getenv("SPCA_TC_CHUNK_MB")) mb = std::max<int64_t>(1, atoll(e));  // tuning knob
   int64_t r = (int64_t)(mb << 20) / (4 * n);
-  r = std::max<int64_t>(256, std::min<int64_t>(8192, r));
+  // wide rows: at least 1024 rows (H units of a full 32 K blocks; config 5,
+  // n = 200 000: 60 ms per pass vs 127 ms at 256 rows) while a chunk stays <= 1 GB
+  const int64_t floor_rows = std::max<int64_t>(256, std::min<int64_t>(1024, (int64_t)(1ll << 30) / (4 * n)));
+  r = std::max<int64_t>(floor_rows, std::min<int64_t>(8192, r));
   return (r / 256) * 256;
 }
 
@@ -67,7 +75,12 @@ FusedSched tc_base_sched(const spca_sketch *h) {
   s.nt = s.R0 / 128;
   s.T = s.nt / 2;
   s.nkb = (int)ceil_div(h->n, 32);
-  s.S = (int)ceil_div(s.nkb, U);
+  // A G unit's epilogue waits for every K segment of its tile, and the
+  // segments are dealt to consecutive pairs: S must not exceed the pairs of
+  // the grid (else a pair would wait on its own later unit). Wide n gets
+  // longer segments instead (S <= max_pairs / 2).
+  const int max_seg = std::max(1, h->max_pairs / 2);
+  s.S = (int)std::min<int64_t>(ceil_div(s.nkb, U), max_seg);
   s.kseg = (int)ceil_div(s.nkb, s.S);
   s.S = (int)ceil_div(s.nkb, s.kseg);
   s.nx = (int)ceil_div(h->n, 128);
@@ -138,10 +151,13 @@ int tc_max_pairs() {
 }
 
 int tc_setup(spca_sketch *h) {
-  const int lp = tc_lpad(h->l);
-  if (lp != h->lpad) {
+  const int lp_total = tc_lpad(h->l);
+  const int lp = tc_launch_lpad(h->l);
+  h->tc_lp = lp;
+  h->tc_groups = lp_total / lp;
+  if (lp_total != h->lpad) {
     // the SIMT layout padded l to 32/64; the tensor-core path needs 64/128
-    h->lpad = lp;
+    h->lpad = lp_total;
     h->bl = 64;
     dfree(h, h->omega_dev);
     h->omega_dev = nullptr;
@@ -151,7 +167,7 @@ int tc_setup(spca_sketch *h) {
     CK(h, dalloc(h, &h->hpart, (size_t)h->n * h->lpad * 4));
     CK(h, cudaMemsetAsync(h->hpart, 0, (size_t)h->n * h->lpad * 4, h->stream));
   }
-  int bad = lp == 64 ? tc_set_smem_attrs<64>() : tc_set_smem_attrs<128>();
+  int bad = lp == 64 ? tc_set_smem_attrs<64>() : tc_set_smem_attrs<128>();  // per-launch template
   if (bad) return set_err(h, SPCA_ERR_CUDA, -1, "cannot raise dynamic shared memory for the tc kernel");
   CK(h, cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
   h->max_pairs = lp == 64 ? tc_max_pairs<64>() : tc_max_pairs<128>();
@@ -162,20 +178,21 @@ int tc_setup(spca_sketch *h) {
   tc_omega_prepare<<<grid_for((int64_t)h->lpad * h->n), 256, 0, h->stream>>>(
       h->omega64_dev, (int)h->n, (int)h->l, (int)h->lpad, whi, wlo);
   CK_LAUNCH(h);
-  // B tiles are loaded as l_pad/2-row halves (one per CTA of a pair)
-  const uint32_t hr = (uint32_t)(h->lpad / 2);
+  // B tiles are loaded as l_pad/2-row halves (one per CTA of a pair) of one
+  // column group; Omega^T holds every group (rows g*lp ..)
+  const uint32_t hr = (uint32_t)(lp / 2);
   int rc = encode_2d(h, &h->tm_whi, whi, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, hr);
   if (rc) return rc;
   rc = encode_2d(h, &h->tm_wlo, wlo, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, hr);
   if (rc) return rc;
   const FusedSched s = tc_base_sched(h);
-  // G^T hi / lo of kSlots chunks: [kSlots][2][lpad][R0], one TMA map
-  h->tc_ws_bytes = (size_t)kSlots * 2 * h->lpad * s.R0 * 4;
+  // G^T hi / lo of kSlots chunks of one launch: [kSlots][2][lp][R0], one TMA map
+  h->tc_ws_bytes = (size_t)kSlots * 2 * lp * s.R0 * 4;
   CK(h, dalloc(h, &h->tc_ws, h->tc_ws_bytes));
-  rc = encode_2d(h, &h->tm_gT, h->tc_ws, (uint64_t)s.R0, (uint64_t)kSlots * 2 * h->lpad, (uint64_t)s.R0 * 4,
+  rc = encode_2d(h, &h->tm_gT, h->tc_ws, (uint64_t)s.R0, (uint64_t)kSlots * 2 * lp, (uint64_t)s.R0 * 4,
                  32, hr);
   if (rc) return rc;
-  h->gpart_elems = (int64_t)kSlots * 2 * s.T * s.S * 128 * h->lpad;
+  h->gpart_elems = (int64_t)kSlots * 2 * s.T * s.S * 128 * lp;
   CK(h, dalloc(h, &h->gpart, (size_t)h->gpart_elems * 4));
   // ordering counters of one launch (at most flush_every chunks)
   h->tc_ctr_chunks = h->flush_every;
@@ -297,6 +314,8 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
     ta_h = &fa_h;
   }
   const size_t ctr_words = (size_t)s.C * (2 * s.T + 2) + 2 * s.X;
+  const int grid = 2 * std::max(1, std::min(h->max_pairs, s.total));
+  for (int grp = 0; grp < h->tc_groups; ++grp) {
   CK(h, cudaMemsetAsync(h->tc_ctr, 0, ctr_words * 4, h->stream));
   FusedArgs args{};
   args.s = s;
@@ -304,8 +323,11 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   args.row_base = row_base;
   args.gpart = (float *)h->gpart;
   args.gT = (float *)h->tc_ws;
-  args.g_out = (float *)h->g_dev + h->rows_done * h->lpad;
-  args.hpart = (float *)h->hpart;
+  args.g_out = (float *)h->g_dev + h->rows_done * h->lpad + grp * h->tc_lp;
+  args.hpart = (float *)h->hpart + grp * h->tc_lp;
+  args.wy0 = grp * h->tc_lp;
+  args.gld = (int)h->lpad;
+  args.colsum_on = grp == 0;
   args.colsum = h->hcs_dev + h->n * h->l;
   args.carry = h->compensated ? h->carry_dev : nullptr;
   args.seg_cnt = h->tc_ctr;
@@ -319,14 +341,14 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   args.bad_row = h->bad_dev;
   args.trace = h->trace;
   args.dbg = h->tc_debug;
-  const int grid = 2 * std::max(1, std::min(h->max_pairs, s.total));
-  if (h->lpad == 64)
+  if (h->tc_lp == 64)
     tc_pass_kernel<64><<<grid, TcCfg<64>::THREADS, TcCfg<64>::SMEM, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo,
                                                                          h->tm_gT, args);
   else
     tc_pass_kernel<128><<<grid, TcCfg<128>::THREADS, TcCfg<128>::SMEM, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo,
                                                                            h->tm_gT, args);
   CK_LAUNCH(h);
+  }
   h->chunks_since_flush += s.C;
   return SPCA_OK;
 }

@@ -152,7 +152,8 @@ class TestSketchPass:
 
     @pytest.mark.parametrize("precision", PRECISIONS_F32)
     @pytest.mark.parametrize("m,n,l", [(5000, 1000, 60), (3000, 4096, 120), (300, 2000, 250),
-                                       (1000, 333, 30), (257, 100, 8)])
+                                       (1000, 333, 30), (257, 100, 8), (3000, 1000, 129),
+                                       (2100, 4096, 250), (1500, 1000, 384)])
     def test_fp32_shapes_vs_oracle(self, precision, m, n, l):
         if precision == "tc" and not _tc_ok():
             pytest.skip("tensor-core path unavailable")
@@ -550,3 +551,18 @@ def test_estimator_errors():
     est.fit(O.gaussian(30, 24, seed=5))
     with pytest.raises(P.DimensionError):
         est.transform(np.ones((2, 5)))
+
+
+@pytest.mark.parametrize("l", [16, 200])
+def test_tc_wide_n(l):
+    """n wide enough that ~32-block K segments would outnumber the CTA pairs:
+    the schedule lengthens the segments (S <= pairs / 2) instead of letting a
+    G epilogue wait on its own pair's later unit."""
+    if not _tc_ok():
+        pytest.skip("no tensor-core path")
+    m, n = 600, 80000
+    a = O.gaussian(m, n, seed=41).astype(np.float32)
+    om = O.gaussian(n, l, seed=42)
+    st = P.sketch_pass(P.ArrayRowStream(a), om, precision="tc")
+    ref = O.oracle_sketch(O.row_blocks(a, 4096), om.astype(np.float32).astype(np.float64))
+    assert rel(st.g, ref.g) <= 2e-5 and rel(st.h, ref.h) <= 2e-5
