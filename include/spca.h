@@ -158,6 +158,14 @@ int spca_center_correct(spca_handle_t h, int64_t m_total, const double *gsum,
 /* Column sums of the finished G (l values, float64) — for center_correct. */
 int spca_g_colsum(spca_handle_t h, double *out, int out_where);
 
+/* Sketch the rows as normalize_rows would leave them (NormalizedRowStream,
+ * sketch.py:142-182): each row minus its mean, divided by its centered norm.
+ * Must precede the first push of a pass (SPCA_ERR_STATE otherwise). On the
+ * tensor-core path the normalisation is fused into the pass (row shifts and
+ * norms folded into G, H and col_sums); on the SIMT path each chunk is
+ * normalized into a workspace first. */
+int spca_sketch_set_normalize(spca_handle_t h, int on);
+
 /* normalize_rows (sketch.py:142-153) on device rows: each row minus its
  * mean, divided by its Euclidean norm (a constant row becomes zero), fp64
  * arithmetic; dtype SPCA_F32 / SPCA_F64 for both src and dst (device

@@ -142,4 +142,47 @@ __global__ void omega_prepare(const double *__restrict__ om, int n, int l, int l
   }
 }
 
+// fused row normalisation, finish-time corrections (sketch_fused.cuh):
+// out[j] = sum_r g[r][j] * coef[r] for j < l, out[l] = sum_r coef[r]
+__global__ void norm_coef_sums(const double *__restrict__ g, int64_t rows, int l,
+                               const double *__restrict__ coef, double *__restrict__ out) {
+  __shared__ double red[256];
+  const int j = blockIdx.x;
+  double s = 0.0;
+  for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) s += j < l ? g[r * l + j] * coef[r] : coef[r];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[j] = red[0];
+}
+
+// H[i][j] -= c[j], colsum[i] -= c[l]  (hcs = [H (n x l) | colsum (n)])
+__global__ void norm_correct(double *__restrict__ hcs, int n, int l, const double *__restrict__ c) {
+  const int64_t total = (int64_t)n * (l + 1);
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    if (idx < (int64_t)n * l) hcs[idx] -= c[idx % l];
+    else hcs[idx] -= c[l];
+  }
+}
+
+// fp64 column sums of Omega (as used) -> fp32, zero padded to lpad
+__global__ void omega_colsums(const double *__restrict__ om, int n, int l, int lpad, float *__restrict__ out) {
+  __shared__ double red[256];
+  const int j = blockIdx.x;
+  double s = 0.0;
+  if (j < l)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += om[(int64_t)i * l + j];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[j] = (float)red[0];
+}
+
 }  // namespace spca

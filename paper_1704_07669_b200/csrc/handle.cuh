@@ -54,6 +54,15 @@ struct spca_sketch {
   int order_C = -1, order_TS = -1, order_TlS = -1, order_XR = -1;
   double order_lag = -1.0;
   int64_t tc_ctr_chunks = 0;     // chunks one launch may cover
+  // row normalisation (spca_sketch_set_normalize)
+  bool normalize = false;
+  void *norm_ws = nullptr;       // SIMT path: normalized copy of one chunk
+  double *rstat_part = nullptr;  // TC: [kSlots][2T][S][128][2] per-segment sums of d, d^2
+  float *row_a0 = nullptr;       // TC: [kSlots][R0] row shifts of the chunks in flight
+  float *row_inv = nullptr;      // TC: [kSlots][R0] 1 / row norms
+  double *row_coef = nullptr;    // TC: [rows] (mean - a0) / norm of every row pushed
+  int64_t row_coef_cap = 0;
+  float *wsum = nullptr;         // TC: [lpad] column sums of Omega (as used)
   int num_sms = 148;
   int max_pairs = 74;             // co-resident CTA pairs of the pass kernel
   unsigned long long *bad_dev = nullptr;

@@ -95,6 +95,13 @@ struct FusedArgs {
   int64_t lda;              //   exact non-finite re-check of a flagged row
   unsigned long long *bad_row;
   unsigned long long *trace;  // null unless profiling
+  // fused row normalisation (normalize_rows, sketch.py:142-153), or all null / 0:
+  int norm;
+  float *rstat_part;          // [kSlots][2T][S][128][2] per-segment sums of d, d^2 (d = a - a0)
+  float *row_a0;              // [kSlots][R0] a0 = each row's first value (the shift)
+  float *row_inv;             // [kSlots][R0] 1 / ||a - mean|| (1 for a zero norm)
+  double *row_coef;           // [launch rows] (mean - a0) / norm, for the finish-time corrections
+  const float *wsum;          // [LPAD] column sums of this group's Omega (as used)
   int wy0;                    // first Omega^T row of this launch's column group
   int gld;                    // row stride (floats) of g_out and hpart (all column groups)
   int colsum_on;              // this launch also accumulates the column sums (group 0)
@@ -213,7 +220,7 @@ struct PairBars {
   uint32_t tmem_base;
 };
 
-template <int LPAD>
+template <int LPAD, bool NORM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<LPAD>::THREADS, 1)
 tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ CUtensorMap tAh,
                const __grid_constant__ CUtensorMap tWhi, const __grid_constant__ CUtensorMap tWlo,
@@ -224,6 +231,9 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
   __shared__ PairBars<LPAD> bars;
   __shared__ double stg_cs[C::NSTG][kGroups * 128];  // H: per converter group, column-sum partial
   __shared__ int stg_bad[128];              // G epilogue: row of the tile has a non-finite partial
+  __shared__ __align__(16) float sst[C::NA][64];      // norm, H blocks: a0 and 1/norm of the block's 32 rows
+  __shared__ double stg_rs[C::NSTG][2][kGroups * 128];  // norm, G units: per group sums of d and d^2
+  __shared__ float sl_stat[128][2];                   // norm, G slice reduction: mean_d, inv per row
   const FusedSched &sc = args.s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -279,6 +289,14 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       const FusedUnit f = fused_decode(sc, u);
       const int rbase = args.row_base + f.c * sc.R0;
       const int tile = 2 * f.a + (int)rank;
+      const bool hstats = NORM && f.kind == 1 && f.nk > 0;
+      if (hstats) {  // the row shifts / scales of chunk c come from its G reductions
+        if (ptx::elect_one()) {
+          ptx::spin_until_geq(&args.ready[f.c], fused_real_tiles(sc, f.c) * sc.S);
+          ptx::fence_proxy_async_global();
+        }
+        __syncwarp();
+      }
 #pragma unroll 1
       for (int kb = 0; kb < f.nk; ++kb, ++gkb) {
         const int s = gkb % C::NA;
@@ -288,7 +306,12 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           if (args.dbg & 8) {
             ptx::mbar_arrive(&bars.a_full[s]);
           } else {
-            ptx::mbar_arrive_expect_tx(&bars.a_full[s], C::A_BYTES);
+            ptx::mbar_arrive_expect_tx(&bars.a_full[s], C::A_BYTES + (hstats ? 256u : 0u));
+            if (hstats) {
+              const size_t o = (size_t)(f.c % kSlots) * sc.R0 + (size_t)(f.k0 + kb) * 32;
+              ptx::bulk_load(&sst[s][0], args.row_a0 + o, 128, &bars.a_full[s]);
+              ptx::bulk_load(&sst[s][32], args.row_inv + o, 128, &bars.a_full[s]);
+            }
             const int kx = (args.dbg & 2048) ? 0 : (f.k0 + kb) * 32;  // profiling knob: L2-resident A
             const int ry = (args.dbg & 2048) ? 0 : rbase;
             if (f.kind == 0) {  // 128 rows x 32 k, row-major (swizzled)
@@ -417,6 +440,13 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
       const FusedUnit f = fused_decode(sc, u);
       float cs = 0.f, cc = 0.f;   // H: column sum (fp32 Kahan over the unit)
+      // fused normalisation, G units: shift every value of the row by its first
+      // value a0 (d = a - a0; exact for nearby values) and sum d, d^2 (Kahan)
+      float a0 = 0.f, s1 = 0.f, s1c = 0.f, s2 = 0.f, s2c = 0.f;
+      if (NORM && f.kind == 0) {
+        const int rt = (2 * f.a + (int)rank) * 128 + t;  // row within the chunk
+        if (rt < f.rows) a0 = __ldg(args.a + ((int64_t)f.c * sc.R0 + rt) * args.lda);
+      }
       if (ct == 0) SPCA_TRACE(ui, 0);
 #pragma unroll 1
       for (int kb = grp; kb < f.nk; kb += kGroups) {
@@ -447,13 +477,53 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
               const float4 x = ptx::lds128(row + ((q4 ^ (t & 7)) << 4));
               v[4 * q4] = x.x; v[4 * q4 + 1] = x.y; v[4 * q4 + 2] = x.z; v[4 * q4 + 3] = x.w;
             }
+            if (NORM) {  // d = a - a0 on the row's real columns; d, d^2 pairwise then Kahan
+              const int col0 = (f.k0 + kb) * 32;
+              float p1[16], p2[16];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = col0 + i < args.n ? v[i] - a0 : 0.f;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                p1[i] = v[2 * i] + v[2 * i + 1];
+                p2[i] = fmaf(v[2 * i], v[2 * i], v[2 * i + 1] * v[2 * i + 1]);
+              }
+#pragma unroll
+              for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+                for (int i = 0; i < w; ++i) {
+                  p1[i] = p1[i] + p1[i + w];
+                  p2[i] = p2[i] + p2[i + w];
+                }
+              float y = p1[0] - s1c, tt = s1 + y;
+              s1c = (tt - s1) - y;
+              s1 = tt;
+              y = p2[0] - s2c;
+              tt = s2 + y;
+              s2c = (tt - s2) - y;
+              s2 = tt;
+            }
           } else {
             const uint32_t raw = ptx::smem_u32(smem + s * C::A_BYTES + t * 4);  // column t
 #pragma unroll
             for (int kq = 0; kq < 32; ++kq) v[kq] = ptx::lds32(raw + kq * 512);
             float p16[16];  // pairwise sum of the 32 values, then one Kahan step
+            if (NORM) {  // d = a - a0 per row; the column sum weights rows by 1/norm
+              const uint32_t st_ = ptx::smem_u32(&sst[s][0]);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) p16[i] = v[2 * i] + v[2 * i + 1];
+              for (int q4 = 0; q4 < 8; ++q4) {
+                const float4 s0 = ptx::lds128(st_ + 16 * q4), w4 = ptx::lds128(st_ + 128 + 16 * q4);
+                v[4 * q4] -= s0.x; v[4 * q4 + 1] -= s0.y; v[4 * q4 + 2] -= s0.z; v[4 * q4 + 3] -= s0.w;
+                hi[4 * q4] = v[4 * q4] * w4.x;
+                hi[4 * q4 + 1] = v[4 * q4 + 1] * w4.y;
+                hi[4 * q4 + 2] = v[4 * q4 + 2] * w4.z;
+                hi[4 * q4 + 3] = v[4 * q4 + 3] * w4.w;
+              }
+#pragma unroll
+              for (int i = 0; i < 16; ++i) p16[i] = hi[2 * i] + hi[2 * i + 1];
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) p16[i] = v[2 * i] + v[2 * i + 1];
+            }
 #pragma unroll
             for (int w = 8; w >= 1; w >>= 1)
 #pragma unroll
@@ -508,6 +578,10 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       const int sb = ui % C::NSTG;  // staging buffer of this unit
       if (ui >= C::NSTG) ptx::mbar_wait(&bars.epi_empty[sb], ((ui / C::NSTG) - 1) & 1);
       if (f.kind == 1) stg_cs[sb][grp * 128 + t] = (double)cs - (double)cc;
+      if (NORM && f.kind == 0) {
+        stg_rs[sb][0][grp * 128 + t] = (double)s1 - (double)s1c;
+        stg_rs[sb][1][grp * 128 + t] = (double)s2 - (double)s2c;
+      }
       ptx::mbar_arrive(&bars.epi_full[sb]);
     }
   } else if (warp >= C::PROMO_BASE / 32 && warp < C::EPI_BASE / 32) {  // ----- promoters
@@ -602,6 +676,12 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             if (!(chk == 0.f)) stg_bad[r] = 1;
             gp[it] = x;
           }
+          if (NORM) {  // this segment's row sums of d, d^2 (the two converter groups, in order)
+            double *rp = reinterpret_cast<double *>(args.rstat_part) +
+                         ((((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 + e) * 2;
+            rp[0] = stg_rs[sb][0][e] + stg_rs[sb][0][128 + e];
+            rp[1] = stg_rs[sb][1][e] + stg_rs[sb][1][128 + e];
+          }
           ptx::named_bar(2, kTcEpi);
           flagged = stg_bad[e] != 0;
           stg_bad[e] = 0;
@@ -636,6 +716,32 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           float *ghi = args.gT + (size_t)(2 * gslot) * LPAD * sc.R0;
           float *glo = ghi + (size_t)LPAD * sc.R0;
           const int items = (r1 - r0) * NQ;
+          if (NORM) {
+            // row statistics of the slice over the S segments (fixed order, fp64):
+            // mean_d = mean(a) - a0, norm = ||a - mean(a)||, from sums of d = a - a0
+            if (e < r1 - r0) {
+              const int r = r0 + e, rc = tile * 128 + r;
+              const double *rp = reinterpret_cast<const double *>(args.rstat_part) +
+                                 (((size_t)gslot * twoT + tile) * sc.S * 128 + r) * 2;
+              double t1 = 0.0, t2 = 0.0;
+              for (int z = 0; z < sc.S; ++z) {
+                t1 += __ldcg(rp + (size_t)z * 256);
+                t2 += __ldcg(rp + (size_t)z * 256 + 1);
+              }
+              const double md = t1 / (double)args.n;
+              const double nrm = sqrt(fmax(t2 - t1 * md, 0.0));
+              const double inv = nrm > 0.0 ? 1.0 / nrm : 1.0;
+              const bool valid = rc < f.rows;
+              const int64_t grow = (int64_t)f.c * sc.R0 + rc;
+              sl_stat[r][0] = (float)md;
+              sl_stat[r][1] = (float)inv;
+              const size_t so = (size_t)gslot * sc.R0 + rc;
+              args.row_a0[so] = valid ? __ldg(args.a + grow * args.lda) : 0.f;
+              args.row_inv[so] = valid ? (float)inv : 1.f;
+              if (valid) args.row_coef[grow] = md * inv;
+            }
+            ptx::named_bar(2, kTcEpi);
+          }
 #pragma unroll 1
           for (int it = e; it < items; it += kTcEpi) {
             const int r = r0 + it / NQ, q = it % NQ;
@@ -648,12 +754,25 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             }
             const int rc = tile * 128 + r;  // row within the chunk
             const bool valid = rc < f.rows;
-            if (valid) reinterpret_cast<float4 *>(args.g_out + ((int64_t)f.c * sc.R0 + rc) * args.gld)[q] = acc;
-            const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+            float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+            float b4[4] = {acc.x, acc.y, acc.z, acc.w};  // B operand of the H units
+            if (NORM) {  // G_hat = (d Omega - mean_d * 1^T Omega) / norm; the H units take G_hat / norm
+              const float md = sl_stat[r][0], inv = sl_stat[r][1];
+              const float4 w4 = __ldg(reinterpret_cast<const float4 *>(args.wsum) + q);
+              const float ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                a4[j] = fmaf(-md, ws[j], a4[j]) * inv;
+                b4[j] = a4[j] * inv;
+              }
+            }
+            if (valid)
+              reinterpret_cast<float4 *>(args.g_out + ((int64_t)f.c * sc.R0 + rc) * args.gld)[q] =
+                  make_float4(a4[0], a4[1], a4[2], a4[3]);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               float h1 = 0.f, l1 = 0.f;
-              if (valid) split3(a4[j], h1, l1);
+              if (valid) split3(b4[j], h1, l1);
               ghi[(size_t)(4 * q + j) * sc.R0 + rc] = h1;
               glo[(size_t)(4 * q + j) * sc.R0 + rc] = l1;
             }

@@ -21,6 +21,7 @@
 #include "epilogue.cuh"
 #include "sketch_simt.cuh"
 #include "handle.cuh"
+#include "normalize.cuh"
 
 using namespace spca;
 
@@ -132,7 +133,6 @@ int ensure_g(spca_sketch *h, int64_t rows_needed) {
 
 // tensor-core path (uses set_err / CK / grid_for above)
 #include "sketch_fused.cuh"
-#include "normalize.cuh"
 #include "tc_host.cuh"
 
 namespace {
@@ -244,11 +244,44 @@ int close_timing(spca_sketch *h, int64_t chunks) {
   return SPCA_OK;
 }
 
+// normalize_rows kernels (csrc/normalize.cuh): the register-resident vector
+// variant when the rows fit and are 16-byte aligned, else the three-sweep one
+cudaError_t launch_normalize(const void *src, int64_t rows, int64_t n, int64_t ld_src, void *dst, int64_t ld_dst,
+                             int dtype, cudaStream_t st) {
+  const unsigned grid = (unsigned)std::min<int64_t>(rows, 148 * 8);
+  const int64_t es = dtype == SPCA_F32 ? 4 : 8, ev = 16 / es;
+  const bool vec = n % ev == 0 && ld_src % ev == 0 && ld_dst % ev == 0 &&
+                   (reinterpret_cast<uintptr_t>(src) % 16) == 0 && (reinterpret_cast<uintptr_t>(dst) % 16) == 0;
+  constexpr int kNV = 12;  // vectors per thread: rows up to 12288 fp32 / 6144 fp64 stay in registers
+  if (vec && n <= (int64_t)kNormThreads * kNV * ev) {
+    if (dtype == SPCA_F32)
+      normalize_rows_vec_kernel<float, kNV><<<grid, kNormThreads, 0, st>>>((const float *)src, rows, n, ld_src,
+                                                                           (float *)dst, ld_dst);
+    else
+      normalize_rows_vec_kernel<double, kNV><<<grid, kNormThreads, 0, st>>>((const double *)src, rows, n, ld_src,
+                                                                            (double *)dst, ld_dst);
+  } else if (dtype == SPCA_F32) {
+    normalize_rows_kernel<float><<<grid, kNormThreads, 0, st>>>((const float *)src, rows, n, ld_src,
+                                                                 (float *)dst, ld_dst);
+  } else {
+    normalize_rows_kernel<double><<<grid, kNormThreads, 0, st>>>((const double *)src, rows, n, ld_src,
+                                                                  (double *)dst, ld_dst);
+  }
+  return cudaGetLastError();
+}
+
 // SIMT path: one canonical chunk (G, H, column sums), flush every ~1M rows
 int process_chunk(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   if (rows <= 0) return SPCA_OK;
   int rc = ensure_g(h, h->rows_done + rows);
   if (rc) return rc;
+  if (h->normalize) {  // unfused on this path: normalize the chunk into a workspace first
+    if (!h->norm_ws) CK(h, dalloc(h, &h->norm_ws, (size_t)h->chunk_rows * h->n * h->ds));
+    CK(h, launch_normalize(a, rows, h->n, lda, h->norm_ws, h->n, h->dtype, h->stream));
+    h->launches++;
+    a = h->norm_ws;
+    lda = h->n;
+  }
   open_timing(h);
   if (h->dtype == SPCA_F32) {
     rc = simt_chunk<float>(h, (const float *)a, lda, (int)rows);
@@ -611,6 +644,14 @@ int spca_sketch_push_final(spca_handle_t h, const void *a, int64_t rows, int64_t
   return push_impl(h, a, rows, ld, first_row, where, true);
 }
 
+int spca_sketch_set_normalize(spca_handle_t h, int on) {
+  if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
+  if (h->rows_seen > 0 || h->tail_rows > 0 || h->rows_done > 0)
+    return set_err(h, SPCA_ERR_STATE, -1, "set_normalize must precede the first push of a pass");
+  h->normalize = on != 0;
+  return SPCA_OK;
+}
+
 int spca_sketch_reset(spca_handle_t h) {
   if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
   DeviceGuard dg(h->device);
@@ -681,6 +722,17 @@ int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out, double *co
                                                                 h->rows_seen, (int)h->l, h->g64_dev);
       CK_LAUNCH(h);
     }
+    if (h->normalize && h->precision == SPCA_PREC_TC && h->rows_seen > 0) {
+      // fused normalisation: H -= 1 (G_hat^T coef)^T, colsum -= sum(coef) (sketch_fused.cuh)
+      double *c = nullptr;
+      CK(h, dalloc(h, &c, (size_t)(h->l + 1) * 8));
+      norm_coef_sums<<<(unsigned)(h->l + 1), 256, 0, h->stream>>>(h->g64_dev, h->rows_seen, (int)h->l,
+                                                                   h->row_coef, c);
+      CK_LAUNCH(h);
+      norm_correct<<<grid_for(h->n * (h->l + 1)), 256, 0, h->stream>>>(h->hcs_dev, (int)h->n, (int)h->l, c);
+      CK_LAUNCH(h);
+      dfree(h, c);
+    }
   }
   const bool first_finish = !h->finished;
   cudaMemcpyKind kind = out_where == SPCA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
@@ -739,30 +791,9 @@ int spca_normalize_rows(const void *src, int64_t rows, int64_t n, int64_t ld_src
                    (long long)rows, (long long)n, (long long)ld_src, (long long)ld_dst);
   if (rows == 0) return SPCA_OK;
   if (!src || !dst) return set_err(nullptr, SPCA_ERR_STATE, -1, "normalize_rows: null pointer");
-  cudaStream_t st = (cudaStream_t)stream;
-  const unsigned grid = (unsigned)std::min<int64_t>(rows, 148 * 8);
-  const int64_t es = dtype == SPCA_F32 ? 4 : 8, ev = 16 / es;
-  const bool vec = (dtype == SPCA_F32 || dtype == SPCA_F64) && n % ev == 0 && ld_src % ev == 0 &&
-                   ld_dst % ev == 0 && (reinterpret_cast<uintptr_t>(src) % 16) == 0 &&
-                   (reinterpret_cast<uintptr_t>(dst) % 16) == 0;
-  constexpr int kNV = 12;  // vectors per thread: rows up to 12288 fp32 / 6144 fp64 stay in registers
-  if (vec && n <= (int64_t)kNormThreads * kNV * ev) {
-    if (dtype == SPCA_F32)
-      normalize_rows_vec_kernel<float, kNV><<<grid, kNormThreads, 0, st>>>((const float *)src, rows, n, ld_src,
-                                                                           (float *)dst, ld_dst);
-    else
-      normalize_rows_vec_kernel<double, kNV><<<grid, kNormThreads, 0, st>>>((const double *)src, rows, n, ld_src,
-                                                                            (double *)dst, ld_dst);
-  } else if (dtype == SPCA_F32) {
-    normalize_rows_kernel<float><<<grid, kNormThreads, 0, st>>>((const float *)src, rows, n, ld_src,
-                                                                 (float *)dst, ld_dst);
-  } else if (dtype == SPCA_F64) {
-    normalize_rows_kernel<double><<<grid, kNormThreads, 0, st>>>((const double *)src, rows, n, ld_src,
-                                                                  (double *)dst, ld_dst);
-  } else {
+  if (dtype != SPCA_F32 && dtype != SPCA_F64)
     return set_err(nullptr, SPCA_ERR_CONFIG, -1, "normalize_rows: bad dtype %d", dtype);
-  }
-  const cudaError_t e = cudaGetLastError();
+  const cudaError_t e = launch_normalize(src, rows, n, ld_src, dst, ld_dst, dtype, (cudaStream_t)stream);
   if (e != cudaSuccess) return set_err(nullptr, SPCA_ERR_CUDA, -1, "normalize_rows launch: %s", cudaGetErrorString(e));
   return SPCA_OK;
 }
@@ -882,7 +913,8 @@ void spca_sketch_destroy(spca_handle_t h) {
   if (h->stream) {
     void *pooled[] = {h->omega_dev, h->omega64_dev, h->tc_omega, h->g_dev, h->g64_dev, h->hcs_dev,
                       h->carry_dev, h->hpart, h->cspart, h->gpart, h->tc_ws, h->bad_dev, h->tail,
-                      h->trace, h->tc_ctr, h->order_dev};
+                      h->trace, h->tc_ctr, h->order_dev, h->norm_ws, h->rstat_part, h->row_a0,
+                      h->row_inv, h->row_coef, h->wsum};
     for (void *p : pooled) dfree(h, p);
   }
   for (void *p : {h->dstage[0], h->dstage[1]})

@@ -119,9 +119,10 @@ template <int LPAD>
 int tc_set_smem_attrs() {
   static bool done = false;
   if (done) return 0;
-  if (cudaFuncSetAttribute(tc_pass_kernel<LPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)TcCfg<LPAD>::SMEM) != cudaSuccess)
-    return 1;
+  for (auto k : {tc_pass_kernel<LPAD, false>, tc_pass_kernel<LPAD, true>})
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcCfg<LPAD>::SMEM) !=
+        cudaSuccess)
+      return 1;
   done = true;
   return 0;
 }
@@ -147,7 +148,7 @@ int tc_max_pairs() {
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && cached[dev] > 0) return cached[dev];
   int nc = 0;
-  if (cudaOccupancyMaxActiveClusters(&nc, tc_pass_kernel<LPAD>, &cfg) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, tc_pass_kernel<LPAD, false>, &cfg) != cudaSuccess) return 0;
   if (dev >= 0 && dev < 64) cached[dev] = nc;
   return nc;
 }
@@ -276,6 +277,31 @@ int tc_unit_order(spca_sketch *h, FusedSched &s) {
   return SPCA_OK;
 }
 
+// Buffers of the fused row normalisation (allocated on first use)
+int tc_norm_buffers(spca_sketch *h, const FusedSched &s, int64_t rows_needed) {
+  if (!h->rstat_part) {
+    CK(h, dalloc(h, &h->rstat_part, (size_t)kSlots * 2 * s.T * s.S * 128 * 2 * sizeof(double)));
+    CK(h, dalloc(h, &h->row_a0, (size_t)kSlots * s.R0 * sizeof(float)));
+    CK(h, dalloc(h, &h->row_inv, (size_t)kSlots * s.R0 * sizeof(float)));
+    CK(h, dalloc(h, &h->wsum, (size_t)h->lpad * sizeof(float)));
+    omega_colsums<<<(unsigned)h->lpad, 256, 0, h->stream>>>(h->omega64_dev, (int)h->n, (int)h->l, (int)h->lpad,
+                                                            h->wsum);
+    CK_LAUNCH(h);
+  }
+  if (rows_needed > h->row_coef_cap) {
+    const int64_t cap = std::max<int64_t>(rows_needed, std::max<int64_t>(2 * h->row_coef_cap, 4096));
+    double *nb = nullptr;
+    CK(h, dalloc(h, &nb, (size_t)cap * sizeof(double)));
+    if (h->row_coef && h->rows_done > 0)
+      CK(h, cudaMemcpyAsync(nb, h->row_coef, (size_t)h->rows_done * sizeof(double), cudaMemcpyDeviceToDevice,
+                            h->stream));
+    dfree(h, h->row_coef);
+    h->row_coef = nb;
+    h->row_coef_cap = cap;
+  }
+  return SPCA_OK;
+}
+
 // One launch of the pass kernel over `rows` rows at `a` (a whole number of
 // canonical chunks, or one partial chunk at the end of the stream).
 int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
@@ -289,6 +315,10 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   s.total = fused_total(s);
   s.order = nullptr;
   if (s.C > h->tc_ctr_chunks) return set_err(h, SPCA_ERR_STATE, -1, "tc launch exceeds its counters");
+  if (h->normalize) {
+    const int rc = tc_norm_buffers(h, s, h->rows_done + rows);
+    if (rc) return rc;
+  }
   if (!getenv("SPCA_TC_CLOSED_FORM")) {
     const int orc = tc_unit_order(h, s);
     if (orc) return orc;
@@ -327,6 +357,14 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   args.gT = (float *)h->tc_ws;
   args.g_out = (float *)h->g_dev + h->rows_done * h->lpad + grp * h->tc_lp;
   args.hpart = (float *)h->hpart + grp * h->tc_lp;
+  if (h->normalize) {
+    args.norm = 1;
+    args.rstat_part = reinterpret_cast<float *>(h->rstat_part);
+    args.row_a0 = h->row_a0;
+    args.row_inv = h->row_inv;
+    args.row_coef = h->row_coef + h->rows_done;
+    args.wsum = h->wsum + grp * h->tc_lp;
+  }
   args.wy0 = grp * h->tc_lp;
   args.gld = (int)h->lpad;
   args.colsum_on = grp == 0;
@@ -343,12 +381,11 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   args.bad_row = h->bad_dev;
   args.trace = h->trace;
   args.dbg = h->tc_debug;
-  if (h->tc_lp == 64)
-    tc_pass_kernel<64><<<grid, TcCfg<64>::THREADS, TcCfg<64>::SMEM, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo,
-                                                                         h->tm_gT, args);
-  else
-    tc_pass_kernel<128><<<grid, TcCfg<128>::THREADS, TcCfg<128>::SMEM, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo,
-                                                                           h->tm_gT, args);
+  auto kern = h->tc_lp == 64 ? (h->normalize ? tc_pass_kernel<64, true> : tc_pass_kernel<64, false>)
+                              : (h->normalize ? tc_pass_kernel<128, true> : tc_pass_kernel<128, false>);
+  const unsigned threads = h->tc_lp == 64 ? TcCfg<64>::THREADS : TcCfg<128>::THREADS;
+  const unsigned smem = h->tc_lp == 64 ? TcCfg<64>::SMEM : TcCfg<128>::SMEM;
+  kern<<<grid, threads, smem, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, args);
   CK_LAUNCH(h);
   }
   h->chunks_since_flush += s.C;

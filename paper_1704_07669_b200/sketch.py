@@ -60,7 +60,8 @@ class GpuSketch:
     """Owner of one libspca handle (single consumer, one GPU)."""
 
     def __init__(self, n: int, omega: np.ndarray, dtype, precision: str = "auto",
-                 device=None, rows_hint: int = 0, compensated: bool = False, stream=None):
+                 device=None, rows_hint: int = 0, compensated: bool = False, stream=None,
+                 normalize: bool = False):
         torch = torch_mod()
         self.lib = _lib.load()
         self.device = default_device(device)
@@ -87,6 +88,8 @@ class GpuSketch:
                 1 if compensated else 0)
         _lib.check(rc)
         self.h = handle
+        if normalize:  # rows are sketched as normalize_rows leaves them (fused on the TC path)
+            _lib.check(self.lib.spca_sketch_set_normalize(self.h, 1), self.h)
         self._keep = []          # host/device sources that must outlive async copies
         self._finished = False
         # what "auto" resolved to: "tc" (tcgen05 3xTF32) or "simt" (FFMA / DFMA)
@@ -220,38 +223,56 @@ def run_pass(stream, omega, block_rows=None, compensated=False, precision="auto"
     """Drive one traversal of ``stream`` through a GpuSketch; returns the
     finished GpuSketch (state still on the device)."""
     om = np.asarray(omega)
-    dtype = np.dtype(getattr(stream, "dtype", np.float64))
     n, l = om.shape
+    outer = stream
+    src = stream.wrapped if isinstance(stream, PassCounter) else stream
+    # NormalizedRowStream: the library normalizes the rows of the wrapped source
+    # (fused into the pass on the tensor-core path); the raw source is pushed
+    normalize = isinstance(src, NormalizedRowStream)
+    if normalize:
+        src = src.wrapped
+    else:
+        src = outer  # a PassCounter counts its own traversal
+    dtype = np.dtype(getattr(src, "dtype", np.float64))
     sk = GpuSketch(n, om, dtype, precision=precision, device=device,
-                   rows_hint=stream.n_rows or 0, compensated=compensated)
-    inner = stream.wrapped if isinstance(stream, PassCounter) else stream
-    fs = _file_source(stream)
-    if fs is not None or isinstance(inner, NormalizedRowStream):
-        if fs is not None:
-            _push_file(sk, fs)
-        else:
-            _push_normalized(sk, inner, block_rows)
-        if isinstance(stream, PassCounter):
-            stream.rows_read += int(sk.rows())
-            stream.passes_completed += 1
-            stream.pass_in_progress = False
-    elif has_whole(stream):
+                   rows_hint=src.n_rows or 0, compensated=compensated, normalize=normalize)
+    fs = _file_source(src)
+    if fs is not None:
+        _push_file(sk, fs)
+        for pc in {id(x): x for x in (src, outer) if isinstance(x, PassCounter)}.values():
+            _count_pass(pc, sk)
+    else:
+        _push_source(sk, src, block_rows, n, l)
+        if normalize and isinstance(outer, PassCounter):
+            _count_pass(outer, sk)
+    return sk
+
+
+def _count_pass(pc: PassCounter, sk: "GpuSketch") -> None:
+    pc.rows_read += int(sk.rows())
+    pc.passes_completed += 1
+    pc.pass_in_progress = False
+
+
+def _push_source(sk: "GpuSketch", stream, block_rows, n: int, l: int) -> None:
+    """Whole in-memory / device / pinned sources in one push (the library
+    re-chunks canonically), anything else block by block as it arrives."""
+    if has_whole(stream):
         kind, mat = stream.whole()
         if mat.shape[0]:
             sk.push(mat, 0, final=True)
-    else:
-        if block_rows is None:
-            block_rows = l
-        # blocks are pushed as they come (a stream may reuse its block buffer,
-        # so no look-ahead); the trailing partial chunk is flushed at finish
-        for block in stream.blocks(block_rows):
-            vals = block.values
-            if getattr(vals, "ndim", None) != 2 or vals.shape[1] != n:
-                raise StreamFormatError(
-                    f"block at row {block.first_row_index} has shape {tuple(vals.shape)}, "
-                    f"expected (*, {n})")
-            sk.push(vals, block.first_row_index)
-    return sk
+        return
+    if block_rows is None:
+        block_rows = l
+    # blocks are pushed as they come (a stream may reuse its block buffer,
+    # so no look-ahead); the trailing partial chunk is flushed at finish
+    for block in stream.blocks(block_rows):
+        vals = block.values
+        if getattr(vals, "ndim", None) != 2 or vals.shape[1] != n:
+            raise StreamFormatError(
+                f"block at row {block.first_row_index} has shape {tuple(vals.shape)}, "
+                f"expected (*, {n})")
+        sk.push(vals, block.first_row_index)
 
 
 def _file_source(stream) -> Optional[FileRowStream]:
@@ -259,7 +280,7 @@ def _file_source(stream) -> Optional[FileRowStream]:
     return inner if isinstance(inner, FileRowStream) else None
 
 
-def _push_file(sk: GpuSketch, fs: FileRowStream, nbuf: int = 3, transform=None) -> None:
+def _push_file(sk: GpuSketch, fs: FileRowStream, nbuf: int = 3) -> None:
     """Stream a matrix file through page-locked buffers: a reader thread fills
     buffer j % nbuf with parallel positional reads (no host-side copy, the
     file's element type kept) while the library copies and sketches the
@@ -304,11 +325,7 @@ def _push_file(sk: GpuSketch, fs: FileRowStream, nbuf: int = 3, transform=None) 
             if isinstance(item, BaseException):
                 raise item
             i, start, rows = item
-            block = bufs[i][:rows]
-            if transform is not None:  # copy to the device, transform there, push device rows
-                with torch.cuda.stream(sk.stream):
-                    block = transform(block.to(sk.device, non_blocking=True))
-            sk.push(block, start, final=start + rows == m)
+            sk.push(bufs[i][:rows], start, final=start + rows == m)
             ev = torch.cuda.Event()
             ev.record(sk.stream)
             released.put((i, ev))
@@ -371,9 +388,10 @@ def normalize_rows(block, device=None):
 class NormalizedRowStream(RowStream):
     """View of a stream with normalize_rows applied to every block
     (sketch.py:156-182). ``blocks`` yields float64 numpy blocks like the
-    reference; the device pass instead normalizes each chunk in HBM right
-    before sketching it (``_push_normalized``), in the wrapped stream's
-    element type."""
+    reference; the device pass instead pushes the wrapped source unchanged
+    and lets the library normalize (spca_sketch_set_normalize: fused into the
+    pass kernel on the tensor-core path, a per-chunk workspace on the SIMT
+    path), in the wrapped stream's element type."""
 
     def __init__(self, wrapped):
         self._wrapped = wrapped
@@ -401,60 +419,6 @@ class NormalizedRowStream(RowStream):
     def blocks(self, block_rows: int):
         for block in self._wrapped.blocks(block_rows):
             yield normalize_rows(block)
-
-
-def _push_normalized(sk: GpuSketch, ns: NormalizedRowStream, block_rows, chunk_bytes: int = 256 << 20) -> None:
-    """Device pass over a NormalizedRowStream: every chunk lands in HBM,
-    spca_normalize_rows writes it into one of two workspaces on the sketch
-    stream, and the library sketches the workspace (same stream: the next
-    normalisation into a workspace queues behind the kernels that read it)."""
-    torch = torch_mod()
-    inner = ns.wrapped
-    n = sk.n
-    tdt = torch.float32 if sk.dtype == np.float32 else torch.float64
-    esz = 4 if tdt == torch.float32 else 8
-    step = max(1, chunk_bytes // (n * esz))
-    ws = []
-
-    def norm(dev_rows):
-        if not ws:
-            ws.extend(torch.empty((step, n), dtype=tdt, device=sk.device) for _ in range(2))
-        k = norm.count % 2
-        norm.count += 1
-        if dev_rows.shape[0] > step:  # one-off larger block
-            return normalize_rows_device(dev_rows.to(tdt))
-        out = ws[k][:dev_rows.shape[0]]
-        return normalize_rows_device(dev_rows.to(tdt), out)
-    norm.count = 0
-
-    with torch.cuda.stream(sk.stream):
-        fs = inner if isinstance(inner, FileRowStream) else None
-        if fs is not None:
-            _push_file(sk, fs, transform=norm)
-            return
-        if has_whole(inner):
-            kind, mat = inner.whole()
-            m = int(mat.shape[0])
-            for start in range(0, m, step):
-                part = mat[start:start + step]
-                dev_rows = part if (is_torch(part) and part.is_cuda) else (
-                    part.to(sk.device, non_blocking=True) if is_torch(part) else torch.from_numpy(
-                        np.ascontiguousarray(part)).to(sk.device))
-                sk.push(norm(dev_rows), start, final=start + step >= m)
-            if m == 0:
-                sk.push(np.empty((0, n), dtype=sk.dtype), 0, final=True)
-            return
-        if block_rows is None:
-            block_rows = sk.l
-        for block in inner.blocks(block_rows):
-            vals = block.values
-            if getattr(vals, "ndim", None) != 2 or vals.shape[1] != n:
-                raise StreamFormatError(
-                    f"block at row {block.first_row_index} has shape {tuple(vals.shape)}, expected (*, {n})")
-            dev_rows = vals.to(sk.device) if is_torch(vals) else torch.from_numpy(
-                np.ascontiguousarray(vals)).to(sk.device)
-            if dev_rows.shape[0]:
-                sk.push(norm(dev_rows), block.first_row_index)
 
 
 def sketch_pass(

@@ -566,3 +566,47 @@ def test_tc_wide_n(l):
     st = P.sketch_pass(P.ArrayRowStream(a), om, precision="tc")
     ref = O.oracle_sketch(O.row_blocks(a, 4096), om.astype(np.float32).astype(np.float64))
     assert rel(st.g, ref.g) <= 2e-5 and rel(st.h, ref.h) <= 2e-5
+
+
+@pytest.mark.parametrize("precision", ["tc", "simt"])
+@pytest.mark.parametrize("m,n,l", [(5000, 1000, 60), (3000, 4096, 120), (2100, 2000, 250), (1000, 96, 16)])
+def test_fused_normalisation_vs_oracle(precision, m, n, l):
+    """spca_sketch_set_normalize: the sketch of normalize_rows(A) — fused into
+    the pass kernel on the tensor-core path — against the oracle sketch of the
+    explicitly normalized rows; rows with offsets, constant and zero rows."""
+    if precision == "tc" and not _tc_ok():
+        pytest.skip("no tensor-core path")
+    rng = np.random.default_rng(m + n)
+    a = (O.gaussian(m, n, seed=m) * rng.uniform(0.1, 10, size=(m, 1)) + rng.normal(0, 30, size=(m, 1)))
+    a = a.astype(np.float32)
+    a[7] = 2.5
+    a[11] = 0.0
+    om = O.gaussian(n, l, seed=n)
+    st = P.sketch_pass(P.NormalizedRowStream(P.ArrayRowStream(a)), om, precision=precision)
+    ref = O.oracle_sketch(O.row_blocks(O.oracle_normalize_rows(a.astype(np.float64)), 4096),
+                          om.astype(np.float32).astype(np.float64))
+    tol = 2e-5
+    assert rel(st.g, ref.g) <= tol, rel(st.g, ref.g)
+    assert rel(st.h, ref.h) <= tol, rel(st.h, ref.h)
+    assert np.abs(st.col_sums - ref.col_sums).max() <= 1e-5 * np.sqrt(m), np.abs(st.col_sums - ref.col_sums).max()
+    assert not np.asarray(st.g)[7].any() and not np.asarray(st.g)[11].any()
+
+
+def test_fused_normalisation_bitwise_and_sources(tmp_path):
+    """Same rows from host, device, pinned and file sources and any push
+    split: bitwise identical normalized sketches; repeatable run to run."""
+    if not _tc_ok():
+        pytest.skip("no tensor-core path")
+    a = (O.gaussian(9000, 700, seed=5) + 3.0).astype(np.float32)
+    om = O.gaussian(700, 40, seed=6)
+    base = P.sketch_pass(P.NormalizedRowStream(P.ArrayRowStream(a)), om)
+    p = tmp_path / "a.spca"
+    P.matfile.write_matrix(p, a, dtype="float32")
+    for src in (P.DeviceRowStream(torch.from_numpy(a).cuda()), P.PinnedRowStream(torch.from_numpy(a)),
+                P.FileRowStream(p, buffer_bytes=777 * 700 * 4),
+                P.GeneratorRowStream(iter([a[:1234], a[1234:5000], a[5000:]]), n_cols=700, dtype=np.float32)):
+        st = P.sketch_pass(P.NormalizedRowStream(src), om)
+        for x, y in ((st.g, base.g), (st.h, base.h), (st.col_sums, base.col_sums)):
+            assert np.array_equal(x, y)
+    again = P.sketch_pass(P.NormalizedRowStream(P.ArrayRowStream(a)), om)
+    assert np.array_equal(again.h, base.h)
