@@ -610,3 +610,57 @@ def test_fused_normalisation_bitwise_and_sources(tmp_path):
             assert np.array_equal(x, y)
     again = P.sketch_pass(P.NormalizedRowStream(P.ArrayRowStream(a)), om)
     assert np.array_equal(again.h, base.h)
+
+
+# ----------------------------------------------------------- edge cases (f)
+def test_empty_file_and_counters(tmp_path):
+    p = tmp_path / "empty.spca"
+    P.matfile.write_matrix(p, np.zeros((0, 8)), dtype="float32")
+    st = P.sketch_pass(P.FileRowStream(p), O.gaussian(8, 4, seed=1))
+    assert st.rows_seen == 0 and np.asarray(st.g).shape == (0, 4)
+    with pytest.raises(P.EmptyStreamError):
+        P.single_pass_pca(P.FileRowStream(p), P.PcaConfig(k=2, oversample=1, block_size=1))
+    # pass counters around a normalized stream, both nestings
+    a = O.gaussian(300, 40, seed=2).astype(np.float32)
+    om = O.gaussian(40, 8, seed=3)
+    outer = P.PassCounter(P.NormalizedRowStream(P.ArrayRowStream(a)))
+    inner = P.PassCounter(P.ArrayRowStream(a))
+    s1 = P.sketch_pass(outer, om)
+    s2 = P.sketch_pass(P.NormalizedRowStream(inner), om)
+    assert outer.passes_completed == 1 and outer.rows_read == 300
+    assert inner.passes_completed == 1 and inner.rows_read == 300
+    assert np.array_equal(s1.h, s2.h)
+
+
+def test_normalize_single_column_and_state_errors():
+    # one column: every row is constant -> the zero row (SIMT: n not a multiple of 4)
+    a = O.gaussian(50, 1, seed=4)
+    st = P.sketch_pass(P.NormalizedRowStream(P.ArrayRowStream(a)), O.gaussian(1, 1, seed=5))
+    assert not np.asarray(st.g).any() and not np.asarray(st.h).any()
+    sk = P.GpuSketch(16, O.gaussian(16, 4, seed=6), np.float32)
+    sk.push(np.ones((3, 16), np.float32), 0)
+    with pytest.raises(P.DeviceError):
+        _lib_set_normalize(sk)
+    sk.close()
+
+
+def _lib_set_normalize(sk):
+    from paper_1704_07669_b200 import _lib
+    _lib.check(sk.lib.spca_sketch_set_normalize(sk.h, 1), sk.h)
+
+
+def test_power_refine_normalized_file(tmp_path):
+    """Two passes over a normalized file stream: the same factorisation as
+    power_refine over the explicitly normalized rows in memory."""
+    rng = np.random.default_rng(7)
+    a = (rng.standard_normal((900, 60)) @ np.diag(1.0 / np.arange(1, 61)) @ rng.standard_normal((60, 256))
+         + rng.normal(0, 2, size=(900, 1))).astype(np.float32)
+    p = tmp_path / "a.spca"
+    P.matfile.write_matrix(p, a, dtype="float32")
+    cfg = P.PcaConfig(k=8, oversample=8, block_size=8, power=1, seed=4)
+    pc = P.PassCounter(P.FileRowStream(p))
+    res = P.power_refine(P.NormalizedRowStream(pc), cfg)
+    want = P.power_refine(O.oracle_normalize_rows(a.astype(np.float64)).astype(np.float32), cfg)
+    assert pc.passes_completed == 2
+    assert rel(res.s, want.s) <= 1e-4
+    assert O.subspace_angle(res.v, want.v) <= 1e-3
