@@ -165,6 +165,7 @@ def run_reference(args):
             rates.append(r)
             times.append(dt)
     value = float(np.mean(rates))
+    one_thread, _ = cpu_oracle_rate(sample_rows // 2, cs["n"], cs["l"], seed=7, threads=1)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(rates),
         "warmup": min(args.warmup, 3), "ms_per_step": 1e3 * float(np.mean(times)),
@@ -173,6 +174,7 @@ def run_reference(args):
         "config": {"workload": f"{args.config} sample", "m": sample_rows, "n": cs["n"], "l": cs["l"],
                    "block_rows": 4096},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "value_1_thread": one_thread,
                          "sample": f"{sample_rows} rows x {cs['n']} fp32 widened to fp64 per step "
                                    "(numpy oracle of sketch.py:52-116, blocked path)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
