@@ -27,7 +27,8 @@ __all__ = [
     "OracleDeficiencyError", "OracleSingularError",
     "sketch_width", "gaussian", "row_blocks", "oracle_sketch", "oracle_center", "oracle_normalize_rows",
     "qr_pos", "solve_upper_t", "thin_svd", "align_signs", "oracle_qb",
-    "oracle_single_pass", "OracleSketch", "OracleQb", "OracleSvd",
+    "oracle_single_pass", "oracle_basic_rand_svd", "oracle_legacy_single_pass",
+    "oracle_lstsq", "STREAM_COSKETCH", "OracleSketch", "OracleQb", "OracleSvd",
     "synth_lowrank_plus_noise", "reference_synth_matrix", "subspace_angle",
 ]
 
@@ -35,6 +36,7 @@ __all__ = [
 RANK_TOL = 1e-12
 # linalg.py:31-35 — Philox substream ids
 STREAM_SKETCH = 0
+STREAM_COSKETCH = 1
 STREAM_FACTOR_U = 2
 STREAM_FACTOR_V = 3
 STREAM_REPAIR = 4
@@ -364,6 +366,91 @@ def oracle_single_pass(
     sv = thin_svd(qb.b)
     u, v = align_signs(qb.q @ sv.u[:, :k], sv.v[:, :k])
     return u, sv.s[:k].copy(), v, mean, st, om
+
+
+def oracle_basic_rand_svd(a, k: int, oversample: int = 10, block_size: int = 10, seed: int = 0,
+                          center: bool = False, block_rows: Optional[int] = None,
+                          omega: Optional[np.ndarray] = None):
+    """algorithms.py:207-263, the two-pass yardstick: pass 1 G = A Omega and
+    col_sums per block (:230-237), optional centering of G (:241-244),
+    Q = orth(G) without rank check (:245), pass 2 B += Q_i^T A_i (:247-250),
+    centering of B (:251-252), SVD of B, U = Q U~ and the sign convention
+    (:254-257). Returns (u, s, v, mean, q, b, omega)."""
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    l = sketch_width(k, oversample, block_size)
+    if m == 0:
+        raise OracleEmptyError("no rows")
+    if k > min(m, n) or l > min(m, n):
+        raise OracleFormatError("k or l exceeds min(m, n)")
+    om = gaussian(n, l, seed, STREAM_SKETCH) if omega is None else np.asarray(omega, np.float64)
+    br = block_rows or l
+    parts, col_sums = [], np.zeros(n)
+    for _, vals in row_blocks(a, br):
+        parts.append(vals @ om)
+        col_sums += vals.sum(axis=0)
+    g = np.vstack(parts)
+    mean = None
+    if center:
+        mean = col_sums / m
+        g = g - np.outer(np.ones(m), mean @ om)
+    q, _ = qr_pos(g, rank_check=False)
+    bm = np.zeros((l, n))
+    for r0, vals in row_blocks(a, br):
+        bm += q[r0:r0 + vals.shape[0]].T @ vals
+    if center:
+        bm -= np.outer(q.sum(axis=0), mean)
+    sv = thin_svd(bm)
+    u, v = align_signs(q @ sv.u[:, :k], sv.v[:, :k])
+    return u, sv.s[:k].copy(), v, mean, q, bm, om
+
+
+def oracle_lstsq(lhs: np.ndarray, rhs: np.ndarray) -> np.ndarray:
+    """np.linalg.lstsq(lhs, rhs, rcond=None) as algorithms.py:364 calls it:
+    LAPACK dgelsd, the minimum-norm solution with singular values below
+    eps * max(M, N) * s_max treated as zero."""
+    return np.linalg.lstsq(lhs, rhs, rcond=None)[0]
+
+
+def oracle_legacy_single_pass(a, k: int, oversample: int = 10, block_size: int = 10, seed: int = 0,
+                              center: bool = False, block_rows: Optional[int] = None,
+                              omega: Optional[np.ndarray] = None,
+                              omega_t: Optional[np.ndarray] = None):
+    """algorithms.py:312-392, the two-sketch one-pass baseline: per block
+    Y_i = A_i Omega, Yt += A_i^T Omega_t[rows] and col_sums (:340-348);
+    centering of Y and Yt (:353-357); Q = orth(Y), Qt = orth(Yt) (:359-360);
+    core = lstsq(Omega_t^T Q, Yt^T Qt) (:361-363); cond of the system
+    (:366); SVD of the core, U = Q U~, V = Qt V~, sign convention
+    (:374-378). Omega_t is Philox(seed, STREAM_COSKETCH) m x l.
+    Returns (u, s, v, mean, cond, y, yt)."""
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    l = sketch_width(k, oversample, block_size)
+    if m == 0:
+        raise OracleEmptyError("no rows")
+    if k > min(m, n) or l > min(m, n):
+        raise OracleFormatError("k or l exceeds min(m, n)")
+    om = gaussian(n, l, seed, STREAM_SKETCH) if omega is None else np.asarray(omega, np.float64)
+    ot = gaussian(m, l, seed, STREAM_COSKETCH) if omega_t is None else np.asarray(omega_t, np.float64)
+    parts, yt, col_sums = [], np.zeros((n, l)), np.zeros(n)
+    for r0, vals in row_blocks(a, block_rows or l):
+        parts.append(vals @ om)
+        yt += vals.T @ ot[r0:r0 + vals.shape[0]]
+        col_sums += vals.sum(axis=0)
+    y = np.vstack(parts)
+    mean = None
+    if center:
+        mean = col_sums / m
+        y = y - np.outer(np.ones(m), mean @ om)
+        yt = yt - np.outer(mean, ot.sum(axis=0))
+    q, _ = qr_pos(y, rank_check=False)
+    qt, _ = qr_pos(yt, rank_check=False)
+    lhs = ot.T @ q
+    core = oracle_lstsq(lhs, yt.T @ qt)
+    cond = float(np.linalg.cond(lhs))
+    sv = thin_svd(core)
+    u, v = align_signs(q @ sv.u[:, :k], qt @ sv.v[:, :k])
+    return u, sv.s[:k].copy(), v, mean, cond, y, yt
 
 
 def reference_synth_matrix(rows: int, cols: int, sigma: np.ndarray, seed: int) -> np.ndarray:

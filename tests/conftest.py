@@ -44,3 +44,14 @@ def has_cuda() -> bool:
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+GOLDEN_ALG = os.path.join(ROOT, "tests", "golden", "golden_alg.npz")
+ALG_CASES = ("f64", "f64c", "f32", "f32c")
+
+
+@pytest.fixture(scope="session")
+def golden_alg():
+    """Reference basic_rand_svd / legacy_single_pass outputs (§8 (f) rank 4,
+    tests/golden/make_golden_alg.py)."""
+    return np.load(GOLDEN_ALG)
