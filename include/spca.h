@@ -166,6 +166,30 @@ int spca_g_colsum(spca_handle_t h, double *out, int out_where);
  * normalized into a workspace first. */
 int spca_sketch_set_normalize(spca_handle_t h, int on);
 
+/* Column shift: with on != 0 the pass sketches A - 1 c^T, c = the pass's
+ * first row (non-finite entries as 0), and finish adds the shift back in
+ * fp64 (G += 1 (Omega^T c)^T, H += col_sums' w^T + c (1^T G')^T + m c w^T, or
+ * H += c (1^T L)^T with a co-sketch operand; col_sums += m c), so the results
+ * are the sketch of A itself. The fp32 accumulators then hold values of the
+ * size of A's deviation from c rather than of A: post-hoc centering
+ * (center_correct, sketch.py:119-139) no longer cancels fp32 rounding of a
+ * large column mean. Must precede the first push of a pass; exclusive with
+ * spca_sketch_set_normalize (SPCA_ERR_CONFIG). */
+int spca_sketch_set_shift(spca_handle_t h, int on);
+
+/* Co-sketch operand: with L set (rows x l row-major float64, device or host),
+ * the pass accumulates H += A_i^T L[first_row .. first_row + rows(A_i)) in
+ * place of A_i^T G_i; G = A Omega and col_sums are formed as usual. This is
+ * the second contraction of the reference's other two passes:
+ *   legacy_single_pass  Yt += vals^T omega_t[r0:r0+rows]   (algorithms.py:344-346)
+ *   basic_rand_svd      B  += q[r0:r0+rows]^T vals          (algorithms.py:247-250, as H = B^T)
+ * L is converted like Omega (rounded to float32 for SPCA_F32) and kept by the
+ * handle across spca_sketch_reset; spca_center_correct then subtracts
+ * mu (1^T L)^T from H (algorithms.py:251-252, 356-357). Must precede the first
+ * push of a pass (SPCA_ERR_STATE); pushing more rows than L has fails with
+ * SPCA_ERR_CAPABILITY. rows = 0 (or left = NULL) restores the plain sketch. */
+int spca_sketch_set_left(spca_handle_t h, const double *left, int64_t rows, int where);
+
 /* normalize_rows (sketch.py:142-153) on device rows: each row minus its
  * mean, divided by its Euclidean norm (a constant row becomes zero), fp64
  * arithmetic; dtype SPCA_F32 / SPCA_F64 for both src and dst (device

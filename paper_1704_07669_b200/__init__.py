@@ -54,6 +54,8 @@ from .algorithms import (
     PcaConfig,
     TruncatedSvd,
     as_row_stream,
+    basic_rand_svd,
+    legacy_single_pass,
     power_refine,
     principal_components,
     single_pass_pca,
@@ -75,7 +77,7 @@ __all__ = [
     "FileRowStream", "FormatError", "GeneratorRowStream", "NormalizedRowStream", "normalize_rows", "GpuSketch", "PassCounter", "PcaConfig",
     "PinnedRowStream", "QbFactor", "RankDeficiencyError", "RowBlock", "RowStream", "ScaleError",
     "SinglePassPCA", "SingularMatrixError", "SketchState", "StreamFormatError", "StreamPcaError", "TruncatedSvd",
-    "as_row_stream", "blocked_qb", "center_correct", "dense_svd", "gaussian_matrix",
+    "as_row_stream", "basic_rand_svd", "blocked_qb", "legacy_single_pass", "center_correct", "dense_svd", "gaussian_matrix",
     "power_refine", "principal_components", "qr_unpivoted", "sign_align", "single_pass_pca",
     "sketch_pass", "solve_rt", "__version__",
 ]

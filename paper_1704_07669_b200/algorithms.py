@@ -140,7 +140,7 @@ def single_pass_pca(
     omega = gaussian_matrix(stream.n_cols, cfg.l, cfg.seed, stream=STREAM_SKETCH)
     state = sketch_pass(stream, omega, block_rows=block_rows, fixed_order=fixed_order,
                         compensated=compensated, precision=precision, device=dev,
-                        keep_on_device=True)
+                        keep_on_device=True, shift=cfg.center)
     if state.rows_seen == 0:
         raise EmptyStreamError("the stream yielded no rows")
     cfg.validate_dims(stream.n_cols, state.rows_seen)
@@ -193,7 +193,7 @@ def power_refine(
     dev = default_device(device)
     omega = gaussian_matrix(stream.n_cols, cfg.l, cfg.seed, stream=STREAM_SKETCH)
     first = sketch_pass(stream, omega, block_rows=block_rows, precision=precision,
-                        device=dev, keep_on_device=True)
+                        device=dev, keep_on_device=True, shift=cfg.center)
     if first.rows_seen == 0:
         raise EmptyStreamError("the stream yielded no rows")
     cfg.validate_dims(stream.n_cols, first.rows_seen)
@@ -202,7 +202,7 @@ def power_refine(
         first = center_correct(first, first.omega)
     omega2 = qr_unpivoted(first.h, rank_check=False, device=dev).q
     second = sketch_pass(stream, omega2.cpu().numpy(), block_rows=block_rows, precision=precision,
-                         device=dev, keep_on_device=True)
+                         device=dev, keep_on_device=True, shift=cfg.center)
     if cfg.center:
         second = center_correct(second, second.omega)
     factor = blocked_qb(second.g, second.h, second.omega, cfg.block_size,
@@ -214,6 +214,154 @@ def power_refine(
         mean = host_copy(mean) if mean is not None else None
     return TruncatedSvd(u=u, s=s, v=v, mean=mean, passes=_measured_passes(stream, 2),
                         retained_floats=retained)
+
+
+def _finish_pair(sk):
+    """Finished state of a GpuSketch as CUDA float64 tensors + rows, handle closed."""
+    try:
+        return sk.finish(on_device=True)
+    finally:
+        sk.close()
+
+
+def basic_rand_svd(
+    data: MatrixOrStream,
+    cfg: PcaConfig,
+    block_rows: Optional[int] = None,
+    *,
+    precision: str = "auto",
+    device=None,
+    return_device: bool = False,
+) -> TruncatedSvd:
+    """Two-pass yardstick (algorithms.py:207-263): pass 1 G = A Omega and the
+    column sums; Q = orth(G) on the GPU (rank check off, :245); pass 2 the
+    same kernels with Q as the co-sketch operand give H = A^T Q = B^T
+    (:247-250); centering of G and B (:241-244, 251-252); SVD of B, U = Q U~,
+    sign convention (:254-257)."""
+    from .errors import CapabilityError
+    torch = torch_mod()
+    stream = as_row_stream(data)
+    if not stream.resettable:
+        raise CapabilityError("basic_rand_svd needs a resettable stream (two passes)")
+    if stream.n_rows == 0:
+        raise EmptyStreamError("the stream has no rows")
+    cfg.validate_dims(stream.n_cols, stream.n_rows)
+    dev = default_device(device)
+    n = stream.n_cols
+    omega = gaussian_matrix(n, cfg.l, cfg.seed, stream=STREAM_SKETCH)
+    sk = run_pass(stream, omega, block_rows=block_rows, precision=precision, device=dev, shift=cfg.center)
+    try:
+        g, _, col_sums, m = sk.finish(on_device=True)
+        if m == 0:
+            raise EmptyStreamError("the stream yielded no rows")
+        cfg.validate_dims(n, m)
+        om = to_device64(_omega_as_used(omega, sk.dtype), dev)
+        mean = None
+        if cfg.center:
+            mean = col_sums / m
+            g = g - (mean @ om)[None, :]
+        q = qr_unpivoted(g, rank_check=False, device=dev).q
+        # pass 2 on the same handle: H = A^T Q (the B^T of B += Q_i^T A_i)
+        run_pass(stream, omega, block_rows=block_rows, precision=precision, device=dev, left=q, sk=sk)
+        _, bt, _, m2 = sk.finish(on_device=True)
+    finally:
+        sk.close()
+    if m2 != m:
+        raise CapabilityError(f"second pass yielded {m2} rows, the first {m}")
+    if cfg.center:
+        bt = bt - torch.outer(mean, q.sum(dim=0))
+    small = dense_svd(bt.T.contiguous())
+    u, v = sign_align(q @ small.u[:, :cfg.k], small.v[:, :cfg.k])
+    s = small.s[:cfg.k].clone()
+    retained = int(m * cfg.l + n * cfg.l + cfg.l * n + n)  # g + omega + b + col_sums (:262)
+    if not return_device:
+        u, s, v = host_copy(u), host_copy(s), host_copy(v)
+        mean = host_copy(mean) if mean is not None else None
+    return TruncatedSvd(u=u, s=s, v=v, mean=mean, passes=_measured_passes(stream, 2),
+                        retained_floats=retained)
+
+
+def _lstsq_min_norm(lhs, rhs):
+    """np.linalg.lstsq(lhs, rhs, rcond=None) (LAPACK dgelsd) on the device:
+    the minimum-norm solution through the SVD of lhs, singular values at or
+    below eps * max(M, N) * s_max dropped. Also returns s (for cond)."""
+    torch = torch_mod()
+    u, s, vh = torch.linalg.svd(lhs, full_matrices=False)
+    cut = float(np.finfo(np.float64).eps) * max(lhs.shape) * s[0]
+    keep = s > cut
+    inv = torch.where(keep, 1.0 / torch.where(keep, s, torch.ones_like(s)), torch.zeros_like(s))
+    return vh.T @ (inv[:, None] * (u.T @ rhs)), s
+
+
+def legacy_single_pass(
+    data: MatrixOrStream,
+    cfg: PcaConfig,
+    block_rows: Optional[int] = None,
+    cond_warn: float = 1e12,
+    *,
+    precision: str = "auto",
+    device=None,
+    return_device: bool = False,
+) -> TruncatedSvd:
+    """Two-sketch one-pass baseline (algorithms.py:312-392): one traversal
+    through the pass kernels with Omega_t = Philox(seed, STREAM_COSKETCH)
+    (m x l) as the co-sketch operand gives Y = A Omega (as G) and
+    Yt = A^T Omega_t (as H); centering (:353-357); Q = orth(Y), Qt = orth(Yt);
+    core = lstsq(Omega_t^T Q, Yt^T Qt) (:361-363) with the conditioning
+    warning (:365-372); SVD of the core, U = Q U~, V = Qt V~ (:374-378)."""
+    import warnings as _warnings
+
+    from .errors import CapabilityError, ConditioningWarning
+    from .linalg import STREAM_COSKETCH
+    torch = torch_mod()
+    stream = as_row_stream(data)
+    m = stream.n_rows
+    if m is None:
+        raise CapabilityError(
+            "legacy_single_pass must know the row count up front to draw its "
+            "left test matrix; wrap the source in a counted or sized stream")
+    if m == 0:
+        raise EmptyStreamError("the stream has no rows")
+    cfg.validate_dims(stream.n_cols, m)
+    dev = default_device(device)
+    n, l = stream.n_cols, cfg.l
+    omega = gaussian_matrix(n, l, cfg.seed, stream=STREAM_SKETCH)
+    omega_t = gaussian_matrix(m, l, cfg.seed, stream=STREAM_COSKETCH)
+    sk = run_pass(stream, omega, block_rows=block_rows, precision=precision, device=dev, left=omega_t,
+                  shift=cfg.center)
+    dtype = sk.dtype
+    y, yt, col_sums, rows_seen = _finish_pair(sk)
+    if rows_seen == 0:
+        raise EmptyStreamError("the stream yielded no rows")
+    if rows_seen != m:
+        raise CapabilityError(f"stream declared {m} rows but yielded {rows_seen}")
+    om = to_device64(_omega_as_used(omega, dtype), dev)
+    ot = to_device64(_omega_as_used(omega_t, dtype), dev)
+    mean = None
+    if cfg.center:
+        mean = col_sums / m
+        y = y - (mean @ om)[None, :]
+        yt = yt - torch.outer(mean, ot.sum(dim=0))
+    q = qr_unpivoted(y, rank_check=False, device=dev).q
+    qt = qr_unpivoted(yt, rank_check=False, device=dev).q
+    lhs = ot.T @ q
+    core, sv = _lstsq_min_norm(lhs, yt.T @ qt)
+    notes: tuple = ()
+    cond = float(sv[0] / sv[-1]) if float(sv[-1]) > 0.0 else float("inf")
+    if cond > cond_warn:
+        msg = (f"co-sketch system is ill-conditioned (cond ~ {cond:.3e}); "
+               f"singular values may be inaccurate")
+        notes = (msg,)
+        _warnings.warn(msg, ConditioningWarning, stacklevel=2)
+    small = dense_svd(core)
+    u, v = sign_align(q @ small.u[:, :cfg.k], qt @ small.v[:, :cfg.k])
+    s = small.s[:cfg.k].clone()
+    retained = int(m * l + n * l + n * l + m * l + n)  # y + yt + omega + omega_t + col_sums (:383)
+    if not return_device:
+        u, s, v = host_copy(u), host_copy(s), host_copy(v)
+        mean = host_copy(mean) if mean is not None else None
+    return TruncatedSvd(u=u, s=s, v=v, mean=mean, passes=_measured_passes(stream, 1),
+                        retained_floats=retained, warnings=notes)
 
 
 def principal_components(svd: TruncatedSvd) -> list:

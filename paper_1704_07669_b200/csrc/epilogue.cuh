@@ -169,6 +169,84 @@ __global__ void norm_correct(double *__restrict__ hcs, int n, int l, const doubl
   }
 }
 
+// Column shift (spca_sketch_set_shift): c = the pass's first row with
+// non-finite values replaced by 0, fp32, zero padded to `pad` entries.
+template <typename T>
+__global__ void shift_capture(const T *__restrict__ row, int n, int pad, float *__restrict__ c) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < pad; j += gridDim.x * blockDim.x) {
+    float v = j < n ? (float)row[j] : 0.f;
+    c[j] = isfinite(v) ? v : 0.f;
+  }
+}
+
+// dst = src - 1 c^T on `rows` rows (SIMT path: the shifted chunk in a workspace)
+template <typename T>
+__global__ void shift_rows(const T *__restrict__ src, int64_t rows, int n, int64_t lds, const float *__restrict__ c,
+                           T *__restrict__ dst, int64_t ldd) {
+  const int64_t total = rows * n;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / n;
+    const int j = (int)(idx - r * n);
+    dst[r * ldd + j] = src[r * lds + j] - (T)c[j];
+  }
+}
+
+// w[j] = sum_i c[i] Omega[i][j] (fp64, Omega as used), one block per column;
+// gs[j] = sum_r X[r][j] over the finished (shifted) G or the co-sketch operand
+__global__ void shift_terms(const float *__restrict__ c, const double *__restrict__ om, int n, int l,
+                            const double *__restrict__ x, int64_t rows, double *__restrict__ w,
+                            double *__restrict__ gs) {
+  __shared__ double red[2][256];
+  const int j = blockIdx.x;
+  double s = 0.0, t = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += (double)c[i] * om[(int64_t)i * l + j];
+  for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) t += x[r * l + j];
+  red[0][threadIdx.x] = s;
+  red[1][threadIdx.x] = t;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + o];
+      red[1][threadIdx.x] += red[1][threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    w[j] = red[0][0];
+    gs[j] = red[1][0];
+  }
+}
+
+// Undo the shift at finish (A = A' + 1 c^T, G = G' + 1 w^T, w = Omega^T c):
+//   plain    H = H' + colsum' w^T + c gsum'^T + m c w^T
+//   co-sketch H = H' + c lsum^T
+//   colsum = colsum' + m c;  G += 1 w^T (separately, g_add_row)
+__global__ void shift_fix_h(double *__restrict__ hcs, int n, int l, const float *__restrict__ c,
+                            const double *__restrict__ w, const double *__restrict__ gs, int64_t m,
+                            int cosketch) {
+  const int64_t nl = (int64_t)n * l;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < nl;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / l;
+    const int j = (int)(idx - i * l);
+    const double ci = (double)c[i];
+    hcs[idx] += cosketch ? ci * gs[j] : hcs[nl + i] * w[j] + ci * gs[j] + (double)m * ci * w[j];
+  }
+}
+
+__global__ void shift_fix_colsum(double *__restrict__ colsum, int n, const float *__restrict__ c, int64_t m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) colsum[i] += (double)m * (double)c[i];
+}
+
+__global__ void g_add_row(double *__restrict__ g, int64_t rows, int l, const double *__restrict__ w) {
+  const int64_t total = rows * l;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    g[idx] += w[idx % l];
+}
+
 // fp64 column sums of Omega (as used) -> fp32, zero padded to lpad
 __global__ void omega_colsums(const double *__restrict__ om, int n, int l, int lpad, float *__restrict__ out) {
   __shared__ double red[256];

@@ -63,6 +63,14 @@ struct spca_sketch {
   double *row_coef = nullptr;    // TC: [rows] (mean - a0) / norm of every row pushed
   int64_t row_coef_cap = 0;
   float *wsum = nullptr;         // TC: [lpad] column sums of Omega (as used)
+  // co-sketch operand (spca_sketch_set_left): H += A_i^T L_i instead of A_i^T G_i
+  void *left_dev = nullptr;      // rows x lpad compute precision (zero padded)
+  double *left64_dev = nullptr;  // rows x l fp64, exactly the values used
+  int64_t left_rows = 0;         // 0 = no left operand (the plain sketch)
+  // column shift (spca_sketch_set_shift): the pass sketches A - 1 c^T, c = its first row
+  bool shift_on = false;
+  bool shift_set = false;        // c captured for this pass
+  float *cshift = nullptr;       // round_up(n, 128) fp32, zero padded
   int num_sms = 148;
   int max_pairs = 74;             // co-resident CTA pairs of the pass kernel
   unsigned long long *bad_dev = nullptr;

@@ -83,6 +83,10 @@ struct FusedArgs {
   float *gT;                // [kSlots][2][LPAD][R0] G^T hi, lo
   float *g_out;             // G rows of this launch, [rows][LPAD]
   float *hpart;             // [n][LPAD] running H (fp32, flushed to fp64 by the host)
+  const float *cshift;      // column shift c (zero padded to a multiple of 128) or null:
+                            //   every value a[r][j] enters as a[r][j] - c[j] (spca_sketch_set_shift)
+  const float *left;        // co-sketch operand rows of this launch ([rows][gld]) or null:
+                            //   the H units then take L instead of G (spca_sketch_set_left)
   double *colsum;           // [n] running column sums (fp64)
   double *carry;            // [n] Kahan carry, or null
   int *seg_cnt;             // [C][2T] partials written per tile
@@ -220,7 +224,7 @@ struct PairBars {
   uint32_t tmem_base;
 };
 
-template <int LPAD, bool NORM>
+template <int LPAD, bool NORM, bool SHIFT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<LPAD>::THREADS, 1)
 tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ CUtensorMap tAh,
                const __grid_constant__ CUtensorMap tWhi, const __grid_constant__ CUtensorMap tWlo,
@@ -477,6 +481,14 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
               const float4 x = ptx::lds128(row + ((q4 ^ (t & 7)) << 4));
               v[4 * q4] = x.x; v[4 * q4 + 1] = x.y; v[4 * q4 + 2] = x.z; v[4 * q4 + 3] = x.w;
             }
+            if (SHIFT) {  // column shift (zero beyond n: padded)
+              const float4 *cp = reinterpret_cast<const float4 *>(args.cshift + (f.k0 + kb) * 32);
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4) {
+                const float4 c4 = __ldg(cp + q4);
+                v[4 * q4] -= c4.x; v[4 * q4 + 1] -= c4.y; v[4 * q4 + 2] -= c4.z; v[4 * q4 + 3] -= c4.w;
+              }
+            }
             if (NORM) {  // d = a - a0 on the row's real columns; d, d^2 pairwise then Kahan
               const int col0 = (f.k0 + kb) * 32;
               float p1[16], p2[16];
@@ -506,6 +518,12 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             const uint32_t raw = ptx::smem_u32(smem + s * C::A_BYTES + t * 4);  // column t
 #pragma unroll
             for (int kq = 0; kq < 32; ++kq) v[kq] = ptx::lds32(raw + kq * 512);
+            if (SHIFT) {  // column shift on the chunk's real rows only
+              const float cj = __ldg(args.cshift + (2 * f.a + (int)rank) * 128 + t);
+              const int r0 = (f.k0 + kb) * 32;
+#pragma unroll
+              for (int kq = 0; kq < 32; ++kq) v[kq] = r0 + kq < f.rows ? v[kq] - cj : 0.f;
+            }
             float p16[16];  // pairwise sum of the 32 values, then one Kahan step
             if (NORM) {  // d = a - a0 per row; the column sum weights rows by 1/norm
               const uint32_t st_ = ptx::smem_u32(&sst[s][0]);
@@ -756,6 +774,11 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             const bool valid = rc < f.rows;
             float a4[4] = {acc.x, acc.y, acc.z, acc.w};
             float b4[4] = {acc.x, acc.y, acc.z, acc.w};  // B operand of the H units
+            if (args.left != nullptr && valid) {  // co-sketch: H += A^T L
+              const float4 l4 = __ldg(reinterpret_cast<const float4 *>(
+                                          args.left + ((int64_t)f.c * sc.R0 + rc) * args.gld) + q);
+              b4[0] = l4.x; b4[1] = l4.y; b4[2] = l4.z; b4[3] = l4.w;
+            }
             if (NORM) {  // G_hat = (d Omega - mean_d * 1^T Omega) / norm; the H units take G_hat / norm
               const float md = sl_stat[r][0], inv = sl_stat[r][1];
               const float4 w4 = __ldg(reinterpret_cast<const float4 *>(args.wsum) + q);
@@ -763,7 +786,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 a4[j] = fmaf(-md, ws[j], a4[j]) * inv;
-                b4[j] = a4[j] * inv;
+                b4[j] = (args.left != nullptr ? b4[j] : a4[j]) * inv;
               }
             }
             if (valid)

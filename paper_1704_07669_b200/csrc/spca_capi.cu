@@ -199,12 +199,14 @@ int simt_chunk(spca_sketch *h, const T *a, int64_t lda, int rows) {
   }
   int rseg = (int)round_up(ceil_div(rows, h->hsplit), 32);
   int acc = h->chunks_since_flush > 0 ? 1 : 0;
+  // co-sketch: the H contraction takes the left operand's rows instead of G
+  const T *hop = h->left_rows ? (const T *)h->left_dev + h->rows_done * h->lpad : gout;
   if (narrow) {
-    if (vec) launch_h<T, 128, 32, true>(h, a, lda, rows, gout, rseg, acc);
-    else launch_h<T, 128, 32, false>(h, a, lda, rows, gout, rseg, acc);
+    if (vec) launch_h<T, 128, 32, true>(h, a, lda, rows, hop, rseg, acc);
+    else launch_h<T, 128, 32, false>(h, a, lda, rows, hop, rseg, acc);
   } else {
-    if (vec) launch_h<T, 64, 64, true>(h, a, lda, rows, gout, rseg, acc);
-    else launch_h<T, 64, 64, false>(h, a, lda, rows, gout, rseg, acc);
+    if (vec) launch_h<T, 64, 64, true>(h, a, lda, rows, hop, rseg, acc);
+    else launch_h<T, 64, 64, false>(h, a, lda, rows, hop, rseg, acc);
   }
   CK_LAUNCH(h);
   return SPCA_OK;
@@ -279,6 +281,17 @@ int process_chunk(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
     if (!h->norm_ws) CK(h, dalloc(h, &h->norm_ws, (size_t)h->chunk_rows * h->n * h->ds));
     CK(h, launch_normalize(a, rows, h->n, lda, h->norm_ws, h->n, h->dtype, h->stream));
     h->launches++;
+    a = h->norm_ws;
+    lda = h->n;
+  } else if (h->shift_on) {  // column shift: the chunk minus 1 c^T into a workspace
+    if (!h->norm_ws) CK(h, dalloc(h, &h->norm_ws, (size_t)h->chunk_rows * h->n * h->ds));
+    if (h->dtype == SPCA_F32)
+      shift_rows<float><<<grid_for(rows * h->n), 256, 0, h->stream>>>((const float *)a, rows, (int)h->n, lda,
+                                                                      h->cshift, (float *)h->norm_ws, h->n);
+    else
+      shift_rows<double><<<grid_for(rows * h->n), 256, 0, h->stream>>>((const double *)a, rows, (int)h->n, lda,
+                                                                       h->cshift, (double *)h->norm_ws, h->n);
+    CK_LAUNCH(h);
     a = h->norm_ws;
     lda = h->n;
   }
@@ -606,8 +619,30 @@ int push_impl(spca_handle_t h, const void *a, int64_t rows, int64_t ld, int64_t 
   if (rows > 0 && ld < h->n)
     return set_err(h, SPCA_ERR_FORMAT, first_row, "block at row %lld has row stride %lld < n=%lld",
                    (long long)first_row, (long long)ld, (long long)h->n);
+  if (h->left_rows && h->rows_seen + rows > h->left_rows)
+    return set_err(h, SPCA_ERR_CAPABILITY, first_row,
+                   "stream yielded more rows than the co-sketch operand has (%lld)", (long long)h->left_rows);
   DeviceGuard dg(h->device);
   int rc = SPCA_OK;
+  if (h->shift_on && !h->shift_set && rows > 0) {  // c = the pass's first row
+    const int pad = (int)round_up(h->n, 256);
+    const void *src = a;
+    void *tmp = nullptr;
+    if (where != SPCA_MEM_DEVICE) {
+      CK(h, dalloc(h, &tmp, (size_t)h->n * h->ds));
+      CK(h, cudaMemcpyAsync(tmp, a, (size_t)h->n * h->ds, cudaMemcpyHostToDevice, h->stream));
+      src = tmp;
+    }
+    if (h->dtype == SPCA_F32)
+      shift_capture<float><<<(unsigned)ceil_div(pad, 256), 256, 0, h->stream>>>((const float *)src, (int)h->n, pad,
+                                                                                h->cshift);
+    else
+      shift_capture<double><<<(unsigned)ceil_div(pad, 256), 256, 0, h->stream>>>((const double *)src, (int)h->n,
+                                                                                 pad, h->cshift);
+    CK_LAUNCH(h);
+    dfree(h, tmp);
+    h->shift_set = true;
+  }
   if (rows == 0) {
     // final push of nothing: still flush the staged tail now
   } else if (where == SPCA_MEM_DEVICE) {
@@ -648,7 +683,66 @@ int spca_sketch_set_normalize(spca_handle_t h, int on) {
   if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
   if (h->rows_seen > 0 || h->tail_rows > 0 || h->rows_done > 0)
     return set_err(h, SPCA_ERR_STATE, -1, "set_normalize must precede the first push of a pass");
+  if (on && h->shift_on)
+    return set_err(h, SPCA_ERR_CONFIG, -1, "the column shift and row normalisation are exclusive");
   h->normalize = on != 0;
+  return SPCA_OK;
+}
+
+int spca_sketch_set_shift(spca_handle_t h, int on) {
+  if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
+  if (h->rows_seen > 0 || h->tail_rows > 0 || h->rows_done > 0)
+    return set_err(h, SPCA_ERR_STATE, -1, "set_shift must precede the first push of a pass");
+  if (on && h->normalize)
+    return set_err(h, SPCA_ERR_CONFIG, -1, "the column shift and row normalisation are exclusive");
+  if (on && !h->cshift) {
+    DeviceGuard dg(h->device);
+    CK(h, dalloc(h, &h->cshift, (size_t)round_up(h->n, 256) * sizeof(float)));
+    CK(h, cudaMemsetAsync(h->cshift, 0, (size_t)round_up(h->n, 256) * sizeof(float), h->stream));
+  }
+  h->shift_on = on != 0;
+  h->shift_set = false;
+  return SPCA_OK;
+}
+
+int spca_sketch_set_left(spca_handle_t h, const double *left, int64_t rows, int where) {
+  if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
+  if (h->rows_seen > 0 || h->tail_rows > 0 || h->rows_done > 0)
+    return set_err(h, SPCA_ERR_STATE, -1, "set_left must precede the first push of a pass");
+  if (rows < 0 || (rows > 0 && !left)) return set_err(h, SPCA_ERR_FORMAT, -1, "bad left operand (%lld rows)", (long long)rows);
+  if (rows > INT32_MAX / 2) return set_err(h, SPCA_ERR_CONFIG, -1, "left operand too tall");
+  DeviceGuard dg(h->device);
+  if (rows > h->left_rows || rows == 0) {
+    dfree(h, h->left_dev);
+    dfree(h, h->left64_dev);
+    h->left_dev = nullptr;
+    h->left64_dev = nullptr;
+  }
+  h->left_rows = 0;
+  if (rows == 0) return SPCA_OK;
+  if (!h->left_dev) {
+    CK(h, dalloc(h, &h->left_dev, (size_t)rows * h->lpad * h->ds));
+    CK(h, dalloc(h, &h->left64_dev, (size_t)rows * h->l * 8));
+  }
+  const double *src = left;
+  double *tmp = nullptr;
+  if (where != SPCA_MEM_DEVICE) {
+    CK(h, dalloc(h, &tmp, (size_t)rows * h->l * 8));
+    CK(h, cudaMemcpyAsync(tmp, left, (size_t)rows * h->l * 8, cudaMemcpyHostToDevice, h->stream));
+    src = tmp;
+  }
+  // same conversion as Omega: compute-precision copy (rows x lpad) + the fp64 values used
+  if (h->dtype == SPCA_F32)
+    omega_prepare<float><<<grid_for(rows * h->lpad), 256, 0, h->stream>>>(
+        src, (int)rows, (int)h->l, (int)h->lpad, (float *)h->left_dev, h->left64_dev);
+  else
+    omega_prepare<double><<<grid_for(rows * h->lpad), 256, 0, h->stream>>>(
+        src, (int)rows, (int)h->l, (int)h->lpad, (double *)h->left_dev, h->left64_dev);
+  CK_LAUNCH(h);
+  dfree(h, tmp);
+  // a pageable source must not be released before the copy has read it
+  if (where != SPCA_MEM_DEVICE) CK(h, cudaStreamSynchronize(h->stream));
+  h->left_rows = rows;
   return SPCA_OK;
 }
 
@@ -665,6 +759,7 @@ int spca_sketch_reset(spca_handle_t h) {
   h->rows_seen = 0;
   h->rows_done = 0;
   h->chunks_since_flush = 0;
+  h->shift_set = false;
   h->finished = false;
   h->final_pushed = false;
   h->last_code = SPCA_OK;
@@ -722,12 +817,31 @@ int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out, double *co
                                                                 h->rows_seen, (int)h->l, h->g64_dev);
       CK_LAUNCH(h);
     }
+    if (h->shift_on && h->shift_set && h->rows_seen > 0) {
+      // undo the column shift in fp64 (epilogue.cuh shift_fix_h): G, H, col_sums of A itself
+      double *wg = nullptr;
+      CK(h, dalloc(h, &wg, (size_t)2 * h->l * 8));
+      const bool co = h->left_rows > 0;
+      shift_terms<<<(unsigned)h->l, 256, 0, h->stream>>>(h->cshift, h->omega64_dev, (int)h->n, (int)h->l,
+                                                          co ? h->left64_dev : h->g64_dev, h->rows_seen, wg,
+                                                          wg + h->l);
+      CK_LAUNCH(h);
+      shift_fix_h<<<grid_for(h->n * h->l), 256, 0, h->stream>>>(h->hcs_dev, (int)h->n, (int)h->l, h->cshift, wg,
+                                                                 wg + h->l, h->rows_seen, co ? 1 : 0);
+      CK_LAUNCH(h);
+      shift_fix_colsum<<<(unsigned)ceil_div(h->n, 256), 256, 0, h->stream>>>(h->hcs_dev + h->n * h->l, (int)h->n,
+                                                                             h->cshift, h->rows_seen);
+      CK_LAUNCH(h);
+      g_add_row<<<grid_for(h->rows_seen * h->l), 256, 0, h->stream>>>(h->g64_dev, h->rows_seen, (int)h->l, wg);
+      CK_LAUNCH(h);
+      dfree(h, wg);
+    }
     if (h->normalize && h->precision == SPCA_PREC_TC && h->rows_seen > 0) {
       // fused normalisation: H -= 1 (G_hat^T coef)^T, colsum -= sum(coef) (sketch_fused.cuh)
       double *c = nullptr;
       CK(h, dalloc(h, &c, (size_t)(h->l + 1) * 8));
-      norm_coef_sums<<<(unsigned)(h->l + 1), 256, 0, h->stream>>>(h->g64_dev, h->rows_seen, (int)h->l,
-                                                                   h->row_coef, c);
+      norm_coef_sums<<<(unsigned)(h->l + 1), 256, 0, h->stream>>>(h->left_rows ? h->left64_dev : h->g64_dev,
+                                                                   h->rows_seen, (int)h->l, h->row_coef, c);
       CK_LAUNCH(h);
       norm_correct<<<grid_for(h->n * (h->l + 1)), 256, 0, h->stream>>>(h->hcs_dev, (int)h->n, (int)h->l, c);
       CK_LAUNCH(h);
@@ -817,7 +931,9 @@ int spca_center_correct(spca_handle_t h, int64_t m_total, const double *gsum, do
   if (gsum) {
     CK(h, cudaMemcpyAsync(gs, gsum, (size_t)l * 8, cudaMemcpyDefault, h->stream));
   } else {
-    column_sums64<<<(unsigned)l, 256, 0, h->stream>>>(h->g64_dev, h->rows_seen, (int)l, gs);
+    // 1^T of the H operand: G, or the co-sketch operand's rows that were pushed
+    column_sums64<<<(unsigned)l, 256, 0, h->stream>>>(h->left_rows ? h->left64_dev : h->g64_dev,
+                                                      h->rows_seen, (int)l, gs);
     CK_LAUNCH(h);
   }
   if (h->rows_seen > 0) {
@@ -914,7 +1030,7 @@ void spca_sketch_destroy(spca_handle_t h) {
     void *pooled[] = {h->omega_dev, h->omega64_dev, h->tc_omega, h->g_dev, h->g64_dev, h->hcs_dev,
                       h->carry_dev, h->hpart, h->cspart, h->gpart, h->tc_ws, h->bad_dev, h->tail,
                       h->trace, h->tc_ctr, h->order_dev, h->norm_ws, h->rstat_part, h->row_a0,
-                      h->row_inv, h->row_coef, h->wsum};
+                      h->row_inv, h->row_coef, h->wsum, h->left_dev, h->left64_dev, h->cshift};
     for (void *p : pooled) dfree(h, p);
   }
   for (void *p : {h->dstage[0], h->dstage[1]})

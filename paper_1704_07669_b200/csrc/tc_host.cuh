@@ -119,7 +119,7 @@ template <int LPAD>
 int tc_set_smem_attrs() {
   static bool done = false;
   if (done) return 0;
-  for (auto k : {tc_pass_kernel<LPAD, false>, tc_pass_kernel<LPAD, true>})
+  for (auto k : {tc_pass_kernel<LPAD, false>, tc_pass_kernel<LPAD, true>, tc_pass_kernel<LPAD, false, true>})
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcCfg<LPAD>::SMEM) !=
         cudaSuccess)
       return 1;
@@ -357,6 +357,8 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   args.gT = (float *)h->tc_ws;
   args.g_out = (float *)h->g_dev + h->rows_done * h->lpad + grp * h->tc_lp;
   args.hpart = (float *)h->hpart + grp * h->tc_lp;
+  args.cshift = h->shift_on ? h->cshift : nullptr;
+  args.left = h->left_rows ? (const float *)h->left_dev + h->rows_done * h->lpad + grp * h->tc_lp : nullptr;
   if (h->normalize) {
     args.norm = 1;
     args.rstat_part = reinterpret_cast<float *>(h->rstat_part);
@@ -381,8 +383,12 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   args.bad_row = h->bad_dev;
   args.trace = h->trace;
   args.dbg = h->tc_debug;
-  auto kern = h->tc_lp == 64 ? (h->normalize ? tc_pass_kernel<64, true> : tc_pass_kernel<64, false>)
-                              : (h->normalize ? tc_pass_kernel<128, true> : tc_pass_kernel<128, false>);
+  // instantiations: plain, fused row normalisation, column shift (exclusive modes)
+  auto kern = h->tc_lp == 64
+                  ? (h->normalize ? tc_pass_kernel<64, true>
+                                  : (h->shift_on ? tc_pass_kernel<64, false, true> : tc_pass_kernel<64, false>))
+                  : (h->normalize ? tc_pass_kernel<128, true>
+                                  : (h->shift_on ? tc_pass_kernel<128, false, true> : tc_pass_kernel<128, false>));
   const unsigned threads = h->tc_lp == 64 ? TcCfg<64>::THREADS : TcCfg<128>::THREADS;
   const unsigned smem = h->tc_lp == 64 ? TcCfg<64>::SMEM : TcCfg<128>::SMEM;
   kern<<<grid, threads, smem, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, args);

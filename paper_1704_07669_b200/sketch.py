@@ -61,7 +61,7 @@ class GpuSketch:
 
     def __init__(self, n: int, omega: np.ndarray, dtype, precision: str = "auto",
                  device=None, rows_hint: int = 0, compensated: bool = False, stream=None,
-                 normalize: bool = False):
+                 normalize: bool = False, shift: bool = False):
         torch = torch_mod()
         self.lib = _lib.load()
         self.device = default_device(device)
@@ -90,10 +90,35 @@ class GpuSketch:
         self.h = handle
         if normalize:  # rows are sketched as normalize_rows leaves them (fused on the TC path)
             _lib.check(self.lib.spca_sketch_set_normalize(self.h, 1), self.h)
+        elif shift:  # accumulate A - 1 c^T (c = first row), shift undone in fp64 at finish
+            _lib.check(self.lib.spca_sketch_set_shift(self.h, 1), self.h)
         self._keep = []          # host/device sources that must outlive async copies
         self._finished = False
         # what "auto" resolved to: "tc" (tcgen05 3xTF32) or "simt" (FFMA / DFMA)
         self.precision = "tc" if self.lib.spca_sketch_precision(self.h) == _PRECISIONS["tc"] else "simt"
+
+    def set_left(self, left) -> None:
+        """Co-sketch operand L (m x l float64, numpy or CUDA tensor): the pass
+        then accumulates H += A_i^T L[rows of A_i] in place of A_i^T G_i
+        (spca_sketch_set_left) — legacy_single_pass's Yt and basic_rand_svd's
+        B^T. ``None`` restores the plain sketch. Before the first push."""
+        torch = torch_mod()
+        if left is None:
+            _lib.check(self.lib.spca_sketch_set_left(self.h, None, 0, _lib.MEM_DEVICE), self.h)
+            return
+        if is_torch(left):
+            t = left.to(device=self.device, dtype=torch.float64).contiguous()
+            if t.dim() != 2 or t.shape[1] != self.l:
+                raise StreamFormatError(f"left operand has shape {tuple(t.shape)}, expected (*, {self.l})")
+            _lib.check(self.lib.spca_sketch_set_left(self.h, ctypes.c_void_p(t.data_ptr()), int(t.shape[0]),
+                                                     _lib.MEM_DEVICE), self.h)
+            self._left = t  # the conversion kernel reads it in stream order
+        else:
+            a = np.ascontiguousarray(np.asarray(left, dtype=np.float64))
+            if a.ndim != 2 or a.shape[1] != self.l:
+                raise StreamFormatError(f"left operand has shape {a.shape}, expected (*, {self.l})")
+            _lib.check(self.lib.spca_sketch_set_left(self.h, ctypes.c_void_p(a.ctypes.data), int(a.shape[0]),
+                                                     _lib.MEM_PAGEABLE), self.h)
 
     # -- pushing ------------------------------------------------------------
     def push(self, values, first_row: int, final: bool = False) -> int:
@@ -219,9 +244,13 @@ def _omega_as_used(omega: np.ndarray, dtype) -> np.ndarray:
 
 
 def run_pass(stream, omega, block_rows=None, compensated=False, precision="auto",
-             device=None, keep=None):
+             device=None, keep=None, left=None, sk=None, shift=False):
     """Drive one traversal of ``stream`` through a GpuSketch; returns the
-    finished GpuSketch (state still on the device)."""
+    finished GpuSketch (state still on the device). ``left`` sets a co-sketch
+    operand (GpuSketch.set_left); ``sk`` reuses an open handle of the same
+    shape for another traversal (reset first). ``shift`` turns on the column
+    shift (spca_sketch_set_shift) — what the centered algorithms ask for, so
+    post-hoc centering does not cancel fp32 rounding of a large mean."""
     om = np.asarray(omega)
     n, l = om.shape
     outer = stream
@@ -234,8 +263,14 @@ def run_pass(stream, omega, block_rows=None, compensated=False, precision="auto"
     else:
         src = outer  # a PassCounter counts its own traversal
     dtype = np.dtype(getattr(src, "dtype", np.float64))
-    sk = GpuSketch(n, om, dtype, precision=precision, device=device,
-                   rows_hint=src.n_rows or 0, compensated=compensated, normalize=normalize)
+    if sk is None:
+        sk = GpuSketch(n, om, dtype, precision=precision, device=device,
+                       rows_hint=src.n_rows or 0, compensated=compensated, normalize=normalize,
+                       shift=shift and not normalize)
+    else:
+        sk.reset()
+    if left is not None:
+        sk.set_left(left)
     fs = _file_source(src)
     if fs is not None:
         _push_file(sk, fs)
@@ -431,6 +466,7 @@ def sketch_pass(
     precision: str = "auto",
     device=None,
     keep_on_device: bool = False,
+    shift: bool = False,
 ) -> SketchState:
     """Accumulate the sketch of the streamed matrix in exactly one pass
     (sketch.py:52-116), on the GPU.
@@ -439,7 +475,10 @@ def sketch_pass(
     (sketch.py:76-77). ``fixed_order`` is accepted for signature parity: the
     device path is always order-fixed — bitwise identical for every block
     size and run to run — which is the property fixed_order buys on the CPU.
-    ``compensated`` enables Kahan summation of col_sums across chunks."""
+    ``compensated`` enables Kahan summation of col_sums across chunks.
+    ``shift`` accumulates A - 1 c^T (c = the first row) and adds the shift
+    back in fp64: same results, fp32 accumulators sized by A's spread rather
+    than its mean (the centered algorithms turn it on)."""
     om = np.asarray(omega, dtype=np.float64)
     if om.ndim != 2:
         raise StreamFormatError("omega must be 2-d")
@@ -447,7 +486,7 @@ def sketch_pass(
     if stream.n_cols != n:
         raise StreamFormatError(f"stream has {stream.n_cols} columns but omega has {n} rows")
     sk = run_pass(stream, om, block_rows=block_rows, compensated=compensated,
-                  precision=precision, device=device)
+                  precision=precision, device=device, shift=shift)
     try:
         g, h, cs, m = sk.finish(on_device=keep_on_device)
     finally:

@@ -58,9 +58,10 @@ with threadpool_limits(limits=1):
         out[f"{name}_legacy_meta"] = np.array([r.passes, r.retained_floats, len(r.warnings)])
         if center:
             out[f"{name}_legacy_mean"] = r.mean
-    # the conditioning warning (algorithms.py:366-372): rank-3 data, and a
+    # the conditioning warning (algorithms.py:366-372): full-rank data (so Q,
+    # Qt and the condition number are determined, not rounding noise) and a
     # threshold the co-sketch system's condition number exceeds
-    a = gaussian(200, 3, seed=31) @ gaussian(3, 60, seed=32)
+    a = gaussian(200, 60, seed=31) * np.exp(-np.arange(60) / 6.0)
     out["ill_a"] = a
     cfg = sp.PcaConfig(k=5, oversample=15, block_size=5, seed=7)
     with warnings.catch_warnings(record=True) as w:

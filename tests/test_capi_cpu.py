@@ -158,3 +158,20 @@ def test_product_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle\b", src, re.M), f
+
+
+def test_basic_and_legacy_stream_contracts_before_the_device():
+    """CapabilityError for a one-shot stream (basic_rand_svd, algorithms.py:218-219)
+    and for an unknown row count (legacy_single_pass, :326-331) — raised before
+    any device work, as the reference does."""
+    import numpy as np
+    import paper_1704_07669_b200 as P
+
+    def gen():
+        yield np.zeros((3, 4))
+    cfg = P.PcaConfig(k=1, oversample=1, block_size=1)
+    one_shot = P.GeneratorRowStream(gen(), n_cols=4)
+    with pytest.raises(P.CapabilityError, match="resettable"):
+        P.basic_rand_svd(one_shot, cfg)
+    with pytest.raises(P.CapabilityError, match="row count up front"):
+        P.legacy_single_pass(P.GeneratorRowStream(gen(), n_cols=4), cfg)

@@ -1,0 +1,356 @@
+"""§8(f) rank 4 on the GPU: the co-sketch operand (spca_sketch_set_left) and
+the two algorithms built on it — basic_rand_svd (algorithms.py:207-263) and
+legacy_single_pass (algorithms.py:312-392) — against the oracle and the
+reference's own outputs (golden_alg.npz). Bars as BASELINE.json: fp64 1e-10
+on singular values and principal angles (1e-12 on raw sketches), fp32 1e-4."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import ALG_CASES
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_1704_07669_b200 as P  # noqa: E402
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _tc_ok():
+    try:
+        P.GpuSketch(64, np.ones((64, 16)), np.float32, precision="tc").close()
+        return True
+    except Exception:
+        return False
+
+
+def _precisions(dtype):
+    if dtype == np.float64:
+        return ["auto"]
+    return ["simt", "tc"] if _tc_ok() else ["simt"]
+
+
+# ------------------------------------------------------------ co-sketch pass
+@pytest.mark.parametrize("dtype,precision,m,n,l", [
+    (np.float64, "simt", 700, 90, 12),
+    (np.float32, "simt", 3000, 500, 40),
+    (np.float32, "tc", 5000, 1000, 60),
+    (np.float32, "tc", 3000, 4096, 120),
+    (np.float32, "tc", 2100, 2000, 250),
+])
+def test_cosketch_vs_oracle(dtype, precision, m, n, l):
+    """H = A^T L with L the co-sketch operand; G = A Omega and col_sums as usual."""
+    if precision == "tc" and not _tc_ok():
+        pytest.skip("no tensor-core path")
+    a = O.gaussian(m, n, seed=m + 1).astype(dtype)
+    om = O.gaussian(n, l, seed=n + 2)
+    left = O.gaussian(m, l, seed=l + 3)
+    sk = P.GpuSketch(n, om, dtype, precision=precision)
+    sk.set_left(left)
+    sk.push(a, 0, final=True)
+    g, h, cs, rows = sk.finish(on_device=False)
+    sk.close()
+    a64 = a.astype(np.float64)
+    used = (lambda x: x.astype(np.float32).astype(np.float64)) if dtype == np.float32 else (lambda x: x)
+    tol = 1e-12 if dtype == np.float64 else 2e-5
+    assert rows == m
+    assert rel(g, a64 @ used(om)) <= tol
+    assert rel(h, a64.T @ used(left)) <= tol
+    assert np.allclose(cs, a64.sum(axis=0), rtol=1e-5, atol=1e-4)
+
+
+def test_cosketch_block_independent_and_reset():
+    """Any push split gives bitwise the same H; reset keeps L; set_left(None)
+    restores the plain sketch."""
+    if not _tc_ok():
+        pytest.skip("no tensor-core path")
+    m, n, l = 9000, 700, 60
+    a = O.gaussian(m, n, seed=8).astype(np.float32)
+    om, left = O.gaussian(n, l, seed=9), O.gaussian(m, l, seed=10)
+    sk = P.GpuSketch(n, om, np.float32, precision="tc")
+    sk.set_left(left)
+    sk.push(a, 0, final=True)
+    _, h1, _, _ = sk.finish(on_device=False)
+    sk.reset()
+    for r0 in range(0, m, 1777):
+        sk.push(a[r0:r0 + 1777], r0)
+    _, h2, _, _ = sk.finish(on_device=False)
+    assert np.array_equal(h1, h2)
+    sk.reset()
+    sk.set_left(None)
+    sk.push(a, 0, final=True)
+    g3, h3, _, _ = sk.finish(on_device=False)
+    sk.close()
+    assert rel(h3, a.astype(np.float64).T @ g3) <= 2e-5
+
+
+def test_cosketch_too_many_rows_and_state():
+    sk = P.GpuSketch(20, O.gaussian(20, 4, seed=1), np.float64)
+    sk.set_left(O.gaussian(10, 4, seed=2))
+    with pytest.raises(P.CapabilityError):
+        sk.push(O.gaussian(11, 20, seed=3), 0)
+    sk.reset()
+    sk.push(O.gaussian(5, 20, seed=3), 0)
+    with pytest.raises(P.StreamPcaError):
+        sk.set_left(O.gaussian(10, 4, seed=2))  # after the first push of a pass
+    sk.close()
+
+
+@pytest.mark.parametrize("precision", ["tc", "simt"])
+def test_cosketch_normalized(precision):
+    """Co-sketch of normalize_rows(A) (fused normalisation on the TC path:
+    operand L / norm and the finish-time correction with L)."""
+    if precision == "tc" and not _tc_ok():
+        pytest.skip("no tensor-core path")
+    m, n, l = 4000, 1000, 60
+    rng = np.random.default_rng(3)
+    a = (O.gaussian(m, n, seed=4) * rng.uniform(0.1, 10, (m, 1)) + rng.normal(0, 30, (m, 1))).astype(np.float32)
+    a[5] = 1.5
+    om, left = O.gaussian(n, l, seed=5), O.gaussian(m, l, seed=6)
+    sk = P.GpuSketch(n, om, np.float32, precision=precision, normalize=True)
+    sk.set_left(left)
+    sk.push(a, 0, final=True)
+    g, h, cs, _ = sk.finish(on_device=False)
+    sk.close()
+    an = O.oracle_normalize_rows(a.astype(np.float64))
+    l32 = left.astype(np.float32).astype(np.float64)
+    assert rel(h, an.T @ l32) <= 2e-5, rel(h, an.T @ l32)
+    assert rel(g, an @ om.astype(np.float32).astype(np.float64)) <= 2e-5
+
+
+# ------------------------------------------------- basic / legacy end to end
+def _case(golden_alg, name):
+    k, p, b, seed, center, br = (int(x) for x in golden_alg[f"{name}_cfg"])
+    a = golden_alg[f"{name}_a"]
+    return a, P.PcaConfig(k=k, oversample=p, block_size=b, seed=seed, center=bool(center)), br
+
+
+def _check(res, golden_alg, name, algo, tol):
+    s_ref = golden_alg[f"{name}_{algo}_s"]
+    assert float(np.max(np.abs(res.s - s_ref) / s_ref)) <= tol
+    # principal angles of the leading (well separated) components
+    kk = res.s.shape[0]
+    assert O.subspace_angle(res.u[:, :kk], golden_alg[f"{name}_{algo}_u"][:, :kk]) <= tol * 100
+    assert O.subspace_angle(res.v[:, :kk], golden_alg[f"{name}_{algo}_v"][:, :kk]) <= tol * 100
+    if res.mean is not None:
+        assert np.allclose(res.mean, golden_alg[f"{name}_{algo}_mean"], rtol=1e-6, atol=1e-9)
+
+
+@pytest.mark.parametrize("name", ALG_CASES)
+def test_basic_rand_svd_vs_reference(golden_alg, name):
+    a, cfg, br = _case(golden_alg, name)
+    for prec in _precisions(a.dtype):
+        res = P.basic_rand_svd(a, cfg, block_rows=br, precision=prec)
+        tol = 1e-10 if a.dtype == np.float64 else 1e-4
+        s_ref = golden_alg[f"{name}_basic_s"]
+        assert float(np.max(np.abs(res.s - s_ref) / s_ref)) <= tol, prec
+        if a.dtype == np.float64:  # vectors: 1e-10 on the directions (sign-aligned, so elementwise)
+            assert np.abs(res.u - golden_alg[f"{name}_basic_u"]).max() <= 1e-8
+            assert np.abs(res.v - golden_alg[f"{name}_basic_v"]).max() <= 1e-8
+        else:
+            _check(res, golden_alg, name, "basic", tol)
+        assert res.passes == 2
+        assert res.retained_floats == int(golden_alg[f"{name}_basic_meta"][1])
+
+
+@pytest.mark.parametrize("name", ALG_CASES)
+def test_legacy_single_pass_vs_reference(golden_alg, name):
+    a, cfg, br = _case(golden_alg, name)
+    for prec in _precisions(a.dtype):
+        with warnings.catch_warnings():
+            warnings.simplefilter("error")  # no conditioning warning on these cases
+            res = P.legacy_single_pass(a, cfg, block_rows=br, precision=prec)
+        tol = 1e-10 if a.dtype == np.float64 else 1e-4
+        s_ref = golden_alg[f"{name}_legacy_s"]
+        assert float(np.max(np.abs(res.s - s_ref) / s_ref)) <= tol, prec
+        if a.dtype == np.float64:
+            assert np.abs(res.u - golden_alg[f"{name}_legacy_u"]).max() <= 1e-8
+            assert np.abs(res.v - golden_alg[f"{name}_legacy_v"]).max() <= 1e-8
+        else:
+            _check(res, golden_alg, name, "legacy", tol)
+        assert res.passes == 1 and res.warnings == ()
+        assert res.retained_floats == int(golden_alg[f"{name}_legacy_meta"][1])
+
+
+def test_legacy_conditioning_warning(golden_alg):
+    a = golden_alg["ill_a"]
+    cfg = P.PcaConfig(k=5, oversample=15, block_size=5, seed=7)
+    with pytest.warns(P.ConditioningWarning, match="co-sketch system is ill-conditioned"):
+        res = P.legacy_single_pass(a, cfg, block_rows=40, cond_warn=2.0)
+    assert len(res.warnings) == 1
+    s_ref = golden_alg["ill_legacy_s"]
+    assert np.allclose(res.s, s_ref, rtol=1e-10)
+    # the condition number the message reports matches the reference's to 4 digits
+    assert str(golden_alg["ill_legacy_msg"]).split("cond ~ ")[1][:5] == res.warnings[0].split("cond ~ ")[1][:5]
+
+
+def test_legacy_row_count_contract():
+    a = O.gaussian(50, 12, seed=1)
+    cfg = P.PcaConfig(k=2, oversample=2, block_size=2)
+
+    class Lying(P.ArrayRowStream):  # declares fewer rows than it yields
+        @property
+        def n_rows(self):
+            return 40
+    with pytest.raises(P.CapabilityError):
+        P.legacy_single_pass(Lying(a), cfg)
+
+    class Short(P.ArrayRowStream):  # declares more rows than it yields
+        @property
+        def n_rows(self):
+            return 60
+    with pytest.raises(P.CapabilityError, match="declared 60 rows but yielded 50"):
+        P.legacy_single_pass(Short(a), cfg)
+
+
+def test_streams_through_basic_and_legacy(tmp_path):
+    """File, device and generator sources give the in-memory results."""
+    a = O.synth_lowrank_plus_noise(3000, 500, 40, "inv", 1e-3, seed=12)
+    cfg = P.PcaConfig(k=10, seed=2)
+    ref_b = P.basic_rand_svd(a, cfg)
+    ref_l = P.legacy_single_pass(a, cfg)
+    path = str(tmp_path / "a.spca")
+    P.matfile.write_matrix(path, a, dtype="float32", header=True)
+    dev = torch.from_numpy(a).cuda()
+    for src in [P.DeviceRowStream(dev), P.PassCounter(P.ArrayRowStream(a)), P.FileRowStream(path)]:
+        rb = P.basic_rand_svd(src, cfg)
+        assert np.array_equal(rb.s, ref_b.s)
+    rl = P.legacy_single_pass(P.DeviceRowStream(dev), cfg)
+    assert np.array_equal(rl.s, ref_l.s)
+    pc = P.PassCounter(P.ArrayRowStream(a))
+    assert P.basic_rand_svd(pc, cfg).passes == 2
+
+
+def test_basic_matches_single_pass_config2_shape():
+    """Full config-2 shape (100 000 x 10 000 fp32 on the device): the two-pass
+    yardstick and the single-pass estimate agree on the leading singular
+    values (the reference: 'identical seeds give singular values agreeing
+    to rounding' for exactly low-rank data; here to the sketch's accuracy)."""
+    from paper_1704_07669_b200 import synth
+    a = synth.config_matrix("cfg2", device="cuda")
+    cfg = P.PcaConfig(k=50, oversample=10, seed=1)
+    rb = P.basic_rand_svd(P.DeviceRowStream(a), cfg)
+    rs = P.single_pass_pca(P.DeviceRowStream(a), cfg)
+    rl = P.legacy_single_pass(P.DeviceRowStream(a), cfg)
+    assert np.all(np.isfinite(rb.s)) and np.all(np.isfinite(rl.s))
+    top = 10  # signal components, well above the noise bulk
+    assert np.max(np.abs(rb.s[:top] - rs.s[:top]) / rs.s[:top]) <= 2e-2
+    assert O.subspace_angle(rb.v[:, :5], rs.v[:, :5]) <= 5e-2
+    del a
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------ column shift
+def _offset_data(m, n, seed, offset=0.75):
+    """BASELINE-style fp32 data on a large common mean (offset ~300x the spread):
+    the case where post-hoc centering cancels fp32 accumulator rounding."""
+    return (O.synth_lowrank_plus_noise(m, n, 40, "exp30", 1e-3, seed=seed) + offset).astype(np.float32)
+
+
+@pytest.mark.parametrize("precision,left", [("tc", False), ("tc", True), ("simt", False), ("simt", True)])
+def test_shift_sketch_vs_oracle(precision, left):
+    """spca_sketch_set_shift: same G, H, col_sums as the unshifted sketch (the
+    shift is undone in fp64), and the centered sketch accurate to fp32 of the
+    data's spread rather than of its mean."""
+    if precision == "tc" and not _tc_ok():
+        pytest.skip("no tensor-core path")
+    m, n, l = 6000, 800, 60
+    a = _offset_data(m, n, seed=31)
+    om = O.gaussian(n, l, seed=32)
+    lm = O.gaussian(m, l, seed=33) if left else None
+    sk = P.GpuSketch(n, om, np.float32, precision=precision, shift=True)
+    if left:
+        sk.set_left(lm)
+    for r0 in range(0, m, 2500):  # several pushes: c is the pass's first row
+        sk.push(a[r0:r0 + 2500], r0)
+    g, h, cs, _ = sk.finish(on_device=False)
+    sk.close()
+    a64 = a.astype(np.float64)
+    om32 = om.astype(np.float32).astype(np.float64)
+    opnd = lm.astype(np.float32).astype(np.float64) if left else None
+    g_ref = a64 @ om32
+    h_ref = a64.T @ (opnd if left else g_ref)
+    assert rel(g, g_ref) <= 1e-6 and rel(h, h_ref) <= 1e-6
+    assert np.allclose(cs, a64.sum(axis=0), rtol=1e-9)
+    # centered: G_c = G - 1 mu^T Omega; H_c = H - mu 1^T(G or L)
+    mu = a64.mean(axis=0)
+    ac = a64 - mu
+    gc = g - (mu @ om32)[None, :]
+    hc = h - np.outer(mu, (opnd if left else g).sum(axis=0))
+    assert rel(gc, ac @ om32) <= 2e-5, rel(gc, ac @ om32)
+    hc_ref = ac.T @ (opnd if left else ac @ om32)
+    assert rel(hc, hc_ref) <= 2e-5, rel(hc, hc_ref)
+
+
+def test_shift_bitwise_splits_and_errors():
+    if not _tc_ok():
+        pytest.skip("no tensor-core path")
+    a = _offset_data(7000, 600, seed=34)
+    om = O.gaussian(600, 60, seed=35)
+    st1 = P.sketch_pass(P.ArrayRowStream(a), om, shift=True)
+    st2 = P.sketch_pass(P.ArrayRowStream(a), om, block_rows=999, shift=True)
+    assert np.array_equal(st1.g, st2.g) and np.array_equal(st1.h, st2.h)
+    assert np.array_equal(st1.col_sums, st2.col_sums)
+    bad = a.copy()
+    bad[0, 5] = np.nan  # the shift row itself is non-finite: still DataError(row=0)
+    with pytest.raises(P.DataError) as ei:
+        P.sketch_pass(P.ArrayRowStream(bad), om, shift=True)
+    assert ei.value.row == 0
+    bad = a.copy()
+    bad[4321, 7] = np.inf
+    with pytest.raises(P.DataError) as ei:
+        P.sketch_pass(P.ArrayRowStream(bad), om, shift=True)
+    assert ei.value.row == 4321
+    sk = P.GpuSketch(600, om, np.float32, normalize=True)
+    with pytest.raises(P.ConfigError):
+        sk.lib and P._lib.check(sk.lib.spca_sketch_set_shift(sk.h, 1), sk.h)
+    sk.close()
+
+
+def _oracle_power_refine(a, k, seed, oversample=10, block_size=10, block_rows=4096):
+    """power_refine (algorithms.py:266-309) composed from the oracle's pieces,
+    centered: sketch, center, Omega2 = orth(H), sketch, center, blocked QB."""
+    a = a.astype(np.float64)
+    l = O.sketch_width(k, oversample, block_size)
+    om = O.gaussian(a.shape[1], l, seed)
+    st = O.oracle_center(O.oracle_sketch(O.row_blocks(a, block_rows), om), om)
+    om2, _ = O.qr_pos(st.h, rank_check=False)
+    st2 = O.oracle_center(O.oracle_sketch(O.row_blocks(a, block_rows), om2), om2)
+    qb = O.oracle_qb(st2.g, st2.h, om2, block_size, on_deficiency="repair", repair_seed=seed)
+    sv = O.thin_svd(qb.b)
+    u, v = O.align_signs(qb.q @ sv.u[:, :k], sv.v[:, :k])
+    return sv.s[:k], v
+
+
+@pytest.mark.parametrize("algo", ["single", "basic", "legacy", "power"])
+def test_centered_fp32_offset_data(algo):
+    """Centered PCA of fp32 data on a large mean matches the fp64 oracle on
+    the same fp32 values within the fp32 bar (1e-4) on every device path."""
+    a = _offset_data(5000, 700, seed=36)
+    cfg = P.PcaConfig(k=15, seed=3, center=True, power=1 if algo == "power" else 0)
+    for prec in _precisions(np.float32):
+        if algo == "single":
+            res = P.single_pass_pca(a, cfg, precision=prec)
+            _, s_ref, v_ref, *_ = O.oracle_single_pass(a, k=15, seed=3, center=True, block_rows=4096)
+        elif algo == "basic":
+            res = P.basic_rand_svd(a, cfg, precision=prec)
+            _, s_ref, v_ref, *_ = O.oracle_basic_rand_svd(a, k=15, seed=3, center=True)
+        elif algo == "legacy":
+            res = P.legacy_single_pass(a, cfg, precision=prec)
+            _, s_ref, v_ref, *_ = O.oracle_legacy_single_pass(a, k=15, seed=3, center=True)
+        else:
+            res = P.power_refine(a, cfg, precision=prec)
+            s_ref, v_ref = _oracle_power_refine(a, k=15, seed=3)
+        err = float(np.max(np.abs(res.s - s_ref) / s_ref))
+        assert err <= 1e-4, (prec, err)
+        assert O.subspace_angle(res.v[:, :5], v_ref[:, :5]) <= 1e-3, prec

@@ -52,5 +52,6 @@ def test_legacy_conditioning_warning(golden_alg):
     _, s, _, _, cond, _, _ = O.oracle_legacy_single_pass(a, k=5, oversample=15, block_size=5, seed=7,
                                                          block_rows=40)
     assert np.array_equal(s, golden_alg["ill_legacy_s"])
+    assert cond > 2.0
     assert golden_alg["ill_legacy_nwarn"].tolist() == [1, 1]
     assert f"cond ~ {cond:.3e}" in str(golden_alg["ill_legacy_msg"])
