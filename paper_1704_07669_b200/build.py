@@ -33,6 +33,8 @@ if os.environ.get("SPCA_BUILD_FINE_TRACE"):  # profiling builds: per-K-block clo
     FLAGS.append("-DSPCA_FINE_TRACE")
 if os.environ.get("SPCA_BUILD_RELAY") is not None:  # experiment: B ring handshakes via the MMA warp
     FLAGS.append("-DSPCA_RELAY=" + os.environ["SPCA_BUILD_RELAY"])
+if os.environ.get("SPCA_BUILD_BCOMB") is not None:  # experiment: separate hi / lo B boxes (0)
+    FLAGS.append("-DSPCA_BCOMB=" + os.environ["SPCA_BUILD_BCOMB"])
 if os.environ.get("SPCA_BUILD_STACKED") is not None:  # experiment: l_pad=64 MMA form
     FLAGS.append("-DSPCA_STACKED_64=" + os.environ["SPCA_BUILD_STACKED"])
 

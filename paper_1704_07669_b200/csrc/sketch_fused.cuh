@@ -366,6 +366,9 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             ptx::tma_load_2d_pair(st, m01, bar, k, y01, keep);
             ptx::tma_load_2d_pair(st + C::BH_BYTES, m01, bar, k, y01 + HR, keep);
             ptx::tma_load_2d_pair(st + 2 * C::BH_BYTES, mh, bar, k, yh + HR * (int)rank, keep);
+          } else if (SPCA_BCOMB) {  // this CTA's hi and lo rows: one box of LPAD rows
+            const int yc = f.kind == 0 ? 2 * args.wy0 + LPAD * (int)rank : (2 * gslot + (int)rank) * LPAD;
+            ptx::tma_load_2d_pair(st, mh, bar, k, yc, keep);
           } else {
             ptx::tma_load_2d_pair(st, mh, bar, k, yh + HR * (int)rank, keep);
             ptx::tma_load_2d_pair(st + C::BH_BYTES, ml, bar, k, yl + HR * (int)rank, keep);
@@ -573,7 +576,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         if (ctr) ctr[2] = clock64();
         ptx::tc_fence_after();
         const uint32_t tst = lane_base + C::A_TMEM + 64 * ts;
-        if (!(args.dbg & 1)) {
+        if (!(args.dbg & (1 | 32))) {  // 32: profiling knob, no TMEM stores (split kept)
           ptx::tmem_st32(tst, hi);
           ptx::tmem_st32(tst + 32, v);
         }
@@ -796,8 +799,13 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             for (int j = 0; j < 4; ++j) {
               float h1 = 0.f, l1 = 0.f;
               if (valid) split3(b4[j], h1, l1);
+#if SPCA_BCOMB
+              ghi[(size_t)bcomb_row(4 * q + j, 0, LPAD) * sc.R0 + rc] = h1;
+              ghi[(size_t)bcomb_row(4 * q + j, 1, LPAD) * sc.R0 + rc] = l1;
+#else
               ghi[(size_t)(4 * q + j) * sc.R0 + rc] = h1;
               glo[(size_t)(4 * q + j) * sc.R0 + rc] = l1;
+#endif
             }
           }
           ptx::fence_proxy_async_global();

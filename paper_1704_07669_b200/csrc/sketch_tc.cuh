@@ -72,6 +72,14 @@ constexpr int kPromote = 4;     // K blocks per accumulator period
 #ifndef SPCA_STACKED_64
 #define SPCA_STACKED_64 0
 #endif
+// B operand layout: 1 = hi and lo rows of each CTA's half interleaved in one
+// matrix (rows ((2g + half) * 2 + part) * l_pad/2 + r for column group g), so
+// a CTA's B stage is ONE TMA box of l_pad rows per K block (TMA request rate,
+// not bytes, limits the per-SM stream: tools/mc_bench.cu); 0 = separate hi /
+// lo matrices, two boxes per K block
+#ifndef SPCA_BCOMB
+#define SPCA_BCOMB 1
+#endif
 // epilogue staging buffers for l_pad = 64. Two (at the cost of two A stages)
 // measured no faster and failed 1 run in 8 (a launch fault not yet understood):
 // kept at one; the staging code is written for either.
@@ -152,6 +160,29 @@ __device__ __forceinline__ void tc_mma_stage2(uint32_t a_hi, uint32_t acc, uint6
       ptx::mma2_tf32_ts(acc, a_hi + kk * 8, dl, idesc, 1u);
       ptx::mma2_tf32_ts(acc, a_hi + 32 + kk * 8, dh, idesc, 1u);
     }
+  }
+}
+
+// row of the combined B matrix holding element j (0 <= j < lpad) of part
+// (0 = hi, 1 = lo), column groups of lp
+__host__ __device__ __forceinline__ int bcomb_row(int j, int part, int lp) {
+  const int hr = lp / 2, g = j / lp, jj = j - g * lp, half = jj / hr;
+  return ((2 * g + half) * 2 + part) * hr + (jj - half * hr);
+}
+
+// Omega -> the combined B matrix (2 lpad x n): Omega^T hi / lo rows interleaved per CTA half
+__global__ void tc_omega_prepare_comb(const double *__restrict__ om64, int n, int l, int lpad, int lp,
+                                      float *__restrict__ w2) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; idx < (int64_t)lpad * n; idx += stride) {
+    const int j = (int)(idx / n);
+    const int i = (int)(idx - (int64_t)j * n);
+    const float v = j < l ? (float)om64[(int64_t)i * l + j] : 0.f;
+    float hi, lo;
+    split3(v, hi, lo);
+    w2[(int64_t)bcomb_row(j, 0, lp) * n + i] = hi;
+    w2[(int64_t)bcomb_row(j, 1, lp) * n + i] = lo;
   }
 }
 

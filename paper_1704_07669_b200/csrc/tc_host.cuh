@@ -178,22 +178,36 @@ int tc_setup(spca_sketch *h) {
   CK(h, dalloc(h, &h->tc_omega, (size_t)2 * h->lpad * h->n * 4));
   float *whi = (float *)h->tc_omega;
   float *wlo = whi + (size_t)h->lpad * h->n;
+  const uint32_t hr = (uint32_t)(lp / 2);
+  int rc;
+#if SPCA_BCOMB
+  // one matrix of 2 lpad rows: each CTA's half of a column group is hi rows
+  // then lo rows, loaded as ONE box of lp rows per K block
+  tc_omega_prepare_comb<<<grid_for((int64_t)h->lpad * h->n), 256, 0, h->stream>>>(
+      h->omega64_dev, (int)h->n, (int)h->l, (int)h->lpad, lp, whi);
+  CK_LAUNCH(h);
+  rc = encode_2d(h, &h->tm_whi, whi, (uint64_t)h->n, (uint64_t)2 * h->lpad, (uint64_t)h->n * 4, 32, lp);
+  if (rc) return rc;
+  h->tm_wlo = h->tm_whi;
+  const uint32_t gbox = (uint32_t)lp;
+#else
   tc_omega_prepare<<<grid_for((int64_t)h->lpad * h->n), 256, 0, h->stream>>>(
       h->omega64_dev, (int)h->n, (int)h->l, (int)h->lpad, whi, wlo);
   CK_LAUNCH(h);
   // B tiles are loaded as l_pad/2-row halves (one per CTA of a pair) of one
   // column group; Omega^T holds every group (rows g*lp ..)
-  const uint32_t hr = (uint32_t)(lp / 2);
-  int rc = encode_2d(h, &h->tm_whi, whi, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, hr);
+  rc = encode_2d(h, &h->tm_whi, whi, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, hr);
   if (rc) return rc;
   rc = encode_2d(h, &h->tm_wlo, wlo, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, hr);
   if (rc) return rc;
+  const uint32_t gbox = hr;
+#endif
   const FusedSched s = tc_base_sched(h);
-  // G^T hi / lo of kSlots chunks of one launch: [kSlots][2][lp][R0], one TMA map
+  // G^T hi / lo of kSlots chunks of one launch: [kSlots][2 lp rows][R0], one TMA map
   h->tc_ws_bytes = (size_t)kSlots * 2 * lp * s.R0 * 4;
   CK(h, dalloc(h, &h->tc_ws, h->tc_ws_bytes));
   rc = encode_2d(h, &h->tm_gT, h->tc_ws, (uint64_t)s.R0, (uint64_t)kSlots * 2 * lp, (uint64_t)s.R0 * 4,
-                 32, hr);
+                 32, gbox);
   if (rc) return rc;
   h->gpart_elems = (int64_t)kSlots * 2 * s.T * s.S * 128 * lp;
   CK(h, dalloc(h, &h->gpart, (size_t)h->gpart_elems * 4));
