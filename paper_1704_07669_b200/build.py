@@ -35,6 +35,8 @@ if os.environ.get("SPCA_BUILD_RELAY") is not None:  # experiment: B ring handsha
     FLAGS.append("-DSPCA_RELAY=" + os.environ["SPCA_BUILD_RELAY"])
 if os.environ.get("SPCA_BUILD_BCOMB") is not None:  # experiment: separate hi / lo B boxes (0)
     FLAGS.append("-DSPCA_BCOMB=" + os.environ["SPCA_BUILD_BCOMB"])
+if os.environ.get("SPCA_BUILD_PAIRA") is not None:  # experiment: one TMA request per A K block (0)
+    FLAGS.append("-DSPCA_PAIRA=" + os.environ["SPCA_BUILD_PAIRA"])
 if os.environ.get("SPCA_BUILD_STACKED") is not None:  # experiment: l_pad=64 MMA form
     FLAGS.append("-DSPCA_STACKED_64=" + os.environ["SPCA_BUILD_STACKED"])
 

@@ -109,6 +109,7 @@ struct spca_sketch {
   const void *src_ptr = nullptr;
   int64_t src_rows = 0, src_lda = 0;
   CUtensorMap src_tg, src_th;
+  CUtensorMap src_tg3, src_th2;  // paired A slots: 3-D box of two K blocks / 64-row box
   double kernel_ms = 0.0;
   int64_t timed_chunks = 0;
 

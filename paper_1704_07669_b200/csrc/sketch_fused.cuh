@@ -109,6 +109,7 @@ struct FusedArgs {
   int wy0;                    // first Omega^T row of this launch's column group
   int gld;                    // row stride (floats) of g_out and hpart (all column groups)
   int colsum_on;              // this launch also accumulates the column sums (group 0)
+  int g3d;                    // tAg3 (3-D box of two K blocks) is valid: n % 32 == 0
   int dbg;                    // profiling knobs (SPCA_TC_DEBUG), 0 in production:
                               // 1 converters skip the split, 2 no MMAs, 4 no B loads, 8 no A loads
 
@@ -228,7 +229,8 @@ template <int LPAD, bool NORM, bool SHIFT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<LPAD>::THREADS, 1)
 tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ CUtensorMap tAh,
                const __grid_constant__ CUtensorMap tWhi, const __grid_constant__ CUtensorMap tWlo,
-               const __grid_constant__ CUtensorMap tGT, const FusedArgs args) {
+               const __grid_constant__ CUtensorMap tGT, const __grid_constant__ CUtensorMap tAg3,
+               const __grid_constant__ CUtensorMap tAh2, const FusedArgs args) {
   using C = TcCfg<LPAD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -249,7 +251,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NA; ++s) {
       ptx::mbar_init(&bars.a_full[s], 1);
-      ptx::mbar_init(&bars.a_empty[s], 4);  // the four warps of one converter group
+      // the four warps of one converter group; paired slots: both groups (barriers [0, NP))
+      ptx::mbar_init(&bars.a_empty[s], SPCA_PAIRA ? 8 : 4);
     }
     for (int s = 0; s < C::NS; ++s) {
       ptx::mbar_init(&bars.kb_full[s], 2 * 4);  // one converter group (4 warps) in each CTA
@@ -273,6 +276,10 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     ptx::tma_prefetch(&tWhi);
     ptx::tma_prefetch(&tWlo);
     ptx::tma_prefetch(&tGT);
+    if (SPCA_PAIRA) {
+      ptx::tma_prefetch(&tAg3);
+      ptx::tma_prefetch(&tAh2);
+    }
   }
   if (threadIdx.x < 128) stg_bad[threadIdx.x] = 0;
   if (warp == 1) ptx::tmem_alloc2(&bars.tmem_base, kTmemCols);
@@ -301,6 +308,42 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         }
         __syncwarp();
       }
+#if SPCA_PAIRA
+      // pairs of K blocks: one request (3-D box of two K blocks / 64-row box) per pair
+#pragma unroll 1
+      for (int kb = 0; kb < f.nk; kb += 2, ++gkb) {
+        const int p = gkb % C::NP, nb = min(2, f.nk - kb);
+        if (gkb >= C::NP) ptx::mbar_wait(&bars.a_empty[p], ((gkb / C::NP) - 1) & 1);
+        if (ptx::elect_one()) {
+          uint8_t *st = smem + 2 * p * C::A_BYTES;
+          if (args.dbg & 8) {
+            ptx::mbar_arrive(&bars.a_full[p]);
+          } else {
+            ptx::mbar_arrive_expect_tx(&bars.a_full[p], nb * (C::A_BYTES + (hstats ? 256u : 0u)));
+            if (hstats) {
+              for (int j = 0; j < nb; ++j) {
+                const size_t o = (size_t)(f.c % kSlots) * sc.R0 + (size_t)(f.k0 + kb + j) * 32;
+                ptx::bulk_load(&sst[2 * p + j][0], args.row_a0 + o, 128, &bars.a_full[p]);
+                ptx::bulk_load(&sst[2 * p + j][32], args.row_inv + o, 128, &bars.a_full[p]);
+              }
+            }
+            if (f.kind == 0) {  // 128 rows x 32 k per block, row-major (swizzled)
+              if (nb == 2 && args.g3d) {
+                ptx::tma_load_3d_hint(st, &tAg3, &bars.a_full[p], 0, rbase + tile * 128, f.k0 + kb, keep);
+              } else {
+                for (int j = 0; j < nb; ++j)
+                  ptx::tma_load_2d_hint(st + j * C::A_BYTES, &tAg, &bars.a_full[p], (f.k0 + kb + j) * 32,
+                                        rbase + tile * 128, keep);
+              }
+            } else {            // 32 rows x 128 columns per block, unswizzled: one box of 64 rows
+              ptx::tma_load_2d_hint(st, nb == 2 ? &tAh2 : &tAh, &bars.a_full[p], tile * 128,
+                                    rbase + (f.k0 + kb) * 32, drop);
+            }
+          }
+        }
+        __syncwarp();
+      }
+#else
 #pragma unroll 1
       for (int kb = 0; kb < f.nk; ++kb, ++gkb) {
         const int s = gkb % C::NA;
@@ -327,6 +370,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         }
         __syncwarp();
       }
+#endif
     }
   } else if (warp == 2) {  // ---------------------------------- B producer (half)
     const uint64_t keep = ptx::policy_evict_last();
@@ -442,7 +486,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     const int grp = ct >> 7;   // converts the K blocks kb = grp (mod kGroups)
     const uint32_t lane_base = tmem + ((uint32_t)(t & ~31) << 16);
     const uint32_t kbfull_l = ptx::mapa(ptx::smem_u32(&bars.kb_full[0]), 0);
-    int gkb = 0, ui = 0;
+    int gkb = 0, ui = 0, gpa = 0;  // gpa: A slot pairs consumed (SPCA_PAIRA)
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
       const FusedUnit f = fused_decode(sc, u);
@@ -458,7 +502,13 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
 #pragma unroll 1
       for (int kb = grp; kb < f.nk; kb += kGroups) {
         const int gk = gkb + kb;
-        const int s = gk % C::NA, ts = gk % C::NS;
+#if SPCA_PAIRA
+        const int ga = gpa + (kb >> 1), ab = ga % C::NP;  // A slot pair of this block
+        const int s = 2 * ab + (kb & 1), ts = gk % C::NS;
+#else
+        const int ga = gk, ab = gk % C::NA;
+        const int s = ab, ts = gk % C::NS;
+#endif
 #ifdef SPCA_FINE_TRACE
         unsigned long long *ctr = (trace && blockIdx.x == 0 && ct == 0 && (gk >> 1) < kTraceConv)
                                       ? args.trace + 256 * kTraceStride + 4 * kTraceMma + 6 * (gk >> 1) : nullptr;
@@ -466,7 +516,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         constexpr unsigned long long *ctr = nullptr;
 #endif
         if (ctr) ctr[0] = clock64();
-        ptx::mbar_wait(&bars.a_full[s], (gk / C::NA) & 1);
+        ptx::mbar_wait(&bars.a_full[ab], (ga / (SPCA_PAIRA ? C::NP : C::NA)) & 1);
         if (ctr) ctr[1] = clock64();
         // Load and split first, then wait for the TMEM stage: the stage is held
         // only for the two stores, which keeps the stage round trip (converters
@@ -564,7 +614,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         // can go back to TMA (one lane's arrive would not order the other lanes'
         // outstanding shared loads against the next TMA write)
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&bars.a_empty[s]);
+        if (lane == 0) ptx::mbar_arrive(&bars.a_empty[ab]);
         if (gk >= C::NS) {
           ptx::mbar_wait(&bars.kb_empty[ts], ((gk / C::NS) - 1) & 1);
 #if SPCA_RELAY
@@ -593,6 +643,15 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         if (lane == 0) ptx::mbar_arrive_cluster(kbfull_l + 8 * ts);
         if (ctr) ctr[5] = clock64();
       }
+#if SPCA_PAIRA
+      if (grp == 1 && (f.nk & 1)) {  // the unit's last pair holds one block: release the empty half
+        const int ga = gpa + (f.nk >> 1), ab = ga % C::NP;
+        ptx::mbar_wait(&bars.a_full[ab], (ga / C::NP) & 1);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&bars.a_empty[ab]);
+      }
+      gpa += (f.nk + 1) >> 1;
+#endif
       gkb += f.nk;
       if (ct == 0) SPCA_TRACE(ui, 1);
       // hand the column-sum partial to the epilogue with the unit's staging

@@ -80,6 +80,16 @@ constexpr int kPromote = 4;     // K blocks per accumulator period
 #ifndef SPCA_BCOMB
 #define SPCA_BCOMB 1
 #endif
+// Experiment (off): A ring in pairs of 16 KB slots, one TMA request bringing
+// two K blocks (a 3-D box of two 128 x 32 tiles for G units, a 64-row box for
+// H units), the two converter groups sharing the pair's barriers. In
+// isolation 2 x 16 KB boxes stream at 118 GB/s per SM from L2 vs 63 GB/s for
+// 16 KB boxes (tools/mc_bench.cu), but in the pass it measured no faster at
+// config 2 (1.699 vs 1.703 ms) and 5% slower at config 3 (shallower ring):
+// the A request rate does not bound the pass.
+#ifndef SPCA_PAIRA
+#define SPCA_PAIRA 0
+#endif
 // epilogue staging buffers for l_pad = 64. Two (at the cost of two A stages)
 // measured no faster and failed 1 run in 8 (a launch fault not yet understood):
 // kept at one; the staging code is written for either.
@@ -107,7 +117,10 @@ struct TcCfg {
   static constexpr uint32_t B_STAGE = STACKED ? 3 * BH_BYTES : 2 * BH_BYTES;
   static constexpr int NB = STACKED ? 7 : (LPAD == 64 ? 8 : 4);  // B ring (12 | 8 | 16 KB stages)
   static constexpr int NSTG = LPAD == 64 ? SPCA_NSTG_64 : 1;  // epilogue staging buffers
-  static constexpr int NA = STACKED ? 6 : (LPAD == 64 ? (NSTG == 2 ? 5 : 7) : 5);  // raw A ring (16 KB stages)
+  static constexpr int NA = SPCA_PAIRA ? (LPAD == 64 ? 6 : 4)
+                                       : (STACKED ? 6 : (LPAD == 64 ? (NSTG == 2 ? 5 : 7) : 5));  // raw A ring (16 KB stages)
+  static constexpr int NP = NA / 2;  // A slot pairs (SPCA_PAIRA)
+  static_assert(!SPCA_PAIRA || (NA % 2 == 0 && !STACKED), "paired A slots");
   static constexpr uint32_t STG_BYTES = 128 * LPAD * 4;  // epilogue staging tile
   static constexpr uint32_t B_OFF = NA * A_BYTES;
   static constexpr uint32_t STG_OFF = B_OFF + NB * B_STAGE;

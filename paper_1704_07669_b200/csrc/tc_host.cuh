@@ -115,6 +115,38 @@ int encode_2d(spca_sketch *h, CUtensorMap *map, const void *ptr, uint64_t inner,
   return SPCA_OK;
 }
 
+// A as K-block tiles for the G units' paired loads: dims {32, rows, n/32},
+// box {32, 128, 2} = two consecutive swizzled 128 x 32 tiles (n % 32 == 0)
+int encode_a3d(spca_sketch *h, CUtensorMap *map, const void *ptr, uint64_t rows, uint64_t row_bytes) {
+  EncodeTiledFn enc = tma_encoder();
+  if (!enc) return set_err(h, SPCA_ERR_CUDA, -1, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {32, rows, (cuuint64_t)(h->n / 32)};
+  cuuint64_t strides[2] = {row_bytes, 128};
+  cuuint32_t box[3] = {32, 128, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_err(h, SPCA_ERR_CUDA, -1, "3-d tensor map encode failed (%d)", (int)r);
+  return SPCA_OK;
+}
+
+// every A map of one source buffer: G tiles (2-D, and 3-D pairs when n % 32 == 0),
+// H tiles of 32 and 64 rows
+int encode_a_maps(spca_sketch *h, const void *a, uint64_t rows, uint64_t row_bytes, CUtensorMap *tg,
+                  CUtensorMap *th, CUtensorMap *tg3, CUtensorMap *th2) {
+  int rc = encode_2d(h, tg, a, (uint64_t)h->n, rows, row_bytes, 32, 128);
+  if (rc) return rc;
+  rc = encode_2d(h, th, a, (uint64_t)h->n, rows, row_bytes, 128, 32, false);
+  if (rc) return rc;
+  rc = encode_2d(h, th2, a, (uint64_t)h->n, rows, row_bytes, 128, 64, false);
+  if (rc) return rc;
+  if (h->n % 32 == 0) return encode_a3d(h, tg3, a, rows, row_bytes);
+  *tg3 = *tg;  // unused (args.g3d = 0)
+  return SPCA_OK;
+}
+
 template <int LPAD>
 int tc_set_smem_attrs() {
   static bool done = false;
@@ -230,9 +262,8 @@ int tc_register_source(spca_sketch *h, const void *a, int64_t rows, int64_t lda)
     return SPCA_OK;
   }
   if (h->src_ptr == a && h->src_rows == rows && h->src_lda == lda) return SPCA_OK;
-  int rc = encode_2d(h, &h->src_tg, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)lda * 4, 32, 128);
-  if (rc) return rc;
-  rc = encode_2d(h, &h->src_th, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)lda * 4, 128, 32, false);
+  int rc = encode_a_maps(h, a, (uint64_t)rows, (uint64_t)lda * 4, &h->src_tg, &h->src_th, &h->src_tg3,
+                         &h->src_th2);
   if (rc) return rc;
   h->src_ptr = a;
   h->src_rows = rows;
@@ -337,8 +368,8 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
     const int orc = tc_unit_order(h, s);
     if (orc) return orc;
   }
-  CUtensorMap fa_g, fa_h;
-  const CUtensorMap *ta_g, *ta_h;
+  CUtensorMap fa_g, fa_h, fa_g3, fa_h2;
+  const CUtensorMap *ta_g, *ta_h, *ta_g3, *ta_h2;
   int row_base = 0;
   const char *base = (const char *)h->src_ptr;
   const int64_t row_bytes = lda * 4;
@@ -351,13 +382,15 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
     row_base = (int)(((const char *)a - base) / row_bytes);
     ta_g = &h->src_tg;
     ta_h = &h->src_th;
+    ta_g3 = &h->src_tg3;
+    ta_h2 = &h->src_th2;
   } else {  // rows beyond the launch must read as zeros (TMA out of bounds)
-    int rc = encode_2d(h, &fa_g, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)row_bytes, 32, 128);
-    if (rc) return rc;
-    rc = encode_2d(h, &fa_h, a, (uint64_t)h->n, (uint64_t)rows, (uint64_t)row_bytes, 128, 32, false);
+    int rc = encode_a_maps(h, a, (uint64_t)rows, (uint64_t)row_bytes, &fa_g, &fa_h, &fa_g3, &fa_h2);
     if (rc) return rc;
     ta_g = &fa_g;
     ta_h = &fa_h;
+    ta_g3 = &fa_g3;
+    ta_h2 = &fa_h2;
   }
   const size_t ctr_words = (size_t)s.C * (2 * s.T + 2) + 2 * s.X;
   const int grid = 2 * std::max(1, std::min(h->max_pairs, s.total));
@@ -372,6 +405,7 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   args.g_out = (float *)h->g_dev + h->rows_done * h->lpad + grp * h->tc_lp;
   args.hpart = (float *)h->hpart + grp * h->tc_lp;
   args.cshift = h->shift_on ? h->cshift : nullptr;
+  args.g3d = h->n % 32 == 0 ? 1 : 0;
   args.left = h->left_rows ? (const float *)h->left_dev + h->rows_done * h->lpad + grp * h->tc_lp : nullptr;
   if (h->normalize) {
     args.norm = 1;
@@ -405,7 +439,7 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
                                   : (h->shift_on ? tc_pass_kernel<128, false, true> : tc_pass_kernel<128, false>));
   const unsigned threads = h->tc_lp == 64 ? TcCfg<64>::THREADS : TcCfg<128>::THREADS;
   const unsigned smem = h->tc_lp == 64 ? TcCfg<64>::SMEM : TcCfg<128>::SMEM;
-  kern<<<grid, threads, smem, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, args);
+  kern<<<grid, threads, smem, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, *ta_g3, *ta_h2, args);
   CK_LAUNCH(h);
   }
   h->chunks_since_flush += s.C;
