@@ -55,7 +55,9 @@ int64_t tc_chunk_rows(int64_t n, int64_t /*l*/) {
   int64_t r = (int64_t)(mb << 20) / (4 * n);
   // wide rows: at least 1024 rows (H units of a full 32 K blocks; config 5,
   // n = 200 000: 60 ms per pass vs 127 ms at 256 rows) while a chunk stays <= 1 GB
-  const int64_t floor_rows = std::max<int64_t>(256, std::min<int64_t>(1024, (int64_t)(1ll << 30) / (4 * n)));
+  int64_t fl = 1024;
+  if (const char *e = getenv("SPCA_TC_MIN_ROWS")) fl = std::max<int64_t>(256, atoll(e));  // tuning knob
+  const int64_t floor_rows = std::max<int64_t>(256, std::min<int64_t>(fl, (int64_t)(1ll << 30) / (4 * n)));
   r = std::max<int64_t>(floor_rows, std::min<int64_t>(8192, r));
   return (r / 256) * 256;
 }
