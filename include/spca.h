@@ -155,6 +155,11 @@ int spca_device_views(spca_handle_t h, double **g_dev, double **hcs_dev);
 int spca_center_correct(spca_handle_t h, int64_t m_total, const double *gsum,
                         double *mean_out, int mean_where);
 
+/* Omega exactly as the pass used it (n x l float64 row-major: the fp32
+ * rounding of the caller's Omega for SPCA_F32) — the test matrix the post-pass
+ * must pair with G and H (blocked_qb, qb.py:59-135). out_where: device or host. */
+int spca_omega_used(spca_handle_t h, double *out, int out_where);
+
 /* Column sums of the finished G (l values, float64) — for center_correct. */
 int spca_g_colsum(spca_handle_t h, double *out, int out_where);
 

@@ -255,7 +255,7 @@ def basic_rand_svd(
         if m == 0:
             raise EmptyStreamError("the stream yielded no rows")
         cfg.validate_dims(n, m)
-        om = to_device64(_omega_as_used(omega, sk.dtype), dev)
+        om = sk.omega_used(on_device=True)
         mean = None
         if cfg.center:
             mean = col_sums / m
@@ -330,12 +330,12 @@ def legacy_single_pass(
     sk = run_pass(stream, omega, block_rows=block_rows, precision=precision, device=dev, left=omega_t,
                   shift=cfg.center)
     dtype = sk.dtype
+    om = sk.omega_used(on_device=True)
     y, yt, col_sums, rows_seen = _finish_pair(sk)
     if rows_seen == 0:
         raise EmptyStreamError("the stream yielded no rows")
     if rows_seen != m:
         raise CapabilityError(f"stream declared {m} rows but yielded {rows_seen}")
-    om = to_device64(_omega_as_used(omega, dtype), dev)
     ot = to_device64(_omega_as_used(omega_t, dtype), dev)
     mean = None
     if cfg.center:

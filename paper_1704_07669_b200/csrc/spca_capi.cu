@@ -882,6 +882,16 @@ int spca_device_views(spca_handle_t h, double **g_dev, double **hcs_dev) {
   return SPCA_OK;
 }
 
+int spca_omega_used(spca_handle_t h, double *out, int out_where) {
+  if (!h || !out) return set_err(h, SPCA_ERR_STATE, -1, "null argument");
+  DeviceGuard dg(h->device);
+  CK(h, cudaMemcpyAsync(out, h->omega64_dev, (size_t)h->n * h->l * 8,
+                        out_where == SPCA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                        h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return SPCA_OK;
+}
+
 int spca_g_colsum(spca_handle_t h, double *out, int out_where) {
   if (!h || !out) return set_err(h, SPCA_ERR_STATE, -1, "null argument");
   if (!h->finished) return set_err(h, SPCA_ERR_STATE, -1, "g_colsum needs a finished sketch");

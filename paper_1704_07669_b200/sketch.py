@@ -203,6 +203,18 @@ class GpuSketch:
         self._finished = True
         return g, hh, cs, m
 
+    def omega_used(self, on_device: bool = True):
+        """Omega exactly as the pass used it (n x l float64; fp32-rounded for
+        fp32 data), copied from the device (spca_omega_used)."""
+        torch = torch_mod()
+        if on_device:
+            out = torch.empty((self.n, self.l), dtype=torch.float64, device=self.device)
+            _lib.check(self.lib.spca_omega_used(self.h, ctypes.c_void_p(out.data_ptr()), _lib.MEM_DEVICE), self.h)
+            return out
+        out = np.empty((self.n, self.l))
+        _lib.check(self.lib.spca_omega_used(self.h, ctypes.c_void_p(out.ctypes.data), _lib.MEM_PAGEABLE), self.h)
+        return out
+
     def rows(self) -> int:
         """Rows pushed so far (spca_sketch_rows)."""
         r = ctypes.c_int64(0)
@@ -489,11 +501,9 @@ def sketch_pass(
                   precision=precision, device=device, shift=shift)
     try:
         g, h, cs, m = sk.finish(on_device=keep_on_device)
+        used = sk.omega_used(on_device=keep_on_device)  # the library's copy: no host re-rounding
     finally:
         sk.close()
-    used = _omega_as_used(om, getattr(stream, "dtype", np.float64))
-    if keep_on_device:
-        used = to_device64(used, default_device(device))
     return SketchState(g=g, h=h, col_sums=cs, rows_seen=int(m), omega=used)
 
 
