@@ -13,6 +13,9 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 from .device import default_device, to_device64, torch_mod
@@ -42,7 +45,72 @@ def gaussian_matrix(rows: int, cols: int, seed: int, stream: int = STREAM_SKETCH
     if seed < 0 or stream < 0:
         raise ConfigError("seed and stream must be nonnegative")
     key = np.array([seed, stream], dtype=np.uint64)
+    n = rows * cols
+    threads = min(_DRAW_THREADS, n // _DRAW_MIN_PER_THREAD)
+    if threads >= 2:
+        out = _parallel_normals(key, n, threads)
+        if out is not None:
+            return out.reshape(rows, cols)
     return np.random.Generator(np.random.Philox(key=key)).standard_normal((rows, cols))
+
+
+_DRAW_THREADS = max(1, min(16, os.cpu_count() or 1))
+_DRAW_MIN_PER_THREAD = 1 << 20
+_OVERLAP = 64
+
+
+def _parallel_normals(key, n: int, threads: int):
+    """The first n values of Generator(Philox(key)).standard_normal, bit for
+    bit, drawn by `threads` threads (numpy releases the GIL while it fills).
+
+    The ziggurat consumes a variable number of raw 64-bit draws per value
+    (1 on its fast path, ~1.022 on average), so segment t cannot be started at
+    its exact counter position. Its thread starts at a lower bound instead —
+    raw draw 4*floor(s_t/4) <= s_t <= the true position of value s_t
+    (Philox.advance moves in blocks of four draws) — and over-generates by the
+    worst expected drift. Every attempt of the ziggurat restarts on a fresh
+    draw, so the thread's sequence of attempts merges with the true one within
+    a few values; segment t - 1 also produces the first _OVERLAP values of
+    segment t, and matching that run of doubles locates value s_t in thread
+    t's output exactly. A segment whose run is not found (its attempts never
+    merged inside the window) returns None and the caller draws serially."""
+    seg = -(-n // threads)
+    starts = [t * seg for t in range(threads)]
+    counts = [min(seg, n - s0) for s0 in starts]
+    lens, outs = [], [None] * threads
+    for t, s0 in enumerate(starts):
+        drift = 0 if t == 0 else int(0.04 * s0) + 4096
+        lens.append(drift + counts[t] + _OVERLAP)
+
+    def draw(t):
+        bg = np.random.Philox(key=key)
+        if t:
+            bg.advance(starts[t] // 4)
+        outs[t] = np.random.Generator(bg).standard_normal(lens[t])
+
+    with ThreadPoolExecutor(threads) as pool:
+        list(pool.map(draw, range(threads)))
+    offs = [0]
+    for t in range(1, threads):
+        prev = outs[t - 1]
+        run = prev[offs[t - 1] + counts[t - 1]: offs[t - 1] + counts[t - 1] + _OVERLAP]
+        window = outs[t][: lens[t] - counts[t] - _OVERLAP + 1]
+        hit = None
+        for j in np.flatnonzero(window == run[0]):
+            if np.array_equal(outs[t][j: j + _OVERLAP], run):
+                hit = int(j)
+                break
+        if hit is None:
+            return None
+        offs.append(hit)
+    out = np.empty(n)
+
+    def place(t):
+        out[starts[t]: starts[t] + counts[t]] = outs[t][offs[t]: offs[t] + counts[t]]
+
+    with ThreadPoolExecutor(threads) as pool:
+        list(pool.map(place, range(threads)))
+    return out
 
 
 @dataclass(frozen=True)
