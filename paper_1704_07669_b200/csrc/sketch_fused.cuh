@@ -229,8 +229,11 @@ template <int LPAD, bool NORM, bool SHIFT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<LPAD>::THREADS, 1)
 tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ CUtensorMap tAh,
                const __grid_constant__ CUtensorMap tWhi, const __grid_constant__ CUtensorMap tWlo,
-               const __grid_constant__ CUtensorMap tGT, const __grid_constant__ CUtensorMap tAg3,
-               const __grid_constant__ CUtensorMap tAh2, const FusedArgs args) {
+               const __grid_constant__ CUtensorMap tGT,
+#if SPCA_PAIRA
+               const __grid_constant__ CUtensorMap tAg3, const __grid_constant__ CUtensorMap tAh2,
+#endif
+               const FusedArgs args) {
   using C = TcCfg<LPAD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -276,10 +279,10 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     ptx::tma_prefetch(&tWhi);
     ptx::tma_prefetch(&tWlo);
     ptx::tma_prefetch(&tGT);
-    if (SPCA_PAIRA) {
-      ptx::tma_prefetch(&tAg3);
-      ptx::tma_prefetch(&tAh2);
-    }
+#if SPCA_PAIRA
+    ptx::tma_prefetch(&tAg3);
+    ptx::tma_prefetch(&tAh2);
+#endif
   }
   if (threadIdx.x < 128) stg_bad[threadIdx.x] = 0;
   if (warp == 1) ptx::tmem_alloc2(&bars.tmem_base, kTmemCols);
@@ -626,7 +629,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         if (ctr) ctr[2] = clock64();
         ptx::tc_fence_after();
         const uint32_t tst = lane_base + C::A_TMEM + 64 * ts;
-        if (!(args.dbg & (1 | 32))) {  // 32: profiling knob, no TMEM stores (split kept)
+        if (!(args.dbg & 1)) {
           ptx::tmem_st32(tst, hi);
           ptx::tmem_st32(tst + 32, v);
         }

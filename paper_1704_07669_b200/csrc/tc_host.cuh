@@ -441,7 +441,13 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
                                   : (h->shift_on ? tc_pass_kernel<128, false, true> : tc_pass_kernel<128, false>));
   const unsigned threads = h->tc_lp == 64 ? TcCfg<64>::THREADS : TcCfg<128>::THREADS;
   const unsigned smem = h->tc_lp == 64 ? TcCfg<64>::SMEM : TcCfg<128>::SMEM;
+#if SPCA_PAIRA
   kern<<<grid, threads, smem, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, *ta_g3, *ta_h2, args);
+#else
+  (void)ta_g3;
+  (void)ta_h2;
+  kern<<<grid, threads, smem, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, args);
+#endif
   CK_LAUNCH(h);
   }
   h->chunks_since_flush += s.C;

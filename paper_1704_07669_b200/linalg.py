@@ -55,7 +55,7 @@ def gaussian_matrix(rows: int, cols: int, seed: int, stream: int = STREAM_SKETCH
 
 
 _DRAW_THREADS = max(1, min(16, os.cpu_count() or 1))
-_DRAW_MIN_PER_THREAD = 1 << 20
+_DRAW_MIN_PER_THREAD = 1 << 17
 _OVERLAP = 64
 
 
