@@ -664,3 +664,44 @@ def test_power_refine_normalized_file(tmp_path):
     assert pc.passes_completed == 2
     assert rel(res.s, want.s) <= 1e-4
     assert O.subspace_angle(res.v, want.v) <= 1e-3
+
+
+# ------------------------------------------- full-size properties (cfg3, cfg5)
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", ["cfg3", "cfg5"])
+def test_full_size_properties(config):
+    """BASELINE configs 3 (1 000 000 x 4096, l = 120) and 5 (50 000 x 200 000,
+    l = 250, column groups) at full size on one device, through
+    size-independent identities in fp64: G = A Omega and y^T H x = (A y)^T (G x)
+    on random probes, Omega^T H = G^T G (both equal Omega^T A^T A Omega), column
+    sums against a direct reduction, bitwise repeatability."""
+    if not _tc_ok():
+        pytest.skip("no tensor-core path")
+    from paper_1704_07669_b200 import synth
+    cs = synth.config_shape(config)
+    a = synth.config_matrix(config, device="cuda")
+    m, n = a.shape
+    l = cs["l"]
+    om = O.gaussian(n, l, 1)
+    st = P.sketch_pass(P.DeviceRowStream(a), om, keep_on_device=True)
+    om32 = st.omega
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(l, 4, device="cuda", dtype=torch.float64, generator=gen)
+    y = torch.randn(n, 4, device="cuda", dtype=torch.float64, generator=gen)
+    step = max(1, int(2e8) // n)
+    rows = min(m, 20 * step)
+    g_ref = a[:rows].double() @ (om32 @ x)
+    assert float(torch.linalg.norm(st.g[:rows] @ x - g_ref) / torch.linalg.norm(g_ref)) < 2e-5
+    ay = torch.cat([a[i:i + step].double() @ y for i in range(0, m, step)])
+    rhs = ay.T @ (st.g @ x)
+    assert float(torch.linalg.norm(y.T @ st.h @ x - rhs) / torch.linalg.norm(rhs)) < 1e-5
+    cross, gram = om32.T @ st.h, st.g.T @ st.g
+    assert float(torch.linalg.norm(cross - gram) / torch.linalg.norm(gram)) < 1e-5
+    cs_ref = torch.zeros(n, dtype=torch.float64, device="cuda")
+    for i in range(0, m, step):
+        cs_ref += a[i:i + step].double().sum(dim=0)
+    assert float(torch.linalg.norm(st.col_sums - cs_ref) / torch.linalg.norm(cs_ref)) < 1e-6
+    st2 = P.sketch_pass(P.DeviceRowStream(a), om, keep_on_device=True)
+    assert torch.equal(st.h, st2.h) and torch.equal(st.g, st2.g) and torch.equal(st.col_sums, st2.col_sums)
+    del a, st, st2, ay
+    torch.cuda.empty_cache()
