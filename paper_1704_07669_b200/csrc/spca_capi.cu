@@ -561,10 +561,10 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
   TRY(cudaMemsetAsync(h->hpart, 0, (size_t)h->hsplit * n * h->lpad * ds, h->stream));
   TRY(dalloc(h, &h->cspart, (size_t)h->hsplit * n * 8));
   TRY(cudaMemsetAsync(h->cspart, 0, (size_t)h->hsplit * n * 8, h->stream));
-  TRY(dalloc(h, &h->bad_dev, sizeof(unsigned long long)));
+  TRY(dalloc(h, &h->bad_dev, 2 * sizeof(unsigned long long)));
   {
-    unsigned long long init = (unsigned long long)kNoBadRow;
-    TRY(cudaMemcpyAsync(h->bad_dev, &init, sizeof init, cudaMemcpyHostToDevice, h->stream));
+    unsigned long long init[2] = {(unsigned long long)kNoBadRow, (unsigned long long)kNoBadRow};
+    TRY(cudaMemcpyAsync(h->bad_dev, init, sizeof init, cudaMemcpyHostToDevice, h->stream));
     TRY(cudaStreamSynchronize(h->stream));
   }
   TRY(dalloc(h, &h->tail, (size_t)h->chunk_rows * n * ds));
@@ -749,12 +749,16 @@ int spca_sketch_set_left(spca_handle_t h, const double *left, int64_t rows, int 
 int spca_sketch_reset(spca_handle_t h) {
   if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
   DeviceGuard dg(h->device);
-  CK(h, cudaStreamSynchronize(h->stream));
+  // after finish the stream has drained (finish ends with its one
+  // synchronization): the reset is then fully asynchronous; an abandoned pass
+  // is drained first so its sources may be released by the caller
+  const bool drained = h->finished || (h->rows_seen == 0 && h->tail_rows == 0);
+  if (!drained) CK(h, cudaStreamSynchronize(h->stream));
   CK(h, cudaMemsetAsync(h->hcs_dev, 0, (size_t)h->n * (h->l + 1) * 8, h->stream));
   if (h->carry_dev) CK(h, cudaMemsetAsync(h->carry_dev, 0, (size_t)h->n * 8, h->stream));
-  unsigned long long init = (unsigned long long)kNoBadRow;
-  CK(h, cudaMemcpyAsync(h->bad_dev, &init, sizeof init, cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaStreamSynchronize(h->stream));
+  // bad_dev[1] holds the "no bad row" sentinel (set at create): a device copy, no host staging
+  CK(h, cudaMemcpyAsync(h->bad_dev, h->bad_dev + 1, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                        h->stream));
   h->tail_rows = 0;
   h->rows_seen = 0;
   h->rows_done = 0;
