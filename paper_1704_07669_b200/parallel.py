@@ -89,7 +89,7 @@ def sharded_single_pass_pca(local_rows, cfg, dist, group=None, precision: str = 
     n = int(local_rows.shape[1])
     omega = gaussian_matrix(n, cfg.l, cfg.seed, stream=STREAM_SKETCH)
     st = sketch_pass(DeviceRowStream(local_rows), omega, precision=precision,
-                     device=device, keep_on_device=True)
+                     device=device, keep_on_device=True, shift=cfg.center)
     h = st.h.clone()
     cs = st.col_sums.clone()
     m_total = allreduce_sketch(h, cs, dist, rows=st.rows_seen, group=group)
