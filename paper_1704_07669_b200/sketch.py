@@ -91,11 +91,17 @@ class GpuSketch:
         if normalize:  # rows are sketched as normalize_rows leaves them (fused on the TC path)
             _lib.check(self.lib.spca_sketch_set_normalize(self.h, 1), self.h)
         elif shift:  # accumulate A - 1 c^T (c = first row), shift undone in fp64 at finish
-            _lib.check(self.lib.spca_sketch_set_shift(self.h, 1), self.h)
+            self.set_shift(True)
         self._keep = []          # host/device sources that must outlive async copies
         self._finished = False
         # what "auto" resolved to: "tc" (tcgen05 3xTF32) or "simt" (FFMA / DFMA)
         self.precision = "tc" if self.lib.spca_sketch_precision(self.h) == _PRECISIONS["tc"] else "simt"
+
+    def set_shift(self, on: bool = True) -> None:
+        """Column shift (spca_sketch_set_shift): accumulate A - 1 c^T, c = the
+        pass's first row, and restore the sketch of A in fp64 at finish.
+        Before the first push of a pass; exclusive with normalisation."""
+        _lib.check(self.lib.spca_sketch_set_shift(self.h, 1 if on else 0), self.h)
 
     def set_left(self, left) -> None:
         """Co-sketch operand L (m x l float64, numpy or CUDA tensor): the pass

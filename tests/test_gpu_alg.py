@@ -312,8 +312,8 @@ def test_shift_bitwise_splits_and_errors():
         P.sketch_pass(P.ArrayRowStream(bad), om, shift=True)
     assert ei.value.row == 4321
     sk = P.GpuSketch(600, om, np.float32, normalize=True)
-    with pytest.raises(P.ConfigError):
-        sk.lib and P._lib.check(sk.lib.spca_sketch_set_shift(sk.h, 1), sk.h)
+    with pytest.raises(P.ConfigError):  # shift and normalisation are exclusive
+        sk.set_shift(True)
     sk.close()
 
 
