@@ -171,8 +171,9 @@ int spca_g_colsum(spca_handle_t h, double *out, int out_where);
  * normalized into a workspace first. */
 int spca_sketch_set_normalize(spca_handle_t h, int on);
 
-/* Column shift: with on != 0 the pass sketches A - 1 c^T, c = the pass's
- * first row (non-finite entries as 0), and finish adds the shift back in
+/* Column shift: with on != 0 the pass sketches A - 1 c^T, c = the mean of
+ * the first (up to 256) rows of the pass's first push (a non-finite mean as
+ * 0), and finish adds the shift back in
  * fp64 (G += 1 (Omega^T c)^T, H += col_sums' w^T + c (1^T G')^T + m c w^T, or
  * H += c (1^T L)^T with a co-sketch operand; col_sums += m c), so the results
  * are the sketch of A itself. The fp32 accumulators then hold values of the

@@ -169,12 +169,17 @@ __global__ void norm_correct(double *__restrict__ hcs, int n, int l, const doubl
   }
 }
 
-// Column shift (spca_sketch_set_shift): c = the pass's first row with
-// non-finite values replaced by 0, fp32, zero padded to `pad` entries.
+// Column shift (spca_sketch_set_shift): c = the mean of the pass's first
+// `rows` rows (fp64 sum, rounded to fp32; a non-finite mean becomes 0), zero
+// padded to `pad` entries. Rows of stride ld.
 template <typename T>
-__global__ void shift_capture(const T *__restrict__ row, int n, int pad, float *__restrict__ c) {
+__global__ void shift_capture(const T *__restrict__ a, int rows, int64_t ld, int n, int pad,
+                              float *__restrict__ c) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < pad; j += gridDim.x * blockDim.x) {
-    float v = j < n ? (float)row[j] : 0.f;
+    double s = 0.0;
+    if (j < n)
+      for (int r = 0; r < rows; ++r) s += (double)a[(int64_t)r * ld + j];
+    const float v = (float)(s / (double)rows);
     c[j] = isfinite(v) ? v : 0.f;
   }
 }

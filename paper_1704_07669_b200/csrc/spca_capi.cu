@@ -624,21 +624,27 @@ int push_impl(spca_handle_t h, const void *a, int64_t rows, int64_t ld, int64_t 
                    "stream yielded more rows than the co-sketch operand has (%lld)", (long long)h->left_rows);
   DeviceGuard dg(h->device);
   int rc = SPCA_OK;
-  if (h->shift_on && !h->shift_set && rows > 0) {  // c = the pass's first row
+  if (h->shift_on && !h->shift_set && rows > 0) {  // c = the mean of the pass's first rows
+    // a sample of up to 256 rows: the sketch then holds deviations of size
+    // ~ spread * sqrt(n / sample) around the mean instead of the mean itself
     const int pad = (int)round_up(h->n, 256);
+    const int sr = (int)std::min<int64_t>(rows, 256);
     const void *src = a;
+    int64_t sld = ld;
     void *tmp = nullptr;
     if (where != SPCA_MEM_DEVICE) {
-      CK(h, dalloc(h, &tmp, (size_t)h->n * h->ds));
-      CK(h, cudaMemcpyAsync(tmp, a, (size_t)h->n * h->ds, cudaMemcpyHostToDevice, h->stream));
+      CK(h, dalloc(h, &tmp, (size_t)sr * h->n * h->ds));
+      CK(h, cudaMemcpy2DAsync(tmp, (size_t)h->n * h->ds, a, (size_t)ld * h->ds, (size_t)h->n * h->ds, (size_t)sr,
+                              cudaMemcpyHostToDevice, h->stream));
       src = tmp;
+      sld = h->n;
     }
     if (h->dtype == SPCA_F32)
-      shift_capture<float><<<(unsigned)ceil_div(pad, 256), 256, 0, h->stream>>>((const float *)src, (int)h->n, pad,
-                                                                                h->cshift);
+      shift_capture<float><<<(unsigned)ceil_div(pad, 256), 256, 0, h->stream>>>((const float *)src, sr, sld,
+                                                                                (int)h->n, pad, h->cshift);
     else
-      shift_capture<double><<<(unsigned)ceil_div(pad, 256), 256, 0, h->stream>>>((const double *)src, (int)h->n,
-                                                                                 pad, h->cshift);
+      shift_capture<double><<<(unsigned)ceil_div(pad, 256), 256, 0, h->stream>>>((const double *)src, sr, sld,
+                                                                                 (int)h->n, pad, h->cshift);
     CK_LAUNCH(h);
     dfree(h, tmp);
     h->shift_set = true;

@@ -90,7 +90,7 @@ class GpuSketch:
         self.h = handle
         if normalize:  # rows are sketched as normalize_rows leaves them (fused on the TC path)
             _lib.check(self.lib.spca_sketch_set_normalize(self.h, 1), self.h)
-        elif shift:  # accumulate A - 1 c^T (c = first row), shift undone in fp64 at finish
+        elif shift:  # accumulate A - 1 c^T (c = mean of the first rows), undone in fp64 at finish
             self.set_shift(True)
         self._keep = []          # host/device sources that must outlive async copies
         self._finished = False
@@ -99,7 +99,7 @@ class GpuSketch:
 
     def set_shift(self, on: bool = True) -> None:
         """Column shift (spca_sketch_set_shift): accumulate A - 1 c^T, c = the
-        pass's first row, and restore the sketch of A in fp64 at finish.
+        mean of the pass's first (up to 256) rows, and restore the sketch of A in fp64 at finish.
         Before the first push of a pass; exclusive with normalisation."""
         _lib.check(self.lib.spca_sketch_set_shift(self.h, 1 if on else 0), self.h)
 
@@ -494,7 +494,7 @@ def sketch_pass(
     device path is always order-fixed — bitwise identical for every block
     size and run to run — which is the property fixed_order buys on the CPU.
     ``compensated`` enables Kahan summation of col_sums across chunks.
-    ``shift`` accumulates A - 1 c^T (c = the first row) and adds the shift
+    ``shift`` accumulates A - 1 c^T (c = the mean of the first rows) and adds the shift
     back in fp64: same results, fp32 accumulators sized by A's spread rather
     than its mean (the centered algorithms turn it on)."""
     om = np.asarray(omega, dtype=np.float64)

@@ -292,6 +292,36 @@ def test_shift_sketch_vs_oracle(precision, left):
     assert rel(hc, hc_ref) <= 2e-5, rel(hc, hc_ref)
 
 
+@pytest.mark.parametrize("dtype,precision,m,n,l", [
+    (np.float32, "tc", 2100, 2000, 250),   # column groups of 128
+    (np.float32, "tc", 3000, 4096, 120),   # l_pad = 128
+    (np.float32, "tc", 1500, 1000, 60),    # n not a multiple of 32 (2-D A loads)
+    (np.float64, "auto", 900, 300, 20),    # DFMA path
+])
+def test_shift_shapes(dtype, precision, m, n, l):
+    if precision == "tc" and not _tc_ok():
+        pytest.skip("no tensor-core path")
+    rng = np.random.default_rng(n)
+    a = (O.gaussian(m, n, seed=m) * 1e-2 + rng.normal(0, 5, size=(1, n))).astype(dtype)
+    om = O.gaussian(n, l, seed=l)
+    st = P.sketch_pass(P.ArrayRowStream(a), om, precision=precision, shift=True)
+    a64 = a.astype(np.float64)
+    om_u = om.astype(np.float32).astype(np.float64) if dtype == np.float32 else om
+    assert np.array_equal(st.omega, om_u)  # spca_omega_used: exactly the values the pass used
+    g_ref = a64 @ om_u
+    tol = 1e-6 if dtype == np.float32 else 1e-12
+    assert rel(st.g, g_ref) <= tol and rel(st.h, a64.T @ g_ref) <= tol
+    # centered sketches: accurate to the data's spread, not its (500x larger)
+    # mean. (fp64: the post-hoc centering below — the reference's own
+    # center_correct, in fp64 — itself loses ~u (mean/spread)^2 sqrt(n) ~ 1e-9.)
+    mu = a64.mean(axis=0)
+    gc = st.g - (mu @ om_u)[None, :]
+    hc = st.h - np.outer(mu, st.g.sum(axis=0))
+    ac = a64 - mu
+    assert rel(gc, ac @ om_u) <= (2e-5 if dtype == np.float32 else 1e-10)
+    assert rel(hc, ac.T @ (ac @ om_u)) <= (2e-5 if dtype == np.float32 else 1e-8)
+
+
 def test_shift_bitwise_splits_and_errors():
     if not _tc_ok():
         pytest.skip("no tensor-core path")
