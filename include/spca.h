@@ -147,6 +147,14 @@ int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out,
 int spca_device_views(spca_handle_t h, double **g_dev, double **hcs_dev);
 
 
+/* Multi-GPU exchange: sum the finished [H | col_sums] of
+ * every rank of `nccl_comm` (an ncclComm_t of the caller's NCCL, one rank per
+ * GPU, each handle on its own GPU) in place with ncclAllReduce on the handle's
+ * stream, and return the global row count. G stays row-sharded. libnccl.so.2
+ * is resolved at run time (SPCA_ERR_CAPABILITY when absent); the row shards
+ * are the reference's consecutive RowStream blocks split by rank. */
+int spca_allreduce(spca_handle_t h, void *nccl_comm, int64_t *rows_total);
+
 /* center_correct (sketch.py:119-139) on the finished device state, in
  * place: mu = colsum / m_total; G -= 1 (mu^T Omega); H -= mu (1^T G) where
  * 1^T G is `gsum` (l values, already summed over every rank's rows; NULL =

@@ -27,6 +27,7 @@ FLAGS = [
     "-Xcompiler", "-fPIC,-O3",
     "-shared", "-cudart", "static",
     "--expt-relaxed-constexpr",
+    "-ldl",
     "-Xptxas", "-v",
 ]
 if os.environ.get("SPCA_BUILD_FINE_TRACE"):  # profiling builds: per-K-block clock64 stamps

@@ -7,6 +7,9 @@
 
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types and enums only: the library is resolved at run time (dlopen)
+
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
@@ -889,6 +892,65 @@ int spca_device_views(spca_handle_t h, double **g_dev, double **hcs_dev) {
   if (!h->finished) return set_err(h, SPCA_ERR_STATE, -1, "device views need a finished sketch");
   if (g_dev) *g_dev = h->g64_dev;
   if (hcs_dev) *hcs_dev = h->hcs_dev;
+  return SPCA_OK;
+}
+
+// NCCL entry points, resolved from the process's libnccl.so.2 at first use
+// (the one the caller's communicator came from when it is already loaded).
+struct NcclFns {
+  ncclResult_t (*all_reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  const char *(*error_string)(ncclResult_t) = nullptr;
+};
+
+static const NcclFns *nccl_fns() {
+  static NcclFns f;
+  static bool tried = false;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!tried) {
+    tried = true;
+    void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW);
+    if (lib) {
+      f.all_reduce = (decltype(f.all_reduce))dlsym(lib, "ncclAllReduce");
+      f.group_start = (decltype(f.group_start))dlsym(lib, "ncclGroupStart");
+      f.group_end = (decltype(f.group_end))dlsym(lib, "ncclGroupEnd");
+      f.error_string = (decltype(f.error_string))dlsym(lib, "ncclGetErrorString");
+    }
+  }
+  return (f.all_reduce && f.group_start && f.group_end) ? &f : nullptr;
+}
+
+int spca_allreduce(spca_handle_t h, void *nccl_comm, int64_t *rows_total) {
+  if (!h || !nccl_comm) return set_err(h, SPCA_ERR_STATE, -1, "null argument");
+  if (!h->finished) return set_err(h, SPCA_ERR_STATE, -1, "allreduce needs a finished sketch");
+  const NcclFns *nf = nccl_fns();
+  if (!nf) return set_err(h, SPCA_ERR_CAPABILITY, -1, "libnccl.so.2 not found");
+  DeviceGuard dg(h->device);
+  double *rows = nullptr;
+  CK(h, dalloc(h, &rows, sizeof(double)));
+  const double local = (double)h->rows_seen;
+  CK(h, cudaMemcpyAsync(rows, &local, sizeof local, cudaMemcpyHostToDevice, h->stream));
+  ncclComm_t comm = (ncclComm_t)nccl_comm;
+  ncclResult_t r = nf->group_start();
+  if (r == ncclSuccess)
+    r = nf->all_reduce(h->hcs_dev, h->hcs_dev, (size_t)h->n * (h->l + 1), ncclFloat64, ncclSum, comm, h->stream);
+  if (r == ncclSuccess) r = nf->all_reduce(rows, rows, 1, ncclFloat64, ncclSum, comm, h->stream);
+  const ncclResult_t r2 = nf->group_end();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) {
+    dfree(h, rows);
+    return set_err(h, SPCA_ERR_CUDA, -1, "NCCL all-reduce failed: %s",
+                   nf->error_string ? nf->error_string(r) : "unknown");
+  }
+  double total = 0.0;
+  CK(h, cudaMemcpyAsync(&total, rows, sizeof total, cudaMemcpyDeviceToHost, h->stream));
+  dfree(h, rows);
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (rows_total) *rows_total = (int64_t)(total + 0.5);
   return SPCA_OK;
 }
 

@@ -221,6 +221,15 @@ class GpuSketch:
         _lib.check(self.lib.spca_omega_used(self.h, ctypes.c_void_p(out.ctypes.data), _lib.MEM_PAGEABLE), self.h)
         return out
 
+    def allreduce_nccl(self, comm) -> int:
+        """spca_allreduce: sum the finished [H | col_sums] over the ranks of an
+        ncclComm_t (an integer pointer from the caller's NCCL) in place; returns
+        the global row count. (torch.distributed callers use
+        parallel.allreduce_sketch, which needs no raw communicator.)"""
+        total = ctypes.c_int64(0)
+        _lib.check(self.lib.spca_allreduce(self.h, ctypes.c_void_p(int(comm)), ctypes.byref(total)), self.h)
+        return total.value
+
     def rows(self) -> int:
         """Rows pushed so far (spca_sketch_rows)."""
         r = ctypes.c_int64(0)

@@ -384,3 +384,44 @@ def test_centered_fp32_offset_data(algo):
         err = float(np.max(np.abs(res.s - s_ref) / s_ref))
         assert err <= 1e-4, (prec, err)
         assert O.subspace_angle(res.v[:, :5], v_ref[:, :5]) <= 1e-3, prec
+
+
+# ------------------------------------------------- spca_allreduce (C ABI, NCCL)
+def _nccl_single_rank_comm():
+    """A one-rank NCCL communicator on the current GPU through ctypes (what a
+    C/C++ host would hold); None when libnccl is not loadable."""
+    import ctypes
+    try:
+        nccl = ctypes.CDLL("libnccl.so.2", mode=ctypes.RTLD_GLOBAL)
+    except OSError:
+        return None, None
+    class UniqueId(ctypes.Structure):  # ncclUniqueId, passed by value
+        _fields_ = [("internal", ctypes.c_char * 128)]
+
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(ctypes.byref(uid)) == 0
+    comm = ctypes.c_void_p()
+    nccl.ncclCommInitRank.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, UniqueId, ctypes.c_int]
+    assert nccl.ncclCommInitRank(ctypes.byref(comm), 1, uid, 0) == 0
+    return nccl, comm
+
+
+def test_spca_allreduce_single_rank():
+    """The C-ABI exchange step on a one-rank communicator: [H | col_sums] and G
+    unchanged bitwise, the global row count returned; state errors."""
+    torch.cuda.set_device(0)
+    nccl, comm = _nccl_single_rank_comm()
+    if nccl is None:
+        pytest.skip("libnccl.so.2 not loadable")
+    a = O.gaussian(3000, 500, seed=41).astype(np.float32)
+    om = O.gaussian(500, 40, seed=42)
+    sk = P.GpuSketch(500, om, np.float32)
+    sk.push(a, 0, final=True)
+    with pytest.raises(P.StreamPcaError):
+        sk.allreduce_nccl(comm.value)  # before finish
+    g, h, cs, m = sk.finish(on_device=False)
+    assert sk.allreduce_nccl(comm.value) == 3000
+    g2, h2, cs2, m2 = sk.finish(on_device=False)
+    assert np.array_equal(h, h2) and np.array_equal(cs, cs2) and np.array_equal(g, g2) and m2 == m
+    sk.close()
+    nccl.ncclCommDestroy(comm)
