@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-pca", action="store_true")
     p.add_argument("--ring-gb", type=float, default=16.0, help="cfg4: pinned host ring size")
+    p.add_argument("--dtype", default="f32", choices=["f32", "f64"],
+                   help="element type of A (f64: the config's values widened, DFMA path)")
     return p.parse_args()
 
 
@@ -331,14 +333,18 @@ def run_ours(args):
     cs = synth.config_shape(args.config)
     m = args.rows or cs["m"]
     n, l = cs["n"], cs["l"]
-    bytes_per_rank = m * n * 4
+    es = 8 if args.dtype == "f64" else 4
+    npdt = np.float64 if args.dtype == "f64" else np.float32
+    bytes_per_rank = m * n * es
     hbm_peak, bf16_peak, peak_kind = peaks()
 
     # this rank's shard: rows [rank*m, (rank+1)*m) of the job's matrix
     a = synth.config_matrix(args.config, device=dev, rows=(rank * m, (rank + 1) * m),
                             m_override=m * world)
+    if args.dtype == "f64":
+        a = a.double()
     omega = gaussian_matrix(n, l, 1)
-    sk = GpuSketch(n, omega, np.float32, precision=args.precision, device=dev, rows_hint=m)
+    sk = GpuSketch(n, omega, npdt, precision=args.precision, device=dev, rows_hint=m)
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -383,12 +389,15 @@ def run_ours(args):
     # the library's stream over the timed region (spca_kernel_time_ms).
     chunk_rows = sk.chunk_rows()
     pass_ms = kern_ms / max(1, args.steps)
-    pass_bytes = m * n * 4
+    pass_bytes = m * n * es
     flops = 4.0 * m * n * l
     used_tc = sk.precision == "tc"
     if used_tc:
         peak_tf = bf16_peak / 2.0 / 3.0   # 3xTF32: tf32 = bf16/2, three products
         peak_desc = "3xTF32 effective = measured bf16 burst / 2 (tf32) / 3 (products)"
+    elif args.dtype == "f64":
+        peak_tf = 148 * 64 * 2 * 1.965e9 / 1e12  # DFMA nominal
+        peak_desc = "DFMA nominal (148 SMs x 64 fp64 lanes x 2 x 1965 MHz)"
     else:
         peak_tf = 148 * 128 * 2 * 1.965e9 / 1e12  # FFMA nominal
         peak_desc = "FFMA nominal (148 SMs x 128 lanes x 2 x 1965 MHz)"
@@ -434,10 +443,10 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": args.config, "m_per_gpu": m, "n": n, "l": l, "k": cs["k"],
                    "rank": cs["rank"], "spectrum": cs["spectrum"], "noise": cs["noise"],
-                   "precision": "3xTF32 tcgen05" if used_tc else "FFMA",
+                   "precision": "3xTF32 tcgen05" if used_tc else ("DFMA" if args.dtype == "f64" else "FFMA"),
                    "parallelism": f"row-shard x{world}",
                    "l2": "inputs larger than L2 (A is %.1f GB per GPU)" % (bytes_per_rank / 1e9)},
         "roofline": roofline,
@@ -458,10 +467,11 @@ def e2e_leg(args, a_dev, omega, dev, steps=3):
     import torch
     from paper_1704_07669_b200 import GpuSketch
     m, n = a_dev.shape
-    host = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
+    host = torch.empty((m, n), dtype=a_dev.dtype, pin_memory=True)
     host.copy_(a_dev)
     torch.cuda.synchronize()
-    sk = GpuSketch(n, omega, np.float32, precision=args.precision, device=dev, rows_hint=m)
+    sk = GpuSketch(n, omega, np.float64 if a_dev.dtype == torch.float64 else np.float32,
+                   precision=args.precision, device=dev, rows_hint=m)
     times = []
     d2h = 0
     for i in range(steps + 1):
@@ -477,7 +487,8 @@ def e2e_leg(args, a_dev, omega, dev, steps=3):
     sk.close()
     del host
     t = float(np.median(times))
-    return {"value": m * n * 4 / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": m * n * 4,
+    es = a_dev.element_size()
+    return {"value": m * n * es / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": m * n * es,
             "d2h_bytes_per_step": int(d2h), "seconds_per_step": t}
 
 
