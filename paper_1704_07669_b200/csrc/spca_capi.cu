@@ -141,6 +141,15 @@ int ensure_g(spca_sketch *h, int64_t rows_needed) {
 namespace {
 
 // ---- SIMT chunk processing ------------------------------------------------
+// Grid sizing of the SIMT path (CTAs per SM aimed at by the G split-K and the
+// H row splits) and its canonical chunk (MB of A); env overrides for tuning.
+int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? std::max(1, atoi(e)) : dflt;
+}
+const int kSimtGTarget = env_int("SPCA_SIMT_G_CTAS", 4);
+const int kSimtHTarget = env_int("SPCA_SIMT_H_CTAS", 8);  // measured: 2 -> 8 = -15% at config 2 (fp64 31.7 -> 27.1 ms)
+const int kSimtChunkMB = env_int("SPCA_SIMT_CHUNK_MB", 160);
 
 template <typename T, int BM, int BL, bool VEC>
 void launch_g(spca_sketch *h, const T *a, int64_t lda, int rows, T *out, int64_t out_stride,
@@ -169,7 +178,7 @@ int simt_chunk(spca_sketch *h, const T *a, int64_t lda, int rows) {
   // split-K so that the G kernel fills the machine (~4 CTAs per SM)
   int64_t tiles = ceil_div(rows, bm) * (h->lpad / h->bl);
   int64_t kmax = std::max<int64_t>(1, ceil_div(h->n, 128));
-  int ksplit = (int)std::min<int64_t>(kmax, std::max<int64_t>(1, ceil_div(148 * 4, tiles)));
+  int ksplit = (int)std::min<int64_t>(kmax, std::max<int64_t>(1, ceil_div(148 * kSimtGTarget, tiles)));
   int kseg = (int)round_up(ceil_div(h->n, ksplit), 32);
   ksplit = (int)ceil_div(h->n, kseg);
   T *gout = (T *)h->g_dev + h->rows_done * h->lpad;
@@ -522,7 +531,7 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
   }
   // canonical chunk: ~160 MB of A, 64..4096 rows, multiple of 128
   {
-    int64_t r = (int64_t)(160ll << 20) / (n * (int64_t)h->ds);
+    int64_t r = (int64_t)((int64_t)kSimtChunkMB << 20) / (n * (int64_t)h->ds);
     r = std::max<int64_t>(128, std::min<int64_t>(4096, r));
     h->chunk_rows = (r / 128) * 128;
     if (h->precision == SPCA_PREC_TC) h->chunk_rows = tc_chunk_rows(n, l);
@@ -534,7 +543,7 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
   {
     int bn = h->bl == 32 ? 128 : 64;
     int64_t tiles = ceil_div(n, bn) * (h->lpad / h->bl);
-    int64_t want = ceil_div(148 * 2, tiles);
+    int64_t want = ceil_div(148 * kSimtHTarget, tiles);
     h->hsplit = (int)std::max<int64_t>(1, std::min<int64_t>(8, want));
     if (h->precision == SPCA_PREC_TC) h->hsplit = 1;  // the pass kernel keeps one running H
   }
