@@ -6,11 +6,12 @@
 //   simt_g_reduce   fixed-order sum of split-K partials of G_c
 //   simt_h_kernel   Hpart[z] (+)= A_c^T G_c     (sketch.py:104)
 //                   + per-chunk column sums     (sketch.py:106) in fp64
-// Both contractions are register-tiled (4x4 outputs per thread, 256 threads)
-// with double-buffered shared-memory tiles; A and Omega/G tiles are loaded
-// with 16-byte vector loads when alignment allows. This is the SIMT path
-// (SPCA_PREC_SIMT) and the fp64 path; the tensor-core path lives in
-// sketch_tc.cuh.
+// fp32: register-tiled FFMA (4x4 outputs per thread, 256 threads); fp64: the
+// same CTA tiles fed to the fp64 tensor cores with warp-level DMMA
+// (mma.sync m16n8k4 .f64: each warp one 16-row tile x four 8-column tiles).
+// Both use double-buffered shared-memory tiles loaded with 16-byte vector
+// loads when alignment allows. This is the SIMT path (SPCA_PREC_SIMT) and the
+// fp64 path; the tensor-core path for fp32 lives in sketch_tc.cuh.
 #pragma once
 
 #include "common.cuh"
@@ -18,6 +19,22 @@
 namespace spca {
 
 constexpr int kSimtThreads = 256;
+
+// fp64 tensor-core step: D(16x8) += A(16x4, row) B(4x8, col), fp64 throughout
+// (fragment: a0 = A[g][t], a1 = A[g+8][t], b = B[t][g], d = D[g][2t..2t+1],
+// D[g+8][2t..2t+1] with g = lane / 4, t = lane % 4)
+__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+               : "d"(a0), "d"(a1), "d"(b));
+}
+
+// shared-row padding: fp64 tiles are read as 4 k-rows x 8 consecutive values
+// per warp load, conflict-free when the row stride is 64 mod 128 bytes
+template <typename T, int W>
+struct SimtRow {
+  static constexpr int value = sizeof(T) == 8 ? W + 8 : W + 16 / (int)sizeof(T);
+};
 
 // ---------------------------------------------------------------- G = A W
 // grid = (row tiles, l tiles, k splits). W is n x ldw (ldw % BL == 0, zero
@@ -33,12 +50,11 @@ simt_g_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
   constexpr int NTM = BM / TM;
   static_assert(NTL * NTM == kSimtThreads, "thread tiling");
   constexpr int VN = Vec<T>::n;
-  constexpr int PAD = 16 / sizeof(T);
   constexpr int A_PER = BM * BK / kSimtThreads;  // elements per thread
   constexpr int W_PER = BK * BL / kSimtThreads;
   static_assert(A_PER % VN == 0 && W_PER % VN == 0, "vector tiling");
-  __shared__ __align__(16) T As[2][BK][BM + PAD];
-  __shared__ __align__(16) T Ws[2][BK][BL];
+  __shared__ __align__(16) T As[2][BK][SimtRow<T, BM>::value];
+  __shared__ __align__(16) T Ws[2][BK][sizeof(T) == 8 ? BL + 8 : BL];
 
   const int tid = threadIdx.x;
   const int tl = tid % NTL, tm = tid / NTL;
@@ -129,6 +145,16 @@ simt_g_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TL; ++j) acc[i][j] = T(0);
+  // fp64: warp (wm, wn) owns rows [16 wm, 16 wm + 16) x columns [32 wn, 32 wn + 32)
+  constexpr int WMT = BM / 16;  // 16-row tiles = warps along M
+  static_assert(sizeof(T) == 4 || (WMT * (BL / 32) == kSimtThreads / 32), "DMMA warp tiling");
+  const int lane = tid & 31, wid = tid >> 5, wm = wid % WMT, wn = wid / WMT;
+  const int fg = lane >> 2, ft = lane & 3;
+  double dacc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dacc[i][j] = 0.0;
 
   const int ntiles = (ke > kb) ? (ke - kb + BK - 1) / BK : 0;
   if (ntiles > 0) {
@@ -139,26 +165,26 @@ simt_g_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
   for (int t = 0; t < ntiles; ++t) {
     const int buf = t & 1;
     if (t + 1 < ntiles) load_tiles(kb + (t + 1) * BK);
+    if constexpr (sizeof(T) == 4) {
 #pragma unroll
-    for (int k = 0; k < BK; ++k) {
-      T a[TM], w[TL];
-      if constexpr (sizeof(T) == 4) {
+      for (int k = 0; k < BK; ++k) {
+        T a[TM], w[TL];
         float4 av = *reinterpret_cast<const float4 *>(&As[buf][k][tm * TM]);
         float4 wv = *reinterpret_cast<const float4 *>(&Ws[buf][k][tl * TL]);
         a[0] = av.x; a[1] = av.y; a[2] = av.z; a[3] = av.w;
         w[0] = wv.x; w[1] = wv.y; w[2] = wv.z; w[3] = wv.w;
-      } else {  // fp64: 16-byte shared loads (half the LDS instructions of scalar loads)
-        const double2 a01 = *reinterpret_cast<const double2 *>(&As[buf][k][tm * TM]);
-        const double2 a23 = *reinterpret_cast<const double2 *>(&As[buf][k][tm * TM + 2]);
-        const double2 w01 = *reinterpret_cast<const double2 *>(&Ws[buf][k][tl * TL]);
-        const double2 w23 = *reinterpret_cast<const double2 *>(&Ws[buf][k][tl * TL + 2]);
-        a[0] = a01.x; a[1] = a01.y; a[2] = a23.x; a[3] = a23.y;
-        w[0] = w01.x; w[1] = w01.y; w[2] = w23.x; w[3] = w23.y;
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TL; ++j) acc[i][j] = fma(a[i], w[j], acc[i][j]);
       }
+    } else {  // fp64: DMMA, four k-steps of 4 per tile
 #pragma unroll
-      for (int i = 0; i < TM; ++i)
+      for (int ks = 0; ks < BK; ks += 4) {
+        const double a0 = As[buf][ks + ft][wm * 16 + fg], a1 = As[buf][ks + ft][wm * 16 + fg + 8];
 #pragma unroll
-        for (int j = 0; j < TL; ++j) acc[i][j] = fma(a[i], w[j], acc[i][j]);
+        for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(dacc[nt], a0, a1, Ws[buf][ks + ft][wn * 32 + nt * 8 + fg]);
+      }
     }
     if (t + 1 < ntiles) {
       store_tiles(buf ^ 1);
@@ -173,6 +199,18 @@ simt_g_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
   }
 
   T *o = out + (int64_t)blockIdx.z * out_split_stride;
+  if constexpr (sizeof(T) == 8) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = m0 + wm * 16 + fg + 8 * h;
+      if (r >= rows) continue;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+        *reinterpret_cast<double2 *>(o + (int64_t)r * ldo + j0 + wn * 32 + nt * 8 + 2 * ft) =
+            make_double2(dacc[nt][2 * h], dacc[nt][2 * h + 1]);
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     int r = m0 + tm * TM + i;
@@ -218,8 +256,8 @@ simt_h_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
   constexpr int A_PER = BK * BN / kSimtThreads;
   constexpr int G_PER = BK * BL / kSimtThreads;
   static_assert(A_PER % VN == 0 && G_PER % VN == 0, "vector tiling");
-  __shared__ __align__(16) T As[2][BK][BN];
-  __shared__ __align__(16) T Gs[2][BK][BL];
+  __shared__ __align__(16) T As[2][BK][sizeof(T) == 8 ? BN + 8 : BN];
+  __shared__ __align__(16) T Gs[2][BK][sizeof(T) == 8 ? BL + 8 : BL];
 
   const int tid = threadIdx.x;
   const int tl = tid % NTL, tn = tid / NTL;
@@ -227,7 +265,9 @@ simt_h_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
   const int j0 = blockIdx.y * BL;
   const int rb = blockIdx.z * rseg;
   const int re = min(rows, rb + rseg);
-  const bool do_cs = (blockIdx.y == 0) && (tl == 0);
+  // column sums: fp32 path, the threads of l-tile 0 for their 4 columns; fp64
+  // path, thread c < BN for column c (the MMA fragments do not own columns)
+  const bool do_cs = (blockIdx.y == 0) && (sizeof(T) == 4 ? (tl == 0) : (tid < BN));
 
   T ra[A_PER];
   T rg[G_PER];
@@ -306,6 +346,15 @@ simt_h_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
     for (int j = 0; j < TL; ++j) acc[i][j] = T(0);
   double cs[TN] = {0.0, 0.0, 0.0, 0.0};
   double cc[TN] = {0.0, 0.0, 0.0, 0.0};  // Kahan carries (compensated mode)
+  constexpr int WMT = BN / 16;  // fp64: warp (wm, wn) owns columns [16 wm, +16) x [32 wn, +32)
+  static_assert(sizeof(T) == 4 || (WMT * (BL / 32) == kSimtThreads / 32), "DMMA warp tiling");
+  const int lane = tid & 31, wid = tid >> 5, wm = wid % WMT, wn = wid / WMT;
+  const int fg = lane >> 2, ft = lane & 3;
+  double dacc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dacc[i][j] = 0.0;
 
   const int ntiles = (re > rb) ? (re - rb + BK - 1) / BK : 0;
   if (ntiles > 0) {
@@ -316,21 +365,36 @@ simt_h_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
   for (int t = 0; t < ntiles; ++t) {
     const int buf = t & 1;
     if (t + 1 < ntiles) load_tiles(rb + (t + 1) * BK);
+    if constexpr (sizeof(T) == 8) {  // fp64: DMMA (A^T: m = column, k = row) + column sums
+#pragma unroll
+      for (int ks = 0; ks < BK; ks += 4) {
+        const double a0 = As[buf][ks + ft][wm * 16 + fg], a1 = As[buf][ks + ft][wm * 16 + fg + 8];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(dacc[nt], a0, a1, Gs[buf][ks + ft][wn * 32 + nt * 8 + fg]);
+      }
+      if (do_cs) {
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+          const double x = As[buf][k][tid];
+          if (kahan) {
+            const double y = x - cc[0];
+            const double t2 = cs[0] + y;
+            cc[0] = (t2 - cs[0]) - y;
+            cs[0] = t2;
+          } else {
+            cs[0] += x;
+          }
+        }
+      }
+    } else
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
       T a[TN], g[TL];
-      if constexpr (sizeof(T) == 4) {
+      {
         float4 av = *reinterpret_cast<const float4 *>(&As[buf][k][tn * TN]);
         float4 gv = *reinterpret_cast<const float4 *>(&Gs[buf][k][tl * TL]);
         a[0] = av.x; a[1] = av.y; a[2] = av.z; a[3] = av.w;
         g[0] = gv.x; g[1] = gv.y; g[2] = gv.z; g[3] = gv.w;
-      } else {  // fp64: 16-byte shared loads
-        const double2 a01 = *reinterpret_cast<const double2 *>(&As[buf][k][tn * TN]);
-        const double2 a23 = *reinterpret_cast<const double2 *>(&As[buf][k][tn * TN + 2]);
-        const double2 g01 = *reinterpret_cast<const double2 *>(&Gs[buf][k][tl * TL]);
-        const double2 g23 = *reinterpret_cast<const double2 *>(&Gs[buf][k][tl * TL + 2]);
-        a[0] = a01.x; a[1] = a01.y; a[2] = a23.x; a[3] = a23.y;
-        g[0] = g01.x; g[1] = g01.y; g[2] = g23.x; g[3] = g23.y;
       }
 #pragma unroll
       for (int i = 0; i < TN; ++i)
@@ -356,6 +420,26 @@ simt_h_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
   }
 
   T *hp = Hpart + (int64_t)blockIdx.z * h_split_stride;
+  if constexpr (sizeof(T) == 8) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = n0 + wm * 16 + fg + 8 * h;
+      if (c >= n) continue;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        double2 *dst = reinterpret_cast<double2 *>(hp + (int64_t)c * ldh + j0 + wn * 32 + nt * 8 + 2 * ft);
+        double2 v = make_double2(dacc[nt][2 * h], dacc[nt][2 * h + 1]);
+        if (accumulate) {
+          const double2 old = *dst;
+          v.x += old.x;
+          v.y += old.y;
+        }
+        *dst = v;
+      }
+    }
+    if (do_cs && n0 + tid < n) cspart[(int64_t)blockIdx.z * n + n0 + tid] = cs[0];
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < TN; ++i) {
     int c = n0 + tn * TN + i;
