@@ -493,7 +493,9 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
   if (!out) return set_err(nullptr, SPCA_ERR_CONFIG, -1, "null handle pointer");
   *out = nullptr;
   if (n < 1 || l < 1) return set_err(nullptr, SPCA_ERR_FORMAT, -1, "omega must be 2-d and non-empty (n=%lld, l=%lld)", (long long)n, (long long)l);
-  if (l > 256) return set_err(nullptr, SPCA_ERR_CONFIG, -1, "sketch width l=%lld > 256 unsupported", (long long)l);
+  // any sketch width the reference accepts (l <= min(m, n), algorithms.py:89-101);
+  // the bound only keeps l_pad * rows and the launch grids inside int range
+  if (l > (1 << 16)) return set_err(nullptr, SPCA_ERR_CONFIG, -1, "sketch width l=%lld > 65536 unsupported", (long long)l);
   if (n > INT32_MAX / 2) return set_err(nullptr, SPCA_ERR_CONFIG, -1, "n too large");
   if (dtype != SPCA_F32 && dtype != SPCA_F64) return set_err(nullptr, SPCA_ERR_CONFIG, -1, "bad dtype %d", dtype);
   if (!omega) return set_err(nullptr, SPCA_ERR_FORMAT, -1, "omega is null");

@@ -38,7 +38,7 @@ bool tc_available(int device) {
 // promoted accumulators of an N = 256 tile fit the register budget.
 // l > 128 runs as column groups of 128 (one launch per group over the same
 // rows): H[:, J] = A^T (A Omega[:, J]) needs only G[:, J].
-constexpr int kTcMaxL = 512;
+constexpr int kTcMaxL = 4096;  // column groups of 128: one launch (one read of A) per group
 bool tc_supported_shape(int64_t n, int64_t l) { return n >= 32 && n % 4 == 0 && l >= 1 && l <= kTcMaxL; }
 
 // l_pad of the whole sketch (accumulator layouts) and of one launch

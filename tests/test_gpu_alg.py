@@ -425,3 +425,32 @@ def test_spca_allreduce_single_rank():
     assert np.array_equal(h, h2) and np.array_equal(cs, cs2) and np.array_equal(g, g2) and m2 == m
     sk.close()
     nccl.ncclCommDestroy(comm)
+
+
+# ------------------------------------------------------------- wide sketches
+@pytest.mark.parametrize("dtype,precision,m,n,l", [
+    (np.float32, "tc", 2000, 1500, 300),    # three column groups of 128
+    (np.float32, "tc", 1500, 2048, 700),    # six groups, l_pad 768
+    (np.float32, "simt", 1200, 900, 330),
+    (np.float64, "auto", 900, 800, 310),    # DMMA, five 64-column l tiles
+])
+def test_wide_sketch_vs_oracle(dtype, precision, m, n, l):
+    """Sketch widths beyond 256 (k + oversample of a few hundred): the
+    reference accepts any l <= min(m, n)."""
+    if precision == "tc" and not _tc_ok():
+        pytest.skip("no tensor-core path")
+    a = O.gaussian(m, n, seed=l).astype(dtype)
+    om = O.gaussian(n, l, seed=l + 1)
+    st = P.sketch_pass(P.ArrayRowStream(a), om, precision=precision)
+    om_u = om.astype(np.float32).astype(np.float64) if dtype == np.float32 else om
+    ref = O.oracle_sketch(O.row_blocks(a.astype(np.float64), 4096), om_u)
+    tol = 2e-5 if dtype == np.float32 else 1e-12
+    assert rel(st.g, ref.g) <= tol and rel(st.h, ref.h) <= tol
+
+
+def test_wide_pca_k300():
+    """single_pass_pca with k = 300 (l = 310) on fp32 data: the 1e-4 bar."""
+    a = O.synth_lowrank_plus_noise(3000, 1200, 400, "exp30", 1e-3, seed=9)
+    res = P.single_pass_pca(a, P.PcaConfig(k=300, seed=1))
+    _, s_ref, v_ref, *_ = O.oracle_single_pass(a, k=300, seed=1, block_rows=4096)
+    assert float(np.max(np.abs(res.s[:100] - s_ref[:100]) / s_ref[:100])) <= 1e-4
