@@ -77,6 +77,10 @@ struct spca_sketch {
   unsigned long long bad_seen = 0;  // first non-finite row, read back at finish
 
   int64_t chunk_rows = 0;        // canonical chunk (R0)
+  int64_t ldp = 0;               // row stride of the library's own row buffers (tail, staging):
+                                 // n, or n rounded up to 4 on the tensor-core path (16-byte TMA rows)
+  void *padbuf = nullptr;        // TC path: rows of a source whose stride TMA cannot address
+  int64_t padbuf_rows = 0;
   void *tail = nullptr;          // R0 x n staging for the partial chunk
   int64_t tail_rows = 0;
   int64_t rows_seen = 0;         // accepted

@@ -185,7 +185,7 @@ __host__ __device__ __forceinline__ int bcomb_row(int j, int part, int lp) {
 
 // Omega -> the combined B matrix (2 lpad x n): Omega^T hi / lo rows interleaved per CTA half
 __global__ void tc_omega_prepare_comb(const double *__restrict__ om64, int n, int l, int lpad, int lp,
-                                      float *__restrict__ w2) {
+                                      float *__restrict__ w2, int ldw) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (; idx < (int64_t)lpad * n; idx += stride) {
@@ -194,8 +194,8 @@ __global__ void tc_omega_prepare_comb(const double *__restrict__ om64, int n, in
     const float v = j < l ? (float)om64[(int64_t)i * l + j] : 0.f;
     float hi, lo;
     split3(v, hi, lo);
-    w2[(int64_t)bcomb_row(j, 0, lp) * n + i] = hi;
-    w2[(int64_t)bcomb_row(j, 1, lp) * n + i] = lo;
+    w2[(int64_t)bcomb_row(j, 0, lp) * ldw + i] = hi;
+    w2[(int64_t)bcomb_row(j, 1, lp) * ldw + i] = lo;
   }
 }
 

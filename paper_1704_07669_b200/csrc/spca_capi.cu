@@ -356,31 +356,49 @@ int process_rows_tc(spca_sketch *h, const char *a, int64_t lda, int64_t rows) {
 int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, bool final = false) {
   const int64_t R0 = h->chunk_rows;
   const size_t row_bytes = (size_t)h->n * h->ds;
+  const size_t pitch = (size_t)h->ldp * h->ds;  // rows of the library's own buffers
   int64_t off = 0;
+  // TMA addresses rows whose stride is a multiple of 16 bytes from a 16-byte
+  // aligned base; other sources are re-strided through padbuf on the way in
+  const bool tma_ok = lda % 4 == 0 && (reinterpret_cast<uintptr_t>(a) % 16) == 0;
   if (h->precision == SPCA_PREC_TC) {
     int rr = tc_register_source(h, a, rows, lda);
     if (rr) return rr;
   }
   if (h->tail_rows > 0) {
     int64_t take = std::min(R0 - h->tail_rows, rows);
-    CK(h, cudaMemcpy2DAsync((char *)h->tail + h->tail_rows * row_bytes, row_bytes, a,
+    CK(h, cudaMemcpy2DAsync((char *)h->tail + h->tail_rows * pitch, pitch, a,
                             (size_t)lda * h->ds, row_bytes, (size_t)take,
                             cudaMemcpyDeviceToDevice, h->stream));
     h->tail_rows += take;
     off = take;
     if (h->tail_rows == R0) {
-      int rc = h->precision == SPCA_PREC_TC ? process_rows_tc(h, (const char *)h->tail, h->n, R0)
-                                            : process_chunk(h, h->tail, h->n, R0);
+      int rc = h->precision == SPCA_PREC_TC ? process_rows_tc(h, (const char *)h->tail, h->ldp, R0)
+                                            : process_chunk(h, h->tail, h->ldp, R0);
       if (rc) return rc;
       h->tail_rows = 0;
     }
   }
   if (h->precision == SPCA_PREC_TC) {  // all whole chunks (and a final partial one) in one go
     const int64_t take = final ? rows - off : ((rows - off) / R0) * R0;
-    if (take > 0) {
+    if (take > 0 && tma_ok) {
       int rc = process_rows_tc(h, a + (size_t)off * lda * h->ds, lda, take);
       if (rc) return rc;
       off += take;
+    } else if (take > 0) {  // re-stride into padbuf, whole chunks per launch
+      if (!h->padbuf) {
+        h->padbuf_rows = std::max<int64_t>(R0, (h->stage_rows / R0) * R0);
+        CK(h, dalloc(h, &h->padbuf, (size_t)h->padbuf_rows * pitch));
+      }
+      const int64_t end = off + take;
+      while (off < end) {
+        const int64_t piece = std::min(end - off, h->padbuf_rows);
+        CK(h, cudaMemcpy2DAsync(h->padbuf, pitch, a + (size_t)off * lda * h->ds, (size_t)lda * h->ds, row_bytes,
+                                (size_t)piece, cudaMemcpyDeviceToDevice, h->stream));
+        int rc = process_rows_tc(h, (const char *)h->padbuf, h->ldp, piece);
+        if (rc) return rc;
+        off += piece;
+      }
     }
   }
   while (rows - off >= R0) {
@@ -395,7 +413,7 @@ int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, b
   }
   if (off < rows) {
     int64_t rem = rows - off;
-    CK(h, cudaMemcpy2DAsync((char *)h->tail, row_bytes, a + (size_t)off * lda * h->ds,
+    CK(h, cudaMemcpy2DAsync((char *)h->tail, pitch, a + (size_t)off * lda * h->ds,
                             (size_t)lda * h->ds, row_bytes, (size_t)rem,
                             cudaMemcpyDeviceToDevice, h->stream));
     h->tail_rows = rem;
@@ -404,7 +422,7 @@ int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, b
 }
 
 int ensure_staging(spca_sketch *h, bool need_pinned) {
-  const size_t bytes = (size_t)h->stage_rows * h->n * h->ds;
+  const size_t bytes = (size_t)h->stage_rows * h->ldp * h->ds;
   for (int i = 0; i < 2; ++i) {
     if (!h->dstage[i]) CK(h, cudaMalloc(&h->dstage[i], bytes));
     if (!h->copy_done[i]) CK(h, cudaEventCreateWithFlags(&h->copy_done[i], cudaEventDisableTiming));
@@ -419,6 +437,7 @@ int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, boo
   int rc = ensure_staging(h, pageable);
   if (rc) return rc;
   const size_t row_bytes = (size_t)h->n * h->ds;
+  const size_t pitch = (size_t)h->ldp * h->ds;  // staging rows (16-byte multiple on the TC path)
   int64_t off = 0;
   while (off < rows) {
     int64_t take = std::min(h->stage_rows, rows - off);
@@ -430,22 +449,22 @@ int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, boo
     if (pageable) {
       if (h->stage_used[i]) CK(h, cudaEventSynchronize(h->copy_done[i]));
       char *dst = (char *)h->pinned[i];
-      if ((size_t)lda * h->ds == row_bytes) {
-        memcpy(dst, src, (size_t)take * row_bytes);
+      if ((size_t)lda * h->ds == pitch) {
+        memcpy(dst, src, (size_t)take * pitch);
       } else {
         for (int64_t r = 0; r < take; ++r)
-          memcpy(dst + r * row_bytes, src + (size_t)r * lda * h->ds, row_bytes);
+          memcpy(dst + r * pitch, src + (size_t)r * lda * h->ds, row_bytes);
       }
       src = dst;
-      CK(h, cudaMemcpyAsync(h->dstage[i], src, (size_t)take * row_bytes, cudaMemcpyHostToDevice,
+      CK(h, cudaMemcpyAsync(h->dstage[i], src, (size_t)take * pitch, cudaMemcpyHostToDevice,
                             h->copy_stream));
     } else {
-      CK(h, cudaMemcpy2DAsync(h->dstage[i], row_bytes, src, (size_t)lda * h->ds, row_bytes,
+      CK(h, cudaMemcpy2DAsync(h->dstage[i], pitch, src, (size_t)lda * h->ds, row_bytes,
                               (size_t)take, cudaMemcpyHostToDevice, h->copy_stream));
     }
     CK(h, cudaEventRecord(h->copy_done[i], h->copy_stream));
     CK(h, cudaStreamWaitEvent(h->stream, h->copy_done[i], 0));
-    rc = push_device_rows(h, (const char *)h->dstage[i], take, h->n, final && off + take == rows);
+    rc = push_device_rows(h, (const char *)h->dstage[i], take, h->ldp, final && off + take == rows);
     if (rc) return rc;
     CK(h, cudaEventRecord(h->comp_done[i], h->stream));
     h->stage_used[i] = true;
@@ -581,7 +600,8 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
     TRY(cudaMemcpyAsync(h->bad_dev, init, sizeof init, cudaMemcpyHostToDevice, h->stream));
     TRY(cudaStreamSynchronize(h->stream));
   }
-  TRY(dalloc(h, &h->tail, (size_t)h->chunk_rows * n * ds));
+  h->ldp = h->precision == SPCA_PREC_TC ? round_up(n, 4) : n;
+  TRY(dalloc(h, &h->tail, (size_t)h->chunk_rows * h->ldp * ds));
   // Omega: upload fp64, derive the compute-precision copy
   {
     double *om_src = nullptr;
@@ -676,8 +696,8 @@ int push_impl(spca_handle_t h, const void *a, int64_t rows, int64_t ld, int64_t 
   }
   if (rc) return rc;
   if (final && h->tail_rows > 0) {  // rows == 0, or a tail left by earlier pushes
-    rc = h->precision == SPCA_PREC_TC ? process_rows_tc(h, (const char *)h->tail, h->n, h->tail_rows)
-                                      : process_chunk(h, h->tail, h->n, h->tail_rows);
+    rc = h->precision == SPCA_PREC_TC ? process_rows_tc(h, (const char *)h->tail, h->ldp, h->tail_rows)
+                                      : process_chunk(h, h->tail, h->ldp, h->tail_rows);
     if (rc) return rc;
     h->tail_rows = 0;
   }
@@ -818,8 +838,8 @@ int spca_sketch_finish(spca_handle_t h, double *g_out, double *h_out, double *co
   int rc;
   if (!h->finished) {
     if (h->tail_rows > 0) {
-      rc = h->precision == SPCA_PREC_TC ? process_rows_tc(h, (const char *)h->tail, h->n, h->tail_rows)
-                                        : process_chunk(h, h->tail, h->n, h->tail_rows);
+      rc = h->precision == SPCA_PREC_TC ? process_rows_tc(h, (const char *)h->tail, h->ldp, h->tail_rows)
+                                        : process_chunk(h, h->tail, h->ldp, h->tail_rows);
       if (rc) return rc;
       h->tail_rows = 0;
     }
@@ -1123,7 +1143,7 @@ void spca_sketch_destroy(spca_handle_t h) {
     void *pooled[] = {h->omega_dev, h->omega64_dev, h->tc_omega, h->g_dev, h->g64_dev, h->hcs_dev,
                       h->carry_dev, h->hpart, h->cspart, h->gpart, h->tc_ws, h->bad_dev, h->tail,
                       h->trace, h->tc_ctr, h->order_dev, h->norm_ws, h->rstat_part, h->row_a0,
-                      h->row_inv, h->row_coef, h->wsum, h->left_dev, h->left64_dev, h->cshift};
+                      h->row_inv, h->row_coef, h->wsum, h->left_dev, h->left64_dev, h->cshift, h->padbuf};
     for (void *p : pooled) dfree(h, p);
   }
   for (void *p : {h->dstage[0], h->dstage[1]})

@@ -39,7 +39,9 @@ bool tc_available(int device) {
 // l > 128 runs as column groups of 128 (one launch per group over the same
 // rows): H[:, J] = A^T (A Omega[:, J]) needs only G[:, J].
 constexpr int kTcMaxL = 4096;  // column groups of 128: one launch (one read of A) per group
-bool tc_supported_shape(int64_t n, int64_t l) { return n >= 32 && n % 4 == 0 && l >= 1 && l <= kTcMaxL; }
+// any n >= 32: rows whose stride is not a multiple of 16 bytes are re-strided
+// through a padded buffer before the pass (push_device_rows)
+bool tc_supported_shape(int64_t n, int64_t l) { return n >= 32 && l >= 1 && l <= kTcMaxL; }
 
 // l_pad of the whole sketch (accumulator layouts) and of one launch
 int tc_lpad(int64_t l) { return l <= 64 ? 64 : (int)(128 * ceil_div(l, 128)); }
@@ -209,7 +211,10 @@ int tc_setup(spca_sketch *h) {
   CK(h, cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
   h->max_pairs = lp == 64 ? tc_max_pairs<64>() : tc_max_pairs<128>();
   if (h->max_pairs < 1) return set_err(h, SPCA_ERR_CUDA, -1, "no CTA pair of the pass kernel fits an SM pair");
-  CK(h, dalloc(h, &h->tc_omega, (size_t)2 * h->lpad * h->n * 4));
+  // Omega^T rows padded to a 16-byte multiple (TMA strides), zero padding
+  const int64_t ldw = round_up(h->n, 4);
+  CK(h, dalloc(h, &h->tc_omega, (size_t)2 * h->lpad * ldw * 4));
+  CK(h, cudaMemsetAsync(h->tc_omega, 0, (size_t)2 * h->lpad * ldw * 4, h->stream));
   float *whi = (float *)h->tc_omega;
   float *wlo = whi + (size_t)h->lpad * h->n;
   const uint32_t hr = (uint32_t)(lp / 2);
@@ -218,9 +223,9 @@ int tc_setup(spca_sketch *h) {
   // one matrix of 2 lpad rows: each CTA's half of a column group is hi rows
   // then lo rows, loaded as ONE box of lp rows per K block
   tc_omega_prepare_comb<<<grid_for((int64_t)h->lpad * h->n), 256, 0, h->stream>>>(
-      h->omega64_dev, (int)h->n, (int)h->l, (int)h->lpad, lp, whi);
+      h->omega64_dev, (int)h->n, (int)h->l, (int)h->lpad, lp, whi, (int)ldw);
   CK_LAUNCH(h);
-  rc = encode_2d(h, &h->tm_whi, whi, (uint64_t)h->n, (uint64_t)2 * h->lpad, (uint64_t)h->n * 4, 32, lp);
+  rc = encode_2d(h, &h->tm_whi, whi, (uint64_t)h->n, (uint64_t)2 * h->lpad, (uint64_t)ldw * 4, 32, lp);
   if (rc) return rc;
   h->tm_wlo = h->tm_whi;
   const uint32_t gbox = (uint32_t)lp;

@@ -454,3 +454,46 @@ def test_wide_pca_k300():
     res = P.single_pass_pca(a, P.PcaConfig(k=300, seed=1))
     _, s_ref, v_ref, *_ = O.oracle_single_pass(a, k=300, seed=1, block_rows=4096)
     assert float(np.max(np.abs(res.s[:100] - s_ref[:100]) / s_ref[:100])) <= 1e-4
+
+
+# ------------------------------------------- any n on the tensor-core path
+@pytest.mark.parametrize("n", [1001, 333, 4098])
+def test_tc_row_stride_not_16_bytes(n, tmp_path):
+    """Row strides that TMA cannot address (n % 4 != 0, or an unaligned view)
+    are re-strided through a padded buffer: same sketch as the oracle from
+    device, pinned, pageable and file sources, bitwise equal across them, and
+    with normalisation, column shift and a co-sketch operand."""
+    if not _tc_ok():
+        pytest.skip("no tensor-core path")
+    m, l = 5000, 60
+    a = (O.gaussian(m, n, seed=n) + 0.5).astype(np.float32)
+    om = O.gaussian(n, l, seed=n + 1)
+    om32 = om.astype(np.float32).astype(np.float64)
+    ref = O.oracle_sketch(O.row_blocks(a.astype(np.float64), 4096), om32)
+    st = P.sketch_pass(P.ArrayRowStream(a), om, precision="tc")
+    assert rel(st.g, ref.g) <= 2e-5 and rel(st.h, ref.h) <= 2e-5
+    dev = torch.from_numpy(a).cuda()
+    pin = torch.from_numpy(a).pin_memory()
+    path = str(tmp_path / "a.spca")
+    P.matfile.write_matrix(path, a, dtype="float32", header=True)
+    for src in [P.DeviceRowStream(dev), P.PinnedRowStream(pin), P.FileRowStream(path)]:
+        s2 = P.sketch_pass(src, om, precision="tc")
+        assert np.array_equal(np.asarray(s2.g), st.g) and np.array_equal(np.asarray(s2.h), st.h)
+    # an unaligned device view (column offset 1): stride n + 1, base not 16-byte aligned
+    wide = torch.zeros((m, n + 1), dtype=torch.float32, device="cuda")
+    wide[:, 1:] = dev
+    s3 = P.sketch_pass(P.DeviceRowStream(wide[:, 1:]), om, precision="tc")
+    assert np.array_equal(np.asarray(s3.h), st.h)
+    # normalisation, shift and co-sketch through the padded path
+    sn = P.sketch_pass(P.NormalizedRowStream(P.ArrayRowStream(a)), om, precision="tc")
+    rn = O.oracle_sketch(O.row_blocks(O.oracle_normalize_rows(a.astype(np.float64)), 4096), om32)
+    assert rel(sn.h, rn.h) <= 2e-5
+    ss = P.sketch_pass(P.ArrayRowStream(a), om, precision="tc", shift=True)
+    assert rel(ss.h, ref.h) <= 1e-6
+    left = O.gaussian(m, l, seed=3)
+    sk = P.GpuSketch(n, om, np.float32, precision="tc")
+    sk.set_left(left)
+    sk.push(a, 0, final=True)
+    _, hl, _, _ = sk.finish(on_device=False)
+    sk.close()
+    assert rel(hl, a.astype(np.float64).T @ left.astype(np.float32).astype(np.float64)) <= 2e-5
