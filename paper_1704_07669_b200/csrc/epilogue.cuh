@@ -169,6 +169,20 @@ __global__ void norm_correct(double *__restrict__ hcs, int n, int l, const doubl
   }
 }
 
+// dst (rows x n, stride ldd) <- src (stride lds): device rows whose stride the
+// pass kernel's TMA cannot address, re-strided into the staging ring
+template <typename T>
+__global__ void restride_rows(const T *__restrict__ src, int64_t lds, int64_t rows, int n, T *__restrict__ dst,
+                              int64_t ldd) {
+  const int64_t total = rows * n;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / n;
+    const int c = (int)(idx - r * n);
+    dst[r * ldd + c] = src[r * lds + c];
+  }
+}
+
 // Column shift (spca_sketch_set_shift): c = the mean of the pass's first
 // `rows` rows (fp64 sum, rounded to fp32; a non-finite mean becomes 0), zero
 // padded to `pad` entries. Rows of stride ld.

@@ -79,8 +79,6 @@ struct spca_sketch {
   int64_t chunk_rows = 0;        // canonical chunk (R0)
   int64_t ldp = 0;               // row stride of the library's own row buffers (tail, staging):
                                  // n, or n rounded up to 4 on the tensor-core path (16-byte TMA rows)
-  void *padbuf = nullptr;        // TC path: rows of a source whose stride TMA cannot address
-  int64_t padbuf_rows = 0;
   void *tail = nullptr;          // R0 x n staging for the partial chunk
   int64_t tail_rows = 0;
   int64_t rows_seen = 0;         // accepted
@@ -98,6 +96,7 @@ struct spca_sketch {
   int64_t stage_rows = 0;
   cudaEvent_t copy_done[2] = {nullptr, nullptr};
   cudaEvent_t comp_done[2] = {nullptr, nullptr};
+  cudaEvent_t src_ready = nullptr;  // device rows re-strided on the copy stream: producer done
   bool stage_used[2] = {false, false};
   int stage_idx = 0;
 

@@ -352,6 +352,9 @@ int process_rows_tc(spca_sketch *h, const char *a, int64_t lda, int64_t rows) {
   return close_timing(h, chunks);
 }
 
+int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, bool pageable, bool final = false,
+                   bool device_src = false);
+
 // Rows already on the device: feed canonical chunks, keep the remainder in `tail`.
 int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, bool final = false) {
   const int64_t R0 = h->chunk_rows;
@@ -359,8 +362,10 @@ int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, b
   const size_t pitch = (size_t)h->ldp * h->ds;  // rows of the library's own buffers
   int64_t off = 0;
   // TMA addresses rows whose stride is a multiple of 16 bytes from a 16-byte
-  // aligned base; other sources are re-strided through padbuf on the way in
+  // aligned base; other sources are re-strided through the staging ring
   const bool tma_ok = lda % 4 == 0 && (reinterpret_cast<uintptr_t>(a) % 16) == 0;
+  if (h->precision == SPCA_PREC_TC && !tma_ok)  // re-strided on the copy stream, overlapped with the pass
+    return push_host_rows(h, a, rows, lda, false, final, true);
   if (h->precision == SPCA_PREC_TC) {
     int rr = tc_register_source(h, a, rows, lda);
     if (rr) return rr;
@@ -381,24 +386,10 @@ int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, b
   }
   if (h->precision == SPCA_PREC_TC) {  // all whole chunks (and a final partial one) in one go
     const int64_t take = final ? rows - off : ((rows - off) / R0) * R0;
-    if (take > 0 && tma_ok) {
+    if (take > 0) {
       int rc = process_rows_tc(h, a + (size_t)off * lda * h->ds, lda, take);
       if (rc) return rc;
       off += take;
-    } else if (take > 0) {  // re-stride into padbuf, whole chunks per launch
-      if (!h->padbuf) {
-        h->padbuf_rows = std::max<int64_t>(R0, (h->stage_rows / R0) * R0);
-        CK(h, dalloc(h, &h->padbuf, (size_t)h->padbuf_rows * pitch));
-      }
-      const int64_t end = off + take;
-      while (off < end) {
-        const int64_t piece = std::min(end - off, h->padbuf_rows);
-        CK(h, cudaMemcpy2DAsync(h->padbuf, pitch, a + (size_t)off * lda * h->ds, (size_t)lda * h->ds, row_bytes,
-                                (size_t)piece, cudaMemcpyDeviceToDevice, h->stream));
-        int rc = process_rows_tc(h, (const char *)h->padbuf, h->ldp, piece);
-        if (rc) return rc;
-        off += piece;
-      }
     }
   }
   while (rows - off >= R0) {
@@ -433,9 +424,18 @@ int ensure_staging(spca_sketch *h, bool need_pinned) {
   return SPCA_OK;
 }
 
-int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, bool pageable, bool final = false) {
+// Rows staged through the double-buffered device staging ring on the copy
+// stream: host rows (pinned or pageable), or device rows whose stride the
+// pass kernel's TMA cannot address (device_src: re-strided D2D copies)
+int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, bool pageable, bool final,
+                   bool device_src) {
   int rc = ensure_staging(h, pageable);
   if (rc) return rc;
+  if (device_src) {  // the copy stream must see the work that produced the rows
+    if (!h->src_ready) CK(h, cudaEventCreateWithFlags(&h->src_ready, cudaEventDisableTiming));
+    CK(h, cudaEventRecord(h->src_ready, h->stream));
+    CK(h, cudaStreamWaitEvent(h->copy_stream, h->src_ready, 0));
+  }
   const size_t row_bytes = (size_t)h->n * h->ds;
   const size_t pitch = (size_t)h->ldp * h->ds;  // staging rows (16-byte multiple on the TC path)
   int64_t off = 0;
@@ -459,8 +459,18 @@ int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, boo
       CK(h, cudaMemcpyAsync(h->dstage[i], src, (size_t)take * pitch, cudaMemcpyHostToDevice,
                             h->copy_stream));
     } else {
-      CK(h, cudaMemcpy2DAsync(h->dstage[i], pitch, src, (size_t)lda * h->ds, row_bytes,
-                              (size_t)take, cudaMemcpyHostToDevice, h->copy_stream));
+      if (device_src) {  // a copy kernel (2-D DMA of odd-pitched rows is slow)
+        if (h->dtype == SPCA_F32)
+          restride_rows<float><<<148 * 8, 256, 0, h->copy_stream>>>((const float *)src, lda, take, (int)h->n,
+                                                                    (float *)h->dstage[i], h->ldp);
+        else
+          restride_rows<double><<<148 * 8, 256, 0, h->copy_stream>>>((const double *)src, lda, take, (int)h->n,
+                                                                     (double *)h->dstage[i], h->ldp);
+        CK_LAUNCH(h);
+      } else {
+        CK(h, cudaMemcpy2DAsync(h->dstage[i], pitch, src, (size_t)lda * h->ds, row_bytes, (size_t)take,
+                                cudaMemcpyHostToDevice, h->copy_stream));
+      }
     }
     CK(h, cudaEventRecord(h->copy_done[i], h->copy_stream));
     CK(h, cudaStreamWaitEvent(h->stream, h->copy_done[i], 0));
@@ -1129,7 +1139,7 @@ void spca_sketch_destroy(spca_handle_t h) {
   // that reads it; device buffers go back to the pool in stream order
   const bool host_side = h->copy_stream || h->pinned[0] || h->pinned[1] || h->dstage[0] || h->dstage[1];
   if (h->stream && host_side) cudaStreamSynchronize(h->stream);
-  for (cudaEvent_t e : {h->t_start, h->t_stop})
+  for (cudaEvent_t e : {h->t_start, h->t_stop, h->src_ready})
     if (e) cudaEventDestroy(e);
   if (h->copy_stream) {
     cudaStreamSynchronize(h->copy_stream);
@@ -1143,7 +1153,7 @@ void spca_sketch_destroy(spca_handle_t h) {
     void *pooled[] = {h->omega_dev, h->omega64_dev, h->tc_omega, h->g_dev, h->g64_dev, h->hcs_dev,
                       h->carry_dev, h->hpart, h->cspart, h->gpart, h->tc_ws, h->bad_dev, h->tail,
                       h->trace, h->tc_ctr, h->order_dev, h->norm_ws, h->rstat_part, h->row_a0,
-                      h->row_inv, h->row_coef, h->wsum, h->left_dev, h->left64_dev, h->cshift, h->padbuf};
+                      h->row_inv, h->row_coef, h->wsum, h->left_dev, h->left64_dev, h->cshift};
     for (void *p : pooled) dfree(h, p);
   }
   for (void *p : {h->dstage[0], h->dstage[1]})
