@@ -148,6 +148,24 @@ def qr_unpivoted(y, rank_check: bool = True, device=None) -> QrPair:
     return QrPair(q=q, r=r)
 
 
+def _cholesky_qr2_flagged(y):
+    """CholeskyQR2 without the host decision: (q, r, ok) with ok a device
+    bool (the acceptance test of _cholesky_qr2). For pipelines that check
+    many factorizations with one synchronization at the end."""
+    torch = torch_mod()
+    b = y.shape[1]
+    eye = torch.eye(b, dtype=y.dtype, device=y.device)
+    r1, info1 = torch.linalg.cholesky_ex(y.T @ y, upper=True)
+    q1 = torch.linalg.solve_triangular(r1, y, upper=True, left=False)
+    w2 = q1.T @ q1
+    defect = torch.abs(w2 - eye).max()
+    r2, info2 = torch.linalg.cholesky_ex(w2, upper=True)
+    q = torch.linalg.solve_triangular(r2, q1, upper=True, left=False)
+    r = r2 @ r1
+    ok = (info1 == 0) & (info2 == 0) & (defect < 1e-5) & torch.isfinite(r).all() & torch.isfinite(defect)
+    return q, r, ok
+
+
 def _cholesky_qr2(y):
     """Thin QR of a tall, well-conditioned y by CholeskyQR2: R1 = chol(y^T y),
     Q1 = y R1^-1, then once more on Q1; R = R2 R1. Two GEMM-shaped sweeps
@@ -160,17 +178,7 @@ def _cholesky_qr2(y):
     cond(y) up to ~2e5 passes, where the two factorizations agree to ~1e-11;
     every block the deficiency test could flag, |r_jj| below 1e-12 of the
     largest G column, goes to Householder)."""
-    torch = torch_mod()
-    b = y.shape[1]
-    eye = torch.eye(b, dtype=y.dtype, device=y.device)
-    r1, info1 = torch.linalg.cholesky_ex(y.T @ y, upper=True)
-    q1 = torch.linalg.solve_triangular(r1, y, upper=True, left=False)
-    w2 = q1.T @ q1
-    defect = torch.abs(w2 - eye).max()
-    r2, info2 = torch.linalg.cholesky_ex(w2, upper=True)
-    q = torch.linalg.solve_triangular(r2, q1, upper=True, left=False)
-    r = r2 @ r1
-    ok = (info1 == 0) & (info2 == 0) & (defect < 1e-5) & torch.isfinite(r).all() & torch.isfinite(defect)
+    q, r, ok = _cholesky_qr2_flagged(y)
     if not bool(ok):  # one host synchronization per QR
         return None
     return q, r
