@@ -38,6 +38,8 @@ if os.environ.get("SPCA_BUILD_BCOMB") is not None:  # experiment: separate hi / 
     FLAGS.append("-DSPCA_BCOMB=" + os.environ["SPCA_BUILD_BCOMB"])
 if os.environ.get("SPCA_BUILD_PAIRA") is not None:  # experiment: one TMA request per A K block (0)
     FLAGS.append("-DSPCA_PAIRA=" + os.environ["SPCA_BUILD_PAIRA"])
+if os.environ.get("SPCA_BUILD_PROMOTE") is not None:  # experiment: K blocks per accumulator period
+    FLAGS.append("-DSPCA_PROMOTE=" + os.environ["SPCA_BUILD_PROMOTE"])
 if os.environ.get("SPCA_BUILD_STACKED") is not None:  # experiment: l_pad=64 MMA form
     FLAGS.append("-DSPCA_STACKED_64=" + os.environ["SPCA_BUILD_STACKED"])
 

@@ -46,7 +46,10 @@ constexpr int kGroups = 2;      // converter groups
 constexpr int kTcConv = 128 * kGroups;  // converter threads
 constexpr int kTcEpi = 128;     // epilogue threads
 constexpr uint32_t kTmemCols = 512;
-constexpr int kPromote = 4;     // K blocks per accumulator period
+#ifndef SPCA_PROMOTE
+#define SPCA_PROMOTE 4
+#endif
+constexpr int kPromote = SPCA_PROMOTE;  // K blocks per accumulator period
 
 // Measured on B200 (tools/mma_bench.cu, tools/mma2_test.cu): a kind::tf32
 // K=8 MMA takes 64 cycles per SM at N = 128 (the full tf32 rate), 44 at N = 64
