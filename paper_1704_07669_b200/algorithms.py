@@ -21,7 +21,7 @@ from .device import default_device, host_copy, to_device64, torch_mod
 from .errors import ConfigError, EmptyStreamError
 from .linalg import STREAM_SKETCH, dense_svd, gaussian_matrix, qr_unpivoted, sign_align
 from .qb import QbFactor, blocked_qb
-from .sketch import SketchState, _omega_as_used, run_pass, sketch_pass
+from .sketch import SketchState, run_pass, sketch_pass
 from .streams import ArrayRowStream, PassCounter, RowStream
 
 
@@ -336,7 +336,9 @@ def legacy_single_pass(
         raise EmptyStreamError("the stream yielded no rows")
     if rows_seen != m:
         raise CapabilityError(f"stream declared {m} rows but yielded {rows_seen}")
-    ot = to_device64(_omega_as_used(omega_t, dtype), dev)
+    ot = to_device64(omega_t, dev)
+    if dtype == np.float32:  # Omega_t as the pass used it, rounded on the device
+        ot = ot.float().double()
     mean = None
     if cfg.center:
         mean = col_sums / m

@@ -16,8 +16,6 @@ from __future__ import annotations
 
 from typing import Optional
 
-import numpy as np
-
 from .device import host_copy, torch_mod
 
 

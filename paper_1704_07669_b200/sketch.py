@@ -31,7 +31,7 @@ import numpy as np
 
 from . import _lib
 from .device import default_device, host_copy, is_torch, to_device64, torch_mod
-from .errors import DeviceError, EmptyStreamError, StreamFormatError
+from .errors import EmptyStreamError, StreamFormatError
 from .streams import FileRowStream, PassCounter, RowBlock, RowStream, has_whole
 
 _PRECISIONS = {"auto": _lib.PREC_AUTO, "simt": _lib.PREC_SIMT, "tc": _lib.PREC_TC}
@@ -261,13 +261,6 @@ class GpuSketch:
             self.close()
         except Exception:
             pass
-
-
-def _omega_as_used(omega: np.ndarray, dtype) -> np.ndarray:
-    om = np.asarray(omega, dtype=np.float64)
-    if np.dtype(dtype) == np.float32:
-        return om.astype(np.float32).astype(np.float64)
-    return om
 
 
 def run_pass(stream, omega, block_rows=None, compensated=False, precision="auto",
