@@ -194,9 +194,10 @@ class SvdTriple:
 def dense_svd(b, device=None) -> SvdTriple:
     """Thin SVD of the l x n sketch factor B on the GPU (linalg.py:110-118).
 
-    Wide B is reduced first: B^T = Q_b R_b (tall QR, cuSOLVER), then the
-    l x l SVD R_b^T = U S W^T gives B = U S (Q_b W)^T — backward stable,
-    as LAPACK's dgesdd does for wide inputs."""
+    Wide B is reduced first: B^T = Q_b R_b (tall QR: CholeskyQR2 when B is
+    well conditioned, else cuSOLVER Householder), then the l x l SVD
+    R_b^T = U S W^T gives B = U S (Q_b W)^T — backward stable, as LAPACK's
+    dgesdd does for wide inputs."""
     torch = torch_mod()
     dev = default_device(device if device is not None else (b.device if getattr(b, "is_cuda", False) else None))
     b = to_device64(b, dev)
@@ -206,7 +207,8 @@ def dense_svd(b, device=None) -> SvdTriple:
         raise DataError("dense_svd input contains non-finite entries")
     p, n = b.shape
     if n > 2 * p:
-        qb, rb = torch.linalg.qr(b.T, mode="reduced")           # n x p, p x p
+        qr = _cholesky_qr2(b.T) if n >= 64 * p else None        # well conditioned: two GEMM sweeps
+        qb, rb = qr if qr is not None else torch.linalg.qr(b.T, mode="reduced")  # n x p, p x p
         u, s, wt = torch.linalg.svd(rb.T, full_matrices=False)
         v = qb @ wt.T
     else:
