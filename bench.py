@@ -191,6 +191,9 @@ def profile_traffic(rows: float, config: str):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
             prof = json.load(fh)
+        per = prof.get("per_config", {}).get(config)
+        if per is not None:
+            return per["dram_bytes_per_row"] * rows
         if prof.get("config", "cfg2") != config:
             return None
         return prof["dram_bytes_per_row"] * rows
