@@ -18,6 +18,9 @@ BLOCK = 4096
 
 # name: (m, n, rank, spectrum, noise, k, l)
 CONFIGS = {
+    # BASELINE config 1 (the reference's CPU-runnable case, fp64): A = U diag(s) V^T,
+    # U, V orthonormal from Philox draws, s_i = 10^(-4 (i-1) / 999)
+    "cfg1": (2_000, 1_000, 1_000, "log4", 0.0, 20, 30),
     "cfg2": (100_000, 10_000, 200, "inv", 1e-3, 50, 60),
     "cfg3": (1_000_000, 4_096, 300, "exp30", 1e-3, 100, 120),
     "cfg4": (5_000_000, 10_000, 100, "invsqrt", 1e-2, 50, 60),
@@ -76,10 +79,38 @@ def fill_rows(out, r0: int, m: int, n: int, r: int, noise: float, seed: int, w):
     return out
 
 
+def reference_style_matrix(m: int, n: int, seed: int = 100, device=None):
+    """BASELINE config 1 on the GPU in fp64: the reference's synth_matrix
+    construction (synthetic.py:141-164) — U = Q(Philox(seed, 2) m x r),
+    V = Q(Philox(seed, 3) n x r) with diag(R) >= 0, A = U diag(s) V^T,
+    s_i = 10^(-4 (i-1) / (r-1)), r = min(m, n). Same draws as the reference
+    (linalg.gaussian_matrix); the product is formed by one GEMM instead of the
+    reference's row-by-row gemv, so A agrees to rounding, not bitwise (the
+    bit-exact matrix is the oracle's, used by the parity tests)."""
+    torch = torch_mod()
+    from .linalg import STREAM_FACTOR_U, STREAM_FACTOR_V, gaussian_matrix
+    dev = default_device(device)
+    r = min(m, n)
+
+    def orth(x):
+        q, rr = torch.linalg.qr(torch.from_numpy(x).to(dev), mode="reduced")
+        return q * torch.where(torch.diagonal(rr) < 0, -1.0, 1.0).to(q.dtype)
+
+    u = orth(gaussian_matrix(m, r, seed, stream=STREAM_FACTOR_U))
+    v = orth(gaussian_matrix(n, r, seed, stream=STREAM_FACTOR_V))
+    s = 10.0 ** (-4.0 * torch.arange(r, dtype=torch.float64, device=dev) / max(1, r - 1))
+    return (u * s) @ v.T
+
+
 def config_matrix(name: str, device=None, rows=None, seed: int = 2024, m_override=None):
-    """A (or rows [r0, r1) of A) of a BASELINE config, fp32 on the GPU."""
+    """A (or rows [r0, r1) of A) of a BASELINE config on the GPU: fp32 for
+    configs 2-5, fp64 for config 1."""
     torch = torch_mod()
     dev = default_device(device)
+    if name == "cfg1":
+        a = reference_style_matrix(CONFIGS["cfg1"][0] if m_override is None else int(m_override),
+                                   CONFIGS["cfg1"][1], device=dev)
+        return a if rows is None else a[rows[0]:rows[1]].contiguous()
     m, n, r, kind, noise, _, _ = CONFIGS[name]
     if m_override is not None:
         m = int(m_override)
