@@ -497,3 +497,17 @@ def test_tc_row_stride_not_16_bytes(n, tmp_path):
     _, hl, _, _ = sk.finish(on_device=False)
     sk.close()
     assert rel(hl, a.astype(np.float64).T @ left.astype(np.float32).astype(np.float64)) <= 2e-5
+
+
+def test_config1_device_construction_matches_reference(golden):
+    """bench.py's config-1 matrix (the reference's synth_matrix construction
+    from the same Philox draws, built on the device) gives the reference's
+    config-1 singular values (golden.npz, reference run) within the fp64 bar."""
+    from paper_1704_07669_b200 import synth
+    g, _ = golden
+    a = synth.config_matrix("cfg1", device="cuda")
+    assert a.dtype == torch.float64 and tuple(a.shape) == (2000, 1000)
+    res = P.single_pass_pca(P.DeviceRowStream(a), P.PcaConfig(k=20, oversample=10, block_size=10, seed=1),
+                            block_rows=200)
+    s_ref = g["cfg1_s"]
+    assert float(np.max(np.abs(res.s - s_ref) / s_ref)) <= 1e-10
