@@ -260,6 +260,16 @@ int tc_setup(spca_sketch *h) {
   return SPCA_OK;
 }
 
+// Per-device ordering of pass-kernel launches across handles (see the launch).
+struct PassSerial {
+  std::mutex mu;
+  cudaEvent_t last = nullptr;  // recorded behind the device's latest pass kernel
+};
+PassSerial &pass_serial(int device) {
+  static PassSerial table[64];
+  return table[device & 63];
+}
+
 // Remember TMA descriptors over a pushed device buffer so its full chunks
 // are addressed by row offset without re-encoding.
 int tc_register_source(spca_sketch *h, const void *a, int64_t rows, int64_t lda) {
@@ -446,6 +456,17 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
                                   : (h->shift_on ? tc_pass_kernel<128, false, true> : tc_pass_kernel<128, false>));
   const unsigned threads = h->tc_lp == 64 ? TcCfg<64>::THREADS : TcCfg<128>::THREADS;
   const unsigned smem = h->tc_lp == 64 ? TcCfg<64>::SMEM : TcCfg<128>::SMEM;
+  // The pass kernel is persistent and its CTAs wait on one another: two of
+  // them sharing the GPU (handles on different streams) could each hold part
+  // of the SMs and wait forever for the rest. Every launch on a device is
+  // therefore ordered after the previous one, whatever its stream.
+  PassSerial &ps = pass_serial(h->device);
+  std::lock_guard<std::mutex> lk(ps.mu);
+  if (ps.last) {
+    CK(h, cudaStreamWaitEvent(h->stream, ps.last, 0));
+  } else {
+    CK(h, cudaEventCreateWithFlags(&ps.last, cudaEventDisableTiming));
+  }
 #if SPCA_PAIRA
   kern<<<grid, threads, smem, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, *ta_g3, *ta_h2, args);
 #else
@@ -454,6 +475,7 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   kern<<<grid, threads, smem, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, args);
 #endif
   CK_LAUNCH(h);
+  CK(h, cudaEventRecord(ps.last, h->stream));
   }
   h->chunks_since_flush += s.C;
   return SPCA_OK;

@@ -511,3 +511,34 @@ def test_config1_device_construction_matches_reference(golden):
                             block_rows=200)
     s_ref = g["cfg1_s"]
     assert float(np.max(np.abs(res.s - s_ref) / s_ref)) <= 1e-10
+
+
+def test_two_handles_on_two_streams():
+    """Pass kernels of different handles on different streams are ordered on
+    the device (a persistent kernel needs every SM): pushes interleaved on two
+    streams complete and equal the single-handle results."""
+    if not _tc_ok():
+        pytest.skip("no tensor-core path")
+    m, n, l = 60000, 4000, 60
+    a = torch.randn((m, n), device="cuda", dtype=torch.float32, generator=torch.Generator("cuda").manual_seed(5))
+    b = torch.randn((m, n), device="cuda", dtype=torch.float32, generator=torch.Generator("cuda").manual_seed(6))
+    om = O.gaussian(n, l, seed=7)
+    ref_a = P.GpuSketch(n, om, np.float32, precision="tc")
+    ref_a.push(a, 0, final=True)
+    ga, ha, _, _ = ref_a.finish()
+    ref_a.close()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    k1 = P.GpuSketch(n, om, np.float32, precision="tc", stream=s1)
+    k2 = P.GpuSketch(n, om, np.float32, precision="tc", stream=s2)
+    for _ in range(3):  # enqueue both before either completes
+        k1.reset()
+        k2.reset()
+        k1.push(a, 0, final=True)
+        k2.push(b, 0, final=True)
+        g1, h1, _, _ = k1.finish()
+        g2, h2, _, _ = k2.finish()
+        assert torch.equal(h1, ha) and torch.equal(g1, ga)
+        assert torch.isfinite(h2).all()
+    k1.close()
+    k2.close()
