@@ -57,6 +57,14 @@ def gaussian_matrix(rows: int, cols: int, seed: int, stream: int = STREAM_SKETCH
 _DRAW_THREADS = max(1, min(16, os.cpu_count() or 1))
 _DRAW_MIN_PER_THREAD = 1 << 17
 _OVERLAP = 64
+_DRAW_POOL = None  # created on first use, reused by every draw (thread start-up is not free)
+
+
+def _draw_pool():
+    global _DRAW_POOL
+    if _DRAW_POOL is None:
+        _DRAW_POOL = ThreadPoolExecutor(_DRAW_THREADS, thread_name_prefix="spca-omega")
+    return _DRAW_POOL
 
 
 def _parallel_normals(key, n: int, threads: int):
@@ -88,8 +96,8 @@ def _parallel_normals(key, n: int, threads: int):
             bg.advance(starts[t] // 4)
         outs[t] = np.random.Generator(bg).standard_normal(lens[t])
 
-    with ThreadPoolExecutor(threads) as pool:
-        list(pool.map(draw, range(threads)))
+    pool = _draw_pool() if threads <= _DRAW_THREADS else ThreadPoolExecutor(threads)
+    list(pool.map(draw, range(threads)))
     offs = [0]
     for t in range(1, threads):
         prev = outs[t - 1]
@@ -108,8 +116,9 @@ def _parallel_normals(key, n: int, threads: int):
     def place(t):
         out[starts[t]: starts[t] + counts[t]] = outs[t][offs[t]: offs[t] + counts[t]]
 
-    with ThreadPoolExecutor(threads) as pool:
-        list(pool.map(place, range(threads)))
+    list(pool.map(place, range(threads)))
+    if pool is not _DRAW_POOL:
+        pool.shutdown()
     return out
 
 
