@@ -48,7 +48,7 @@ simt_g_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
   constexpr int TM = 4, TL = 4;
   constexpr int NTL = BL / TL;
   constexpr int NTM = BM / TM;
-  static_assert(NTL * NTM == kSimtThreads, "thread tiling");
+  static_assert(sizeof(T) == 8 || NTL * NTM == kSimtThreads, "thread tiling");
   constexpr int VN = Vec<T>::n;
   constexpr int A_PER = BM * BK / kSimtThreads;  // elements per thread
   constexpr int W_PER = BK * BL / kSimtThreads;
@@ -146,15 +146,18 @@ simt_g_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
 #pragma unroll
     for (int j = 0; j < TL; ++j) acc[i][j] = T(0);
   // fp64: warp (wm, wn) owns rows [16 wm, 16 wm + 16) x columns [32 wn, 32 wn + 32)
-  constexpr int WMT = BM / 16;  // 16-row tiles = warps along M
-  static_assert(sizeof(T) == 4 || (WMT * (BL / 32) == kSimtThreads / 32), "DMMA warp tiling");
-  const int lane = tid & 31, wid = tid >> 5, wm = wid % WMT, wn = wid / WMT;
+  // fp64: warps WM (rows) x WN (32-column slices); each warp MPW 16-row tiles x four 8-column tiles
+  constexpr int WN = BL / 32 > 0 ? BL / 32 : 1, WM = (kSimtThreads / 32) / WN, MPW = BM / 16 / WM;
+  static_assert(sizeof(T) == 4 || (MPW >= 1 && MPW * WM * 16 == BM && WN * 32 == BL), "DMMA warp tiling");
+  const int lane = tid & 31, wid = tid >> 5, wm = wid % WM, wn = wid / WM;
   const int fg = lane >> 2, ft = lane & 3;
-  double dacc[4][4];
+  double dacc[MPW][4][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int mi = 0; mi < MPW; ++mi)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) dacc[i][j] = 0.0;
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dacc[mi][i][j] = 0.0;
 
   const int ntiles = (ke > kb) ? (ke - kb + BK - 1) / BK : 0;
   if (ntiles > 0) {
@@ -181,9 +184,18 @@ simt_g_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
     } else {  // fp64: DMMA, four k-steps of 4 per tile
 #pragma unroll
       for (int ks = 0; ks < BK; ks += 4) {
-        const double a0 = As[buf][ks + ft][wm * 16 + fg], a1 = As[buf][ks + ft][wm * 16 + fg + 8];
+        double a0[MPW], a1[MPW];
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(dacc[nt], a0, a1, Ws[buf][ks + ft][wn * 32 + nt * 8 + fg]);
+        for (int mi = 0; mi < MPW; ++mi) {
+          a0[mi] = As[buf][ks + ft][(wm * MPW + mi) * 16 + fg];
+          a1[mi] = As[buf][ks + ft][(wm * MPW + mi) * 16 + fg + 8];
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const double bw = Ws[buf][ks + ft][wn * 32 + nt * 8 + fg];
+#pragma unroll
+          for (int mi = 0; mi < MPW; ++mi) dmma_16x8x4(dacc[mi][nt], a0[mi], a1[mi], bw);
+        }
       }
     }
     if (t + 1 < ntiles) {
@@ -201,14 +213,16 @@ simt_g_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
   T *o = out + (int64_t)blockIdx.z * out_split_stride;
   if constexpr (sizeof(T) == 8) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = m0 + wm * 16 + fg + 8 * h;
-      if (r >= rows) continue;
+    for (int mi = 0; mi < MPW; ++mi)
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-        *reinterpret_cast<double2 *>(o + (int64_t)r * ldo + j0 + wn * 32 + nt * 8 + 2 * ft) =
-            make_double2(dacc[nt][2 * h], dacc[nt][2 * h + 1]);
-    }
+      for (int h = 0; h < 2; ++h) {
+        const int r = m0 + (wm * MPW + mi) * 16 + fg + 8 * h;
+        if (r >= rows) continue;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          *reinterpret_cast<double2 *>(o + (int64_t)r * ldo + j0 + wn * 32 + nt * 8 + 2 * ft) =
+              make_double2(dacc[mi][nt][2 * h], dacc[mi][nt][2 * h + 1]);
+      }
     return;
   }
 #pragma unroll
@@ -251,7 +265,7 @@ simt_h_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
   constexpr int TN = 4, TL = 4;
   constexpr int NTL = BL / TL;
   constexpr int NTN = BN / TN;
-  static_assert(NTL * NTN == kSimtThreads, "thread tiling");
+  static_assert(sizeof(T) == 8 || NTL * NTN == kSimtThreads, "thread tiling");
   constexpr int VN = Vec<T>::n;
   constexpr int A_PER = BK * BN / kSimtThreads;
   constexpr int G_PER = BK * BL / kSimtThreads;
@@ -346,15 +360,18 @@ simt_h_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
     for (int j = 0; j < TL; ++j) acc[i][j] = T(0);
   double cs[TN] = {0.0, 0.0, 0.0, 0.0};
   double cc[TN] = {0.0, 0.0, 0.0, 0.0};  // Kahan carries (compensated mode)
-  constexpr int WMT = BN / 16;  // fp64: warp (wm, wn) owns columns [16 wm, +16) x [32 wn, +32)
-  static_assert(sizeof(T) == 4 || (WMT * (BL / 32) == kSimtThreads / 32), "DMMA warp tiling");
-  const int lane = tid & 31, wid = tid >> 5, wm = wid % WMT, wn = wid / WMT;
+  // fp64: warps WM (columns) x WN (32-wide l slices); each warp MPW 16-column tiles x four 8-wide tiles
+  constexpr int WN = BL / 32 > 0 ? BL / 32 : 1, WM = (kSimtThreads / 32) / WN, MPW = BN / 16 / WM;
+  static_assert(sizeof(T) == 4 || (MPW >= 1 && MPW * WM * 16 == BN && WN * 32 == BL), "DMMA warp tiling");
+  const int lane = tid & 31, wid = tid >> 5, wm = wid % WM, wn = wid / WM;
   const int fg = lane >> 2, ft = lane & 3;
-  double dacc[4][4];
+  double dacc[MPW][4][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int mi = 0; mi < MPW; ++mi)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) dacc[i][j] = 0.0;
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dacc[mi][i][j] = 0.0;
 
   const int ntiles = (re > rb) ? (re - rb + BK - 1) / BK : 0;
   if (ntiles > 0) {
@@ -368,9 +385,18 @@ simt_h_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
     if constexpr (sizeof(T) == 8) {  // fp64: DMMA (A^T: m = column, k = row) + column sums
 #pragma unroll
       for (int ks = 0; ks < BK; ks += 4) {
-        const double a0 = As[buf][ks + ft][wm * 16 + fg], a1 = As[buf][ks + ft][wm * 16 + fg + 8];
+        double a0[MPW], a1[MPW];
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(dacc[nt], a0, a1, Gs[buf][ks + ft][wn * 32 + nt * 8 + fg]);
+        for (int mi = 0; mi < MPW; ++mi) {
+          a0[mi] = As[buf][ks + ft][(wm * MPW + mi) * 16 + fg];
+          a1[mi] = As[buf][ks + ft][(wm * MPW + mi) * 16 + fg + 8];
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const double bg = Gs[buf][ks + ft][wn * 32 + nt * 8 + fg];
+#pragma unroll
+          for (int mi = 0; mi < MPW; ++mi) dmma_16x8x4(dacc[mi][nt], a0[mi], a1[mi], bg);
+        }
       }
       if (do_cs) {
 #pragma unroll
@@ -422,13 +448,15 @@ simt_h_kernel(const T *__restrict__ A, int64_t lda, int rows, int n,
   T *hp = Hpart + (int64_t)blockIdx.z * h_split_stride;
   if constexpr (sizeof(T) == 8) {
 #pragma unroll
+    for (int mi = 0; mi < MPW; ++mi)
+#pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int c = n0 + wm * 16 + fg + 8 * h;
+      const int c = n0 + (wm * MPW + mi) * 16 + fg + 8 * h;
       if (c >= n) continue;
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
         double2 *dst = reinterpret_cast<double2 *>(hp + (int64_t)c * ldh + j0 + wn * 32 + nt * 8 + 2 * ft);
-        double2 v = make_double2(dacc[nt][2 * h], dacc[nt][2 * h + 1]);
+        double2 v = make_double2(dacc[mi][nt][2 * h], dacc[mi][nt][2 * h + 1]);
         if (accumulate) {
           const double2 old = *dst;
           v.x += old.x;

@@ -138,6 +138,10 @@ int ensure_g(spca_sketch *h, int64_t rows_needed) {
 #include "sketch_fused.cuh"
 #include "tc_host.cuh"
 
+#ifndef SPCA_SIMT_F64_TILE
+#define SPCA_SIMT_F64_TILE 64  // 128 (two DMMA row tiles per warp, 8-deep K) measured 14.0 vs 12.3 ms
+#endif
+
 namespace {
 
 // ---- SIMT chunk processing ------------------------------------------------
@@ -155,7 +159,8 @@ template <typename T, int BM, int BL, bool VEC>
 void launch_g(spca_sketch *h, const T *a, int64_t lda, int rows, T *out, int64_t out_stride,
               int ksplit, int kseg) {
   dim3 grid((unsigned)ceil_div(rows, BM), (unsigned)(h->lpad / BL), (unsigned)ksplit);
-  simt_g_kernel<T, BM, BL, (sizeof(T) == 4 ? 32 : 16), VEC><<<grid, kSimtThreads, 0, h->stream>>>(
+  // fp64 with 128-row tiles: 8-deep K steps keep the double-buffered tiles under 48 KB
+  simt_g_kernel<T, BM, BL, (sizeof(T) == 4 ? 32 : (BM > 64 && BL > 32 ? 8 : 16)), VEC><<<grid, kSimtThreads, 0, h->stream>>>(
       a, lda, rows, (int)h->n, (const T *)h->omega_dev, (int)h->lpad, out, (int)h->lpad,
       out_stride, kseg, h->rows_done, h->bad_dev);
 }
@@ -163,10 +168,15 @@ void launch_g(spca_sketch *h, const T *a, int64_t lda, int rows, T *out, int64_t
 template <typename T, int BN, int BL, bool VEC>
 void launch_h(spca_sketch *h, const T *a, int64_t lda, int rows, const T *g, int rseg, int accumulate) {
   dim3 grid((unsigned)ceil_div(h->n, BN), (unsigned)(h->lpad / BL), (unsigned)h->hsplit);
-  simt_h_kernel<T, BN, BL, (sizeof(T) == 4 ? 32 : 16), VEC><<<grid, kSimtThreads, 0, h->stream>>>(
+  simt_h_kernel<T, BN, BL, (sizeof(T) == 4 ? 32 : (BN > 64 && BL > 32 ? 8 : 16)), VEC><<<grid, kSimtThreads, 0, h->stream>>>(
       a, lda, rows, (int)h->n, g, (int)h->lpad, (T *)h->hpart, (int)h->lpad,
       (int64_t)h->n * h->lpad, h->cspart, rseg, accumulate, h->compensated ? 1 : 0);
 }
+
+// tile rows (G) / columns (H) of the 64-wide l tiles: 64 for FFMA, 128 for
+// fp64 (two 16-row DMMA tiles per warp: each B fragment feeds two MMAs)
+template <typename T>
+constexpr int kGM = sizeof(T) == 8 ? SPCA_SIMT_F64_TILE : 64;
 
 template <typename T>
 int simt_chunk(spca_sketch *h, const T *a, int64_t lda, int rows) {
@@ -174,7 +184,7 @@ int simt_chunk(spca_sketch *h, const T *a, int64_t lda, int rows) {
   const bool vec = (lda % VN == 0) && (h->n % VN == 0) &&
                    ((reinterpret_cast<uintptr_t>(a) % 16) == 0);
   const bool narrow = (h->bl == 32);
-  const int bm = narrow ? 128 : 64;
+  const int bm = narrow ? 128 : kGM<T>;
   // split-K so that the G kernel fills the machine (~4 CTAs per SM)
   int64_t tiles = ceil_div(rows, bm) * (h->lpad / h->bl);
   int64_t kmax = std::max<int64_t>(1, ceil_div(h->n, 128));
@@ -199,8 +209,8 @@ int simt_chunk(spca_sketch *h, const T *a, int64_t lda, int rows) {
     if (vec) launch_g<T, 128, 32, true>(h, a, lda, rows, p1_out, p1_stride, ksplit, kseg);
     else launch_g<T, 128, 32, false>(h, a, lda, rows, p1_out, p1_stride, ksplit, kseg);
   } else {
-    if (vec) launch_g<T, 64, 64, true>(h, a, lda, rows, p1_out, p1_stride, ksplit, kseg);
-    else launch_g<T, 64, 64, false>(h, a, lda, rows, p1_out, p1_stride, ksplit, kseg);
+    if (vec) launch_g<T, kGM<T>, 64, true>(h, a, lda, rows, p1_out, p1_stride, ksplit, kseg);
+    else launch_g<T, kGM<T>, 64, false>(h, a, lda, rows, p1_out, p1_stride, ksplit, kseg);
   }
   CK_LAUNCH(h);
   if (ksplit > 1) {
@@ -217,8 +227,8 @@ int simt_chunk(spca_sketch *h, const T *a, int64_t lda, int rows) {
     if (vec) launch_h<T, 128, 32, true>(h, a, lda, rows, hop, rseg, acc);
     else launch_h<T, 128, 32, false>(h, a, lda, rows, hop, rseg, acc);
   } else {
-    if (vec) launch_h<T, 64, 64, true>(h, a, lda, rows, hop, rseg, acc);
-    else launch_h<T, 64, 64, false>(h, a, lda, rows, hop, rseg, acc);
+    if (vec) launch_h<T, kGM<T>, 64, true>(h, a, lda, rows, hop, rseg, acc);
+    else launch_h<T, kGM<T>, 64, false>(h, a, lda, rows, hop, rseg, acc);
   }
   CK_LAUNCH(h);
   return SPCA_OK;
