@@ -17,6 +17,7 @@
 #include <cstring>
 #include <mutex>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "../../include/spca.h"
@@ -422,6 +423,36 @@ int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, b
   return SPCA_OK;
 }
 
+// Pageable rows into the page-locked staging buffer on several host threads:
+// one thread's memcpy (~14 GB/s) would cap a numpy input far below the
+// host link (~55 GB/s); pieces of >= 32 MB per thread.
+const unsigned kCopyThreads = (unsigned)env_int("SPCA_COPY_THREADS", 16);
+
+void host_rows_copy(char *dst, size_t dpitch, const char *src, size_t spitch, size_t row_bytes, int64_t rows) {
+  auto copy = [=](int64_t r0, int64_t r1) {
+    if (dpitch == spitch && dpitch == row_bytes) {
+      memcpy(dst + r0 * dpitch, src + r0 * spitch, (size_t)(r1 - r0) * row_bytes);
+    } else {
+      for (int64_t r = r0; r < r1; ++r) memcpy(dst + r * dpitch, src + r * spitch, row_bytes);
+    }
+  };
+  const int64_t bytes = rows * (int64_t)row_bytes;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = (int)std::min<int64_t>(std::min<unsigned>(hw, kCopyThreads), std::max<int64_t>(1, bytes >> 25));
+  if (nt <= 1) {
+    copy(0, rows);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const int64_t per = (rows + nt - 1) / nt;
+  for (int t = 1; t < nt; ++t) {
+    const int64_t r0 = t * per, r1 = std::min(rows, r0 + per);
+    if (r0 < r1) pool.emplace_back(copy, r0, r1);
+  }
+  copy(0, std::min(rows, per));
+  for (auto &th : pool) th.join();
+}
+
 int ensure_staging(spca_sketch *h, bool need_pinned) {
   const size_t bytes = (size_t)h->stage_rows * h->ldp * h->ds;
   for (int i = 0; i < 2; ++i) {
@@ -459,12 +490,7 @@ int push_host_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, boo
     if (pageable) {
       if (h->stage_used[i]) CK(h, cudaEventSynchronize(h->copy_done[i]));
       char *dst = (char *)h->pinned[i];
-      if ((size_t)lda * h->ds == pitch) {
-        memcpy(dst, src, (size_t)take * pitch);
-      } else {
-        for (int64_t r = 0; r < take; ++r)
-          memcpy(dst + r * pitch, src + (size_t)r * lda * h->ds, row_bytes);
-      }
+      host_rows_copy(dst, pitch, src, (size_t)lda * h->ds, row_bytes, take);
       src = dst;
       CK(h, cudaMemcpyAsync(h->dstage[i], src, (size_t)take * pitch, cudaMemcpyHostToDevice,
                             h->copy_stream));
