@@ -197,13 +197,17 @@ class FileRowStream(RowStream):
     files are sketched in fp32, like every other float32 source), with no
     widening and no host-side copy (sketch.py ``_push_file``)."""
 
-    def __init__(self, path, rows=None, cols=None, dtype=None, layout=None, read_threads: int = 8,
+    def __init__(self, path, rows=None, cols=None, dtype=None, layout=None, read_threads: Optional[int] = None,
                  buffer_bytes: int = 64 << 20):
         self._path = str(path)
         self.buffer_bytes = max(1, int(buffer_bytes))  # page-locked buffer size of the device pass
         self._layout = layout if layout is not None else matfile.sniff_layout(self._path, rows, cols, dtype)
         self.read_seconds = 0.0
         self.bytes_read = 0
+        # parallel positional reads from the page cache: 16 threads 35.9 GB/s,
+        # 8 31.1, 4 23.7 at config 2 (tools/file_bench.py, 16-core host)
+        if read_threads is None:
+            read_threads = min(16, os.cpu_count() or 1)
         self.read_threads = max(1, int(read_threads))
 
     @property

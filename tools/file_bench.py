@@ -29,7 +29,7 @@ P.matfile.write_matrix(path, host, dtype="float32")
 write_s = time.perf_counter() - t0
 try:
     res = {}
-    for threads in (1, 4, 8):
+    for threads in (1, 4, 8, 12, 16):
         times, read_s = [], []
         for rep in range(3):
             fs = P.FileRowStream(path, read_threads=threads)
