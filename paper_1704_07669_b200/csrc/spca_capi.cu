@@ -437,6 +437,13 @@ void host_rows_copy(char *dst, size_t dpitch, const char *src, size_t spitch, si
     }
   };
   const int64_t bytes = rows * (int64_t)row_bytes;
+  if (rows == 1 && row_bytes >= (8u << 20)) {  // one long run: split it into byte ranges
+    constexpr int64_t kSeg = 4 << 20;
+    host_rows_copy(dst, (size_t)kSeg, src, (size_t)kSeg, (size_t)kSeg, bytes / kSeg);
+    const int64_t done = (bytes / kSeg) * kSeg;
+    if (done < bytes) memcpy(dst + done, src + done, (size_t)(bytes - done));
+    return;
+  }
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
   const int nt = (int)std::min<int64_t>(std::min<unsigned>(hw, kCopyThreads), std::max<int64_t>(1, bytes >> 25));
   if (nt <= 1) {
@@ -451,6 +458,44 @@ void host_rows_copy(char *dst, size_t dpitch, const char *src, size_t spitch, si
   }
   copy(0, std::min(rows, per));
   for (auto &th : pool) th.join();
+}
+
+// Large pageable uploads (Omega, the co-sketch operand): through two
+// page-locked 32 MB bounce buffers, filled by host_rows_copy's threads while
+// the previous one is in flight (a pageable cudaMemcpy runs at ~10-14 GB/s).
+// The buffers are allocated once per process. Synchronous on return.
+cudaError_t upload_pageable(void *dst, const void *src, size_t bytes, cudaStream_t st) {
+  constexpr size_t kBounce = 32u << 20;
+  static std::mutex mu;
+  static void *bounce[2] = {nullptr, nullptr};
+  static cudaEvent_t done[2] = {nullptr, nullptr};
+  if (bytes < 2 * kBounce) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+  std::lock_guard<std::mutex> lk(mu);
+  for (int i = 0; i < 2; ++i) {
+    if (!bounce[i]) {
+      cudaError_t e = cudaHostAlloc(&bounce[i], kBounce, cudaHostAllocDefault);
+      if (e != cudaSuccess) return e;
+    }
+    if (!done[i]) {
+      cudaError_t e = cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  size_t off = 0;
+  for (int k = 0; off < bytes; ++k) {
+    const int i = k & 1;
+    const size_t n = std::min(kBounce, bytes - off);
+    if (k >= 2) {
+      cudaError_t e = cudaEventSynchronize(done[i]);  // the buffer's previous copy has landed
+      if (e != cudaSuccess) return e;
+    }
+    host_rows_copy((char *)bounce[i], n, (const char *)src + off, n, n, 1);
+    cudaError_t e = cudaMemcpyAsync((char *)dst + off, bounce[i], n, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaEventRecord(done[i], st);
+    if (e != cudaSuccess) return e;
+    off += n;
+  }
+  return cudaStreamSynchronize(st);
 }
 
 int ensure_staging(spca_sketch *h, bool need_pinned) {
@@ -655,7 +700,9 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
       om_src = const_cast<double *>(omega);
     } else {
       TRY(dalloc(h, &om_src, (size_t)n * l * 8));
-      TRY(cudaMemcpyAsync(om_src, omega, (size_t)n * l * 8, cudaMemcpyHostToDevice, h->stream));
+      TRY(omega_where == SPCA_MEM_PAGEABLE ? upload_pageable(om_src, omega, (size_t)n * l * 8, h->stream)
+                                           : cudaMemcpyAsync(om_src, omega, (size_t)n * l * 8,
+                                                             cudaMemcpyHostToDevice, h->stream));
     }
     if (dtype == SPCA_F32)
       omega_prepare<float><<<grid_for(n * h->lpad), 256, 0, h->stream>>>(
@@ -814,7 +861,9 @@ int spca_sketch_set_left(spca_handle_t h, const double *left, int64_t rows, int 
   double *tmp = nullptr;
   if (where != SPCA_MEM_DEVICE) {
     CK(h, dalloc(h, &tmp, (size_t)rows * h->l * 8));
-    CK(h, cudaMemcpyAsync(tmp, left, (size_t)rows * h->l * 8, cudaMemcpyHostToDevice, h->stream));
+    CK(h, where == SPCA_MEM_PAGEABLE ? upload_pageable(tmp, left, (size_t)rows * h->l * 8, h->stream)
+                                     : cudaMemcpyAsync(tmp, left, (size_t)rows * h->l * 8, cudaMemcpyHostToDevice,
+                                                       h->stream));
     src = tmp;
   }
   // same conversion as Omega: compute-precision copy (rows x lpad) + the fp64 values used
