@@ -452,10 +452,18 @@ void host_rows_copy(char *dst, size_t dpitch, const char *src, size_t spitch, si
   }
   std::vector<std::thread> pool;
   const int64_t per = (rows + nt - 1) / nt;
+  int64_t mine_end = std::min(rows, per);  // this thread's share (grows if a spawn fails)
   for (int t = 1; t < nt; ++t) {
     const int64_t r0 = t * per, r1 = std::min(rows, r0 + per);
-    if (r0 < r1) pool.emplace_back(copy, r0, r1);
+    if (r0 >= r1) break;
+    try {
+      pool.emplace_back(copy, r0, r1);
+    } catch (...) {  // no more threads: this thread copies the rest itself
+      mine_end = -r0;
+      break;
+    }
   }
+  if (mine_end < 0) copy(-mine_end, rows);  // the part no thread took
   copy(0, std::min(rows, per));
   for (auto &th : pool) th.join();
 }
