@@ -86,6 +86,7 @@ struct spca_sketch {
   int chunks_since_flush = 0;
   int flush_every = 64;
   int tc_debug = 0;              // SPCA_TC_DEBUG bitmask (profiling experiments only)
+  int tc_coop = 1;               // cooperative pass launches (SPCA_TC_COOP=0: plain launch, A/B only)
   unsigned long long *trace = nullptr;  // SPCA_TC_TRACE per-CTA timeline
   bool finished = false;
   bool final_pushed = false;     // spca_sketch_push_final was called (no more rows)

@@ -428,7 +428,8 @@ int push_device_rows(spca_sketch *h, const char *a, int64_t rows, int64_t lda, b
 // host link (~55 GB/s); pieces of >= 32 MB per thread.
 const unsigned kCopyThreads = (unsigned)env_int("SPCA_COPY_THREADS", 16);
 
-void host_rows_copy(char *dst, size_t dpitch, const char *src, size_t spitch, size_t row_bytes, int64_t rows) {
+void host_rows_copy(char *dst, size_t dpitch, const char *src, size_t spitch, size_t row_bytes, int64_t rows,
+                    int min_shift = 25) {
   auto copy = [=](int64_t r0, int64_t r1) {
     if (dpitch == spitch && dpitch == row_bytes) {
       memcpy(dst + r0 * dpitch, src + r0 * spitch, (size_t)(r1 - r0) * row_bytes);
@@ -439,13 +440,13 @@ void host_rows_copy(char *dst, size_t dpitch, const char *src, size_t spitch, si
   const int64_t bytes = rows * (int64_t)row_bytes;
   if (rows == 1 && row_bytes >= (8u << 20)) {  // one long run: split it into byte ranges
     constexpr int64_t kSeg = 4 << 20;
-    host_rows_copy(dst, (size_t)kSeg, src, (size_t)kSeg, (size_t)kSeg, bytes / kSeg);
+    host_rows_copy(dst, (size_t)kSeg, src, (size_t)kSeg, (size_t)kSeg, bytes / kSeg, min_shift);
     const int64_t done = (bytes / kSeg) * kSeg;
     if (done < bytes) memcpy(dst + done, src + done, (size_t)(bytes - done));
     return;
   }
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const int nt = (int)std::min<int64_t>(std::min<unsigned>(hw, kCopyThreads), std::max<int64_t>(1, bytes >> 25));
+  const int nt = (int)std::min<int64_t>(std::min<unsigned>(hw, kCopyThreads), std::max<int64_t>(1, bytes >> min_shift));
   if (nt <= 1) {
     copy(0, rows);
     return;
@@ -469,41 +470,47 @@ void host_rows_copy(char *dst, size_t dpitch, const char *src, size_t spitch, si
 }
 
 // Large pageable uploads (Omega, the co-sketch operand): through two
-// page-locked 32 MB bounce buffers, filled by host_rows_copy's threads while
-// the previous one is in flight (a pageable cudaMemcpy runs at ~10-14 GB/s).
-// The buffers are allocated once per process. Synchronous on return.
+// page-locked 32 MB bounce buffers, each filled by host_rows_copy on up to
+// 8 threads (4 MB per thread) while the previous one is in flight (a pageable
+// cudaMemcpy runs at ~10-14 GB/s). The buffers are allocated once per process
+// (portable: any device may use them, one upload at a time under the mutex);
+// the completion events belong to the call and to the current device.
+// Synchronous on return, also on every error path (no copy out of a bounce
+// buffer is left in flight for the next caller to overwrite).
 cudaError_t upload_pageable(void *dst, const void *src, size_t bytes, cudaStream_t st) {
   constexpr size_t kBounce = 32u << 20;
   static std::mutex mu;
   static void *bounce[2] = {nullptr, nullptr};
-  static cudaEvent_t done[2] = {nullptr, nullptr};
   if (bytes < 2 * kBounce) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
   std::lock_guard<std::mutex> lk(mu);
   for (int i = 0; i < 2; ++i) {
     if (!bounce[i]) {
-      cudaError_t e = cudaHostAlloc(&bounce[i], kBounce, cudaHostAllocDefault);
-      if (e != cudaSuccess) return e;
-    }
-    if (!done[i]) {
-      cudaError_t e = cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+      cudaError_t e = cudaHostAlloc(&bounce[i], kBounce, cudaHostAllocPortable);
       if (e != cudaSuccess) return e;
     }
   }
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  bool recorded[2] = {false, false};
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
   size_t off = 0;
-  for (int k = 0; off < bytes; ++k) {
+  for (int k = 0; e == cudaSuccess && off < bytes; ++k) {
     const int i = k & 1;
     const size_t n = std::min(kBounce, bytes - off);
-    if (k >= 2) {
-      cudaError_t e = cudaEventSynchronize(done[i]);  // the buffer's previous copy has landed
-      if (e != cudaSuccess) return e;
+    if (recorded[i]) {
+      e = cudaEventSynchronize(done[i]);  // the buffer's previous copy has landed
+      if (e != cudaSuccess) break;
     }
-    host_rows_copy((char *)bounce[i], n, (const char *)src + off, n, n, 1);
-    cudaError_t e = cudaMemcpyAsync((char *)dst + off, bounce[i], n, cudaMemcpyHostToDevice, st);
+    host_rows_copy((char *)bounce[i], n, (const char *)src + off, n, n, 1, 22);
+    e = cudaMemcpyAsync((char *)dst + off, bounce[i], n, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaEventRecord(done[i], st);
-    if (e != cudaSuccess) return e;
+    if (e == cudaSuccess) recorded[i] = true;
     off += n;
   }
-  return cudaStreamSynchronize(st);
+  cudaError_t es = cudaStreamSynchronize(st);  // nothing left in flight, success or not
+  for (int i = 0; i < 2; ++i)
+    if (done[i]) cudaEventDestroy(done[i]);
+  return e != cudaSuccess ? e : es;
 }
 
 int ensure_staging(spca_sketch *h, bool need_pinned) {
@@ -670,6 +677,7 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
   // flush the fp32 H partials into fp64 every ~1M rows
   h->flush_every = (int)std::max<int64_t>(1, (1 << 20) / h->chunk_rows);
   if (const char *d = getenv("SPCA_TC_DEBUG")) h->tc_debug = atoi(d);
+  if (const char *d = getenv("SPCA_TC_COOP")) h->tc_coop = atoi(d);
 
   const size_t ds = h->ds;
   int rc;
@@ -708,9 +716,13 @@ int spca_sketch_create(spca_handle_t *out, int64_t n, int64_t l, int dtype, int 
       om_src = const_cast<double *>(omega);
     } else {
       TRY(dalloc(h, &om_src, (size_t)n * l * 8));
-      TRY(omega_where == SPCA_MEM_PAGEABLE ? upload_pageable(om_src, omega, (size_t)n * l * 8, h->stream)
-                                           : cudaMemcpyAsync(om_src, omega, (size_t)n * l * 8,
-                                                             cudaMemcpyHostToDevice, h->stream));
+      cudaError_t ue = omega_where == SPCA_MEM_PAGEABLE
+                           ? upload_pageable(om_src, omega, (size_t)n * l * 8, h->stream)
+                           : cudaMemcpyAsync(om_src, omega, (size_t)n * l * 8, cudaMemcpyHostToDevice, h->stream);
+      if (ue != cudaSuccess) {
+        dfree(h, om_src);  // not yet owned by the handle: fail() would not release it
+        TRY(ue);
+      }
     }
     if (dtype == SPCA_F32)
       omega_prepare<float><<<grid_for(n * h->lpad), 256, 0, h->stream>>>(
@@ -869,9 +881,14 @@ int spca_sketch_set_left(spca_handle_t h, const double *left, int64_t rows, int 
   double *tmp = nullptr;
   if (where != SPCA_MEM_DEVICE) {
     CK(h, dalloc(h, &tmp, (size_t)rows * h->l * 8));
-    CK(h, where == SPCA_MEM_PAGEABLE ? upload_pageable(tmp, left, (size_t)rows * h->l * 8, h->stream)
-                                     : cudaMemcpyAsync(tmp, left, (size_t)rows * h->l * 8, cudaMemcpyHostToDevice,
-                                                       h->stream));
+    cudaError_t ue = where == SPCA_MEM_PAGEABLE
+                         ? upload_pageable(tmp, left, (size_t)rows * h->l * 8, h->stream)
+                         : cudaMemcpyAsync(tmp, left, (size_t)rows * h->l * 8, cudaMemcpyHostToDevice, h->stream);
+    if (ue != cudaSuccess) {
+      cudaStreamSynchronize(h->stream);
+      dfree(h, tmp);
+      CK(h, ue);
+    }
     src = tmp;
   }
   // same conversion as Omega: compute-precision copy (rows x lpad) + the fp64 values used

@@ -13,17 +13,17 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+// Resolved once per process (thread-safe function-local static): two threads
+// creating handles at once must both see the entry point.
 EncodeTiledFn tma_encoder() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static const EncodeTiledFn fn = []() -> EncodeTiledFn {
     void *p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = (EncodeTiledFn)p;
-  }
+      return (EncodeTiledFn)p;
+    return nullptr;
+  }();
   return fn;
 }
 
@@ -151,15 +151,14 @@ int encode_a_maps(spca_sketch *h, const void *a, uint64_t rows, uint64_t row_byt
   return SPCA_OK;
 }
 
+// The attribute takes effect on the current device only: set it on every
+// handle's setup (cheap, once per handle), never cached process-wide.
 template <int LPAD>
 int tc_set_smem_attrs() {
-  static bool done = false;
-  if (done) return 0;
   for (auto k : {tc_pass_kernel<LPAD, false>, tc_pass_kernel<LPAD, true>, tc_pass_kernel<LPAD, false, true>})
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcCfg<LPAD>::SMEM) !=
         cudaSuccess)
       return 1;
-  done = true;
   return 0;
 }
 
@@ -472,7 +471,29 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
 #else
   (void)ta_g3;
   (void)ta_h2;
-  kern<<<grid, threads, smem, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, args);
+  {
+    // Cooperative launch: the driver co-schedules the whole grid (every CTA
+    // resident at once, whatever else runs on the device), which the
+    // persistent pass's inter-CTA waits rely on; a grid that cannot be
+    // co-resident fails here (cudaErrorCooperativeLaunchTooLarge) instead of
+    // hanging. The kernel's cluster shape (2, 1, 1) is compiled in.
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)grid, 1, 1);
+    lc.blockDim = dim3(threads, 1, 1);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = h->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = h->tc_coop ? 1 : 0;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaError_t le = cudaLaunchKernelEx(&lc, kern, *ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, args);
+    if (le != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(h, SPCA_ERR_CUDA, -1, "pass kernel launch (grid %d, cooperative %d) failed: %s", grid,
+                     h->tc_coop ? 1 : 0, cudaGetErrorString(le));
+    }
+  }
 #endif
   CK_LAUNCH(h);
   CK(h, cudaEventRecord(ps.last, h->stream));

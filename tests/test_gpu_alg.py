@@ -542,3 +542,36 @@ def test_two_handles_on_two_streams():
         assert torch.isfinite(h2).all()
     k1.close()
     k2.close()
+
+
+@pytest.mark.gpu
+def test_pass_beside_foreign_kernels():
+    """The persistent pass kernel is launched cooperatively (every CTA
+    co-scheduled): with foreign work holding SMs on other streams — a
+    long-running spin kernel and a stream of torch GEMMs — the pass still
+    completes and equals the undisturbed result bit for bit."""
+    if not _tc_ok():
+        pytest.skip("no tensor-core path")
+    m, n, l = 40000, 3000, 60
+    a = torch.randn((m, n), device="cuda", dtype=torch.float32, generator=torch.Generator("cuda").manual_seed(8))
+    om = O.gaussian(n, l, seed=9)
+    ref = P.GpuSketch(n, om, np.float32, precision="tc")
+    ref.push(a, 0, final=True)
+    g0, h0, c0, _ = ref.finish()
+    ref.close()
+    s_spin, s_gemm, s_pass = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    x = torch.randn((2048, 2048), device="cuda")
+    torch.cuda.synchronize()
+    k = P.GpuSketch(n, om, np.float32, precision="tc", stream=s_pass)
+    for _ in range(2):
+        with torch.cuda.stream(s_spin):
+            torch.cuda._sleep(50_000_000)  # ~25 ms on one SM
+        with torch.cuda.stream(s_gemm):
+            for _ in range(20):
+                x = (x @ x).clamp_(-1, 1)
+        k.reset()
+        k.push(a, 0, final=True)
+        g1, h1, c1, _ = k.finish()
+        assert torch.equal(h1, h0) and torch.equal(g1, g0) and torch.equal(c1, c0)
+    torch.cuda.synchronize()
+    k.close()
