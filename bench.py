@@ -1,18 +1,25 @@
-"""Benchmark of the sketch pass (BASELINE.json metric: sketch-pass GB/s of A).
+"""Benchmark of the sketch pass (BASELINE.json metric: sketch-pass GB/s of A,
+% of roofline, end-to-end PCA seconds).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg2] [--precision auto|simt|tc]
+                    [--config cfg2] [--scaling auto|weak|strong] [--precision auto|simt|tc]
 
 A step = one full sketch pass (Algorithm 4 steps 4-8) over the config's A,
 resident in HBM: every row pushed through libspca, H flushed, G widened, the
-state finished on the device; with N > 1 ranks each rank owns its own row
-shard (weak scaling: the per-GPU shard is the config's full m) and the step
-ends with the NCCL all-reduce of [H | col_sums | rows].
+state finished on the device; with N > 1 ranks each rank owns a contiguous
+row shard and the step ends with the NCCL all-reduce of [H | col_sums | rows].
+Scaling: config 2 (a one-GPU config) is weak — every rank a full 100 000-row
+matrix; configs 3 and 5 (fixed matrices, BASELINE.json) are strong — the
+config's m rows split over the ranks.  ``--gpus N`` without WORLD_SIZE in the
+environment re-launches itself under torch.distributed.run with N ranks.
 
 The JSON line (rank 0) carries: value (whole-job GB/s of A), e2e (same
 metric through the public API with A in pinned host memory, H2D and the D2H
-of the sketch inside the timed region), roofline (dominant kernel group),
-cpu_baseline (the numpy oracle port on this host's cores, bounded sample),
+of the sketch inside the timed region; e2e_pageable the same from a plain
+numpy array), roofline (the pass kernel, CUDA events on its stream),
+pca_seconds (A in HBM) and pca_seconds_host (numpy input), parity (our U, S, V
+against the unmodified reference's single_pass_pca on the same A and Omega,
+N = 1), cpu_baseline (the reference timed on this host's cores on the full A),
 clocks sampled during the timed region, gpu_launches.
 """
 
@@ -21,6 +28,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -33,6 +41,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "sketch-pass GB/s of A"
 UNIT = "GB/s"
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
 def parse():
@@ -42,15 +51,58 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="cfg2")
+    p.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"],
+                   help="auto: weak for cfg1/cfg2 (one-GPU configs), strong for cfg3/cfg5")
     p.add_argument("--precision", default="auto")
     p.add_argument("--rows", type=int, default=None, help="override m (debug)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-pca", action="store_true")
+    p.add_argument("--no-parity", action="store_true")
+    p.add_argument("--ref-budget-s", type=float, default=240.0,
+                   help="--impl reference: bound on the whole timed run (rows sampled above it)")
     p.add_argument("--ring-gb", type=float, default=16.0, help="cfg4: pinned host ring size")
     p.add_argument("--dtype", default="f32", choices=["f32", "f64"],
                    help="element type of A (f64: the config's values widened, DFMA path)")
     return p.parse_args()
+
+
+def scaling_mode(args) -> str:
+    if args.scaling != "auto":
+        return args.scaling
+    return "strong" if args.config in ("cfg3", "cfg5") else "weak"
+
+
+def host_cores():
+    """(threads usable by this process, physical cores)."""
+    try:
+        logical = len(os.sched_getaffinity(0))
+    except Exception:
+        logical = os.cpu_count() or 1
+    try:
+        import psutil
+        phys = psutil.cpu_count(logical=False) or logical
+    except Exception:
+        phys = logical
+    return logical, phys
+
+
+def ref_module():
+    """The unmodified reference package, installed into baseline/_ref by
+    tools/install_reference.sh (pip --target; travels with the repo
+    snapshot), or None when it is absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "streampca")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import streampca
+    return streampca
+
+
+def max_angle(x, y) -> float:
+    """Largest principal angle between the column spaces of x and y."""
+    from scipy.linalg import subspace_angles
+    return float(np.max(subspace_angles(np.asarray(x, dtype=np.float64), np.asarray(y, dtype=np.float64))))
 
 
 def peaks():
@@ -150,55 +202,115 @@ def cpu_oracle_rate(n_rows: int, n: int, l: int, seed: int, threads: int):
     return a.nbytes / dt / 1e9, dt
 
 
+def host_config_matrix(config: str, rows: int):
+    """The config's A (first ``rows`` rows) generated on the host for the
+    reference arm, which runs without the GPU: configs 2-5 by the same
+    block-seeded construction as synth.config_matrix (torch CPU generator,
+    so the values differ from the GPU-generated matrix, the distribution does
+    not); config 1 by the reference's own synth_matrix (seed 100)."""
+    import math
+    import torch
+    from paper_1704_07669_b200 import synth
+    torch.set_num_threads(host_cores()[0])
+    if config == "cfg1":
+        ref = ref_module()
+        m, n = synth.CONFIGS["cfg1"][:2]
+        spec_vals = tuple(10.0 ** (-4.0 * np.arange(n) / (n - 1)))
+        if ref is not None:
+            return ref.synth_matrix(m, n, ref.SpectrumSpec("custom", values=spec_vals), seed=100).materialize()
+        import oracle as O
+        return O.reference_synth_matrix(m, n, spec_vals, 100)
+    m, n, r, kind, noise, _, _ = synth.CONFIGS[config]
+    dev = torch.device("cpu")
+    w = synth.right_factor(n, r, kind, 2024, dev)
+    out = torch.empty((rows, n), dtype=torch.float32)
+    synth.fill_rows(out, 0, m, n, r, noise, 2024, w)
+    return out.numpy()
+
+
 def run_reference(args):
-    """Reference arm: the CPU implementation of the path (the oracle port —
-    the reference is pure Python/numpy, nothing to compile), all host
-    threads, a bounded sample of the same workload per step."""
+    """Reference arm: the unmodified reference package (baseline/_ref, its
+    public API: ``sketch_pass(ArrayRowStream(A), Omega, block_rows)``,
+    sketch.py:52-116, streams.py:55-80) on this host's cores, every step one
+    pass over the config's A (fp32, widened to fp64 inside the timed step by
+    ArrayRowStream as for any numpy input), W warm-up + K timed steps. A config
+    whose K + W passes would exceed --ref-budget-s passes a stated row prefix
+    instead. Falls back to the numpy oracle port when baseline/_ref is absent.
+    Under torchrun only rank 0 runs."""
     world, rank, _ = dist_setup()
     if rank != 0:
         return
+    from threadpoolctl import threadpool_limits
     from paper_1704_07669_b200.synth import config_shape
     cs = config_shape(args.config)
-    threads = os.cpu_count() or 1
-    sample_rows = 8192
-    rates, times = [], []
-    for i in range(min(args.warmup, 3) + min(args.steps, 10)):
-        r, dt = cpu_oracle_rate(sample_rows, cs["n"], cs["l"], seed=i, threads=threads)
-        if i >= min(args.warmup, 3):
-            rates.append(r)
-            times.append(dt)
-    value = float(np.mean(rates))
-    one_thread, _ = cpu_oracle_rate(sample_rows // 2, cs["n"], cs["l"], seed=7, threads=1)
+    n, l = cs["n"], cs["l"]
+    es = 8 if args.config == "cfg1" else 4
+    threads, phys = host_cores()
+    ref = ref_module()
+    kind = "reference" if ref is not None else "port"
+    m = args.rows or cs["m"]
+    if args.config != "cfg1":
+        # ~1 GB/s of fp32 A per pass on 16 cores (measured): bound the run
+        per_step_cap = max(4096, int(args.ref_budget_s / max(1, args.steps + args.warmup) * 1.0e9 / (n * es)))
+        m = min(m, (per_step_cap // 4096) * 4096 or 4096)
+    a = host_config_matrix(args.config, m)
+    br = 200 if args.config == "cfg1" else 4096
+    if ref is not None:
+        omega = ref.linalg.gaussian_matrix(n, l, 1)
+
+        def one_pass():
+            return ref.sketch_pass(ref.ArrayRowStream(a), omega, block_rows=br)
+    else:
+        import oracle as O
+        omega = O.gaussian(n, l, 1)
+
+        def one_pass():
+            return O.oracle_sketch(((r0, a[r0:r0 + br].astype(np.float64)) for r0 in range(0, m, br)), omega)
+    times = []
+    with threadpool_limits(limits=threads):
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            one_pass()
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+    sec = float(np.mean(times))
+    value = m * n * es / sec / 1e9
+    full = m == cs["m"]
+    sample = (f"{'full' if full else 'row prefix of the'} config A: {m} x {n} "
+              f"{'fp64' if es == 8 else 'fp32 widened to fp64 by ArrayRowStream'} per step, "
+              f"block_rows {br}, {'unmodified reference streampca (baseline/_ref)' if ref else 'numpy oracle port'}")
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(rates),
-        "warmup": min(args.warmup, 3), "ms_per_step": 1e3 * float(np.mean(times)),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sec,
+        "higher_is_better": True, "scaling": scaling_mode(args), "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{args.config} sample", "m": sample_rows, "n": cs["n"], "l": cs["l"],
-                   "block_rows": 4096},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "value_1_thread": one_thread,
-                         "sample": f"{sample_rows} rows x {cs['n']} fp32 widened to fp64 per step "
-                                   "(numpy oracle of sketch.py:52-116, blocked path)"},
+        "config": {"workload": args.config if full else f"{args.config} row prefix", "m": m, "n": n, "l": l,
+                   "k": cs["k"], "block_rows": br},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "cores_physical": phys, "kind": kind,
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 def profile_traffic(rows: float, config: str):
-    """dram read+write bytes of the pass kernel over `rows` rows, scaled from the
-    committed ncu --set full capture (profiles/ncu_summary.json) of the same config."""
+    """(dram read+write bytes of the pass kernel over `rows` rows, source):
+    scaled from the committed ncu --set full capture (profiles/ncu_summary.json)
+    of the same config — a profile figure, not measured in this run."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
             prof = json.load(fh)
+        src = "ncu --set full capture, profiles/ncu_summary.json (%s), per-row bytes x rows" % prof.get(
+            "capture", "committed profile")
         per = prof.get("per_config", {}).get(config)
         if per is not None:
-            return per["dram_bytes_per_row"] * rows
+            return per["dram_bytes_per_row"] * rows, src
         if prof.get("config", "cfg2") != config:
-            return None
-        return prof["dram_bytes_per_row"] * rows
+            return None, None
+        return prof["dram_bytes_per_row"] * rows, src
     except Exception:
-        return None
+        return None, None
 
 
 def run_stream(args):
@@ -331,11 +443,18 @@ def run_ours(args):
         pg = dist
 
     from paper_1704_07669_b200 import GpuSketch, gaussian_matrix, synth
-    from paper_1704_07669_b200.parallel import allreduce_sketch
+    from paper_1704_07669_b200.parallel import allreduce_sketch, shard_rows
 
     cs = synth.config_shape(args.config)
-    m = args.rows or cs["m"]
+    mode = scaling_mode(args)
     n, l = cs["n"], cs["l"]
+    if mode == "weak":  # every rank a full config matrix: rows [rank m, (rank + 1) m) of a world*m job
+        m_total = (args.rows or cs["m"]) * world
+        r0, r1 = rank * (m_total // world), (rank + 1) * (m_total // world)
+    else:  # the config's fixed matrix split over the ranks
+        m_total = args.rows or cs["m"]
+        r0, r1 = shard_rows(m_total, world, rank)
+    m = r1 - r0
     if args.config == "cfg1":  # the reference's fp64 case
         args.dtype = "f64"
     es = 8 if args.dtype == "f64" else 4
@@ -343,9 +462,7 @@ def run_ours(args):
     bytes_per_rank = m * n * es
     hbm_peak, bf16_peak, peak_kind = peaks()
 
-    # this rank's shard: rows [rank*m, (rank+1)*m) of the job's matrix
-    a = synth.config_matrix(args.config, device=dev, rows=(rank * m, (rank + 1) * m),
-                            m_override=m * world)
+    a = synth.config_matrix(args.config, device=dev, rows=(r0, r1), m_override=m_total)
     if args.dtype == "f64" and a.dtype != torch.float64:
         a = a.double()
     omega = gaussian_matrix(n, l, 1)
@@ -401,7 +518,7 @@ def run_ours(args):
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * bytes_per_rank / (ms_step * 1e-3) / 1e9
+    value = m_total * n * es / (ms_step * 1e-3) / 1e9
 
     # Roofline of the dominant kernel: the pass kernel (tc_pass_kernel, one
     # persistent launch per push) timed with CUDA events around its launches on
@@ -430,29 +547,29 @@ def run_ours(args):
     else:
         roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": achieved_gbs / hbm_peak}
+    traffic, traffic_src = profile_traffic(m, args.config) if used_tc else (None, None)
     roofline.update({
-        "traffic": profile_traffic(m, args.config) if used_tc else None,
+        "traffic": traffic, "traffic_source": traffic_src,
         "peak_kind": peak_kind, "peak_desc": peak_desc,
         "kernel": "tc_pass_kernel (persistent, CTA pairs; G + H + column sums of all chunks)" if used_tc
                   else "sketch chunk: simt_g_kernel + simt_h_kernel + colsum (DMMA for fp64)",
-        "kernel_ms_per_pass": pass_ms, "chunk_rows": chunk_rows,
+        "kernel_ms_per_pass": pass_ms, "kernel_share": kern_ms / max(1e-9, ms), "chunk_rows": chunk_rows,
         "hbm": {"achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved_gbs / hbm_peak},
         "algorithmic_bytes_per_pass": pass_bytes, "flops_per_pass": flops,
         "floors_ms_per_pass": {"hbm": hbm_floor * 1e3, "tensor": tc_floor * 1e3},
     })
+    sk.close()
 
     out = {}
-    if rank == 0 and not args.no_e2e:
-        out["e2e"] = e2e_leg(args, a, omega, dev)
-    if rank == 0 and not args.no_pca:
-        out["pca_seconds"] = pca_leg(args, a, dev)
-    if rank == 0 and not args.no_cpu:
-        r, dt = cpu_oracle_rate(4096 * 2, n, l, seed=0, threads=os.cpu_count() or 1)
-        out["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-                               "sample": f"8192 rows x {n} fp32 (widened to fp64), numpy oracle sketch, "
-                                         f"{dt:.1f} s"}
-    sk.close()
+    if not args.no_e2e:
+        out.update(e2e_leg(args, a, omega, dev, pg, world, rank))
+    res_dev = None
+    if not args.no_pca:
+        pca, res_dev = pca_leg(args, a, dev, pg, world, rank)
+        out.update(pca)
+    if rank == 0 and world == 1 and not (args.no_cpu and args.no_parity):
+        out.update(reference_leg(args, a, res_dev, cs))
     if pg is not None:
         pg.barrier()
     if rank != 0:
@@ -462,11 +579,11 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": args.config, "m_per_gpu": m, "n": n, "l": l, "k": cs["k"],
+        "scaling": mode, "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": args.config, "m": m_total, "m_per_gpu": m, "n": n, "l": l, "k": cs["k"],
                    "rank": cs["rank"], "spectrum": cs["spectrum"], "noise": cs["noise"],
                    "precision": "3xTF32 tcgen05" if used_tc else ("DMMA fp64" if args.dtype == "f64" else "FFMA"),
-                   "parallelism": f"row-shard x{world}",
+                   "parallelism": f"row-shard x{world} ({mode})",
                    "l2": ("inputs larger than L2 (A is %.1f GB per GPU)" % (bytes_per_rank / 1e9)
                           if flush is None else
                           "L2 flushed before every timed step (512 MB write, untimed; A is %.0f MB)"
@@ -474,7 +591,7 @@ def run_ours(args):
         "roofline": roofline,
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
-        "tflops": 4.0 * m * n * l * world / (ms_step * 1e-3) / 1e12,
+        "tflops": 4.0 * m_total * n * l / (ms_step * 1e-3) / 1e12,
     }
     line.update(out)
     print(json.dumps(line), flush=True)
@@ -482,56 +599,182 @@ def run_ours(args):
         pg.destroy_process_group()
 
 
-def e2e_leg(args, a_dev, omega, dev, steps=3):
-    """Same metric through the public API: A in pinned host memory; each
-    step pushes it (H2D inside the library, overlapped with compute) and
-    reads the finished sketch back to the host."""
+def _max_over_ranks(x: float, pg, dev) -> float:
+    if pg is None:
+        return x
+    import torch
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def e2e_leg(args, a_dev, omega, dev, pg, world, rank):
+    """Same metric through the public API (GpuSketch.push / finish), every
+    step from HOST memory: (e2e) A in page-locked memory, (e2e_pageable) A in a
+    plain numpy array — the reference's own input type. Each step pushes all
+    of A (H2D inside the library, overlapped with the pass), finishes, reads
+    G, H and the column sums back to the host, and (N > 1) all-reduces the
+    sketch. K timed steps after one warm-up; wall clock, max over ranks."""
     import torch
     from paper_1704_07669_b200 import GpuSketch
+    from paper_1704_07669_b200.parallel import allreduce_sketch
     m, n = a_dev.shape
+    es = a_dev.element_size()
     host = torch.empty((m, n), dtype=a_dev.dtype, pin_memory=True)
     host.copy_(a_dev)
     torch.cuda.synchronize()
-    sk = GpuSketch(n, omega, np.float64 if a_dev.dtype == torch.float64 else np.float32,
-                   precision=args.precision, device=dev, rows_hint=m)
-    times = []
-    d2h = 0
-    for i in range(steps + 1):
+    npdt = np.float64 if a_dev.dtype == torch.float64 else np.float32
+    sk = GpuSketch(n, omega, npdt, precision=args.precision, device=dev, rows_hint=m)
+    out = {}
+    for key, src in (("e2e", host), ("e2e_pageable", None)):
+        if src is None:
+            src = host.numpy().copy()  # plain pageable numpy array
+        d2h = 0
+
+        def one():
+            sk.reset()
+            sk.push(src, 0, final=True)
+            g, h, c, rows = sk.finish(on_device=pg is not None)
+            if pg is not None:
+                allreduce_sketch(h, c, pg, rows=rows)
+                g, h, c = g.cpu(), h.cpu(), c.cpu()
+            return int(g.nbytes + h.nbytes + c.nbytes) if hasattr(g, "nbytes") else 0
+
+        one()
         torch.cuda.synchronize()
+        if pg is not None:
+            pg.barrier()
+        steps = args.steps if key == "e2e" else max(3, min(args.steps, 10))
         t0 = time.perf_counter()
-        sk.reset()
-        sk.push(host, 0, final=True)
-        g, h, c, rows = sk.finish(on_device=False)
-        dt = time.perf_counter() - t0
-        d2h = g.nbytes + h.nbytes + c.nbytes
-        if i:
-            times.append(dt)
+        for _ in range(steps):
+            d2h = one()
+        torch.cuda.synchronize()
+        t = _max_over_ranks((time.perf_counter() - t0) / steps, pg, dev)
+        out[key] = {"value": world * m * n * es / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": m * n * es,
+                    "d2h_bytes_per_step": int(d2h), "seconds_per_step": t, "steps": steps,
+                    "source": "page-locked host tensor" if key == "e2e" else "pageable numpy array"}
+        del src
     sk.close()
     del host
-    t = float(np.median(times))
-    es = a_dev.element_size()
-    return {"value": m * n * es / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": m * n * es,
-            "d2h_bytes_per_step": int(d2h), "seconds_per_step": t}
+    return out
 
 
-def pca_leg(args, a_dev, dev):
-    """End-to-end PCA seconds (sketch + GPU post-pass) on the resident A."""
+def pca_leg(args, a_dev, dev, pg, world, rank):
+    """End-to-end PCA seconds through the public entry point: with A resident
+    in HBM (DeviceRowStream), and (N = 1) from a plain numpy array as the
+    reference receives it (H2D inside). N > 1: sharded_single_pass_pca (the
+    row-sum of Eq. 10, one all-reduce, gathered G), max over ranks.
+    Returns (fields, the HBM-resident result)."""
     import torch
     from paper_1704_07669_b200 import DeviceRowStream, PcaConfig, single_pass_pca
+    from paper_1704_07669_b200.parallel import sharded_single_pass_pca
     from paper_1704_07669_b200.synth import config_shape
     cs = config_shape(args.config)
     cfg = PcaConfig(k=cs["k"], oversample=cs["l"] - cs["k"], seed=1)
+    out = {}
+    if pg is not None:
+        sharded_single_pass_pca(a_dev, cfg, pg, precision=args.precision, device=dev)
+        torch.cuda.synchronize()
+        pg.barrier()
+        t0 = time.perf_counter()
+        res = sharded_single_pass_pca(a_dev, cfg, pg, precision=args.precision, device=dev)
+        torch.cuda.synchronize()
+        t = _max_over_ranks(time.perf_counter() - t0, pg, dev)
+        out["pca_seconds"] = {"value": t, "unit": "s", "k": cfg.k, "l": cfg.l, "s0": float(res.s[0]),
+                              "includes": "Omega draw, sharded sketch pass, all-reduce, G gather, QB, SVD, "
+                                          "U/S/V to host (max over ranks)"}
+        return out, res
     single_pass_pca(DeviceRowStream(a_dev), cfg, precision=args.precision, device=dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = single_pass_pca(DeviceRowStream(a_dev), cfg, precision=args.precision, device=dev)
     torch.cuda.synchronize()
-    return {"value": time.perf_counter() - t0, "unit": "s", "k": cfg.k, "l": cfg.l,
-            "s0": float(res.s[0]), "includes": "Omega draw, sketch pass, QB, SVD, U/S/V to host"}
+    out["pca_seconds"] = {"value": time.perf_counter() - t0, "unit": "s", "k": cfg.k, "l": cfg.l,
+                          "s0": float(res.s[0]),
+                          "includes": "Omega draw, sketch pass (A in HBM), QB, SVD, U/S/V to host"}
+    a_np = a_dev.cpu().numpy()
+    single_pass_pca(a_np, cfg, precision=args.precision, device=dev)
+    t0 = time.perf_counter()
+    single_pass_pca(a_np, cfg, precision=args.precision, device=dev)
+    torch.cuda.synchronize()
+    out["pca_seconds_host"] = {"value": time.perf_counter() - t0, "unit": "s",
+                               "includes": "same, A a pageable numpy array (H2D of A inside)"}
+    del a_np
+    return out, res
+
+
+def reference_leg(args, a_dev, res, cs):
+    """N = 1: the unmodified reference (baseline/_ref) on this host's cores
+    over the SAME A (the device matrix copied to the host, fp32 widened to
+    fp64 by the reference's ArrayRowStream) and the same seeded Omega:
+    (cpu_baseline) its sketch_pass GB/s over the full A and its
+    single_pass_pca seconds; (parity) our U, S, V against its U, S, V —
+    max relative S error and the largest principal angles of U and V
+    (BASELINE.json bar: 1e-4 fp32, 1e-10 fp64)."""
+    from threadpoolctl import threadpool_limits
+    ref = ref_module()
+    threads, phys = host_cores()
+    out = {}
+    if ref is None:
+        if not args.no_cpu:
+            r, dt = cpu_oracle_rate(8192, cs["n"], cs["l"], seed=0, threads=threads)
+            out["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": threads, "cores_physical": phys,
+                                   "kind": "port", "sample": f"8192 rows x {cs['n']} fp32 (widened to fp64), "
+                                   f"numpy oracle sketch, {dt:.1f} s (baseline/_ref absent)"}
+        return out
+    a_host = a_dev.cpu().numpy()
+    m, n = a_host.shape
+    l = cs["l"]
+    br = 200 if args.config == "cfg1" else 4096
+    cfg = ref.PcaConfig(k=cs["k"], oversample=l - cs["k"], seed=1)
+    with threadpool_limits(limits=threads):
+        omega = ref.linalg.gaussian_matrix(n, l, 1)
+        t0 = time.perf_counter()
+        ref.sketch_pass(ref.ArrayRowStream(a_host), omega, block_rows=br)
+        t_sketch = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rs = ref.single_pass_pca(a_host, cfg, block_rows=br)
+        t_pca = time.perf_counter() - t0
+    del a_host
+    out["cpu_baseline"] = {
+        "value": m * n * a_dev.element_size() / t_sketch / 1e9, "unit": UNIT, "cores": threads,
+        "cores_physical": phys, "kind": "reference", "pass_seconds": t_sketch, "pca_seconds": t_pca,
+        "sample": f"full config A ({m} x {n} {'fp64' if a_dev.element_size() == 8 else 'fp32 widened to fp64'}), "
+                  f"unmodified reference streampca (baseline/_ref): sketch_pass(ArrayRowStream(A), Omega, "
+                  f"block_rows={br}) and single_pass_pca(A, PcaConfig(k={cs['k']}, oversample={l - cs['k']}, "
+                  f"seed=1), block_rows={br}), threadpoolctl {threads} threads"}
+    if res is not None and not args.no_parity:
+        s_ours = np.asarray(res.s, dtype=np.float64)
+        s_ref = np.asarray(rs.s, dtype=np.float64)
+        out["parity"] = {
+            "s_rel_max": float(np.max(np.abs(s_ours - s_ref) / np.abs(s_ref))),
+            "angle_u_max": max_angle(res.u, rs.u), "angle_v_max": max_angle(res.v, rs.v),
+            "k": int(cs["k"]), "bar": 1e-10 if a_dev.element_size() == 8 else 1e-4,
+            "against": "reference single_pass_pca (baseline/_ref) on the same A and seeded Omega, "
+                       "this host, this run"}
+        p = out["parity"]
+        p["pass"] = bool(max(p["s_rel_max"], p["angle_u_max"], p["angle_v_max"]) <= p["bar"])
+    return out
+
+
+def spawn(args) -> int:
+    """--gpus N without a launcher: re-run this script under
+    torch.distributed.run with N ranks on this node (127.0.0.1)."""
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "cfg4":

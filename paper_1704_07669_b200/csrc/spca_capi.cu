@@ -100,6 +100,53 @@ void dfree(spca_sketch *h, void *p) {
   if (p) cudaFreeAsync(p, h->stream);
 }
 
+// Page-locked staging buffers cost ~0.3 s per GB to create (cudaHostAlloc
+// pins every page), which a one-shot call such as single_pass_pca on a numpy
+// array would pay on each call: handles take them from, and give them back
+// to, a process-wide free list (portable allocations, any device; at most
+// kPinnedCache bytes kept).
+constexpr size_t kPinnedCache = size_t(4) << 30;
+struct PinnedPool {
+  std::mutex mu;
+  std::vector<std::pair<size_t, void *>> free;
+  size_t cached = 0;
+};
+PinnedPool &pinned_pool() {
+  static PinnedPool *p = new PinnedPool;  // never destroyed: handles may outlive static teardown
+  return *p;
+}
+cudaError_t pinned_get(void **p, size_t bytes) {
+  PinnedPool &pp = pinned_pool();
+  {
+    std::lock_guard<std::mutex> lk(pp.mu);
+    for (size_t i = 0; i < pp.free.size(); ++i) {
+      if (pp.free[i].first == bytes) {
+        *p = pp.free[i].second;
+        pp.cached -= bytes;
+        pp.free.erase(pp.free.begin() + (long)i);
+        return cudaSuccess;
+      }
+    }
+  }
+  return cudaHostAlloc(p, bytes, cudaHostAllocPortable);
+}
+void pinned_put(void *p, size_t bytes) {
+  if (!p) return;
+  PinnedPool &pp = pinned_pool();
+  std::lock_guard<std::mutex> lk(pp.mu);
+  while (pp.cached + bytes > kPinnedCache && !pp.free.empty()) {  // oldest first
+    cudaFreeHost(pp.free.front().second);
+    pp.cached -= pp.free.front().first;
+    pp.free.erase(pp.free.begin());
+  }
+  if (bytes > kPinnedCache) {
+    cudaFreeHost(p);
+    return;
+  }
+  pp.free.emplace_back(bytes, p);
+  pp.cached += bytes;
+}
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -519,7 +566,7 @@ int ensure_staging(spca_sketch *h, bool need_pinned) {
     if (!h->dstage[i]) CK(h, cudaMalloc(&h->dstage[i], bytes));
     if (!h->copy_done[i]) CK(h, cudaEventCreateWithFlags(&h->copy_done[i], cudaEventDisableTiming));
     if (!h->comp_done[i]) CK(h, cudaEventCreateWithFlags(&h->comp_done[i], cudaEventDisableTiming));
-    if (need_pinned && !h->pinned[i]) CK(h, cudaHostAlloc(&h->pinned[i], bytes, cudaHostAllocDefault));
+    if (need_pinned && !h->pinned[i]) CK(h, pinned_get(&h->pinned[i], bytes));
   }
   if (!h->copy_stream) CK(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
   return SPCA_OK;
@@ -1269,7 +1316,7 @@ void spca_sketch_destroy(spca_handle_t h) {
   for (void *p : {h->dstage[0], h->dstage[1]})
     if (p) cudaFree(p);
   for (int i = 0; i < 2; ++i) {
-    if (h->pinned[i]) cudaFreeHost(h->pinned[i]);
+    pinned_put(h->pinned[i], (size_t)h->stage_rows * h->ldp * h->ds);
     if (h->copy_done[i]) cudaEventDestroy(h->copy_done[i]);
     if (h->comp_done[i]) cudaEventDestroy(h->comp_done[i]);
   }

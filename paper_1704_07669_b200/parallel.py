@@ -19,6 +19,12 @@ from typing import Optional
 from .device import host_copy, torch_mod
 
 
+def _host_staged(dist, group, t) -> bool:
+    """gloo has no all_gather on CUDA tensors: such collectives go through
+    host copies (NCCL takes the device tensors as they are)."""
+    return bool(getattr(t, "is_cuda", False)) and dist.get_backend(group) == "gloo"
+
+
 def allreduce_sketch(h, col_sums, dist, rows: Optional[int] = None, group=None):
     """Sum H (n x l) and col_sums (n) over ranks in place with ONE collective;
     returns the global row count when ``rows`` is given."""
@@ -30,7 +36,12 @@ def allreduce_sketch(h, col_sums, dist, rows: Optional[int] = None, group=None):
     buf[n * l: n * (l + 1)].copy_(col_sums)
     if extra:
         buf[-1] = float(rows)
-    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    if _host_staged(dist, group, buf):
+        hb = buf.cpu()
+        dist.all_reduce(hb, op=dist.ReduceOp.SUM, group=group)
+        buf.copy_(hb)
+    else:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     h.copy_(buf[: n * l].view(n, l))
     col_sums.copy_(buf[n * l: n * (l + 1)])
     return int(round(float(buf[-1]))) if extra else None
@@ -47,6 +58,9 @@ def gather_rows(g, dist, group=None):
     """All-gather row shards of different lengths into the full matrix."""
     torch = torch_mod()
     world = dist.get_world_size(group)
+    if _host_staged(dist, group, g):
+        full, counts = gather_rows(g.cpu(), dist, group)
+        return full.to(g.device), counts
     cnt = torch.tensor([g.shape[0]], dtype=torch.int64, device=g.device)
     counts = [torch.zeros_like(cnt) for _ in range(world)]
     dist.all_gather(counts, cnt, group=group)
@@ -65,7 +79,12 @@ def center_sharded(g_local, h, col_sums, omega, m_total: int, dist, group=None):
     torch = torch_mod()
     mu = col_sums / m_total
     gsum = g_local.sum(dim=0)
-    dist.all_reduce(gsum, op=dist.ReduceOp.SUM, group=group)
+    if _host_staged(dist, group, gsum):
+        gh = gsum.cpu()
+        dist.all_reduce(gh, op=dist.ReduceOp.SUM, group=group)
+        gsum = gh.to(g_local.device)
+    else:
+        dist.all_reduce(gsum, op=dist.ReduceOp.SUM, group=group)
     g_c = g_local - (mu @ omega)[None, :]
     h_c = h - torch.outer(mu, gsum)
     return g_c, h_c, torch.zeros_like(col_sums), mu
