@@ -727,20 +727,31 @@ def reference_leg(args, a_dev, res, cs):
     l = cs["l"]
     br = 200 if args.config == "cfg1" else 4096
     cfg = ref.PcaConfig(k=cs["k"], oversample=l - cs["k"], seed=1)
+    # A above 6 GB goes through the reference's GeneratorRowStream over fp32
+    # row blocks (widened to fp64 per block, as FileRowStream does at
+    # streams.py:128) instead of ArrayRowStream's whole fp64 copy, which
+    # would not fit host memory beside A at config 5 (40 GB -> 80 GB)
+    streamed = a_host.nbytes > (6 << 30)
+
+    def src():
+        if streamed:
+            return ref.GeneratorRowStream((a_host[r:r + br] for r in range(0, m, br)), n)
+        return ref.ArrayRowStream(a_host)
     with threadpool_limits(limits=threads):
         omega = ref.linalg.gaussian_matrix(n, l, 1)
         t0 = time.perf_counter()
-        ref.sketch_pass(ref.ArrayRowStream(a_host), omega, block_rows=br)
+        ref.sketch_pass(src(), omega, block_rows=br)
         t_sketch = time.perf_counter() - t0
         t0 = time.perf_counter()
-        rs = ref.single_pass_pca(a_host, cfg, block_rows=br)
+        rs = ref.single_pass_pca(src() if streamed else a_host, cfg, block_rows=br)
         t_pca = time.perf_counter() - t0
     del a_host
     out["cpu_baseline"] = {
         "value": m * n * a_dev.element_size() / t_sketch / 1e9, "unit": UNIT, "cores": threads,
         "cores_physical": phys, "kind": "reference", "pass_seconds": t_sketch, "pca_seconds": t_pca,
         "sample": f"full config A ({m} x {n} {'fp64' if a_dev.element_size() == 8 else 'fp32 widened to fp64'}), "
-                  f"unmodified reference streampca (baseline/_ref): sketch_pass(ArrayRowStream(A), Omega, "
+                  f"unmodified reference streampca (baseline/_ref): sketch_pass("
+                  f"{'GeneratorRowStream(fp32 row blocks)' if streamed else 'ArrayRowStream(A)'}, Omega, "
                   f"block_rows={br}) and single_pass_pca(A, PcaConfig(k={cs['k']}, oversample={l - cs['k']}, "
                   f"seed=1), block_rows={br}), threadpoolctl {threads} threads"}
     if res is not None and not args.no_parity:

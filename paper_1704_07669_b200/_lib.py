@@ -54,6 +54,9 @@ SIGNATURES = {
     "spca_omega_used": (c_int, [c_void_p, c_void_p, c_int]),
     "spca_allreduce": (c_int, [c_void_p, c_void_p, POINTER(c_int64)]),
     "spca_normalize_rows": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int, c_void_p]),
+    "spca_qb_workspace_elems": (c_int64, [c_int64, c_int, c_int]),
+    "spca_qb_block": (c_int, [c_int64, c_int, c_int, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
+                              c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "spca_last_error": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int64), c_char_p, c_size_t]),
     "spca_kernel_launches": (c_int64, [c_void_p]),
     "spca_enable_kernel_timing": (c_int, [c_void_p, c_int]),

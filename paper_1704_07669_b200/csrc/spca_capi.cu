@@ -26,6 +26,7 @@
 #include "sketch_simt.cuh"
 #include "handle.cuh"
 #include "normalize.cuh"
+#include "postpass.cuh"
 
 using namespace spca;
 
@@ -1189,6 +1190,117 @@ int spca_normalize_rows(const void *src, int64_t rows, int64_t n, int64_t ld_src
     return set_err(nullptr, SPCA_ERR_CONFIG, -1, "normalize_rows: bad dtype %d", dtype);
   const cudaError_t e = launch_normalize(src, rows, n, ld_src, dst, ld_dst, dtype, (cudaStream_t)stream);
   if (e != cudaSuccess) return set_err(nullptr, SPCA_ERR_CUDA, -1, "normalize_rows launch: %s", cudaGetErrorString(e));
+  return SPCA_OK;
+}
+
+// ---------------------------------------------------------------- post-pass
+namespace {
+int qb_rows_per_tile(int c0, int b) {
+  // ~96 KB of [Q | y] per stage (enough bytes in flight per SM for HBM),
+  // within the shared-memory budget at two stages
+  int tr = (int)std::max<int64_t>(16, std::min<int64_t>(256, (96 << 10) / (8 * (int64_t)((c0 | 1) + b))));
+  while (tr > 16 && spca::qb_sweep_smem(c0, b, tr) > (200u << 10)) tr /= 2;
+  return tr;
+}
+int qb_parts(int64_t m, int tr) {
+  const int64_t tiles = (m + tr - 1) / tr;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * 148));
+}
+}  // namespace
+
+int64_t spca_qb_workspace_elems(int64_t m, int c0_max, int b) {
+  if (m < 1 || c0_max < 0 || b < 1) return 0;
+  int64_t most = 0;
+  for (int c0 = 0; c0 <= c0_max; c0 += b) {  // partials of the widest sweep, the reduced sums, x
+    const int ncat = c0 + b;
+    most = std::max<int64_t>(most, (int64_t)qb_parts(m, qb_rows_per_tile(c0, b)) * b * ncat);
+  }
+  return most + (int64_t)b * (c0_max + b) + (int64_t)c0_max * b + 64;
+}
+
+int spca_qb_block(int64_t m, int c0, int b, double *q, int64_t ldq, const double *g, int64_t ldg,
+                  const double *x, double *ybuf, double *ws, int64_t ws_elems, double *p_out,
+                  double *factors, int *flag, const double *tol, void *stream) {
+  if (m < 1 || c0 < 0 || b < 1 || b > spca::kQbMaxB || c0 + b > spca::kQbMaxCat || ldq < c0 + b || ldg < b)
+    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "qb_block: unsupported shape m %lld c0 %d b %d", (long long)m,
+                   c0, b);
+  if (!q || !g || !ybuf || !ws || !p_out || !factors || !flag || !tol || (c0 > 0 && !x))
+    return set_err(nullptr, SPCA_ERR_STATE, -1, "qb_block: null pointer");
+  if (ws_elems < spca_qb_workspace_elems(m, c0, b))
+    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "qb_block: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int tr = qb_rows_per_tile(c0, b);
+  const int parts = qb_parts(m, tr);
+  const int ncat = c0 + b;
+  const size_t smem = spca::qb_sweep_smem(c0, b, tr);
+  cudaError_t e = cudaFuncSetAttribute(spca::qb_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return set_err(nullptr, SPCA_ERR_CUDA, -1, "qb_block smem: %s", cudaGetErrorString(e));
+  double *part = ws;
+  double *red = part + (size_t)parts * b * ncat;  // b x ncat
+  double *xt = red + (size_t)b * ncat;            // c0 x b
+  const int bb = b * b;
+  double *R1 = factors, *R2 = factors + bb, *R3 = factors + 3 * bb, *R4 = factors + 4 * bb;
+  const unsigned rblocks = (unsigned)ceil_div((int64_t)b * ncat, 256);
+  auto sweep = [&](const double *yin, int64_t ldy, const double *ra, const double *rb, const double *xx,
+                   double *out, int64_t ldo, int wp, int ww) -> cudaError_t {
+    spca::QbSweepArgs a{};
+    a.m = m;
+    a.c0 = c0;
+    a.b = b;
+    a.tr = tr;
+    a.q = c0 ? q : nullptr;
+    a.ldq = ldq;
+    a.yin = yin;
+    a.ldy = ldy;
+    a.ra = ra;
+    a.rb = rb;
+    a.x = xx;
+    a.out = out;
+    a.ldo = ldo;
+    a.want_p = wp;
+    a.want_w = ww;
+    a.part = part;
+    spca::qb_sweep_kernel<<<parts, spca::kQbThreads, smem, st>>>(a);
+    return cudaGetLastError();
+  };
+  auto reduce = [&](double *dst, double *xtrans) -> cudaError_t {
+    spca::qb_reduce_kernel<<<rblocks, 256, 0, st>>>(part, parts, b, ncat, dst, xtrans, c0);
+    return cudaGetLastError();
+  };
+  auto small = [&](int op, const double *r) -> cudaError_t {
+    spca::qb_small_kernel<<<1, 32, 0, st>>>(op, b, ncat, c0, r, factors, flag, tol);
+    return cudaGetLastError();
+  };
+#define QB_TRY(call)                                                                             \
+  do {                                                                                           \
+    cudaError_t _e = (call);                                                                     \
+    if (_e != cudaSuccess)                                                                       \
+      return set_err(nullptr, SPCA_ERR_CUDA, -1, "qb_block %s: %s", #call, cudaGetErrorString(_e)); \
+  } while (0)
+  // S1: y = G_i - Q X; [y^T Q | y^T y] (kept for the B update)
+  QB_TRY(sweep(g, ldg, nullptr, nullptr, c0 ? x : nullptr, ybuf, b, 1, 1));
+  QB_TRY(reduce(p_out, nullptr));
+  QB_TRY(small(1, p_out));
+  // S2: Q1 = y R1^-1, Q1^T Q1
+  QB_TRY(sweep(ybuf, b, R1, nullptr, nullptr, nullptr, 0, 0, 1));
+  QB_TRY(reduce(red, nullptr));
+  QB_TRY(small(2, red));
+  if (c0 > 0) {  // S3: Q^T Q2 (Q2 = Q1 R2^-1), kept transposed as the next x
+    QB_TRY(sweep(ybuf, b, R1, R2, nullptr, nullptr, 0, 1, 0));
+    QB_TRY(reduce(red, xt));
+  }
+  // S4: z = Q2 - Q (Q^T Q2), z^T z
+  QB_TRY(sweep(ybuf, b, R1, R2, c0 ? xt : nullptr, ybuf, b, 0, 1));
+  QB_TRY(reduce(red, nullptr));
+  QB_TRY(small(3, red));
+  // S5: Z1 = z R3^-1, Z1^T Z1
+  QB_TRY(sweep(ybuf, b, R3, nullptr, nullptr, nullptr, 0, 0, 1));
+  QB_TRY(reduce(red, nullptr));
+  QB_TRY(small(4, red));
+  // S6: Q_i = Z1 R4^-1 into Q's columns [c0, c0 + b)
+  QB_TRY(sweep(ybuf, b, R3, R4, nullptr, q + c0, ldq, 0, 0));
+#undef QB_TRY
   return SPCA_OK;
 }
 
