@@ -224,13 +224,15 @@ int spca_normalize_rows(const void *src, int64_t rows, int64_t n, int64_t ld_src
  * Q is m x ldq row-major: columns [0, c0) are read, [c0, c0 + b) written.
  * G_i points at the block's first column (row stride ldg). On return (stream
  * ordered): p_out = [y^T Q | y^T y] (b x (c0 + b), row-major), factors =
- * six b x b upper-triangular matrices R1, R2, r_i, R3, R4, R_i (R_i feeds the
+ * ten b x b upper-triangular matrices R1, R2, r_i, R3, R4, R_i, R1^-1,
+ * R1^-1 R2^-1, R3^-1, R3^-1 R4^-1 (R_i = factors[5] feeds the
  * caller's B_i = R_i^-T (H_i^T - (y^T Q) B - (Omega_i^T B^T) B)), and *flag
  * set to 1 if any test of the optimistic path failed (Cholesky breakdown,
  * CholeskyQR2 defect >= 1e-5, |r_jj| < *tol (qb.py:100), solve_rt's
  * singularity guard (linalg.py:131-135)): the caller then redoes the
- * factorization on the general path. Every pointer is device memory; 1 <= b
- * <= 16, c0 + b <= 512. ws: spca_qb_workspace_elems(m, c0, b) doubles. */
+ * factorization on the general path. Every pointer is device memory; b even,
+ * 2 <= b <= 16, c0 even, c0 + b <= 256, ldq and ldg even, 16-byte aligned
+ * operands. ws: spca_qb_workspace_elems(m, c0, b) doubles. */
 int64_t spca_qb_workspace_elems(int64_t m, int c0_max, int b);
 int spca_qb_block(int64_t m, int c0, int b, double *q, int64_t ldq, const double *g, int64_t ldg,
                   const double *x, double *ybuf, double *ws, int64_t ws_elems, double *p_out,

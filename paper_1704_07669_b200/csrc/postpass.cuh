@@ -10,281 +10,435 @@
 //   R_i <- Rt R_i;  B_i from R_i^-T (H_i^T - (y^T Q) B - (Omega_i^T B^T) B)  qb.py:115-118
 //
 // The tall-skinny work of a block (Q is m x c0 with m up to 5e6) is six
-// sweeps over the rows, each ONE kernel that streams its operands once and
-// folds every product the step needs into per-CTA partial sums:
+// sweeps over the rows. Every sweep is ONE kernel computing, per row,
 //
-//   S1  t = G_i - Q X            write y = t;  reduce [t^T Q | t^T t]   (X = B Omega_i)
-//   S2  t = y R1^-1                            reduce t^T t
-//   S3  t = (y R1^-1) R2^-1                    reduce t^T Q
-//   S4  t = (y R1^-1) R2^-1 - Q P2^T  write z = t;  reduce t^T t
-//   S5  t = z R3^-1                            reduce t^T t
-//   S6  t = (z R3^-1) R4^-1           write Q[:, c0:c0+b] = t
+//   t = y M - Q X        (M: b x b, X: c0 x b; either term may be absent)
 //
-// (the triangular solves are applied per row by substitution, as a right-side
-// trsm does), with one fixed-order reduction of the partials and one small
-// single-CTA kernel for the b x b algebra after each reducing sweep
-// (Cholesky factors, CholeskyQR2's acceptance test, the deficiency test
-// |r_jj| < RANK_TOL max ||G_j|| of qb.py:100 and solve_rt's singularity
-// guard of linalg.py:131-135). Any failed test sets a device flag; the host
-// checks it once per factorization and falls back to the general
-// (Householder / repair) path, which handles every such block. No float
+// and folding t^T [Q | t] into per-CTA partial sums; the sweeps differ only
+// in M, X, the output and the sums kept:
+//
+//   S1  M = I,               X = B Omega_i   write y = t;  [t^T Q | t^T t]
+//   S2  M = R1^-1                            t^T t
+//   S3  M = R1^-1 R2^-1                      t^T Q      (-> X of S4, transposed)
+//   S4  M = R1^-1 R2^-1,     X = Q^T Q2      write z = t;  t^T t
+//   S5  M = R3^-1                            t^T t
+//   S6  M = R3^-1 R4^-1                      write Q[:, c0:c0+b] = t
+//
+// (CholeskyQR2: R = chol(y^T y), Q1 = y R^-1, twice). The right-side
+// triangular solves of the library form become products with the inverse
+// triangular factors (formed once per block, b <= 16), so a sweep is a pure
+// fp64 tensor-core contraction: M = rows, N = b, K = b + c0 — no serial
+// per-row substitution holding the tile. One fixed-order reduction of the
+// partials and one single-warp kernel for the b x b algebra follow each
+// reducing sweep (Cholesky factors, triangular inverses, CholeskyQR2's
+// acceptance test, the deficiency test |r_jj| < RANK_TOL max ||G_j|| of
+// qb.py:100 and solve_rt's singularity guard of linalg.py:131-135). Any
+// failed test sets a device flag; the host checks it once per factorization
+// and falls back to the general (Householder / repair) path. No float
 // atomics: results are bitwise reproducible.
 //
 // Roofline: HBM. Per block the sweeps read Q three times (S1, S3, S4) and
-// the m x b blocks y / z seven times: ~ 8 m (3 c0 + 9 b) bytes; the DFMA work
-// (~4 m c0 b per block) stays below the fp64 rate for c0 <= 512.
+// the m x b blocks y / z seven times: ~ 8 m (3 c0 + 9 b) bytes; the DMMA work
+// (b padded to 16 columns) stays below the fp64 tensor rate for c0 <= 512.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "tc_ptx.cuh"
+
 namespace spca {
 
-constexpr int kQbThreads = 256;
-constexpr int kQbMaxB = 16;    // block sizes up to 16 (the reference's default is 10)
-constexpr int kQbMaxCat = 512; // c0 + b columns reduced per sweep (2 per thread)
+constexpr int kQbMaxB = 16;     // block sizes up to 16 (the reference's default is 10)
+constexpr int kQbMaxCat = 256;  // c0 + b columns reduced per sweep (l <= 256: config 5 has 250)
+constexpr int kQbThreads = 256; // 8 warps; thread 0 also issues the TMA loads
+constexpr int kQbWarps = kQbThreads / 32;
+// Row strides (doubles) of the t tile and of the [M; -X] operand block: 24
+// = 8 mod 16, so a DMMA fragment load (4 rows x 8 consecutive doubles) hits
+// each bank once per 128-byte wavefront (a stride of 16 made it 4-way)
+constexpr int kQbLdt = 24;
+constexpr int kQbLdw = 24;
+constexpr int kQbNtw = kQbMaxCat / 8 / kQbWarps;   // 8-column tiles of [Q | t] per warp (at most)
+constexpr int kQbMaxStages = 3;
 
 struct QbSweepArgs {
   int64_t m;
-  int c0, b, tr;          // accepted Q columns, block width, rows per tile
-  const double *q;        // m x c0 (row stride ldq) or null when c0 == 0
-  int64_t ldq;
-  const double *yin;      // m x b input rows (row stride ldy)
-  int64_t ldy;
-  const double *ra, *rb;  // b x b upper triangular (row-major): t = (yin ra^-1) rb^-1, either may be null
+  int c0, b, tr, stages;  // accepted Q columns, block width, rows per tile (16/32/64), ring depth (2/3)
+  int nslab;              // 16-column slabs of Q loaded per tile (0: Q not read)
+  const double *mt;       // b x b (row-major): t = y mt, or null (identity)
   const double *x;        // c0 x b: t -= Q x, or null
   double *out;            // m x b output rows (row stride ldo) or null
   int64_t ldo;
-  int want_p, want_w;     // reduce t^T Q (b x c0) / t^T t (b x b)
   double *part;           // [gridDim.x][b][c0 + b]
+  const double *y1d;      // y rows as one contiguous m x b block (row stride b): each tile is
+                          // one 1-D bulk copy instead of a tensor-map box of narrow rows
 };
 
-// right-side substitution t <- t R^-1 (R upper, row-major b x b): solves
-// x R = t column by column, x_j = (t_j - sum_{i<j} x_i R_ij) / R_jj
-__device__ __forceinline__ void qb_rsolve(double *t, const double *r, int b) {
-#pragma unroll
-  for (int j = 0; j < kQbMaxB; ++j) {
-    if (j < b) {
-      double s = t[j];
-#pragma unroll
-      for (int i = 0; i < kQbMaxB; ++i)
-        if (i < j) s = fma(-t[i], r[i * b + j], s);
-      t[j] = s / r[j * b + j];
-    }
-  }
+// fp64 tensor-core step D(16x8) += A(16x4, row) B(4x8, col) (fragments: a0 =
+// A[g][t], a1 = A[g+8][t], b = B[t][g]; d = D[g][2t..2t+1], D[g+8][2t..2t+1];
+// g = lane / 4, t = lane % 4)
+__device__ __forceinline__ void qb_dmma(double (&d)[4], double a0, double a1, double b) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+               : "d"(a0), "d"(a1), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async8(double *dst, const double *src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src)
-               : "memory");
+// Stage layout (bytes): nslab Q slabs of [tr][16] doubles with the TMA's
+// 128-byte swizzle (16-byte chunk c of row r at chunk c ^ (r & 7)), then the
+// y tile [tr][b] (unswizzled).
+__host__ __device__ inline size_t qb_stage_bytes(int nslab, int b, int tr) {
+  return (size_t)nslab * tr * 128 + (((size_t)tr * b * 8 + 1023) & ~(size_t)1023);
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-
-// shared-memory doubles of one sweep CTA (two tile stages of [Q | y] plus t,
-// x and the two triangular factors)
-__host__ __device__ inline size_t qb_sweep_smem(int c0, int b, int tr) {
-  const int ldqs = c0 | 1;
-  return sizeof(double) * ((size_t)2 * tr * (ldqs + b) + (size_t)tr * (kQbMaxB + 1) + (size_t)c0 * b + 2 * b * b);
+// operand block [M; -X] as one K x 16 matrix, K = b (padded to 4) + c0 (padded to 4)
+__host__ __device__ inline int qb_km(int b) { return (b + 3) & ~3; }
+__host__ __device__ inline int qb_kb(int c0, int b) { return qb_km(b) + ((c0 + 3) & ~3); }
+__host__ __device__ inline size_t qb_sweep_smem(int c0, int b, int tr, int nslab, int stages) {
+  return 1024 + stages * qb_stage_bytes(nslab, b, tr) +
+         sizeof(double) * ((size_t)tr * kQbLdt + (size_t)qb_kb(c0, b) * kQbLdw + kQbThreads * 4);
+}
+// element (r, k) of a swizzled Q slab set
+__device__ __forceinline__ double qb_qs(const uint8_t *qs, int tr, int r, int k) {
+  const int j = k >> 4, kk = k & 15;
+  return *reinterpret_cast<const double *>(qs + (size_t)j * tr * 128 + r * 128 + ((((kk >> 1) ^ (r & 7))) << 4) +
+                                           ((kk & 1) << 3));
 }
 
-// One sweep: rows in tiles of tr, staged in shared memory by cp.async two
-// tiles deep (the next tile streams in while this one is computed).
-__global__ void __launch_bounds__(kQbThreads) qb_sweep_kernel(const QbSweepArgs a) {
-  extern __shared__ double qsm[];
-  const int c0 = a.c0, b = a.b, tr = a.tr;
-  const int ldqs = c0 | 1;                  // odd row stride: conflict-free column reads
-  const int ldt = kQbMaxB + 1;
-  const bool need_q = c0 > 0 && (a.x != nullptr || a.want_p);
-  double *qst[2], *yst[2];
-  qst[0] = qsm;
-  yst[0] = qst[0] + (size_t)tr * ldqs;
-  qst[1] = yst[0] + (size_t)tr * b;
-  yst[1] = qst[1] + (size_t)tr * ldqs;
-  double *ts = yst[1] + (size_t)tr * b;     // [tr][ldt]
-  double *xs = ts + (size_t)tr * ldt;       // [c0][b]
-  double *ras = xs + (size_t)c0 * b;        // [b][b]
-  double *rbs = ras + b * b;                // [b][b]
-  const int tid = threadIdx.x;
-  for (int i = tid; i < c0 * b; i += kQbThreads) xs[i] = a.x ? a.x[i] : 0.0;
-  for (int i = tid; i < b * b; i += kQbThreads) {
-    ras[i] = a.ra ? a.ra[i] : 0.0;
-    rbs[i] = a.rb ? a.rb[i] : 0.0;
-  }
-  const int ncat = c0 + b;
-  double acc[2][kQbMaxB];
-#pragma unroll
-  for (int u = 0; u < 2; ++u)
-#pragma unroll
-    for (int i = 0; i < kQbMaxB; ++i) acc[u][i] = 0.0;
-
+// One sweep over the rows in tiles of tr. Thread 0 streams each tile's Q
+// slabs and y rows into a two- or three-stage ring (tensor-map boxes; the
+// contiguous y scratch as one bulk copy); a stage is refilled as soon as
+// the tile it held is done. KIND (compile time): kX t -= Q X, kP reduce
+// t^T Q, kW reduce t^T t, kOut write t. Per tile:
+//   A. t = y M - Q X on the fp64 tensor cores (DMMA m16n8k4): one task per
+//      (16-row tile, 8-column half of b), K = b (padded to 4) then c0; the
+//      task writes its fragments to the output rows and to the t tile;
+//   B. accumulate t^T [Q | t] (M = b padded to 16, N = 8-column tiles,
+//      K = the tile's rows): the Q part in ceil(c0 / 8) column tiles, the t
+//      part in NH tiles after them, dealt to the warps; with fewer tiles than
+//      warps the rows are split over the warps (kspl row groups), whose sums
+//      are added in a fixed order at the end.
+constexpr int kQbX = 1, kQbP = 2, kQbW = 4, kQbOut = 8;
+template <int B, int KIND>
+__global__ void __launch_bounds__(kQbThreads, 2) qb_sweep_kernel(const __grid_constant__ CUtensorMap tq,
+                                                                 const __grid_constant__ CUtensorMap ty,
+                                                                 const QbSweepArgs a) {
+  extern __shared__ __align__(1024) uint8_t qsm_raw[];
+  // 1024-byte aligned base by offset arithmetic on the shared pointer (an
+  // integer round trip would hide the address space: generic loads)
+  uint8_t *qsm = qsm_raw + ((1024u - (ptx::smem_u32(qsm_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t full[kQbMaxStages];
+  constexpr int b = B;
+  constexpr int NH = B > 8 ? 2 : 1;  // 8-column halves of b
+  constexpr int KM = (B + 3) & ~3;   // rows of M in the operand block
+  constexpr bool HX = KIND & kQbX, WP = KIND & kQbP, WW = KIND & kQbW, WO = KIND & kQbOut;
+  const int c0 = a.c0, tr = a.tr, nslab = a.nslab, nst = a.stages;
+  const int c04 = (c0 + 3) & ~3, kb = qb_kb(c0, b);
+  const size_t sbytes = qb_stage_bytes(nslab, b, tr);
+  const size_t qbytes = (size_t)nslab * tr * 128;
+  double *ts = reinterpret_cast<double *>(qsm + nst * sbytes);  // [tr][kQbLdt]
+  double *ws = ts + (size_t)tr * kQbLdt;                        // [kb][kQbLdw]: M rows [0, KM), -X rows [KM, kb)
+  double *red = ws + (size_t)kb * kQbLdw;                       // [warps][32][4] end-of-sweep sums
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, fg = lane >> 2, ft = lane & 3;
   const int64_t ntiles = (a.m + tr - 1) / tr;
-  auto issue = [&](int64_t tile, int st) {  // tile -> stage st (rows past m read as zeros)
+  if (tid == 0) {
+    for (int s = 0; s < nst; ++s) ptx::mbar_init(&full[s], 1);
+    ptx::fence_mbar_init();
+  }
+  for (int i = tid; i < kb * kQbLdw; i += kQbThreads) {
+    const int k = i / kQbLdw, j = i - k * kQbLdw;
+    double v = 0.0;
+    if (k < KM) {
+      if (k < b && j < b) v = a.mt ? a.mt[k * b + j] : (k == j ? 1.0 : 0.0);
+    } else if (HX && k - KM < c0 && j < b) {
+      v = -a.x[(k - KM) * b + j];
+    }
+    ws[i] = v;
+  }
+  for (int i = tid; i < tr * kQbLdt; i += kQbThreads) ts[i] = 0.0;
+  __syncthreads();
+  auto issue = [&](int it) {  // tile `it` of this CTA -> stage it % nst
+    const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
     if (tile >= ntiles) return;
-    const int64_t row0 = tile * tr;
-    const int rows = (int)(a.m - row0 < (int64_t)tr ? a.m - row0 : (int64_t)tr);
-    if (need_q) {
-      for (int i = tid; i < tr * c0; i += kQbThreads) {
-        const int r = i / c0, k = i - r * c0;
-        if (r < rows) cp_async8(qst[st] + r * ldqs + k, a.q + (row0 + r) * a.ldq + k);
-        else qst[st][r * ldqs + k] = 0.0;
-      }
-    }
-    for (int i = tid; i < tr * b; i += kQbThreads) {
-      const int r = i / b, j = i - r * b;
-      if (r < rows) cp_async8(yst[st] + r * b + j, a.yin + (row0 + r) * a.ldy + j);
-      else yst[st][r * b + j] = 0.0;
-    }
+    const int s = it % nst;
+    uint8_t *st = qsm + s * sbytes;
+    const int y0 = (int)(tile * tr);
+    const int rows = (int)(a.m - y0 < (int64_t)tr ? a.m - y0 : (int64_t)tr);
+    // tensor-map boxes arrive whole (rows past m as zeros); the bulk copy
+    // takes the valid rows only (consumers mask the rest)
+    const uint32_t ybytes = a.y1d ? (uint32_t)rows * b * 8 : (uint32_t)tr * b * 8;
+    ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)qbytes + ybytes);
+    for (int j = 0; j < nslab; ++j) ptx::tma_load_2d(st + (size_t)j * tr * 128, &tq, &full[s], 16 * j, y0);
+    if (a.y1d)
+      ptx::bulk_load(st + qbytes, a.y1d + (size_t)y0 * b, ybytes, &full[s]);
+    else
+      ptx::tma_load_2d(st + qbytes, &ty, &full[s], 0, y0);
   };
-  int st = 0;
-  issue(blockIdx.x, 0);
-  cp_async_commit();
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, st ^= 1) {
-    issue(tile + gridDim.x, st ^ 1);  // the other stage was released by the last barrier
-    cp_async_commit();
-    cp_async_wait1();                 // this tile's group has landed (for this thread)
-    __syncthreads();                  // ... and for every thread
+  if (tid == 0)
+    for (int it = 0; it < nst; ++it) issue(it);
+
+  // column tiles of the reduction: [0, ntq) Q columns 8 nt.., [ntq, ntq + NH) t columns
+  const int ntq = WP ? (c0 + 7) / 8 : 0;
+  const int nlive = ntq + (WW ? NH : 0);
+  const int kspl = nlive >= kQbWarps ? 1 : (nlive >= 4 ? 2 : (nlive >= 2 ? 4 : 8));  // row groups
+  const int cgs = kQbWarps / kspl;                                                  // column-tile stride
+  const int rsub = warp % kspl, cg = warp / kspl;
+  double acc[kQbNtw][4];
+#pragma unroll
+  for (int u = 0; u < kQbNtw; ++u)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[u][i] = 0.0;
+
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = it % nst;
+    ptx::mbar_wait(&full[s], (it / nst) & 1);
+    const uint8_t *qs = qsm + s * sbytes;
+    const double *ys = reinterpret_cast<const double *>(qs + qbytes);
     const int64_t row0 = tile * tr;
     const int rows = (int)(a.m - row0 < (int64_t)tr ? a.m - row0 : (int64_t)tr);
-    const double *qs = qst[st], *ys = yst[st];
-    for (int r = tid; r < tr; r += kQbThreads) {  // triangular solves: one thread per row
-      double t[kQbMaxB];
+    // A. t = y M - Q X
+    for (int task = warp; task < (tr / 16) * NH; task += kQbWarps) {
+      const int rt = task / NH, nh = task - rt * NH;
+      const int r0 = rt * 16 + fg, col = 8 * nh + fg;
+      double d[4][4] = {};  // four independent accumulation chains, summed in a fixed order
 #pragma unroll
-      for (int j = 0; j < kQbMaxB; ++j) t[j] = j < b ? ys[r * b + j] : 0.0;
-      if (a.ra) qb_rsolve(t, ras, b);
-      if (a.rb) qb_rsolve(t, rbs, b);
+      for (int k = 0; k < KM; k += 4) {  // y M (K = b padded to 4)
+        const int kk = k + ft;
+        const double a0 = kk < b && r0 < rows ? ys[r0 * b + kk] : 0.0;
+        const double a1 = kk < b && r0 + 8 < rows ? ys[(r0 + 8) * b + kk] : 0.0;
+        qb_dmma(d[(k >> 2) & 3], a0, a1, ws[kk * kQbLdw + col]);
+      }
+      if (HX) {  // - Q X
+        const double *wx = ws + (size_t)(KM + ft) * kQbLdw + col;
+        int k = 0;
+        for (; k + 16 <= c04; k += 16) {
 #pragma unroll
-      for (int j = 0; j < kQbMaxB; ++j)
-        if (j < b) ts[r * ldt + j] = r < rows ? t[j] : 0.0;
-    }
-    if (a.x && c0 > 0) {  // t -= Q x: (row, column) pairs over all threads
-      __syncthreads();
-      for (int i = tid; i < tr * b; i += kQbThreads) {
-        const int r = i / b, j = i - r * b;
-        const double *qr = qs + r * ldqs;
-        double s = 0.0;
-        for (int k = 0; k < c0; ++k) s = fma(qr[k], xs[k * b + j], s);
-        ts[r * ldt + j] -= s;  // only this thread touches (r, j)
+          for (int c = 0; c < 4; ++c) {
+            const int kc = k + 4 * c + ft;
+            qb_dmma(d[c], qb_qs(qs, tr, r0, kc), qb_qs(qs, tr, r0 + 8, kc), wx[(k + 4 * c) * kQbLdw]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {  // the last K steps (fewer than 16)
+          if (k + 4 * c < c04) {
+            const int kc = k + 4 * c + ft;
+            qb_dmma(d[c], qb_qs(qs, tr, r0, kc), qb_qs(qs, tr, r0 + 8, kc), wx[(k + 4 * c) * kQbLdw]);
+          }
+        }
+      }
+      double v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = (d[0][q] + d[1][q]) + (d[2][q] + d[3][q]);
+      const int cc = 8 * nh + 2 * ft;  // this lane's two columns; rows r0 and r0 + 8
+      double *t0 = ts + (size_t)r0 * kQbLdt + cc;
+      t0[0] = v[0];
+      t0[1] = v[1];
+      t0[8 * kQbLdt] = v[2];
+      t0[8 * kQbLdt + 1] = v[3];
+      if (WO && cc < b) {  // b is even: both columns are real
+        if (r0 < rows) *reinterpret_cast<double2 *>(a.out + (row0 + r0) * a.ldo + cc) = make_double2(v[0], v[1]);
+        if (r0 + 8 < rows)
+          *reinterpret_cast<double2 *>(a.out + (row0 + r0 + 8) * a.ldo + cc) = make_double2(v[2], v[3]);
       }
     }
-    __syncthreads();
-    if (a.out) {
-      for (int i = tid; i < rows * b; i += kQbThreads) {
-        const int r = i / b, j = i - r * b;
-        a.out[(row0 + r) * a.ldo + j] = ts[r * ldt + j];
-      }
-    }
-    if (a.want_p || a.want_w) {  // thread owns columns k = tid, tid + 256 of [Q | t]
+    if (WP || WW) {
+      __syncthreads();  // t complete
+      // B. acc[u] += t^T [Q | t], column tile cg + u cgs of this warp, its row group
+#pragma unroll 2
+      for (int r = 4 * rsub; r < tr; r += 4 * kspl) {
+        const double a0 = ts[(r + ft) * kQbLdt + fg], a1 = B > 8 ? ts[(r + ft) * kQbLdt + fg + 8] : 0.0;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int k = tid + u * kQbThreads;
-        if (k >= ncat) continue;
-        const bool isq = k < c0;
-        if ((isq && !a.want_p) || (!isq && !a.want_w)) continue;
-        for (int r = 0; r < rows; ++r) {
-          const double cv = isq ? qs[r * ldqs + k] : ts[r * ldt + (k - c0)];
-          const double *tr_ = ts + r * ldt;
-#pragma unroll
-          for (int i = 0; i < kQbMaxB; ++i)
-            if (i < b) acc[u][i] = fma(tr_[i], cv, acc[u][i]);
+        for (int u = 0; u < kQbNtw; ++u) {
+          const int nt = cg + u * cgs;
+          if (nt >= nlive) break;
+          const double bv = nt < ntq ? qb_qs(qs, tr, r + ft, nt * 8 + fg)
+                                     : ts[(r + ft) * kQbLdt + (nt - ntq) * 8 + fg];
+          qb_dmma(acc[u], a0, a1, bv);
         }
       }
     }
-    __syncthreads();  // stage st and ts are free for the next issue / tile
+    __syncthreads();  // every warp is done with stage s and ts: refill the stage
+    if (tid == 0) issue(it + nst);
   }
-  if (a.want_p || a.want_w) {
-    double *p = a.part + (size_t)blockIdx.x * b * ncat;
+  if (!(WP || WW)) return;
+  // this CTA's partial [t^T Q | t^T t] (b x (c0 + b)): the row groups of a
+  // column tile added in the fixed order rsub = 0, 1, .. (one owned tile
+  // per round through shared memory)
+  const int ncat = c0 + b;
+  double *p = a.part + (size_t)blockIdx.x * b * ncat;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int k = tid + u * kQbThreads;
-      if (k >= ncat) continue;
-      for (int i = 0; i < b; ++i) p[(size_t)i * ncat + k] = acc[u][i];
+  for (int u = 0; u < kQbNtw; ++u) {
+    if (u * cgs >= nlive) break;  // uniform over the CTA
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red[(warp * 32 + lane) * 4 + q] = acc[u][q];
+    __syncthreads();
+    const int nt = cg + u * cgs;
+    if (rsub == 0 && nt < nlive) {
+      double v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        v[q] = 0.0;
+        for (int g = 0; g < kspl; ++g) v[q] += red[((warp + g) * 32 + lane) * 4 + q];
+      }
+      // columns of [Q | t]: Q tiles cover [8 nt, 8 nt + 8) (only < c0 kept),
+      // t tiles cover t columns [8 (nt - ntq), ..) (only < b kept)
+      const bool isq = nt < ntq;
+      const int kc = (isq ? nt : nt - ntq) * 8 + 2 * ft, lim = isq ? c0 : b, off = isq ? 0 : c0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = fg + 8 * h;
+        if (i >= b) continue;
+        if (kc < lim) p[(size_t)i * ncat + off + kc] = v[2 * h];
+        if (kc + 1 < lim) p[(size_t)i * ncat + off + kc + 1] = v[2 * h + 1];
+      }
     }
+    __syncthreads();
   }
 }
 
-// red[i][k] = sum over the parts in order (fixed-order, deterministic);
-// xt (optional): c0 x b transpose of the t^T Q part, the next sweep's x
-__global__ void qb_reduce_kernel(const double *__restrict__ part, int nparts, int b, int ncat, double *red,
-                                 double *xt, int c0) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= b * ncat) return;
-  double s = 0.0;
-  for (int z = 0; z < nparts; ++z) s += part[(size_t)z * b * ncat + e];
-  red[e] = s;
-  const int i = e / ncat, k = e - i * ncat;
-  if (xt && k < c0) xt[(size_t)k * b + i] = s;
+// red[e] = sum of part[z][e] over z in a fixed order: a block takes 32
+// entries, its 8 warps the parts z = w (mod 8), each lane summing its
+// entry's parts in order; the 8 partial sums are combined pairwise in a
+// fixed tree (deterministic). Only the entries of the sweep's reduced
+// columns are meaningful. xt (optional): c0 x b transpose of the t^T Q part,
+// the next sweep's X.
+__global__ void __launch_bounds__(256) qb_reduce_kernel(const double *__restrict__ part, int nparts, int b,
+                                                        int ncat, double *red, double *xt, int c0) {
+  __shared__ double sh[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  const int ne = b * ncat;
+  double s0 = 0.0, s1 = 0.0;
+  if (e < ne) {
+    int z = w;
+    for (; z + 8 < nparts; z += 16) {  // two loads in flight per lane
+      s0 += part[(size_t)z * ne + e];
+      s1 += part[(size_t)(z + 8) * ne + e];
+    }
+    if (z < nparts) s0 += part[(size_t)z * ne + e];
+  }
+  sh[w][lane] = s0 + s1;
+  __syncthreads();
+  if (w == 0 && e < ne) {
+    const double v = ((sh[0][lane] + sh[1][lane]) + (sh[2][lane] + sh[3][lane])) +
+                     ((sh[4][lane] + sh[5][lane]) + (sh[6][lane] + sh[7][lane]));
+    red[e] = v;
+    const int i = e / ncat, k = e - i * ncat;
+    if (xt && k < c0) xt[(size_t)k * b + i] = v;
+  }
 }
 
-// upper Cholesky W = R^T R of a b x b symmetric matrix (row-major); false
-// when W is not numerically positive definite (cholesky_ex info != 0)
-__device__ bool qb_chol_upper(const double *w, int ldw, double *r, int b) {
-  for (int i = 0; i < b * b; ++i) r[i] = 0.0;
+// ------------------------------------------------- b x b algebra (one warp)
+// upper Cholesky W = R^T R (row-major b x b in shared memory); false when W
+// is not numerically positive definite (cholesky_ex info != 0)
+__device__ bool qb_chol_upper_w(const double *w, double *r, int b) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < b * b; e += 32) r[e] = 0.0;
+  __syncwarp();
+  bool ok = true;
   for (int j = 0; j < b; ++j) {
-    double d = w[j * ldw + j];
-    for (int k = 0; k < j; ++k) d = fma(-r[k * b + j], r[k * b + j], d);
-    if (!(d > 0.0)) return false;
-    const double rjj = sqrt(d);
-    r[j * b + j] = rjj;
-    for (int i = j + 1; i < b; ++i) {
-      double s = w[j * ldw + i];
+    if (lane == 0) {
+      double d = w[j * b + j];
+      for (int k = 0; k < j; ++k) d = fma(-r[k * b + j], r[k * b + j], d);
+      r[j * b + j] = d > 0.0 ? sqrt(d) : nan("");
+    }
+    __syncwarp();
+    const double rjj = r[j * b + j];
+    ok = ok && rjj > 0.0;
+    const int i = j + 1 + lane;
+    if (i < b) {
+      double s = w[j * b + i];
       for (int k = 0; k < j; ++k) s = fma(-r[k * b + j], r[k * b + i], s);
       r[j * b + i] = s / rjj;
     }
+    __syncwarp();
   }
-  return true;
+  return ok;
 }
-
-// c = a b for upper triangular b x b matrices (row-major)
-__device__ void qb_mul_upper(const double *x, const double *y, double *c, int b) {
-  for (int i = 0; i < b; ++i)
-    for (int j = 0; j < b; ++j) {
+// c = x y for upper triangular b x b matrices
+__device__ void qb_mul_upper_w(const double *x, const double *y, double *c, int b) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < b * b; e += 32) {
+    const int i = e / b, j = e - i * b;
+    double s = 0.0;
+    for (int k = i; k <= j; ++k) s = fma(x[i * b + k], y[k * b + j], s);
+    c[e] = j >= i ? s : 0.0;
+  }
+  __syncwarp();
+}
+// ri = r^-1 (upper triangular): lane j solves r x = e_j by back substitution
+__device__ void qb_inv_upper_w(const double *r, double *ri, int b) {
+  const int j = threadIdx.x & 31;
+  if (j < b) {
+    double x[kQbMaxB];
+#pragma unroll
+    for (int i = 0; i < kQbMaxB; ++i) x[i] = 0.0;
+    x[j] = 1.0 / r[j * b + j];
+    for (int i = j - 1; i >= 0; --i) {
       double s = 0.0;
-      for (int k = i; k <= j; ++k) s = fma(x[i * b + k], y[k * b + j], s);
-      c[i * b + j] = j >= i ? s : 0.0;
+      for (int k = i + 1; k <= j; ++k) s = fma(r[i * b + k], x[k], s);
+      x[i] = -s / r[i * b + i];
     }
+    for (int i = 0; i < b; ++i) ri[i * b + j] = x[i];
+  }
+  __syncwarp();
 }
 
-// Small b x b algebra between sweeps (one thread; b <= 16). `st` holds the
-// block's factors: [R1 | R2 | r_i | R3 | R4 | R_i], each b x b.
-//  op 1: R1 = chol(W)
+// Small b x b algebra between sweeps (b <= 16, one warp). `st` holds the
+// block's matrices, each b x b row-major:
+//   [0] R1  [1] R2  [2] r_i = R2 R1  [3] R3  [4] R4  [5] R_i = R4 R3 r_i
+//   [6] R1^-1  [7] R1^-1 R2^-1  [8] R3^-1  [9] R3^-1 R4^-1
+//  op 1: R1 = chol(W), [6]
 //  op 2: CholeskyQR2 test on W = Q1^T Q1 (max |W - I| < 1e-5), R2 = chol(W),
-//        r_i = R2 R1, deficiency test |r_i,jj| >= tol (qb.py:100)
-//  op 3: R3 = chol(W)
-//  op 4: test on W = Z1^T Z1, R4 = chol(W), R_i = (R4 R3) r_i, singularity
-//        guard on diag(R_i) (linalg.py:131-135)
-__global__ void qb_small_kernel(int op, int b, int ncat, int c0, const double *red, double *st, int *flag,
+//        r_i, [7], deficiency test |r_i,jj| >= tol (qb.py:100)
+//  op 3: R3 = chol(W), [8]
+//  op 4: test on W = Z1^T Z1, R4 = chol(W), R_i, [9], singularity guard on
+//        diag(R_i) (linalg.py:131-135)
+__global__ void qb_small_kernel(int op, int b, int ncat, int c0, const double *redm, double *st, int *flag,
                                 const double *tol) {
-  if (threadIdx.x != 0) return;
-  const double *w = red + c0;  // the t^T t block of the reduced [t^T Q | t^T t]
-  const int bb = b * b;
-  double *R1 = st, *R2 = st + bb, *ri = st + 2 * bb, *R3 = st + 3 * bb, *R4 = st + 4 * bb, *Ri = st + 5 * bb;
+  __shared__ double w[kQbMaxB * kQbMaxB], f[10][kQbMaxB * kQbMaxB], tmp[kQbMaxB * kQbMaxB];
+  const int bb = b * b, lane = threadIdx.x & 31;
+  for (int e = lane; e < bb; e += 32) {
+    w[e] = redm[(size_t)(e / b) * ncat + c0 + e % b];  // the t^T t block of [t^T Q | t^T t]
+    for (int q = 0; q < 10; ++q) f[q][e] = st[q * bb + e];
+  }
+  __syncwarp();
   bool ok = true;
   if (op == 1 || op == 3) {
-    ok = qb_chol_upper(w, ncat, op == 1 ? R1 : R3, b);
+    double *R = op == 1 ? f[0] : f[3];
+    ok = qb_chol_upper_w(w, R, b);
+    qb_inv_upper_w(R, op == 1 ? f[6] : f[8], b);
   } else {
     double defect = 0.0;
-    for (int i = 0; i < b; ++i)
-      for (int j = 0; j < b; ++j) defect = fmax(defect, fabs(w[i * ncat + j] - (i == j ? 1.0 : 0.0)));
+    for (int e = lane; e < bb; e += 32) defect = fmax(defect, fabs(w[e] - (e % (b + 1) == 0 ? 1.0 : 0.0)));
+    for (int o = 16; o > 0; o >>= 1) defect = fmax(defect, __shfl_xor_sync(0xffffffffu, defect, o));
     ok = defect < 1e-5 && isfinite(defect);
-    ok = qb_chol_upper(w, ncat, op == 2 ? R2 : R4, b) && ok;
+    double *R = op == 2 ? f[1] : f[4];
+    ok = qb_chol_upper_w(w, R, b) && ok;
+    qb_inv_upper_w(R, tmp, b);
+    qb_mul_upper_w(op == 2 ? f[6] : f[8], tmp, op == 2 ? f[7] : f[9], b);  // Ra^-1 Rb^-1
     if (op == 2) {
-      qb_mul_upper(R2, R1, ri, b);
-      for (int j = 0; j < b; ++j) ok = ok && isfinite(ri[j * b + j]) && !(fabs(ri[j * b + j]) < *tol);
+      qb_mul_upper_w(f[1], f[0], f[2], b);  // r_i = R2 R1
+      const double tl = *tol;
+      for (int j = lane; j < b; j += 32) {
+        const double d = f[2][j * b + j];
+        ok = ok && isfinite(d) && !(fabs(d) < tl);
+      }
     } else {
-      double rt[kQbMaxB * kQbMaxB];
-      qb_mul_upper(R4, R3, rt, b);
-      qb_mul_upper(rt, ri, Ri, b);
+      qb_mul_upper_w(f[4], f[3], tmp, b);  // Rt = R4 R3
+      qb_mul_upper_w(tmp, f[2], f[5], b);  // R_i = Rt r_i
       double mx = 0.0;
-      for (int j = 0; j < b; ++j) mx = fmax(mx, fabs(Ri[j * b + j]));
-      for (int j = 0; j < b; ++j) {
-        const double d = fabs(Ri[j * b + j]);
+      for (int j = 0; j < b; ++j) mx = fmax(mx, fabs(f[5][j * b + j]));
+      for (int j = lane; j < b; j += 32) {
+        const double d = fabs(f[5][j * b + j]);
         ok = ok && isfinite(d) && !(d < 1e-300) && !(d < 1e-15 * mx);
       }
     }
   }
-  if (!ok) *flag = 1;
+  ok = __all_sync(0xffffffffu, ok);
+  for (int e = lane; e < bb; e += 32)
+    for (int q = 0; q < 10; ++q) st[q * bb + e] = f[q][e];
+  if (lane == 0 && !ok) *flag = 1;
 }
 
 }  // namespace spca

@@ -1195,74 +1195,160 @@ int spca_normalize_rows(const void *src, int64_t rows, int64_t n, int64_t ld_src
 
 // ---------------------------------------------------------------- post-pass
 namespace {
-int qb_rows_per_tile(int c0, int b) {
-  // ~96 KB of [Q | y] per stage (enough bytes in flight per SM for HBM),
-  // within the shared-memory budget at two stages
-  int tr = (int)std::max<int64_t>(16, std::min<int64_t>(256, (96 << 10) / (8 * (int64_t)((c0 | 1) + b))));
-  while (tr > 16 && spca::qb_sweep_smem(c0, b, tr) > (200u << 10)) tr /= 2;
-  return tr;
+// the sweep kernel instantiated for an even block width 2..16 and one of
+// the five sweep kinds of spca_qb_block
+extern "C++" {  // templates inside the extern "C" block
+template <int B>
+const void *qb_kernel_b(int kind) {
+  using namespace spca;
+  switch (kind) {
+    case kQbX | kQbP | kQbW | kQbOut: return (const void *)qb_sweep_kernel<B, kQbX | kQbP | kQbW | kQbOut>;
+    case kQbW: return (const void *)qb_sweep_kernel<B, kQbW>;
+    case kQbP: return (const void *)qb_sweep_kernel<B, kQbP>;
+    case kQbX | kQbW | kQbOut: return (const void *)qb_sweep_kernel<B, kQbX | kQbW | kQbOut>;
+    case kQbW | kQbOut: return (const void *)qb_sweep_kernel<B, kQbW | kQbOut>;
+    default: return (const void *)qb_sweep_kernel<B, kQbOut>;
+  }
 }
-int qb_parts(int64_t m, int tr) {
+const void *qb_kernel(int b, int kind) {
+  switch (b) {
+    case 2: return qb_kernel_b<2>(kind);
+    case 4: return qb_kernel_b<4>(kind);
+    case 6: return qb_kernel_b<6>(kind);
+    case 8: return qb_kernel_b<8>(kind);
+    case 10: return qb_kernel_b<10>(kind);
+    case 12: return qb_kernel_b<12>(kind);
+    case 14: return qb_kernel_b<14>(kind);
+    default: return qb_kernel_b<16>(kind);
+  }
+}
+}  // extern "C++"
+// rows per tile and ring depth: the largest tile (up to 256 rows) whose
+// three-stage ring fits two CTAs per SM (110 KB each), else one CTA per SM
+// (up to 220 KB), else 16 rows and two stages. SPCA_QB_TR / SPCA_QB_ST
+// override (tuning).
+void qb_tiling(int c0, int b, int nslab, int *tr, int *stages) {
+  static const int env_tr = getenv("SPCA_QB_TR") ? atoi(getenv("SPCA_QB_TR")) : 0;
+  static const int env_st = getenv("SPCA_QB_ST") ? atoi(getenv("SPCA_QB_ST")) : 0;
+  if (env_tr >= 16 && env_tr % 16 == 0 && env_tr <= 256 && (env_st == 2 || env_st == 3) &&
+      spca::qb_sweep_smem(c0, b, env_tr, nslab, env_st) <= (220u << 10)) {
+    *tr = env_tr;
+    *stages = env_st;
+    return;
+  }
+  for (size_t cap : {(size_t)110 << 10, (size_t)220 << 10})
+    for (int t : {256, 128, 64, 32, 16})
+      for (int st : {3, 2})
+        if (spca::qb_sweep_smem(c0, b, t, nslab, st) <= cap) {
+          *tr = t;
+          *stages = st;
+          return;
+        }
+  *tr = 16;
+  *stages = 2;
+}
+constexpr int kQbMaxOcc = 4;  // resident sweep CTAs per SM counted for the partials (bound)
+// CTAs of one sweep: one wave of resident CTAs of that kernel and tiling
+// (the kernel loops over row tiles); raises the kernels' shared-memory limit
+int qb_parts(int64_t m, int c0, int b, int nslab, int kind, int tr, int stages) {
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const void *kern = qb_kernel(b, kind);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 << 10);
+  cudaGetLastError();  // a refused attribute must not surface as the next launch's error
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, spca::kQbThreads,
+                                                    spca::qb_sweep_smem(c0, b, tr, nslab, stages)) != cudaSuccess)
+    occ = 1;
+  occ = std::max(1, std::min(kQbMaxOcc, occ));
   const int64_t tiles = (m + tr - 1) / tr;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * 148));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * occ));
+}
+// 2-D fp64 tensor map over rows of a row-major matrix (TMA), box {bi, bo}
+bool qb_map(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t bi,
+            uint32_t bo, bool swz) {
+  EncodeTiledFn enc = tma_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {bi, bo};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 }  // namespace
 
 int64_t spca_qb_workspace_elems(int64_t m, int c0_max, int b) {
   if (m < 1 || c0_max < 0 || b < 1) return 0;
-  int64_t most = 0;
-  for (int c0 = 0; c0 <= c0_max; c0 += b) {  // partials of the widest sweep, the reduced sums, x
-    const int ncat = c0 + b;
-    most = std::max<int64_t>(most, (int64_t)qb_parts(m, qb_rows_per_tile(c0, b)) * b * ncat);
-  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // partials of the widest sweep (at most kQbMaxOcc CTAs per SM), the reduced sums, x
+  const int64_t most = (int64_t)sms * kQbMaxOcc * b * (c0_max + b);
   return most + (int64_t)b * (c0_max + b) + (int64_t)c0_max * b + 64;
 }
 
 int spca_qb_block(int64_t m, int c0, int b, double *q, int64_t ldq, const double *g, int64_t ldg,
                   const double *x, double *ybuf, double *ws, int64_t ws_elems, double *p_out,
                   double *factors, int *flag, const double *tol, void *stream) {
-  if (m < 1 || c0 < 0 || b < 1 || b > spca::kQbMaxB || c0 + b > spca::kQbMaxCat || ldq < c0 + b || ldg < b)
-    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "qb_block: unsupported shape m %lld c0 %d b %d", (long long)m,
-                   c0, b);
+  if (m < 1 || m > INT32_MAX || c0 < 0 || b < 2 || b > spca::kQbMaxB || (b & 1) || (c0 & 1) ||
+      c0 + b > spca::kQbMaxCat || ldq < c0 + b || (ldq & 1) || ldg < b || (ldg & 1))
+    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "qb_block: unsupported shape m %lld c0 %d b %d ldq %lld",
+                   (long long)m, c0, b, (long long)ldq);
   if (!q || !g || !ybuf || !ws || !p_out || !factors || !flag || !tol || (c0 > 0 && !x))
     return set_err(nullptr, SPCA_ERR_STATE, -1, "qb_block: null pointer");
+  if (((uintptr_t)q | (uintptr_t)g | (uintptr_t)ybuf) & 15)
+    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "qb_block: operands must be 16-byte aligned");
   if (ws_elems < spca_qb_workspace_elems(m, c0, b))
     return set_err(nullptr, SPCA_ERR_CONFIG, -1, "qb_block: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
-  const int tr = qb_rows_per_tile(c0, b);
-  const int parts = qb_parts(m, tr);
   const int ncat = c0 + b;
-  const size_t smem = spca::qb_sweep_smem(c0, b, tr);
-  cudaError_t e = cudaFuncSetAttribute(spca::qb_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return set_err(nullptr, SPCA_ERR_CUDA, -1, "qb_block smem: %s", cudaGetErrorString(e));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   double *part = ws;
-  double *red = part + (size_t)parts * b * ncat;  // b x ncat
-  double *xt = red + (size_t)b * ncat;            // c0 x b
-  const int bb = b * b;
-  double *R1 = factors, *R2 = factors + bb, *R3 = factors + 3 * bb, *R4 = factors + 4 * bb;
-  const unsigned rblocks = (unsigned)ceil_div((int64_t)b * ncat, 256);
-  auto sweep = [&](const double *yin, int64_t ldy, const double *ra, const double *rb, const double *xx,
-                   double *out, int64_t ldo, int wp, int ww) -> cudaError_t {
+  double *red = part + (size_t)sms * kQbMaxOcc * b * ncat;  // b x ncat
+  double *xt = red + (size_t)b * ncat;                      // c0 x b
+  int parts = 1;  // of the last sweep (its reduction)
+  const int bb = b * b;  // factors: see qb_small_kernel
+  double *M1 = factors + 6 * bb, *M12 = factors + 7 * bb, *M3 = factors + 8 * bb, *M34 = factors + 9 * bb;
+  const unsigned rblocks = (unsigned)ceil_div((int64_t)b * ncat, 32);
+  // from_g: the sweep's y rows are G_i (tensor map, row stride ldg), else the
+  // contiguous scratch ybuf (one bulk copy per tile)
+  auto sweep = [&](bool from_g, const double *mt, const double *xx, double *out, int64_t ldo, int wp,
+                   int ww) -> cudaError_t {
     spca::QbSweepArgs a{};
+    const bool need_q = c0 > 0 && (xx != nullptr || wp);
+    const int nslab = need_q ? (c0 + 15) / 16 : 0;
+    const int kind = (xx ? spca::kQbX : 0) | (wp ? spca::kQbP : 0) | (ww ? spca::kQbW : 0) | (out ? spca::kQbOut : 0);
+    int tr = 16, stages = 2;
+    qb_tiling(c0, b, nslab, &tr, &stages);
+    parts = qb_parts(m, c0, b, nslab, kind, tr, stages);
     a.m = m;
     a.c0 = c0;
     a.b = b;
     a.tr = tr;
-    a.q = c0 ? q : nullptr;
-    a.ldq = ldq;
-    a.yin = yin;
-    a.ldy = ldy;
-    a.ra = ra;
-    a.rb = rb;
+    a.stages = stages;
+    a.nslab = nslab;
+    a.mt = mt;
+    a.y1d = from_g ? nullptr : ybuf;  // ybuf is m x b contiguous
+    CUtensorMap tq, ty;  // boxes of tr rows (the Q map also stands in for an unused y map)
+    if (!qb_map(&tq, q, (uint64_t)ldq, (uint64_t)m, (uint64_t)ldq * 8, 16, (uint32_t)tr, true))
+      return cudaErrorInvalidValue;
+    if (from_g) {
+      if (!qb_map(&ty, g, (uint64_t)b, (uint64_t)m, (uint64_t)ldg * 8, (uint32_t)b, (uint32_t)tr, false))
+        return cudaErrorInvalidValue;
+    } else {
+      ty = tq;
+    }
     a.x = xx;
     a.out = out;
     a.ldo = ldo;
-    a.want_p = wp;
-    a.want_w = ww;
     a.part = part;
-    spca::qb_sweep_kernel<<<parts, spca::kQbThreads, smem, st>>>(a);
-    return cudaGetLastError();
+    const size_t smem = spca::qb_sweep_smem(c0, b, tr, a.nslab, stages);
+    void *args[] = {(void *)&tq, (void *)&ty, (void *)&a};
+    return cudaLaunchKernel(qb_kernel(b, kind), dim3(parts), dim3(spca::kQbThreads), args, smem, st);
   };
   auto reduce = [&](double *dst, double *xtrans) -> cudaError_t {
     spca::qb_reduce_kernel<<<rblocks, 256, 0, st>>>(part, parts, b, ncat, dst, xtrans, c0);
@@ -1272,34 +1358,36 @@ int spca_qb_block(int64_t m, int c0, int b, double *q, int64_t ldq, const double
     spca::qb_small_kernel<<<1, 32, 0, st>>>(op, b, ncat, c0, r, factors, flag, tol);
     return cudaGetLastError();
   };
+  static const bool sync_each = getenv("SPCA_QB_SYNC") != nullptr;  // debugging: fault localisation
 #define QB_TRY(call)                                                                             \
   do {                                                                                           \
     cudaError_t _e = (call);                                                                     \
+    if (_e == cudaSuccess && sync_each) _e = cudaStreamSynchronize(st);                          \
     if (_e != cudaSuccess)                                                                       \
       return set_err(nullptr, SPCA_ERR_CUDA, -1, "qb_block %s: %s", #call, cudaGetErrorString(_e)); \
   } while (0)
   // S1: y = G_i - Q X; [y^T Q | y^T y] (kept for the B update)
-  QB_TRY(sweep(g, ldg, nullptr, nullptr, c0 ? x : nullptr, ybuf, b, 1, 1));
+  QB_TRY(sweep(true, nullptr, c0 ? x : nullptr, ybuf, b, c0 ? 1 : 0, 1));
   QB_TRY(reduce(p_out, nullptr));
   QB_TRY(small(1, p_out));
   // S2: Q1 = y R1^-1, Q1^T Q1
-  QB_TRY(sweep(ybuf, b, R1, nullptr, nullptr, nullptr, 0, 0, 1));
+  QB_TRY(sweep(false, M1, nullptr, nullptr, 0, 0, 1));
   QB_TRY(reduce(red, nullptr));
   QB_TRY(small(2, red));
-  if (c0 > 0) {  // S3: Q^T Q2 (Q2 = Q1 R2^-1), kept transposed as the next x
-    QB_TRY(sweep(ybuf, b, R1, R2, nullptr, nullptr, 0, 1, 0));
+  if (c0 > 0) {  // S3: Q^T Q2 (Q2 = y R1^-1 R2^-1), kept transposed as the next X
+    QB_TRY(sweep(false, M12, nullptr, nullptr, 0, 1, 0));
     QB_TRY(reduce(red, xt));
   }
   // S4: z = Q2 - Q (Q^T Q2), z^T z
-  QB_TRY(sweep(ybuf, b, R1, R2, c0 ? xt : nullptr, ybuf, b, 0, 1));
+  QB_TRY(sweep(false, M12, c0 ? xt : nullptr, ybuf, b, 0, 1));
   QB_TRY(reduce(red, nullptr));
   QB_TRY(small(3, red));
   // S5: Z1 = z R3^-1, Z1^T Z1
-  QB_TRY(sweep(ybuf, b, R3, nullptr, nullptr, nullptr, 0, 0, 1));
+  QB_TRY(sweep(false, M3, nullptr, nullptr, 0, 0, 1));
   QB_TRY(reduce(red, nullptr));
   QB_TRY(small(4, red));
-  // S6: Q_i = Z1 R4^-1 into Q's columns [c0, c0 + b)
-  QB_TRY(sweep(ybuf, b, R3, R4, nullptr, q + c0, ldq, 0, 0));
+  // S6: Q_i = z R3^-1 R4^-1 into Q's columns [c0, c0 + b)
+  QB_TRY(sweep(false, M34, nullptr, q + c0, ldq, 0, 0));
 #undef QB_TRY
   return SPCA_OK;
 }
