@@ -40,6 +40,8 @@ if os.environ.get("SPCA_BUILD_PAIRA") is not None:  # experiment: one TMA reques
     FLAGS.append("-DSPCA_PAIRA=" + os.environ["SPCA_BUILD_PAIRA"])
 if os.environ.get("SPCA_BUILD_PROMOTE") is not None:  # experiment: K blocks per accumulator period
     FLAGS.append("-DSPCA_PROMOTE=" + os.environ["SPCA_BUILD_PROMOTE"])
+if os.environ.get("SPCA_BUILD_NSTG") is not None:  # experiment: epilogue staging buffers (l_pad 64)
+    FLAGS.append("-DSPCA_NSTG_64=" + os.environ["SPCA_BUILD_NSTG"])
 if os.environ.get("SPCA_BUILD_STACKED") is not None:  # experiment: l_pad=64 MMA form
     FLAGS.append("-DSPCA_STACKED_64=" + os.environ["SPCA_BUILD_STACKED"])
 

@@ -1,15 +1,18 @@
-// sketch_fused.cuh — the single-read tensor-core sketch pass (sm_100a, fp32).
+// sketch_fused.cuh — the fused tensor-core sketch pass (sm_100a, fp32).
 //
 // One persistent kernel per push walks the pushed rows in canonical chunks of
-// R0 rows small enough to stay resident in the 126 MB L2 (R0 * n * 4 B ~ 40 MB)
-// and computes, per chunk c (reference sketch.py:85-113, paper Alg. 4 steps 5-7):
+// R0 rows (R0 * n * 4 B ~ 40 MB) and computes, per chunk c (reference
+// sketch.py:85-113, paper Alg. 4 steps 5-7):
 //
 //   G_c = A_c Omega          ("G units": 128-row tile x K segment of n)
 //   H  += A_c^T G_c          ("H units": 128-column tile x row segment of R0)
 //   col_sums += 1^T A_c      (inside the H units)
 //
-// A_c is read from HBM once, by the G units (TMA, L2 evict_last); the H units
-// re-read it from L2 one stage later (evict_first). The units form one global
+// A_c is read from HBM by the G units (TMA, L2 evict_last) and re-read by the
+// H units D stages later (evict_first). The re-read is meant to hit L2, but
+// with three 40 MB chunks live it mostly misses: ncu measures ~2.05x the
+// bytes of A read from DRAM at config 2 (8.2 GB per 4 GB pass; 512-row chunks
+// read 1.2x but run slower). The units form one global
 // sequence of stages {G(s), H(s-1)}, s = 0..C, dealt round robin to CTA
 // pairs (clusters of 2, one CTA per SM), so the H contraction of chunk c
 // overlaps the G contraction of chunk c+1 inside one launch and every pair

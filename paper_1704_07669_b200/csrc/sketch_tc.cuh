@@ -96,7 +96,9 @@ constexpr int kPromote = SPCA_PROMOTE;  // K blocks per accumulator period
 // epilogue staging buffers for l_pad = 64. Two (at the cost of two A stages)
 // measured no faster and failed 1 run in 8 (a launch fault not yet understood):
 // kept at one; the staging code is written for either.
+#ifndef SPCA_NSTG_64
 #define SPCA_NSTG_64 1
+#endif
 template <int LPAD>
 struct TcCfg {
   static_assert(LPAD == 64 || LPAD == 128, "tensor-core path covers l <= 128");

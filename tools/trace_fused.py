@@ -84,6 +84,9 @@ for cta in range(len(t)):
     for i in range(UNITS):
         uu = (cta // 2) + i * ncl
         kinds[cta, i] = kind_of(sc, uu)[0]
+mmv = (u[:, :, 5] > 0) & (u[:, :, 6] > 0)
+for k, nm in ((0, "G"), (1, "H")):
+    stat(f"{nm} units: MMA issue span (leader)", np.where(mmv & (kinds == k), u[:, :, 6] - u[:, :, 5], np.nan).ravel())
 for k, nm in ((0, "G"), (1, "H")):
     sel = valid & (kinds == k)
     stat(f"{nm} units: converter main loop", np.where(sel, u[:, :, 1] - u[:, :, 0], np.nan).ravel())
