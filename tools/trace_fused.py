@@ -50,9 +50,9 @@ stat("B producer dep-wait end - conv start", np.where(valid & (u[:, :, 7] > 0), 
 
 # per unit kind (replicates fused_decode for the single launch of this run)
 def sched(m, n, R0, U=32):
-    nkb = -(-n // 32); S = -(-nkb // U); kseg = -(-nkb // S); S = -(-nkb // kseg)
+    nkb = -(-n // 32); S = min(-(-nkb // U), 37); kseg = -(-nkb // S); S = -(-nkb // kseg)
     nt = R0 // 128; T = nt // 2; nx = -(-n // 128); X = -(-nx // 2)
-    rkb = R0 // 32; RS = -(-rkb // U); hseg = -(-rkb // RS); RS = -(-rkb // hseg)
+    rkb = R0 // 32; RS = -(-rkb // max(U, 48)); hseg = -(-rkb // RS); RS = -(-rkb // hseg)
     C = -(-m // R0); rows_last = m - (C - 1) * R0; ntl = -(-rows_last // 128); Tl = -(-ntl // 2)
     return dict(C=C, T=T, Tl=Tl, S=S, X=X, RS=RS)
 
@@ -79,11 +79,30 @@ def kind_of(s, u):
 R0 = sk.chunk_rows()
 sc = sched(rows, n, R0)
 ncl = len(t) // 2
+
+
+def host_order_kinds(s, lag=float(os.environ.get("SPCA_TC_LAGF", "2.0"))):
+    # the host-built unit order of tc_unit_order (tc_host.cuh): G units of chunk
+    # c at c*P + r, H units at c*P + TS + lag*P + r + 0.25, stable sort
+    TS, XR = s["T"] * s["S"], s["X"] * s["RS"]
+    TlS = s["Tl"] * s["S"]
+    P = TS + XR
+    keys = []
+    for c in range(s["C"]):
+        g = TlS if c == s["C"] - 1 else TS
+        keys += [(c * P + r, 0) for r in range(g)]
+        keys += [(c * P + TS + lag * P + r + 0.25, 1) for r in range(XR)]
+    keys.sort(key=lambda kv: kv[0])
+    return [k for _, k in keys]
+
+
+order = host_order_kinds(sc)
 kinds = np.full(u.shape[:2], -1)
 for cta in range(len(t)):
     for i in range(UNITS):
         uu = (cta // 2) + i * ncl
-        kinds[cta, i] = kind_of(sc, uu)[0]
+        if uu < len(order):
+            kinds[cta, i] = order[uu]
 mmv = (u[:, :, 5] > 0) & (u[:, :, 6] > 0)
 for k, nm in ((0, "G"), (1, "H")):
     stat(f"{nm} units: MMA issue span (leader)", np.where(mmv & (kinds == k), u[:, :, 6] - u[:, :, 5], np.nan).ravel())
