@@ -57,6 +57,10 @@ def gaussian_matrix(rows: int, cols: int, seed: int, stream: int = STREAM_SKETCH
 _DRAW_THREADS = max(1, min(16, os.cpu_count() or 1))
 _DRAW_MIN_PER_THREAD = 1 << 17
 _OVERLAP = 64
+# raw 64-bit draws per value of numpy's ziggurat standard_normal (measured:
+# 1.0220616 over 2e7 values) and the lower-bound margin around the estimate
+_DRAWS_PER_VALUE = 1.02206
+_MARGIN = 1 << 16
 _DRAW_POOL = None  # created on first use, reused by every draw (thread start-up is not free)
 
 
@@ -72,11 +76,13 @@ def _parallel_normals(key, n: int, threads: int):
     bit, drawn by `threads` threads (numpy releases the GIL while it fills).
 
     The ziggurat consumes a variable number of raw 64-bit draws per value
-    (1 on its fast path, ~1.022 on average), so segment t cannot be started at
+    (1 on its fast path, 1.022 on average), so segment t cannot be started at
     its exact counter position. Its thread starts at a lower bound instead —
-    raw draw 4*floor(s_t/4) <= s_t <= the true position of value s_t
-    (Philox.advance moves in blocks of four draws) — and over-generates by the
-    worst expected drift. Every attempt of the ziggurat restarts on a fresh
+    _MARGIN (65 536) raw draws before the expected position 1.022 s_t of value
+    s_t, rounded down to a Philox block of four draws; the spread of the true
+    position is ~sqrt(s_t)/5 draws (~1 500 at 5e7), so the bound holds with a
+    wide margin — and over-generates by 2 _MARGIN (every thread draws about
+    n / threads values). Every attempt of the ziggurat restarts on a fresh
     draw, so the thread's sequence of attempts merges with the true one within
     a few values; segment t - 1 also produces the first _OVERLAP values of
     segment t, and matching that run of doubles locates value s_t in thread
@@ -85,15 +91,19 @@ def _parallel_normals(key, n: int, threads: int):
     seg = -(-n // threads)
     starts = [t * seg for t in range(threads)]
     counts = [min(seg, n - s0) for s0 in starts]
-    lens, outs = [], [None] * threads
+    lens, outs, raw0 = [], [None] * threads, []
     for t, s0 in enumerate(starts):
-        drift = 0 if t == 0 else int(0.04 * s0) + 4096
-        lens.append(drift + counts[t] + _OVERLAP)
+        # value s0 sits near raw draw _DRAWS_PER_VALUE * s0 (std ~ sqrt(s0) / 5):
+        # start _MARGIN draws before that estimate and run 2 _MARGIN past the
+        # segment, so every thread draws about the same number of values
+        r0 = 0 if t == 0 else max(0, int(_DRAWS_PER_VALUE * s0) - _MARGIN) // 4 * 4
+        raw0.append(r0)
+        lens.append(counts[t] + _OVERLAP + (0 if t == 0 else 2 * _MARGIN + 64))
 
     def draw(t):
         bg = np.random.Philox(key=key)
         if t:
-            bg.advance(starts[t] // 4)
+            bg.advance(raw0[t] // 4)
         outs[t] = np.random.Generator(bg).standard_normal(lens[t])
 
     pool = _draw_pool() if threads <= _DRAW_THREADS else ThreadPoolExecutor(threads)
