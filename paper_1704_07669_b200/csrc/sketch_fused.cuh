@@ -834,7 +834,17 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             // partials of other CTAs: read through L2 (.cg), never a stale L1 line
             const float4 *src = reinterpret_cast<const float4 *>(p0 + (size_t)r * LPAD) + q;
             float4 acc = __ldcg(src);
-            for (int z = 1; z < sc.S; ++z) {
+            int z = 1;
+            for (; z + 4 <= sc.S; z += 4) {  // four loads in flight, added in order z
+              float4 b4[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) b4[j] = __ldcg(src + (size_t)(z + j) * 128 * NQ);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                acc.x += b4[j].x; acc.y += b4[j].y; acc.z += b4[j].z; acc.w += b4[j].w;
+              }
+            }
+            for (; z < sc.S; ++z) {
               const float4 b4 = __ldcg(src + (size_t)z * 128 * NQ);
               acc.x += b4.x; acc.y += b4.y; acc.z += b4.z; acc.w += b4.w;
             }
@@ -891,16 +901,28 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             const bool overwrite = !args.accumulate && seq == 0;
             const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF + sb * C::STG_BYTES);
             const int items = min(128, args.n - tile * 128) * NQ;
-#pragma unroll 4
-            for (int it = e; it < items; it += kTcEpi) {
-              const int r = it / NQ, q = it % NQ;
-              float4 w = ptx::lds128(stg0 + r * LPAD * 4 + ((q ^ (r & 7)) << 4));
-              float4 *hp = reinterpret_cast<float4 *>(hp0 + (int64_t)r * args.gld) + q;
-              if (!overwrite) {
-                const float4 o = __ldcg(hp);
-                w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+            // batches of 8 items: the 8 old values are loaded before any store
+            // (a store between loads would serialize them on the L2 round trip:
+            // the compiler cannot tell the rows apart)
+            constexpr int kB = 8;
+            for (int it0 = e; it0 < items; it0 += kB * kTcEpi) {
+              float4 o[kB];
+#pragma unroll
+              for (int j = 0; j < kB; ++j) {
+                const int it = it0 + j * kTcEpi;
+                o[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (!overwrite && it < items)
+                  o[j] = __ldcg(reinterpret_cast<const float4 *>(hp0 + (int64_t)(it / NQ) * args.gld) + it % NQ);
               }
-              *hp = w;
+#pragma unroll
+              for (int j = 0; j < kB; ++j) {
+                const int it = it0 + j * kTcEpi;
+                if (it >= items) break;
+                const int r = it / NQ, q = it % NQ;
+                float4 w = ptx::lds128(stg0 + r * LPAD * 4 + ((q ^ (r & 7)) << 4));
+                w.x += o[j].x; w.y += o[j].y; w.z += o[j].z; w.w += o[j].w;
+                reinterpret_cast<float4 *>(hp0 + (int64_t)r * args.gld)[q] = w;
+              }
             }
           }
           csv = stg_cs[sb][e] + stg_cs[sb][128 + e];
