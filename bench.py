@@ -403,6 +403,24 @@ def run_stream(args):
         ms, wall = float(t[0]), float(t[1])
     ms_step = ms / args.steps
     value = world * m * n * 4 / (ms_step * 1e-3) / 1e9
+    extra = {}
+    if rank == 0 and world == 1 and not (args.no_cpu and args.no_parity):
+        # config-4 prefix: the first P distinct blocks of the host ring (4 GB),
+        # PCA through the streaming path (PinnedRowStream: H2D inside the
+        # pass) against the unmodified reference on the same rows
+        from paper_1704_07669_b200 import PcaConfig, PinnedRowStream, single_pass_pca
+        pblk = min(ring, max(1, (4 << 30) // (B * n * 4)))
+        pre = host[:pblk].reshape(pblk * B, n)
+        cfg = PcaConfig(k=cs["k"], oversample=cs["l"] - cs["k"], seed=1)
+        single_pass_pca(PinnedRowStream(pre), cfg, precision=args.precision, device=dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = single_pass_pca(PinnedRowStream(pre), cfg, precision=args.precision, device=dev)
+        torch.cuda.synchronize()
+        extra["pca_seconds_prefix"] = {"value": time.perf_counter() - t0, "unit": "s", "rows": int(pre.shape[0]),
+                                       "includes": "Omega draw, pass streamed from pinned host memory, QB, SVD, "
+                                                   "U/S/V to host"}
+        extra.update(reference_leg(args, pre, res, cs, what=f"config-4 prefix of {pblk} blocks"))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -426,6 +444,7 @@ def run_stream(args):
                     "h2d_bytes_per_step": m * n * 4, "d2h_bytes_per_step": int(hh.numel() * 8),
                     "seconds_per_step": wall / args.steps},
         }
+        line.update(extra)
         print(json.dumps(line), flush=True)
     if pg is not None:
         pg.destroy_process_group()
@@ -703,7 +722,7 @@ def pca_leg(args, a_dev, dev, pg, world, rank):
     return out, res
 
 
-def reference_leg(args, a_dev, res, cs):
+def reference_leg(args, a_dev, res, cs, what: str = "full config A"):
     """N = 1: the unmodified reference (baseline/_ref) on this host's cores
     over the SAME A (the device matrix copied to the host, fp32 widened to
     fp64 by the reference's ArrayRowStream) and the same seeded Omega:
@@ -749,7 +768,7 @@ def reference_leg(args, a_dev, res, cs):
     out["cpu_baseline"] = {
         "value": m * n * a_dev.element_size() / t_sketch / 1e9, "unit": UNIT, "cores": threads,
         "cores_physical": phys, "kind": "reference", "pass_seconds": t_sketch, "pca_seconds": t_pca,
-        "sample": f"full config A ({m} x {n} {'fp64' if a_dev.element_size() == 8 else 'fp32 widened to fp64'}), "
+        "sample": f"{what} ({m} x {n} {'fp64' if a_dev.element_size() == 8 else 'fp32 widened to fp64'}), "
                   f"unmodified reference streampca (baseline/_ref): sketch_pass("
                   f"{'GeneratorRowStream(fp32 row blocks)' if streamed else 'ArrayRowStream(A)'}, Omega, "
                   f"block_rows={br}) and single_pass_pca(A, PcaConfig(k={cs['k']}, oversample={l - cs['k']}, "
