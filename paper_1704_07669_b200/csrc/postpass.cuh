@@ -308,16 +308,19 @@ __global__ void __launch_bounds__(256) qb_reduce_kernel(const double *__restrict
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int e = blockIdx.x * 32 + lane;
   const int ne = b * ncat;
-  double s0 = 0.0, s1 = 0.0;
+  double s = 0.0;
   if (e < ne) {
     int z = w;
-    for (; z + 8 < nparts; z += 16) {  // two loads in flight per lane
-      s0 += part[(size_t)z * ne + e];
-      s1 += part[(size_t)(z + 8) * ne + e];
+    for (; z + 8 * 7 < nparts; z += 8 * 8) {  // eight loads in flight, added in order
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = part[(size_t)(z + 8 * j) * ne + e];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[j];
     }
-    if (z < nparts) s0 += part[(size_t)z * ne + e];
+    for (; z < nparts; z += 8) s += part[(size_t)z * ne + e];
   }
-  sh[w][lane] = s0 + s1;
+  sh[w][lane] = s;
   __syncthreads();
   if (w == 0 && e < ne) {
     const double v = ((sh[0][lane] + sh[1][lane]) + (sh[2][lane] + sh[3][lane])) +
@@ -394,14 +397,13 @@ __device__ void qb_inv_upper_w(const double *r, double *ri, int b) {
 //  op 3: R3 = chol(W), [8]
 //  op 4: test on W = Z1^T Z1, R4 = chol(W), R_i, [9], singularity guard on
 //        diag(R_i) (linalg.py:131-135)
-__global__ void qb_small_kernel(int op, int b, int ncat, int c0, const double *redm, double *st, int *flag,
-                                const double *tol) {
-  __shared__ double w[kQbMaxB * kQbMaxB], f[10][kQbMaxB * kQbMaxB], tmp[kQbMaxB * kQbMaxB];
+// the b x b algebra of one step on W (shared memory, row-major b x b), by
+// warp 0 of the calling block
+__device__ void qb_small_ops(int op, int b, const double *w, double *st, int *flag, const double *tol) {
+  __shared__ double f[10][kQbMaxB * kQbMaxB], tmp[kQbMaxB * kQbMaxB];
   const int bb = b * b, lane = threadIdx.x & 31;
-  for (int e = lane; e < bb; e += 32) {
-    w[e] = redm[(size_t)(e / b) * ncat + c0 + e % b];  // the t^T t block of [t^T Q | t^T t]
+  for (int e = lane; e < bb; e += 32)
     for (int q = 0; q < 10; ++q) f[q][e] = st[q * bb + e];
-  }
   __syncwarp();
   bool ok = true;
   if (op == 1 || op == 3) {
@@ -439,6 +441,57 @@ __global__ void qb_small_kernel(int op, int b, int ncat, int c0, const double *r
   for (int e = lane; e < bb; e += 32)
     for (int q = 0; q < 10; ++q) st[q * bb + e] = f[q][e];
   if (lane == 0 && !ok) *flag = 1;
+}
+
+// Small b x b algebra between sweeps (b <= 16, one warp). `st` holds the
+// block's matrices, each b x b row-major:
+//   [0] R1  [1] R2  [2] r_i = R2 R1  [3] R3  [4] R4  [5] R_i = R4 R3 r_i
+//   [6] R1^-1  [7] R1^-1 R2^-1  [8] R3^-1  [9] R3^-1 R4^-1
+//  op 1: R1 = chol(W), [6]
+//  op 2: CholeskyQR2 test on W = Q1^T Q1 (max |W - I| < 1e-5), R2 = chol(W),
+//        r_i, [7], deficiency test |r_i,jj| >= tol (qb.py:100)
+//  op 3: R3 = chol(W), [8]
+//  op 4: test on W = Z1^T Z1, R4 = chol(W), R_i, [9], singularity guard on
+//        diag(R_i) (linalg.py:131-135)
+// W is the t^T t block of the reduced [t^T Q | t^T t] (b x ncat).
+__global__ void qb_small_kernel(int op, int b, int ncat, int c0, const double *redm, double *st, int *flag,
+                                const double *tol) {
+  __shared__ double w[kQbMaxB * kQbMaxB];
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < b * b; e += 32) w[e] = redm[(size_t)(e / b) * ncat + c0 + e % b];
+  __syncwarp();
+  qb_small_ops(op, b, w, st, flag, tol);
+}
+
+// W-only sweeps (S2, S4, S5): the fixed-order reduction of the t^T t block
+// of the partials AND the b x b step in one launch (one block): thread
+// (entry e, group g) sums the parts z = g (mod 8) eight loads at a time, the
+// eight group sums are added in a fixed tree, then warp 0 runs the step.
+__global__ void __launch_bounds__(256) qb_wfinish_kernel(int op, int b, int ncat, int c0,
+                                                         const double *__restrict__ part, int nparts, double *st,
+                                                         int *flag, const double *tol) {
+  __shared__ double sh[8][kQbMaxB * kQbMaxB], w[kQbMaxB * kQbMaxB];
+  const int bb = b * b, ne = b * ncat;
+  for (int i = threadIdx.x; i < 8 * bb; i += blockDim.x) {
+    const int g = i / bb, e = i - g * bb;
+    const size_t col = (size_t)(e / b) * ncat + c0 + e % b;  // t^T t entry in the b x ncat partial
+    double s = 0.0;
+    int z = g;
+    for (; z + 8 * 7 < nparts; z += 8 * 8) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = part[(size_t)(z + 8 * j) * ne + col];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[j];
+    }
+    for (; z < nparts; z += 8) s += part[(size_t)z * ne + col];
+    sh[g][e] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < bb; e += blockDim.x)
+    w[e] = ((sh[0][e] + sh[1][e]) + (sh[2][e] + sh[3][e])) + ((sh[4][e] + sh[5][e]) + (sh[6][e] + sh[7][e]));
+  __syncthreads();
+  if (threadIdx.x < 32) qb_small_ops(op, b, w, st, flag, tol);
 }
 
 }  // namespace spca

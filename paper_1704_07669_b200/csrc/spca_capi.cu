@@ -1358,6 +1358,10 @@ int spca_qb_block(int64_t m, int c0, int b, double *q, int64_t ldq, const double
     spca::qb_small_kernel<<<1, 32, 0, st>>>(op, b, ncat, c0, r, factors, flag, tol);
     return cudaGetLastError();
   };
+  auto wfinish = [&](int op) -> cudaError_t {  // reduction of the t^T t block + the b x b step
+    spca::qb_wfinish_kernel<<<1, 256, 0, st>>>(op, b, ncat, c0, part, parts, factors, flag, tol);
+    return cudaGetLastError();
+  };
   static const bool sync_each = getenv("SPCA_QB_SYNC") != nullptr;  // debugging: fault localisation
 #define QB_TRY(call)                                                                             \
   do {                                                                                           \
@@ -1372,20 +1376,17 @@ int spca_qb_block(int64_t m, int c0, int b, double *q, int64_t ldq, const double
   QB_TRY(small(1, p_out));
   // S2: Q1 = y R1^-1, Q1^T Q1
   QB_TRY(sweep(false, M1, nullptr, nullptr, 0, 0, 1));
-  QB_TRY(reduce(red, nullptr));
-  QB_TRY(small(2, red));
+  QB_TRY(wfinish(2));
   if (c0 > 0) {  // S3: Q^T Q2 (Q2 = y R1^-1 R2^-1), kept transposed as the next X
     QB_TRY(sweep(false, M12, nullptr, nullptr, 0, 1, 0));
     QB_TRY(reduce(red, xt));
   }
   // S4: z = Q2 - Q (Q^T Q2), z^T z
   QB_TRY(sweep(false, M12, c0 ? xt : nullptr, ybuf, b, 0, 1));
-  QB_TRY(reduce(red, nullptr));
-  QB_TRY(small(3, red));
+  QB_TRY(wfinish(3));
   // S5: Z1 = z R3^-1, Z1^T Z1
   QB_TRY(sweep(false, M3, nullptr, nullptr, 0, 0, 1));
-  QB_TRY(reduce(red, nullptr));
-  QB_TRY(small(4, red));
+  QB_TRY(wfinish(4));
   // S6: Q_i = z R3^-1 R4^-1 into Q's columns [c0, c0 + b)
   QB_TRY(sweep(false, M34, nullptr, q + c0, ldq, 0, 0));
 #undef QB_TRY
