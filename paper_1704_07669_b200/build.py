@@ -42,6 +42,10 @@ if os.environ.get("SPCA_BUILD_PROMOTE") is not None:  # experiment: K blocks per
     FLAGS.append("-DSPCA_PROMOTE=" + os.environ["SPCA_BUILD_PROMOTE"])
 if os.environ.get("SPCA_BUILD_NSTG") is not None:  # experiment: epilogue staging buffers (l_pad 64)
     FLAGS.append("-DSPCA_NSTG_64=" + os.environ["SPCA_BUILD_NSTG"])
+if os.environ.get("SPCA_BUILD_BRAW") is not None:  # experiment: raw fp32 B operand, lo split on chip (1)
+    FLAGS.append("-DSPCA_BRAW=" + os.environ["SPCA_BUILD_BRAW"])
+if os.environ.get("SPCA_BUILD_BULK") is not None:  # experiment: epilogue data movement on the TMA engine (1)
+    FLAGS.append("-DSPCA_BULK_EPI=" + os.environ["SPCA_BUILD_BULK"])
 if os.environ.get("SPCA_BUILD_STACKED") is not None:  # experiment: l_pad=64 MMA form
     FLAGS.append("-DSPCA_STACKED_64=" + os.environ["SPCA_BUILD_STACKED"])
 

@@ -401,6 +401,19 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           uint8_t *st = smem + C::B_OFF + s * C::B_STAGE;
           const uint32_t bar = ptx::mapa(ptx::smem_u32(&bars.b_full[s]), 0);
           const int k = (f.k0 + kb) * 32;
+#if SPCA_BRAW
+          (void)bar;
+          if (args.dbg & 4) {
+            ptx::mbar_arrive(&bars.b_full[s]);
+          } else {
+            // this CTA's l_pad/2 raw rows of Omega^T (G units) or of G^T slot (H units),
+            // completing on its own barrier (its converters split them)
+            constexpr int HR = LPAD / 2;
+            ptx::mbar_arrive_expect_tx(&bars.b_full[s], C::BH_BYTES);
+            const int y = (f.kind == 0 ? args.wy0 : gslot * LPAD) + HR * (int)rank;
+            ptx::tma_load_2d_hint(st, f.kind == 0 ? &tWhi : &tGT, &bars.b_full[s], k, y, keep);
+          }
+#else
           if (args.dbg & 4) {
             if (rank == 0) ptx::mbar_arrive(&bars.b_full[s]);
           } else {
@@ -424,6 +437,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             ptx::tma_load_2d_pair(st + C::BH_BYTES, ml, bar, k, yl + HR * (int)rank, keep);
           }
           }
+#endif
         }
         __syncwarp();
       }
@@ -639,7 +653,23 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         if (ctr) ctr[3] = clock64();
         ptx::tmem_wait_st();
         if (ctr) ctr[4] = clock64();
-#if SPCA_RELAY
+#if SPCA_BRAW
+        {  // this CTA's raw B half landed: write its lo part beside it (16-byte
+           // chunks at the same offsets, so the swizzled layout carries over)
+          const int bs = gk % C::NB;
+          ptx::mbar_wait(&bars.b_full[bs], (gk / C::NB) & 1);
+          const uint32_t b0 = ptx::smem_u32(smem + C::B_OFF + bs * C::B_STAGE);
+          constexpr int PER = (int)(C::BH_BYTES / (16 * 128));  // chunks per thread of the group
+#pragma unroll
+          for (int i = 0; i < PER; ++i) {
+            const uint32_t off = (uint32_t)(i * 128 + t) * 16;
+            const float4 x = ptx::lds128(b0 + off);
+            ptx::st_shared_v4(b0 + C::BH_BYTES + off,
+                              make_float4(braw_lo(x.x), braw_lo(x.y), braw_lo(x.z), braw_lo(x.w)));
+          }
+          ptx::fence_proxy_async_smem();  // generic writes -> the tensor core's reads
+        }
+#elif SPCA_RELAY
         // the leader's converters also vouch for the block's B stage (both CTAs'
         // halves complete on the leader's barrier): the MMA warp waits on kb_full only
         if (rank == 0) ptx::mbar_wait(&bars.b_full[gk % C::NB], (gk / C::NB) & 1);
@@ -719,9 +749,10 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int q = c0 / 4 + i;
-        ptx::st_shared_v4(stg_row + sb * C::STG_BYTES + ((q ^ (t & 7)) << 4),
+        ptx::st_shared_v4(stg_row + sb * C::STG_BYTES + ((SPCA_BULK_EPI ? q : (q ^ (t & 7))) << 4),
                           make_float4(racc[4 * i], racc[4 * i + 1], racc[4 * i + 2], racc[4 * i + 3]));
       }
+      if (SPCA_BULK_EPI) ptx::fence_proxy_async_smem();  // the staging leaves through the TMA engine
       ptx::mbar_arrive(&bars.epi_full[sb]);
     }
   } else if (warp >= C::EPI_BASE / 32) {  // --------------------------------- epilogue
@@ -754,6 +785,20 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           float4 *gp = reinterpret_cast<float4 *>(
               args.gpart + (((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 * LPAD);
           const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF + sb * C::STG_BYTES);
+#if SPCA_BULK_EPI
+          if (e == 0) {  // the whole staged tile -> its partial slot, one bulk copy
+            ptx::bulk_store(gp, stg0, 128 * LPAD * 4);
+            ptx::bulk_commit();
+          }
+#pragma unroll 4
+          for (int it = e; it < 128 * NQ; it += kTcEpi) {  // non-finite check only
+            const int r = it / NQ, q = it % NQ;
+            const float4 x = ptx::lds128(stg0 + r * LPAD * 4 + (q << 4));
+            const float chk = fmaf(x.x, 0.f, fmaf(x.y, 0.f, fmaf(x.z, 0.f, x.w * 0.f)));
+            if (!(chk == 0.f)) stg_bad[r] = 1;
+          }
+          if (e == 0) ptx::bulk_wait_read0();
+#else
 #pragma unroll 4
           for (int it = e; it < 128 * NQ; it += kTcEpi) {
             const int r = it / NQ, q = it % NQ;
@@ -762,6 +807,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             if (!(chk == 0.f)) stg_bad[r] = 1;
             gp[it] = x;
           }
+#endif
           if (NORM) {  // this segment's row sums of d, d^2 (the two converter groups, in order)
             double *rp = reinterpret_cast<double *>(args.rstat_part) +
                          ((((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 + e) * 2;
@@ -787,6 +833,12 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           }
           // every writer fences its own stores before the count (a fence by one
           // thread does not drain the other warps' outstanding stores)
+#if SPCA_BULK_EPI
+          if (e == 0) {  // the partial's bulk copy is performed and ordered before the count
+            ptx::bulk_wait0();
+            ptx::fence_proxy_async_global();
+          }
+#endif
           __threadfence();
           ptx::named_bar(2, kTcEpi);
           int *cnt = &args.seg_cnt[f.c * twoT + tile];
@@ -799,8 +851,12 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           // reduce this segment's slice of the tile's rows over the S partials (fixed order)
           const int r0 = (f.b * 128) / sc.S, r1 = ((f.b + 1) * 128) / sc.S;
           const float *p0 = args.gpart + (((size_t)gslot * twoT + tile) * sc.S) * 128 * LPAD;
+#if SPCA_BRAW
+          float *ghi = args.gT + (size_t)gslot * LPAD * sc.R0;  // raw G^T of the slot
+#else
           float *ghi = args.gT + (size_t)(2 * gslot) * LPAD * sc.R0;
           float *glo = ghi + (size_t)LPAD * sc.R0;
+#endif
           const int items = (r1 - r0) * NQ;
           if (NORM) {
             // row statistics of the slice over the S segments (fixed order, fp64):
@@ -870,6 +926,10 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             if (valid)
               reinterpret_cast<float4 *>(args.g_out + ((int64_t)f.c * sc.R0 + rc) * args.gld)[q] =
                   make_float4(a4[0], a4[1], a4[2], a4[3]);
+#if SPCA_BRAW
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ghi[(size_t)(4 * q + j) * sc.R0 + rc] = valid ? b4[j] : 0.f;
+#else
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               float h1 = 0.f, l1 = 0.f;
@@ -882,6 +942,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
               glo[(size_t)(4 * q + j) * sc.R0 + rc] = l1;
 #endif
             }
+#endif
           }
           ptx::fence_proxy_async_global();
           __threadfence();
@@ -896,6 +957,17 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         if (real) {
           if (e == 0) ptx::spin_until_geq(&args.hseq[tile], seq);
           ptx::named_bar(2, kTcEpi);
+#if SPCA_BULK_EPI
+          {  // H row e += staged row e, one bulk reduce-add per row (at L2); the launch
+             // zeroed H when it does not accumulate (the first unit of a tile adds to 0)
+            const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF + sb * C::STG_BYTES);
+            if (col < args.n) {
+              ptx::bulk_reduce_add_f32(args.hpart + (int64_t)col * args.gld, stg0 + e * LPAD * 4, LPAD * 4);
+              ptx::bulk_commit();
+              ptx::bulk_wait_read0();
+            }
+          }
+#else
           {  // H rows of the tile's columns, NQ consecutive lanes per column (coalesced)
             float *hp0 = args.hpart + (int64_t)tile * 128 * args.gld;
             const bool overwrite = !args.accumulate && seq == 0;
@@ -925,6 +997,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
               }
             }
           }
+#endif
           csv = stg_cs[sb][e] + stg_cs[sb][128 + e];
         }
         ptx::mbar_arrive(&bars.epi_empty[sb]);
@@ -940,6 +1013,12 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
               args.colsum[col] = __ldcg(args.colsum + col) + csv;
             }
           }
+#if SPCA_BULK_EPI
+          if (col < args.n) {  // this row's reduce-add is performed before the release
+            ptx::bulk_wait0();
+            ptx::fence_proxy_async_global();
+          }
+#endif
           __threadfence();
           ptx::named_bar(2, kTcEpi);
           if (e == 0) {

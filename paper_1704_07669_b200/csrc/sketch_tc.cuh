@@ -93,11 +93,37 @@ constexpr int kPromote = SPCA_PROMOTE;  // K blocks per accumulator period
 #ifndef SPCA_PAIRA
 #define SPCA_PAIRA 0
 #endif
+// B operand as raw fp32 (1): Omega^T and G^T reach shared memory unsplit (half
+// the B bytes through L2 -> SM, the pass's scarcest resource: 24 -> 20 KB of
+// ingress per CTA and K block at l_pad = 64), and the converter group of the
+// block writes lo = rna_tf32(b - trunc_tf32(b)) next to it in shared memory.
+// The tensor core reads the raw b as tf32 by dropping its 13 low mantissa
+// bits, i.e. as trunc_tf32(b), so hi + lo = b as in the host split.
+// 0 = hi / lo split once in global memory (Omega^T at create, G^T in the G
+// epilogue), both loaded per K block. Measured (round 2): parity unchanged
+// (which confirms the truncating read), but config 2 1.647 -> 1.676 ms and
+// config 3 11.60 -> 12.35 ms: the L2 -> SM bytes of B are not what bounds
+// the pass, the converters' extra wait and shared-memory traffic cost more.
+#ifndef SPCA_BRAW
+#define SPCA_BRAW 0
+#endif
 // epilogue staging buffers for l_pad = 64. Two (at the cost of two A stages)
 // measured no faster and failed 1 run in 8 (a launch fault not yet understood):
 // kept at one; the staging code is written for either.
 #ifndef SPCA_NSTG_64
 #define SPCA_NSTG_64 1
+#endif
+// Epilogue data movement on the TMA engine (1): the staged unit result leaves
+// shared memory as ONE bulk copy (G: K-split partial -> its slot) or as one
+// bulk fp32 reduce-add per H row (performed at L2: H += partial, in chunk
+// order under hseq as before), instead of 128 epilogue threads loading,
+// adding and storing 32-64 KB per unit. The staging tile is then unswizzled
+// ([128][l_pad], the layout of the partial slots and of H's rows). Measured
+// (round 2): parity unchanged, but config 2 1.647 -> 1.680 ms, config 3
+// 11.60 -> 12.28 ms, 512-row chunks 1.709 -> 1.766 ms: the bulk operations
+// queue on the same per-SM TMA engine as the A and B loads of the next unit.
+#ifndef SPCA_BULK_EPI
+#define SPCA_BULK_EPI 0
 #endif
 template <int LPAD>
 struct TcCfg {
@@ -126,6 +152,7 @@ struct TcCfg {
                                        : (STACKED ? 6 : (LPAD == 64 ? (NSTG == 2 ? 5 : 7) : 5));  // raw A ring (16 KB stages)
   static constexpr int NP = NA / 2;  // A slot pairs (SPCA_PAIRA)
   static_assert(!SPCA_PAIRA || (NA % 2 == 0 && !STACKED), "paired A slots");
+  static_assert(!SPCA_BRAW || (!STACKED && !SPCA_PAIRA), "raw B operand: three-MMA form");
   static constexpr uint32_t STG_BYTES = 128 * LPAD * 4;  // epilogue staging tile
   static constexpr uint32_t B_OFF = NA * A_BYTES;
   static constexpr uint32_t STG_OFF = B_OFF + NB * B_STAGE;
@@ -203,6 +230,23 @@ __global__ void tc_omega_prepare_comb(const double *__restrict__ om64, int n, in
     w2[(int64_t)bcomb_row(j, 1, lp) * ldw + i] = lo;
   }
 }
+
+// Omega (fp64 n x l, rounded to fp32) -> raw Omega^T (lpad x n, zero padded,
+// row stride ldw) for the raw B operand (SPCA_BRAW)
+__global__ void tc_omega_prepare_raw(const double *__restrict__ om64, int n, int l, int lpad,
+                                     float *__restrict__ w, int ldw) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; idx < (int64_t)lpad * n; idx += stride) {
+    const int j = (int)(idx / n);
+    const int i = (int)(idx - (int64_t)j * n);
+    w[(int64_t)j * ldw + i] = j < l ? (float)om64[(int64_t)i * l + j] : 0.f;
+  }
+}
+
+// lo part of a raw B value as the tensor core completes it: it reads b as
+// trunc_tf32(b); the remainder (exact in fp32) is rounded to tf32
+__device__ __forceinline__ float braw_lo(float b) { return rna_tf32_fast(b - trunc_tf32(b)); }
 
 // Omega (fp64 n x l, rounded to fp32) -> Omega^T hi/lo (lpad x n, zero padded)
 __global__ void tc_omega_prepare(const double *__restrict__ om64, int n, int l, int lpad,

@@ -218,7 +218,17 @@ int tc_setup(spca_sketch *h) {
   float *wlo = whi + (size_t)h->lpad * h->n;
   const uint32_t hr = (uint32_t)(lp / 2);
   int rc;
-#if SPCA_BCOMB
+#if SPCA_BRAW
+  // raw Omega^T (lpad rows): each CTA loads its l_pad/2 rows of the group per K block
+  tc_omega_prepare_raw<<<grid_for((int64_t)h->lpad * h->n), 256, 0, h->stream>>>(
+      h->omega64_dev, (int)h->n, (int)h->l, (int)h->lpad, whi, (int)ldw);
+  CK_LAUNCH(h);
+  rc = encode_2d(h, &h->tm_whi, whi, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)ldw * 4, 32, hr);
+  if (rc) return rc;
+  h->tm_wlo = h->tm_whi;
+  const uint32_t gbox = hr;
+  constexpr int kGtParts = 1;  // raw G^T
+#elif SPCA_BCOMB
   // one matrix of 2 lpad rows: each CTA's half of a column group is hi rows
   // then lo rows, loaded as ONE box of lp rows per K block
   tc_omega_prepare_comb<<<grid_for((int64_t)h->lpad * h->n), 256, 0, h->stream>>>(
@@ -228,6 +238,7 @@ int tc_setup(spca_sketch *h) {
   if (rc) return rc;
   h->tm_wlo = h->tm_whi;
   const uint32_t gbox = (uint32_t)lp;
+  constexpr int kGtParts = 2;
 #else
   tc_omega_prepare<<<grid_for((int64_t)h->lpad * h->n), 256, 0, h->stream>>>(
       h->omega64_dev, (int)h->n, (int)h->l, (int)h->lpad, whi, wlo);
@@ -239,12 +250,13 @@ int tc_setup(spca_sketch *h) {
   rc = encode_2d(h, &h->tm_wlo, wlo, (uint64_t)h->n, (uint64_t)h->lpad, (uint64_t)h->n * 4, 32, hr);
   if (rc) return rc;
   const uint32_t gbox = hr;
+  constexpr int kGtParts = 2;
 #endif
   const FusedSched s = tc_base_sched(h);
-  // G^T hi / lo of kSlots chunks of one launch: [kSlots][2 lp rows][R0], one TMA map
-  h->tc_ws_bytes = (size_t)kSlots * 2 * lp * s.R0 * 4;
+  // G^T (raw, or hi / lo) of kSlots chunks of one launch: [kSlots][parts x lp rows][R0], one TMA map
+  h->tc_ws_bytes = (size_t)kSlots * kGtParts * lp * s.R0 * 4;
   CK(h, dalloc(h, &h->tc_ws, h->tc_ws_bytes));
-  rc = encode_2d(h, &h->tm_gT, h->tc_ws, (uint64_t)s.R0, (uint64_t)kSlots * 2 * lp, (uint64_t)s.R0 * 4,
+  rc = encode_2d(h, &h->tm_gT, h->tc_ws, (uint64_t)s.R0, (uint64_t)kSlots * kGtParts * lp, (uint64_t)s.R0 * 4,
                  32, gbox);
   if (rc) return rc;
   h->gpart_elems = (int64_t)kSlots * 2 * s.T * s.S * 128 * lp;
@@ -410,6 +422,11 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   }
   const size_t ctr_words = (size_t)s.C * (2 * s.T + 2) + 2 * s.X;
   const int grid = 2 * std::max(1, std::min(h->max_pairs, s.total));
+#if SPCA_BULK_EPI
+  // H units add into the running H at L2 (bulk reduce-add): a launch that
+  // starts a flush period starts from zero instead of overwriting
+  if (h->chunks_since_flush == 0) CK(h, cudaMemsetAsync(h->hpart, 0, (size_t)h->n * h->lpad * 4, h->stream));
+#endif
   for (int grp = 0; grp < h->tc_groups; ++grp) {
   CK(h, cudaMemsetAsync(h->tc_ctr, 0, ctr_words * 4, h->stream));
   FusedArgs args{};
