@@ -114,7 +114,9 @@ struct FusedArgs {
   int colsum_on;              // this launch also accumulates the column sums (group 0)
   int g3d;                    // tAg3 (3-D box of two K blocks) is valid: n % 32 == 0
   int dbg;                    // profiling knobs (SPCA_TC_DEBUG), 0 in production:
-                              // 1 converters skip the split, 2 no MMAs, 4 no B loads, 8 no A loads
+                              // 1 converters skip the split, 2 no MMAs, 4 no B loads, 8 no A loads,
+                              // 2048 A tiles at one address (L2), 16384 no epilogue, 32768 no G^T
+                              // stores, 65536 no H read-modify-write, 131072 no G partial copy
 
 };
 
@@ -805,7 +807,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             const float4 x = ptx::lds128(stg0 + r * LPAD * 4 + ((q ^ (r & 7)) << 4));
             const float chk = fmaf(x.x, 0.f, fmaf(x.y, 0.f, fmaf(x.z, 0.f, x.w * 0.f)));
             if (!(chk == 0.f)) stg_bad[r] = 1;
-            gp[it] = x;
+            if (!(args.dbg & 131072)) gp[it] = x;  // profiling knob: no partial copy
           }
 #endif
           if (NORM) {  // this segment's row sums of d, d^2 (the two converter groups, in order)
@@ -857,7 +859,6 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           float *ghi = args.gT + (size_t)(2 * gslot) * LPAD * sc.R0;
           float *glo = ghi + (size_t)LPAD * sc.R0;
 #endif
-          const int items = (r1 - r0) * NQ;
           if (NORM) {
             // row statistics of the slice over the S segments (fixed order, fp64):
             // mean_d = mean(a) - a0, norm = ||a - mean(a)||, from sums of d = a - a0
@@ -884,65 +885,77 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             }
             ptx::named_bar(2, kTcEpi);
           }
+          // items = (row, 8-column group), ROW fastest: consecutive threads take
+          // consecutive rows, so each G^T store of a warp covers consecutive rows
+          // of one G^T row (coalesced; the row-major order scattered them one
+          // row of G^T per lane: 1.5 ms of config 3's pass); a thread's two
+          // float4 loads per partial fill one 32-byte sector
+          const int nrs = r1 - r0;
+          constexpr int NO = LPAD / 8;  // 8-column groups
 #pragma unroll 1
-          for (int it = e; it < items; it += kTcEpi) {
-            const int r = r0 + it / NQ, q = it % NQ;
-            // partials of other CTAs: read through L2 (.cg), never a stale L1 line
-            const float4 *src = reinterpret_cast<const float4 *>(p0 + (size_t)r * LPAD) + q;
-            float4 acc = __ldcg(src);
-            int z = 1;
-            for (; z + 4 <= sc.S; z += 4) {  // four loads in flight, added in order z
-              float4 b4[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) b4[j] = __ldcg(src + (size_t)(z + j) * 128 * NQ);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                acc.x += b4[j].x; acc.y += b4[j].y; acc.z += b4[j].z; acc.w += b4[j].w;
-              }
-            }
-            for (; z < sc.S; ++z) {
-              const float4 b4 = __ldcg(src + (size_t)z * 128 * NQ);
-              acc.x += b4.x; acc.y += b4.y; acc.z += b4.z; acc.w += b4.w;
-            }
+          for (int it = e; it < nrs * NO; it += kTcEpi) {
+            const int r = r0 + it % nrs, o = it / nrs;
             const int rc = tile * 128 + r;  // row within the chunk
             const bool valid = rc < f.rows;
-            float a4[4] = {acc.x, acc.y, acc.z, acc.w};
-            float b4[4] = {acc.x, acc.y, acc.z, acc.w};  // B operand of the H units
-            if (args.left != nullptr && valid) {  // co-sketch: H += A^T L
-              const float4 l4 = __ldg(reinterpret_cast<const float4 *>(
-                                          args.left + ((int64_t)f.c * sc.R0 + rc) * args.gld) + q);
-              b4[0] = l4.x; b4[1] = l4.y; b4[2] = l4.z; b4[3] = l4.w;
-            }
-            if (NORM) {  // G_hat = (d Omega - mean_d * 1^T Omega) / norm; the H units take G_hat / norm
-              const float md = sl_stat[r][0], inv = sl_stat[r][1];
-              const float4 w4 = __ldg(reinterpret_cast<const float4 *>(args.wsum) + q);
-              const float ws[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                a4[j] = fmaf(-md, ws[j], a4[j]) * inv;
-                b4[j] = (args.left != nullptr ? b4[j] : a4[j]) * inv;
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int q = 2 * o + h2;
+              // partials of other CTAs: read through L2 (.cg), never a stale L1 line
+              const float4 *src = reinterpret_cast<const float4 *>(p0 + (size_t)r * LPAD) + q;
+              float4 acc = __ldcg(src);
+              int z = 1;
+              for (; z + 4 <= sc.S; z += 4) {  // four loads in flight, added in order z
+                float4 b4[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) b4[j] = __ldcg(src + (size_t)(z + j) * 128 * NQ);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  acc.x += b4[j].x; acc.y += b4[j].y; acc.z += b4[j].z; acc.w += b4[j].w;
+                }
               }
-            }
-            if (valid)
-              reinterpret_cast<float4 *>(args.g_out + ((int64_t)f.c * sc.R0 + rc) * args.gld)[q] =
-                  make_float4(a4[0], a4[1], a4[2], a4[3]);
+              for (; z < sc.S; ++z) {
+                const float4 b4 = __ldcg(src + (size_t)z * 128 * NQ);
+                acc.x += b4.x; acc.y += b4.y; acc.z += b4.z; acc.w += b4.w;
+              }
+              float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+              float b4[4] = {acc.x, acc.y, acc.z, acc.w};  // B operand of the H units
+              if (args.left != nullptr && valid) {  // co-sketch: H += A^T L
+                const float4 l4 = __ldg(reinterpret_cast<const float4 *>(
+                                            args.left + ((int64_t)f.c * sc.R0 + rc) * args.gld) + q);
+                b4[0] = l4.x; b4[1] = l4.y; b4[2] = l4.z; b4[3] = l4.w;
+              }
+              if (NORM) {  // G_hat = (d Omega - mean_d * 1^T Omega) / norm; the H units take G_hat / norm
+                const float md = sl_stat[r][0], inv = sl_stat[r][1];
+                const float4 w4 = __ldg(reinterpret_cast<const float4 *>(args.wsum) + q);
+                const float ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  a4[j] = fmaf(-md, ws[j], a4[j]) * inv;
+                  b4[j] = (args.left != nullptr ? b4[j] : a4[j]) * inv;
+                }
+              }
+              if (valid)
+                reinterpret_cast<float4 *>(args.g_out + ((int64_t)f.c * sc.R0 + rc) * args.gld)[q] =
+                    make_float4(a4[0], a4[1], a4[2], a4[3]);
 #if SPCA_BRAW
 #pragma unroll
-            for (int j = 0; j < 4; ++j) ghi[(size_t)(4 * q + j) * sc.R0 + rc] = valid ? b4[j] : 0.f;
+              for (int j = 0; j < 4; ++j) ghi[(size_t)(4 * q + j) * sc.R0 + rc] = valid ? b4[j] : 0.f;
 #else
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float h1 = 0.f, l1 = 0.f;
-              if (valid) split3(b4[j], h1, l1);
+              for (int j = 0; j < 4; ++j) {
+                if (args.dbg & 32768) break;  // profiling knob: no G^T stores
+                float h1 = 0.f, l1 = 0.f;
+                if (valid) split3(b4[j], h1, l1);
 #if SPCA_BCOMB
-              ghi[(size_t)bcomb_row(4 * q + j, 0, LPAD) * sc.R0 + rc] = h1;
-              ghi[(size_t)bcomb_row(4 * q + j, 1, LPAD) * sc.R0 + rc] = l1;
+                ghi[(size_t)bcomb_row(4 * q + j, 0, LPAD) * sc.R0 + rc] = h1;
+                ghi[(size_t)bcomb_row(4 * q + j, 1, LPAD) * sc.R0 + rc] = l1;
 #else
-              ghi[(size_t)(4 * q + j) * sc.R0 + rc] = h1;
-              glo[(size_t)(4 * q + j) * sc.R0 + rc] = l1;
+                ghi[(size_t)(4 * q + j) * sc.R0 + rc] = h1;
+                glo[(size_t)(4 * q + j) * sc.R0 + rc] = l1;
+#endif
+              }
 #endif
             }
-#endif
           }
           ptx::fence_proxy_async_global();
           __threadfence();
@@ -977,7 +990,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             // (a store between loads would serialize them on the L2 round trip:
             // the compiler cannot tell the rows apart)
             constexpr int kB = 8;
-            for (int it0 = e; it0 < items; it0 += kB * kTcEpi) {
+            for (int it0 = e; it0 < ((args.dbg & 65536) ? 0 : items); it0 += kB * kTcEpi) {  // knob: no H RMW
               float4 o[kB];
 #pragma unroll
               for (int j = 0; j < kB; ++j) {

@@ -108,6 +108,8 @@ for k, nm in ((0, "G"), (1, "H")):
     stat(f"{nm} units: MMA issue span (leader)", np.where(mmv & (kinds == k), u[:, :, 6] - u[:, :, 5], np.nan).ravel())
 for k, nm in ((0, "G"), (1, "H")):
     sel = valid & (kinds == k)
+    stat(f"{nm} units: epilogue duration", np.where(sel, u[:, :, 4] - u[:, :, 3], np.nan).ravel())
+    stat(f"{nm} units: staging waits for epilogue", np.where(sel, u[:, :, 3] - u[:, :, 2], np.nan).ravel())
     stat(f"{nm} units: converter main loop", np.where(sel, u[:, :, 1] - u[:, :, 0], np.nan).ravel())
     stat(f"{nm} units: B producer ready - conv start", np.where(sel & (u[:, :, 7] > 0), u[:, :, 7] - u[:, :, 0], np.nan).ravel())
 
