@@ -46,6 +46,8 @@ if os.environ.get("SPCA_BUILD_BRAW") is not None:  # experiment: raw fp32 B oper
     FLAGS.append("-DSPCA_BRAW=" + os.environ["SPCA_BUILD_BRAW"])
 if os.environ.get("SPCA_BUILD_BULK") is not None:  # experiment: epilogue data movement on the TMA engine (1)
     FLAGS.append("-DSPCA_BULK_EPI=" + os.environ["SPCA_BUILD_BULK"])
+if os.environ.get("SPCA_BUILD_PROMO_GP") is not None:  # G partials written by the promoters (0/1/2)
+    FLAGS.append("-DSPCA_PROMO_GP=" + os.environ["SPCA_BUILD_PROMO_GP"])
 if os.environ.get("SPCA_BUILD_STACKED") is not None:  # experiment: l_pad=64 MMA form
     FLAGS.append("-DSPCA_STACKED_64=" + os.environ["SPCA_BUILD_STACKED"])
 

@@ -744,8 +744,35 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         if (lane == 0) ptx::mbar_arrive_cluster(accempty_l + 8 * buf);
       }
       if (pt == 0) SPCA_TRACE(ui, 6);
-      // stage the result for the epilogue warps (16-byte chunks XOR-swizzled by row)
+      constexpr bool kPGP = SPCA_PROMO_GP == 2 || (SPCA_PROMO_GP == 1 && LPAD == 128);
       const int sb = ui % C::NSTG;  // staging buffer of this unit
+      if (kPGP && f.kind == 0) {
+        // G partial straight to its slot (row t, columns c0..c0+63); the slot was
+        // last used kSlots chunks ago: its slices must have been reduced
+        const int tile = 2 * f.a + (int)rank;
+        float chk = 0.f;
+        if (tile < fused_real_tiles(sc, f.c) && !(args.dbg & 131072)) {
+          if (f.c >= kSlots) {
+            if (lane == 0) ptx::spin_until_geq(&args.ready[f.c - kSlots], sc.nt * sc.S);
+            __syncwarp();
+          }
+          float4 *gp = reinterpret_cast<float4 *>(
+              args.gpart + ((((size_t)(f.c % kSlots) * 2 * sc.T + tile) * sc.S + f.b) * 128 + t) * LPAD + c0);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            gp[i] = make_float4(racc[4 * i], racc[4 * i + 1], racc[4 * i + 2], racc[4 * i + 3]);
+            chk = fmaf(racc[4 * i], 0.f, fmaf(racc[4 * i + 1], 0.f, fmaf(racc[4 * i + 2], 0.f, fmaf(racc[4 * i + 3], 0.f, chk))));
+          }
+          __threadfence();  // the partial is visible before the epilogue counts it
+        }
+        // the epilogue has cleared the previous unit's flags once it released that unit
+        if (ui >= C::NSTG) ptx::mbar_wait(&bars.epi_empty[sb], ((ui / C::NSTG) - 1) & 1);
+        if (!(chk == 0.f)) stg_bad[t] = 1;  // a non-finite value in this row's partial
+        if (pt == 0) SPCA_TRACE(ui, 2);
+        ptx::mbar_arrive(&bars.epi_full[sb]);
+        continue;
+      }
+      // stage the result for the epilogue warps (16-byte chunks XOR-swizzled by row)
       if (ui >= C::NSTG) ptx::mbar_wait(&bars.epi_empty[sb], ((ui / C::NSTG) - 1) & 1);
       if (pt == 0) SPCA_TRACE(ui, 2);
 #pragma unroll
@@ -778,7 +805,19 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         const bool real = tile < fused_real_tiles(sc, f.c);
         const int row = tile * 128 + e;
         bool flagged = false;
-        if (real) {
+        constexpr bool kPGP = SPCA_PROMO_GP == 2 || (SPCA_PROMO_GP == 1 && LPAD == 128);
+        if (kPGP && real) {  // the promoters wrote the partial and flagged non-finite rows
+          ptx::named_bar(2, kTcEpi);
+          if (NORM) {  // this segment's row sums of d, d^2 (the two converter groups, in order)
+            double *rp = reinterpret_cast<double *>(args.rstat_part) +
+                         ((((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 + e) * 2;
+            rp[0] = stg_rs[sb][0][e] + stg_rs[sb][0][128 + e];
+            rp[1] = stg_rs[sb][1][e] + stg_rs[sb][1][128 + e];
+          }
+          flagged = stg_bad[e] != 0;
+          ptx::named_bar(2, kTcEpi);  // every flag read before it is cleared for the next unit
+          stg_bad[e] = 0;
+        } else if (real) {
           // the partial slot was last used kSlots chunks ago: its slices must be reduced
           if (f.c >= kSlots && e == 0) ptx::spin_until_geq(&args.ready[f.c - kSlots], sc.nt * sc.S);
           ptx::named_bar(2, kTcEpi);

@@ -125,6 +125,17 @@ constexpr int kPromote = SPCA_PROMOTE;  // K blocks per accumulator period
 #ifndef SPCA_BULK_EPI
 #define SPCA_BULK_EPI 0
 #endif
+// G units' K-split partials written to global memory by the promoter warps
+// straight from their registers (the epilogue then only waits for the tile's
+// segments and reduces its slice, and the staging tile is free at once):
+// 0 = off (staged, copied by the epilogue), 1 = l_pad 128 only, 2 = both.
+// Measured (round 2, =2): parity green; config 2 1.652 -> 1.735 ms, config 3
+// 11.31 -> 11.55, config 5 59.7 -> 60.3: the G epilogue's time is its wait for
+// the tile's other K segments (23 us at config 3 with or without the copy),
+// and the promoters' global stores delay the next unit's accumulator folds.
+#ifndef SPCA_PROMO_GP
+#define SPCA_PROMO_GP 0
+#endif
 template <int LPAD>
 struct TcCfg {
   static_assert(LPAD == 64 || LPAD == 128, "tensor-core path covers l <= 128");
