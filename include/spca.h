@@ -238,6 +238,21 @@ int spca_qb_block(int64_t m, int c0, int b, double *q, int64_t ldq, const double
                   const double *x, double *ybuf, double *ws, int64_t ws_elems, double *p_out,
                   double *factors, int *flag, const double *tol, void *stream);
 
+/* ---- the reference's seeded Gaussian draw on the device ----------------
+ * Replaces gaussian_matrix (/root/reference/pkg/src/streampca/linalg.py:46-56):
+ * writes the first `count` values of numpy's
+ *   Generator(Philox(key=[seed, stream])).standard_normal()
+ * bit for bit into `out` (device fp64; an n x l Omega is the first n*l values
+ * in row-major order). w, k, f, r_tail, inv_r: numpy's ziggurat constants
+ * (host arrays of 256; paper_1704_07669_b200/ziggurat.py recovers them).
+ * Enqueued on `stream`; returns after one host synchronization (tail values
+ * are recomputed on the host with libm's log1p). SPCA_ERR_STATE when the
+ * device cannot vouch for every value (a layer or tail test within 1e-12 of
+ * its threshold, or the speculative walk failing its chain check): the
+ * caller then draws on the host. */
+int spca_gaussian_device(double *out, int64_t count, uint64_t seed, uint64_t stream_id, const double *w,
+                         const uint64_t *k, const double *f, double r_tail, double inv_r, void *stream);
+
 int spca_last_error(spca_handle_t h, int *code, int64_t *bad_row, char *msg,
                     size_t msg_len);
 

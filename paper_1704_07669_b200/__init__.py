@@ -49,7 +49,7 @@ from .sketch import (
     sketch_pass,
 )
 from .qb import QbFactor, blocked_qb
-from .linalg import dense_svd, gaussian_matrix, qr_unpivoted, sign_align, solve_rt
+from .linalg import dense_svd, gaussian_matrix, gaussian_matrix_device, qr_unpivoted, sign_align, solve_rt
 from .algorithms import (
     PcaConfig,
     TruncatedSvd,
@@ -77,7 +77,7 @@ __all__ = [
     "FileRowStream", "FormatError", "GeneratorRowStream", "NormalizedRowStream", "normalize_rows", "GpuSketch", "PassCounter", "PcaConfig",
     "PinnedRowStream", "QbFactor", "RankDeficiencyError", "RowBlock", "RowStream", "ScaleError",
     "SinglePassPCA", "SingularMatrixError", "SketchState", "StreamFormatError", "StreamPcaError", "TruncatedSvd",
-    "as_row_stream", "basic_rand_svd", "blocked_qb", "legacy_single_pass", "center_correct", "dense_svd", "gaussian_matrix",
+    "as_row_stream", "basic_rand_svd", "blocked_qb", "legacy_single_pass", "center_correct", "dense_svd", "gaussian_matrix", "gaussian_matrix_device",
     "power_refine", "principal_components", "qr_unpivoted", "sign_align", "single_pass_pca",
     "sketch_pass", "solve_rt", "__version__",
 ]

@@ -19,7 +19,7 @@ import numpy as np
 
 from .device import default_device, host_copy, to_device64, torch_mod
 from .errors import ConfigError, EmptyStreamError
-from .linalg import STREAM_SKETCH, dense_svd, gaussian_matrix, qr_unpivoted, sign_align
+from .linalg import STREAM_SKETCH, dense_svd, gaussian_matrix_device, qr_unpivoted, sign_align
 from .qb import QbFactor, blocked_qb
 from .sketch import SketchState, run_pass, sketch_pass
 from .streams import ArrayRowStream, PassCounter, RowStream
@@ -137,7 +137,7 @@ def single_pass_pca(
         raise EmptyStreamError("the stream has no rows")
     cfg.validate_dims(stream.n_cols, stream.n_rows)
     dev = default_device(device)
-    omega = gaussian_matrix(stream.n_cols, cfg.l, cfg.seed, stream=STREAM_SKETCH)
+    omega = gaussian_matrix_device(stream.n_cols, cfg.l, cfg.seed, stream=STREAM_SKETCH, device=dev)
     state = sketch_pass(stream, omega, block_rows=block_rows, fixed_order=fixed_order,
                         compensated=compensated, precision=precision, device=dev,
                         keep_on_device=True, shift=cfg.center)
@@ -191,7 +191,7 @@ def power_refine(
         raise EmptyStreamError("the stream has no rows")
     cfg.validate_dims(stream.n_cols, stream.n_rows)
     dev = default_device(device)
-    omega = gaussian_matrix(stream.n_cols, cfg.l, cfg.seed, stream=STREAM_SKETCH)
+    omega = gaussian_matrix_device(stream.n_cols, cfg.l, cfg.seed, stream=STREAM_SKETCH, device=dev)
     first = sketch_pass(stream, omega, block_rows=block_rows, precision=precision,
                         device=dev, keep_on_device=True, shift=cfg.center)
     if first.rows_seen == 0:
@@ -248,7 +248,7 @@ def basic_rand_svd(
     cfg.validate_dims(stream.n_cols, stream.n_rows)
     dev = default_device(device)
     n = stream.n_cols
-    omega = gaussian_matrix(n, cfg.l, cfg.seed, stream=STREAM_SKETCH)
+    omega = gaussian_matrix_device(n, cfg.l, cfg.seed, stream=STREAM_SKETCH, device=dev)
     sk = run_pass(stream, omega, block_rows=block_rows, precision=precision, device=dev, shift=cfg.center)
     try:
         g, _, col_sums, m = sk.finish(on_device=True)
@@ -325,8 +325,8 @@ def legacy_single_pass(
     cfg.validate_dims(stream.n_cols, m)
     dev = default_device(device)
     n, l = stream.n_cols, cfg.l
-    omega = gaussian_matrix(n, l, cfg.seed, stream=STREAM_SKETCH)
-    omega_t = gaussian_matrix(m, l, cfg.seed, stream=STREAM_COSKETCH)
+    omega = gaussian_matrix_device(n, l, cfg.seed, stream=STREAM_SKETCH, device=dev)
+    omega_t = gaussian_matrix_device(m, l, cfg.seed, stream=STREAM_COSKETCH, device=dev)
     sk = run_pass(stream, omega, block_rows=block_rows, precision=precision, device=dev, left=omega_t,
                   shift=cfg.center)
     dtype = sk.dtype

@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "libspca.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["spca_capi.cu"]
-HEADERS = ["common.cuh", "epilogue.cuh", "handle.cuh", "sketch_simt.cuh", "sketch_tc.cuh", "sketch_fused.cuh", "tc_ptx.cuh", "tc_host.cuh", "normalize.cuh", "postpass.cuh"]
+HEADERS = ["common.cuh", "epilogue.cuh", "handle.cuh", "sketch_simt.cuh", "sketch_tc.cuh", "sketch_fused.cuh", "tc_ptx.cuh", "tc_host.cuh", "normalize.cuh", "postpass.cuh", "omega_rng.cuh"]
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1,0 +1,304 @@
+// omega_rng.cuh — the reference's seeded Gaussian draw on the device, bit for
+// bit: the first `count` values of numpy's
+//   Generator(Philox(key=[seed, stream])).standard_normal()
+// (reference gaussian_matrix, /root/reference/pkg/src/streampca/linalg.py:46-56),
+// which is how the reference draws Omega (n x l, row-major = stream order).
+//
+// Raw stream: Philox4x64-10 (Random123 constants), 256-bit counter starting
+// at 1 for the first block, four 64-bit words per block; raw draw k is word
+// k % 4 of block k / 4 + 1. next_double(v) = (v >> 11) 2^-53.
+//
+// Sampler: numpy's 256-layer ziggurat (tables recovered by probing numpy,
+// paper_1704_07669_b200/ziggurat.py): an attempt takes one raw draw r
+// (idx = r & 255, sign = bit 8, rabs = bits 9..60, x = +-rabs w[idx]) and
+// returns x when rabs < k[idx] (the fast path, ~99.2%); otherwise layer 0
+// samples the tail (pairs of doubles until accepted) and the other layers
+// take one double u and accept x when (f[idx-1] - f[idx]) u + f[idx] <
+// exp(-x^2/2), else the attempt restarts on the next raw draw.
+//
+// A value therefore consumes a variable number of raw draws, so value j's
+// position in the raw stream is only known sequentially. The device walk:
+// the raw stream is cut into segments of L draws, one warp per segment. A
+// warp starts M draws before its segment as if a value started there (an
+// attempt always begins on a fresh raw draw, so a speculative chain of
+// value starts merges with the true one within a few values) and walks the
+// chain 32 draws at a time: a ballot over 32 consecutive draws finds the
+// first one that is not a fast-path start; every draw before it is a value
+// start, and lane 0 evaluates the slow start alone. Pass 1 counts the value
+// starts inside each segment and records the first start at or after the
+// segment's beginning (entry) and after its end (exit); segment w + 1 is
+// the true chain exactly when entry[w + 1] == exit[w] (segment 0 starts at
+// draw 0, the true start), which the scan checks; pass 2 walks again and
+// writes value j = offset[w] + local index.
+//
+// Exactness: the fast path and accepted layer values are x = rabs * w[idx]
+// (one IEEE product, no contraction): exact. The layer and tail tests use
+// the device exp / log1p, which may differ from libm's by an ulp: a test
+// within 1e-12 (relative) of its threshold marks the draw undecided and
+// spca_gaussian_device returns SPCA_ERR_STATE (the caller draws on the host;
+// expected once in ~1e6 config-5 draws). Tail values (~2.6e-4 of them) are
+// recorded and recomputed on the host with libm's log1p, numpy's function,
+// and patched in. A broken chain check also returns SPCA_ERR_STATE.
+#pragma once
+
+#include <cstdint>
+
+namespace spca {
+namespace rng {
+
+constexpr uint64_t kM0 = 0xD2E7470EE14C6C93ull, kM1 = 0xCA5A826395121157ull;
+constexpr uint64_t kW0 = 0x9E3779B97F4A7C15ull, kW1 = 0xBB67AE8584CAA73Bull;
+constexpr uint64_t kMask52 = (1ull << 52) - 1;
+
+struct Tables {
+  double w[256];
+  uint64_t k[256];
+  double f[256];
+  double r_tail, inv_r;
+};
+
+// a tail value, recomputed on the host with libm's log1p (numpy's)
+struct TailEvent {
+  int64_t j;     // value index
+  uint64_t u1;   // raw draw of the accepted pair's first double
+  int64_t neg;   // sign bit
+  int64_t pad;
+};
+
+__host__ __device__ inline void philox_block(uint64_t ctr0, uint64_t key0, uint64_t key1, uint64_t out[4]) {
+  uint64_t x0 = ctr0, x1 = 0, x2 = 0, x3 = 0, k0 = key0, k1 = key1;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#ifdef __CUDA_ARCH__
+    const uint64_t hi0 = __umul64hi(kM0, x0), lo0 = kM0 * x0;
+    const uint64_t hi1 = __umul64hi(kM1, x2), lo1 = kM1 * x2;
+#else
+    const unsigned __int128 p0 = (unsigned __int128)kM0 * x0, p1 = (unsigned __int128)kM1 * x2;
+    const uint64_t hi0 = (uint64_t)(p0 >> 64), lo0 = (uint64_t)p0;
+    const uint64_t hi1 = (uint64_t)(p1 >> 64), lo1 = (uint64_t)p1;
+#endif
+    const uint64_t y0 = hi1 ^ x1 ^ k0, y2 = hi0 ^ x3 ^ k1;
+    x0 = y0;
+    x1 = lo1;
+    x2 = y2;
+    x3 = lo0;
+    k0 += kW0;
+    k1 += kW1;
+  }
+  out[0] = x0;
+  out[1] = x1;
+  out[2] = x2;
+  out[3] = x3;
+}
+
+// raw draw k of the stream (counter k / 4 + 1; the counter never exceeds 64 bits here)
+__host__ __device__ inline uint64_t raw_at(uint64_t k, uint64_t key0, uint64_t key1) {
+  uint64_t b[4];
+  philox_block((k >> 2) + 1, key0, key1, b);
+  const int wd = (int)(k & 3);
+  return wd == 0 ? b[0] : (wd == 1 ? b[1] : (wd == 2 ? b[2] : b[3]));
+}
+
+__host__ __device__ inline double next_double(uint64_t v) { return (double)(v >> 11) * (1.0 / 9007199254740992.0); }
+
+struct Walk {
+  const Tables *t;  // in shared memory
+  uint64_t key0, key1;
+};
+
+// One value whose first attempt is NOT a fast-path draw, starting at raw
+// position pos: its value, the raw position after it, and for a tail value
+// the draw the host needs to recompute it. `undecided` is set when a layer
+// or tail test lies within 1e-12 (relative) of its threshold, where the
+// device's exp / log1p could decide differently from libm's.
+struct SlowValue {
+  double v;
+  int64_t next;
+  uint64_t u1;  // tail: raw draw of u1 of the accepted pair
+  int tail, neg, undecided;
+};
+
+__device__ inline SlowValue slow_value(const Walk &W, int64_t pos) {
+  const Tables &T = *W.t;
+  SlowValue s{};
+  for (;;) {
+    const uint64_t r0 = raw_at((uint64_t)pos, W.key0, W.key1);
+    const int idx = (int)(r0 & 0xff);
+    const uint64_t rr = r0 >> 8;
+    const uint64_t rabs = (rr >> 1) & kMask52;
+    double x = __dmul_rn((double)rabs, T.w[idx]);
+    if (rr & 1) x = -x;
+    if (rabs < T.k[idx]) {  // fast path on a restarted attempt
+      s.v = x;
+      s.next = pos + 1;
+      return s;
+    }
+    if (idx == 0) {  // tail beyond R: pairs of doubles until accepted
+      int64_t q = pos + 1;
+      for (;;) {
+        const uint64_t a = raw_at((uint64_t)q, W.key0, W.key1);
+        const double xx = __dmul_rn(-T.inv_r, log1p(-next_double(a)));
+        const double yy = -log1p(-next_double(raw_at((uint64_t)q + 1, W.key0, W.key1)));
+        q += 2;
+        const double lhs = __dadd_rn(yy, yy), rhs = __dmul_rn(xx, xx);
+        if (fabs(lhs - rhs) <= 1e-12 * fmax(lhs, rhs)) s.undecided = 1;
+        if (lhs > rhs) {
+          s.neg = (int)((rabs >> 8) & 1);
+          s.v = s.neg ? -(T.r_tail + xx) : T.r_tail + xx;
+          s.next = q;
+          s.u1 = a;
+          s.tail = 1;
+          return s;
+        }
+      }
+    }
+    // layer test, evaluated as numpy's C does (no contraction)
+    const double u = next_double(raw_at((uint64_t)pos + 1, W.key0, W.key1));
+    const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(T.f[idx - 1], T.f[idx]), u), T.f[idx]);
+    const double e = exp(__dmul_rn(__dmul_rn(-0.5, x), x));
+    if (fabs(lhs - e) <= 1e-12 * e) s.undecided = 1;
+    if (lhs < e) {
+      s.v = x;
+      s.next = pos + 2;
+      return s;
+    }
+    pos += 2;  // rejected: a fresh attempt
+  }
+}
+
+// Walk the chain of value starts over segment w = [A, A + L) of the raw
+// stream (one warp). PASS 1: cnt[w], entry[w], exit_[w]. PASS 2: values
+// j = off[w] + i (j < count) into out, tail events appended at ev.
+template <int PASS>
+__global__ void __launch_bounds__(256) gauss_walk(Tables tab_in, uint64_t key0, uint64_t key1, int64_t L,
+                                                  int64_t margin, int nseg, int64_t *cnt, int64_t *entry,
+                                                  int64_t *exit_, const int64_t *off, double *out, int64_t count,
+                                                  TailEvent *ev, int64_t ev_cap, unsigned long long *ev_n,
+                                                  int *undecided) {
+  __shared__ Tables tab;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    tab.w[i] = tab_in.w[i];
+    tab.k[i] = tab_in.k[i];
+    tab.f[i] = tab_in.f[i];
+  }
+  if (threadIdx.x == 0) {
+    tab.r_tail = tab_in.r_tail;
+    tab.inv_r = tab_in.inv_r;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= nseg) return;
+  Walk W{&tab, key0, key1};
+  const int64_t A = (int64_t)w * L, E = A + L;
+  int64_t pos = w == 0 ? 0 : A - margin;  // always a value start (speculatively before A)
+  int64_t n_in = 0, first = -1, after = -1;
+  int64_t j = PASS == 2 ? off[w] : 0;
+  bool und = false;
+  while (after < 0) {
+    if (first < 0 && pos >= A) first = pos;
+    const int64_t kk = pos + lane;
+    const uint64_t r = raw_at((uint64_t)kk, key0, key1);
+    const int idx = (int)(r & 0xff);
+    const uint64_t rabs = (r >> 9) & kMask52;
+    const bool fast = rabs < tab.k[idx];
+    const unsigned slow_mask = __ballot_sync(0xffffffffu, !fast);
+    const int p = slow_mask ? __ffs(slow_mask) - 1 : 32;
+    // draws pos .. pos + p - 1 are value starts (fast path); those inside [A, E) are this segment's
+    const bool mine = lane < p && kk >= A && kk < E;
+    const unsigned mm = __ballot_sync(0xffffffffu, mine);
+    if (first < 0 && mm) first = pos + (__ffs(mm) - 1);
+    if (PASS == 2 && mine) {
+      const int64_t jj = j + __popc(mm & ((1u << lane) - 1));
+      if (jj < count) {
+        double x = __dmul_rn((double)rabs, tab.w[idx]);
+        if ((r >> 8) & 1) x = -x;
+        out[jj] = x;
+      }
+    }
+    n_in += __popc(mm);
+    j += __popc(mm);
+    if (pos + p > E) {  // E itself is a (fast) value start
+      after = E;
+      break;
+    }
+    pos += p;
+    if (pos >= E) {
+      after = pos;
+      break;
+    }
+    if (p < 32) {  // a slow start at pos < E: lane 0 evaluates it
+      if (first < 0 && pos >= A) first = pos;
+      SlowValue sv{};
+      if (lane == 0) sv = slow_value(W, pos);
+      const int64_t next = __shfl_sync(0xffffffffu, sv.next, 0);
+      if (pos >= A) {
+        if (lane == 0) {
+          und |= sv.undecided != 0;
+          if (PASS == 2 && j < count) {
+            out[j] = sv.v;
+            if (sv.tail) {
+              const unsigned long long e = atomicAdd(ev_n, 1ull);
+              if ((int64_t)e < ev_cap) ev[e] = TailEvent{j, sv.u1, sv.neg, 0};
+            }
+          }
+        }
+        ++n_in;
+        ++j;
+      }
+      pos = next;
+      if (pos >= E) after = pos;
+    }
+    if (PASS == 2 && j >= count) break;
+  }
+  if (lane == 0) {
+    if (PASS == 1) {
+      cnt[w] = n_in;
+      entry[w] = first < 0 ? after : first;
+      exit_[w] = after;
+    }
+    if (und) atomicOr(undecided, 1);
+  }
+}
+
+// Exclusive scan of the segment counts (one block) and the chain check:
+// entry[w + 1] must equal exit[w]. Flags: bit 0 chain broken, bit 1 too few values.
+__global__ void gauss_scan(const int64_t *cnt, const int64_t *entry, const int64_t *exit_, int nseg, int64_t count,
+                           int64_t *off, int *flags) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int per = (nseg + nt - 1) / nt;
+  const int s0 = min(nseg, t * per), s1 = min(nseg, s0 + per);
+  int64_t sum = 0;
+  int bad = 0;
+  for (int w = s0; w < s1; ++w) {
+    sum += cnt[w];
+    if (w + 1 < nseg && entry[w + 1] != exit_[w]) bad = 1;
+  }
+  part[t] = sum;
+  __syncthreads();
+  if (t == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < nt; ++i) {
+      const int64_t v = part[i];
+      part[i] = run;
+      run += v;
+    }
+    if (run < count) atomicOr(flags, 2);
+  }
+  __syncthreads();
+  int64_t run = part[t];
+  for (int w = s0; w < s1; ++w) {
+    off[w] = run;
+    run += cnt[w];
+  }
+  if (bad) atomicOr(flags, 1);
+}
+
+__global__ void gauss_patch(double *out, const int64_t *j, const double *v, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[j[i]] = v[i];
+}
+
+}  // namespace rng
+}  // namespace spca

@@ -11,6 +11,7 @@
 #include <nccl.h>  // types and enums only: the library is resolved at run time (dlopen)
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -27,6 +28,7 @@
 #include "handle.cuh"
 #include "normalize.cuh"
 #include "postpass.cuh"
+#include "omega_rng.cuh"
 
 using namespace spca;
 
@@ -1432,6 +1434,96 @@ int spca_center_correct(spca_handle_t h, int64_t m_total, const double *gsum, do
   dfree(h, gs);
   CK(h, cudaStreamSynchronize(h->stream));
   return SPCA_OK;
+}
+
+int spca_gaussian_device(double *out, int64_t count, uint64_t seed, uint64_t stream_id, const double *w,
+                         const uint64_t *k, const double *f, double r_tail, double inv_r, void *stream) {
+  using namespace spca::rng;
+  if (count < 0 || (count > 0 && (!out || !w || !k || !f)))
+    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "gaussian_device: bad arguments");
+  if (count == 0) return SPCA_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Tables tab;
+  memcpy(tab.w, w, sizeof(tab.w));
+  memcpy(tab.k, k, sizeof(tab.k));
+  memcpy(tab.f, f, sizeof(tab.f));
+  tab.r_tail = r_tail;
+  tab.inv_r = inv_r;
+  // raw draws to cover: 1.0222 per value on average (std ~0.15 per value)
+  const int64_t n_raw = (int64_t)(1.03 * (double)count) + 4096;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want_seg = (int64_t)sms * 32;  // ~4 resident warps of 8 per SM
+  int64_t L = std::max<int64_t>(1024, (n_raw + want_seg - 1) / want_seg);
+  L = (L + 31) / 32 * 32;
+  const int nseg = (int)((n_raw + L - 1) / L);
+  const int64_t margin = 512;
+  const int64_t ev_cap = count / 512 + 1024;  // tails: ~2.6e-4 per value
+  struct Ctl {
+    unsigned long long ev_n;
+    int flags, undecided;
+  };
+  char *buf = nullptr;
+  const size_t seg_bytes = (size_t)nseg * 8;
+  const size_t bytes = 4 * seg_bytes + sizeof(Ctl) + (size_t)ev_cap * sizeof(TailEvent) + 64;
+  if (cudaMallocAsync((void **)&buf, bytes, st) != cudaSuccess)
+    return set_err(nullptr, SPCA_ERR_CUDA, -1, "gaussian_device: allocation of %zu bytes failed", bytes);
+  int64_t *cnt = (int64_t *)buf, *entry = cnt + nseg, *exit_ = entry + nseg, *off = exit_ + nseg;
+  Ctl *ctl = (Ctl *)(off + nseg);
+  TailEvent *ev = (TailEvent *)(((uintptr_t)(ctl + 1) + 31) & ~(uintptr_t)31);
+  int rc = SPCA_OK;
+  Ctl hc{};
+  std::vector<TailEvent> hev;
+  const unsigned blocks = (unsigned)((nseg + 7) / 8);
+  const uint64_t key0 = seed, key1 = stream_id;
+  cudaMemsetAsync(ctl, 0, sizeof(Ctl), st);
+  gauss_walk<1><<<blocks, 256, 0, st>>>(tab, key0, key1, L, margin, nseg, cnt, entry, exit_, nullptr, out, count,
+                                        ev, ev_cap, &ctl->ev_n, &ctl->undecided);
+  gauss_scan<<<1, 1024, 0, st>>>(cnt, entry, exit_, nseg, count, off, &ctl->flags);
+  gauss_walk<2><<<blocks, 256, 0, st>>>(tab, key0, key1, L, margin, nseg, cnt, entry, exit_, off, out, count, ev,
+                                        ev_cap, &ctl->ev_n, &ctl->undecided);
+  if (cudaGetLastError() != cudaSuccess || cudaMemcpyAsync(&hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st) ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    cudaFreeAsync(buf, st);
+    return set_err(nullptr, SPCA_ERR_CUDA, -1, "gaussian_device: kernel failed: %s",
+                   cudaGetErrorString(cudaGetLastError()));
+  }
+  if (hc.flags || hc.undecided || (int64_t)hc.ev_n > ev_cap) {
+    rc = set_err(nullptr, SPCA_ERR_STATE, -1,
+                 "gaussian_device: cannot vouch for the draw (chain %d, undecided %d, tails %llu): draw on the host",
+                 hc.flags, hc.undecided, hc.ev_n);
+  } else if (hc.ev_n > 0) {
+    // tail values: numpy computes R + (-1/R) log1p(-u1) with libm's log1p
+    hev.resize(hc.ev_n);
+    std::vector<int64_t> pj(hc.ev_n);
+    std::vector<double> pv(hc.ev_n);
+    if (cudaMemcpy(hev.data(), ev, hc.ev_n * sizeof(TailEvent), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      rc = set_err(nullptr, SPCA_ERR_CUDA, -1, "gaussian_device: event copy failed");
+    } else {
+      for (size_t i = 0; i < hev.size(); ++i) {
+        const double xx = (-inv_r) * std::log1p(-next_double(hev[i].u1));
+        pj[i] = hev[i].j;
+        pv[i] = hev[i].neg ? -(r_tail + xx) : r_tail + xx;
+      }
+      int64_t *dj = nullptr;
+      if (cudaMallocAsync((void **)&dj, hev.size() * 16, st) != cudaSuccess ||
+          cudaMemcpyAsync(dj, pj.data(), hev.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+          cudaMemcpyAsync(dj + hev.size(), pv.data(), hev.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+        rc = set_err(nullptr, SPCA_ERR_CUDA, -1, "gaussian_device: patch upload failed");
+      } else {
+        gauss_patch<<<(unsigned)((hev.size() + 255) / 256), 256, 0, st>>>(out, dj, (const double *)(dj + hev.size()),
+                                                                          (int64_t)hev.size());
+        if (cudaGetLastError() != cudaSuccess) rc = set_err(nullptr, SPCA_ERR_CUDA, -1, "gaussian_device: patch failed");
+      }
+      if (dj) cudaFreeAsync(dj, st);
+      // the host vectors must outlive the async copies
+      if (cudaStreamSynchronize(st) != cudaSuccess && rc == SPCA_OK)
+        rc = set_err(nullptr, SPCA_ERR_CUDA, -1, "gaussian_device: patch sync failed");
+    }
+  }
+  cudaFreeAsync(buf, st);
+  return rc;
 }
 
 int spca_last_error(spca_handle_t h, int *code, int64_t *bad_row, char *msg, size_t msg_len) {

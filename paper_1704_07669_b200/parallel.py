@@ -98,13 +98,13 @@ def sharded_single_pass_pca(local_rows, cfg, dist, group=None, precision: str = 
     torch = torch_mod()
     from .algorithms import TruncatedSvd, finish_svd
     from .errors import EmptyStreamError
-    from .linalg import STREAM_SKETCH, gaussian_matrix
+    from .linalg import STREAM_SKETCH, gaussian_matrix_device
     from .qb import blocked_qb
     from .sketch import sketch_pass
     from .streams import DeviceRowStream
 
     n = int(local_rows.shape[1])
-    omega = gaussian_matrix(n, cfg.l, cfg.seed, stream=STREAM_SKETCH)
+    omega = gaussian_matrix_device(n, cfg.l, cfg.seed, stream=STREAM_SKETCH, device=device)
     st = sketch_pass(DeviceRowStream(local_rows), omega, precision=precision,
                      device=device, keep_on_device=True, shift=cfg.center)
     h = st.h.clone()

@@ -66,7 +66,13 @@ class GpuSketch:
         self.lib = _lib.load()
         self.device = default_device(device)
         self.n = int(n)
-        om = np.ascontiguousarray(np.asarray(omega, dtype=np.float64))
+        om_dev = is_torch(omega) and omega.is_cuda  # drawn on the device (gaussian_matrix_device)
+        if om_dev:
+            om = omega.to(device=self.device, dtype=torch.float64).contiguous()
+            om_ptr, om_where = ctypes.c_void_p(om.data_ptr()), _lib.MEM_DEVICE
+        else:
+            om = np.ascontiguousarray(np.asarray(omega, dtype=np.float64))
+            om_ptr, om_where = om.ctypes.data_as(ctypes.c_void_p), _lib.MEM_PAGEABLE
         self.l = int(om.shape[1])
         self.dtype = np.dtype(dtype)
         if self.dtype not in (np.dtype(np.float32), np.dtype(np.float64)):
@@ -80,7 +86,7 @@ class GpuSketch:
         with torch.cuda.device(self.device):
             rc = self.lib.spca_sketch_create(
                 ctypes.byref(handle), self.n, self.l, code, prec,
-                om.ctypes.data_as(ctypes.c_void_p), _lib.MEM_PAGEABLE,
+                om_ptr, om_where,
                 # torch's default stream is the legacy NULL stream: hand the library
                 # cudaStreamLegacy (0x1) so both order on it (NULL would mean a
                 # private stream that does not synchronize with torch's work)
@@ -271,7 +277,7 @@ def run_pass(stream, omega, block_rows=None, compensated=False, precision="auto"
     shape for another traversal (reset first). ``shift`` turns on the column
     shift (spca_sketch_set_shift) — what the centered algorithms ask for, so
     post-hoc centering does not cancel fp32 rounding of a large mean."""
-    om = np.asarray(omega)
+    om = omega if is_torch(omega) else np.asarray(omega)
     n, l = om.shape
     outer = stream
     src = stream.wrapped if isinstance(stream, PassCounter) else stream
@@ -499,7 +505,7 @@ def sketch_pass(
     ``shift`` accumulates A - 1 c^T (c = the mean of the first rows) and adds the shift
     back in fp64: same results, fp32 accumulators sized by A's spread rather
     than its mean (the centered algorithms turn it on)."""
-    om = np.asarray(omega, dtype=np.float64)
+    om = omega if is_torch(omega) else np.asarray(omega, dtype=np.float64)
     if om.ndim != 2:
         raise StreamFormatError("omega must be 2-d")
     n, l = om.shape

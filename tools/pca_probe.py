@@ -29,7 +29,7 @@ for rep in range(3):
         T[name] = round(1e3 * (now - t), 2)
         t = now
 
-    om = P.gaussian_matrix(a.shape[1], cfg.l, cfg.seed, stream=STREAM_SKETCH)
+    om = P.gaussian_matrix_device(a.shape[1], cfg.l, cfg.seed, stream=STREAM_SKETCH)
     lap("omega")
     st = P.sketch_pass(P.DeviceRowStream(a), om, keep_on_device=True)
     lap("pass")
