@@ -253,13 +253,20 @@ def dense_svd(b, device=None) -> SvdTriple:
     b = to_device64(b, dev)
     if b.dim() != 2 or b.shape[0] < 1 or b.shape[1] < 1:
         raise DimensionError("dense_svd expects a nonempty 2-d array")
-    if not bool(torch.isfinite(b).all()):
-        raise DataError("dense_svd input contains non-finite entries")
     p, n = b.shape
+    gram_ok = False
     if n >= 4 * p:
-        tri = _gram_svd(b)
-        if tri is not None:
-            return tri
+        # any non-finite entry of B leaves a non-finite entry in B B^T, so a
+        # finite Gram matrix spares the n-long check (an overflowing Gram of a
+        # finite B only skips the Gram route)
+        w = b @ b.T
+        gram_ok = bool(torch.isfinite(w).all())
+        if gram_ok:
+            tri = _gram_svd(b, w)
+            if tri is not None:
+                return tri
+    if not gram_ok and not bool(torch.isfinite(b).all()):
+        raise DataError("dense_svd input contains non-finite entries")
     if n > 2 * p:
         qr = _cholesky_qr2(b.T) if n >= 64 * p else None        # well conditioned: two GEMM sweeps
         qb, rb = qr if qr is not None else torch.linalg.qr(b.T, mode="reduced")  # n x p, p x p
@@ -271,25 +278,31 @@ def dense_svd(b, device=None) -> SvdTriple:
     return SvdTriple(u=u, s=s, v=v)
 
 
-def _gram_svd(b):
+def _gram_svd(b, w=None):
     """Thin SVD of a wide, well-conditioned B (p x n, n >> p) from its Gram
     matrix: B B^T = U S^2 U^T (p x p symmetric eigenproblem), V = B^T U S^-1 —
     two GEMM sweeps over B and a p x p eigensolver instead of a tall QR of
     B^T plus a p x p SVD. The Gram squares the condition number, so it is
     taken only when every singular value is within a factor 100 of the
-    largest (relative errors then ~ eps * 1e4 ~ 1e-12 on S; the vectors'
-    orthogonality is checked below); otherwise None and the QR route runs
-    (the sketches of all five BASELINE configs have cond(B) < 3). Orientation of each pair (u_j, v_j) is left to sign_align, as the
+    largest (relative errors then ~ eps * 1e4 ~ 1e-12 on S); otherwise None
+    and the QR route runs (the sketches of all five BASELINE configs have
+    cond(B) < 3). V^T V = S^-1 U^T (B B^T) U S^-1 is checked on the p x p
+    side (U^T W U against S^2, U^T U against I: the eigensolver's accuracy;
+    forming V adds ~eps cond(B) on top), not with a third n-long GEMM.
+    Orientation of each pair (u_j, v_j) is left to sign_align, as the
     reference's dgesdd output is."""
     torch = torch_mod()
-    w = b @ b.T
+    if w is None:
+        w = b @ b.T
     evals, evecs = torch.linalg.eigh(w)  # ascending
     lmax = evals[-1]
     ok = (lmax > 0) & (evals[0] > 1e-4 * lmax) & torch.isfinite(evals).all()
     s = torch.sqrt(torch.clamp(evals.flip(0), min=0.0))
     u = evecs.flip(1)
     v = (b.T @ u) / s
-    defect = torch.abs(v.T @ v - torch.eye(b.shape[0], dtype=b.dtype, device=b.device)).max()
+    eye = torch.eye(b.shape[0], dtype=b.dtype, device=b.device)
+    vtv = (u.T @ w @ u) / (s[:, None] * s[None, :])
+    defect = torch.maximum(torch.abs(vtv - eye).max(), torch.abs(u.T @ u - eye).max())
     ok = ok & (defect < 1e-9)
     if not bool(ok):  # one host synchronization
         return None
