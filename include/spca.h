@@ -225,7 +225,10 @@ int spca_normalize_rows(const void *src, int64_t rows, int64_t n, int64_t ld_src
  * G_i points at the block's first column (row stride ldg). On return (stream
  * ordered): p_out = [y^T Q | y^T y] (b x (c0 + b), row-major), factors =
  * ten b x b upper-triangular matrices R1, R2, r_i, R3, R4, R_i, R1^-1,
- * R1^-1 R2^-1, R3^-1, R3^-1 R4^-1 (R_i = factors[5] feeds the
+ * R1^-1 R2^-1, R3^-1, R3^-1 R4^-1, then an eleventh b x b scratch whose first
+ * two entries flag a skipped second CholeskyQR pass (R2 = I / R4 = I: a block
+ * with cond_F(R) <= 16, where one pass is accurate to ~1e-13; SPCA_QB_CQ2=1
+ * forces both passes) (R_i = factors[5] feeds the
  * caller's B_i = R_i^-T (H_i^T - (y^T Q) B - (Omega_i^T B^T) B)), and *flag
  * set to 1 if any test of the optimistic path failed (Cholesky breakdown,
  * CholeskyQR2 defect >= 1e-5, |r_jj| < *tol (qb.py:100), solve_rt's

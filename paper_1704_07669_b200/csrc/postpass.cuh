@@ -61,6 +61,7 @@ constexpr int kQbLdt = 24;
 constexpr int kQbLdw = 24;
 constexpr int kQbNtw = kQbMaxCat / 8 / kQbWarps;   // 8-column tiles of [Q | t] per warp (at most)
 constexpr int kQbMaxStages = 3;
+constexpr double kQbCq1Cond = 16.0;  // one-pass CholeskyQR up to this Frobenius condition number
 
 struct QbSweepArgs {
   int64_t m;
@@ -73,6 +74,7 @@ struct QbSweepArgs {
   double *part;           // [gridDim.x][b][c0 + b]
   const double *y1d;      // y rows as one contiguous m x b block (row stride b): each tile is
                           // one 1-D bulk copy instead of a tensor-map box of narrow rows
+  const double *skip;     // nonzero *skip: the sweep is not needed (one-pass CholeskyQR), or null
 };
 
 // fp64 tensor-core step D(16x8) += A(16x4, row) B(4x8, col) (fragments: a0 =
@@ -131,6 +133,7 @@ __global__ void __launch_bounds__(kQbThreads, 2) qb_sweep_kernel(const __grid_co
   constexpr int NH = B > 8 ? 2 : 1;  // 8-column halves of b
   constexpr int KM = (B + 3) & ~3;   // rows of M in the operand block
   constexpr bool HX = KIND & kQbX, WP = KIND & kQbP, WW = KIND & kQbW, WO = KIND & kQbOut;
+  if (a.skip && *a.skip != 0.0) return;  // uniform over the grid
   const int c0 = a.c0, tr = a.tr, nslab = a.nslab, nst = a.stages;
   const int c04 = (c0 + 3) & ~3, kb = qb_kb(c0, b);
   const size_t sbytes = qb_stage_bytes(nslab, b, tr);
@@ -399,7 +402,8 @@ __device__ void qb_inv_upper_w(const double *r, double *ri, int b) {
 //        diag(R_i) (linalg.py:131-135)
 // the b x b algebra of one step on W (shared memory, row-major b x b), by
 // warp 0 of the calling block
-__device__ void qb_small_ops(int op, int b, const double *w, double *st, int *flag, const double *tol) {
+__device__ void qb_small_ops(int op, int b, const double *w, double *st, int *flag, const double *tol,
+                             bool allow_one = false, double *skip_out = nullptr) {
   __shared__ double f[10][kQbMaxB * kQbMaxB], tmp[kQbMaxB * kQbMaxB];
   const int bb = b * b, lane = threadIdx.x & 31;
   for (int e = lane; e < bb; e += 32)
@@ -408,8 +412,50 @@ __device__ void qb_small_ops(int op, int b, const double *w, double *st, int *fl
   bool ok = true;
   if (op == 1 || op == 3) {
     double *R = op == 1 ? f[0] : f[3];
+    double *Ri = op == 1 ? f[6] : f[8];
     ok = qb_chol_upper_w(w, R, b);
-    qb_inv_upper_w(R, op == 1 ? f[6] : f[8], b);
+    qb_inv_upper_w(R, Ri, b);
+    // One-pass CholeskyQR suffices when the block is well conditioned: its
+    // orthogonality defect is ~ eps cond(y)^2, so with cond_F(R) = ||R||_F
+    // ||R^-1||_F <= kQbCq1Cond (cond_2 <= cond_F) the second pass would only
+    // correct ~1e-13. Then R2 = I (R4 = I): the steps of op 2 (op 4) run here
+    // and the second pass's sweep and reduction are skipped on the device.
+    double fr = 0.0, fi = 0.0;
+    for (int e = lane; e < bb; e += 32) {
+      fr += R[e] * R[e];
+      fi += Ri[e] * Ri[e];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      fr += __shfl_xor_sync(0xffffffffu, fr, o);
+      fi += __shfl_xor_sync(0xffffffffu, fi, o);
+    }
+    const bool one = allow_one && ok && sqrt(fr) * sqrt(fi) <= kQbCq1Cond && isfinite(fr * fi);
+    if (one) {
+      double *Rb = op == 1 ? f[1] : f[4];
+      for (int e = lane; e < bb; e += 32) {
+        Rb[e] = (e / b == e % b) ? 1.0 : 0.0;
+        (op == 1 ? f[7] : f[9])[e] = Ri[e];
+      }
+      __syncwarp();
+      if (op == 1) {
+        for (int e = lane; e < bb; e += 32) f[2][e] = R[e];  // r_i = R1
+        __syncwarp();
+        const double tl = *tol;
+        for (int j = lane; j < b; j += 32) {
+          const double d = f[2][j * b + j];
+          ok = ok && isfinite(d) && !(fabs(d) < tl);
+        }
+      } else {
+        qb_mul_upper_w(f[3], f[2], f[5], b);  // R_i = R3 r_i
+        double mx = 0.0;
+        for (int j = 0; j < b; ++j) mx = fmax(mx, fabs(f[5][j * b + j]));
+        for (int j = lane; j < b; j += 32) {
+          const double d = fabs(f[5][j * b + j]);
+          ok = ok && isfinite(d) && !(d < 1e-300) && !(d < 1e-15 * mx);
+        }
+      }
+    }
+    if (lane == 0 && skip_out) *skip_out = one ? 1.0 : 0.0;
   } else {
     double defect = 0.0;
     for (int e = lane; e < bb; e += 32) defect = fmax(defect, fabs(w[e] - (e % (b + 1) == 0 ? 1.0 : 0.0)));
@@ -455,12 +501,12 @@ __device__ void qb_small_ops(int op, int b, const double *w, double *st, int *fl
 //        diag(R_i) (linalg.py:131-135)
 // W is the t^T t block of the reduced [t^T Q | t^T t] (b x ncat).
 __global__ void qb_small_kernel(int op, int b, int ncat, int c0, const double *redm, double *st, int *flag,
-                                const double *tol) {
+                                const double *tol, int allow_one, double *skip_out) {
   __shared__ double w[kQbMaxB * kQbMaxB];
   const int lane = threadIdx.x & 31;
   for (int e = lane; e < b * b; e += 32) w[e] = redm[(size_t)(e / b) * ncat + c0 + e % b];
   __syncwarp();
-  qb_small_ops(op, b, w, st, flag, tol);
+  qb_small_ops(op, b, w, st, flag, tol, allow_one != 0, skip_out);
 }
 
 // W-only sweeps (S2, S4, S5): the fixed-order reduction of the t^T t block
@@ -469,8 +515,10 @@ __global__ void qb_small_kernel(int op, int b, int ncat, int c0, const double *r
 // eight group sums are added in a fixed tree, then warp 0 runs the step.
 __global__ void __launch_bounds__(256) qb_wfinish_kernel(int op, int b, int ncat, int c0,
                                                          const double *__restrict__ part, int nparts, double *st,
-                                                         int *flag, const double *tol) {
+                                                         int *flag, const double *tol, const double *skip,
+                                                         int allow_one, double *skip_out) {
   __shared__ double sh[8][kQbMaxB * kQbMaxB], w[kQbMaxB * kQbMaxB];
+  if (skip && *skip != 0.0) return;  // one-pass CholeskyQR: op 1 / op 3 did this step
   const int bb = b * b, ne = b * ncat;
   for (int i = threadIdx.x; i < 8 * bb; i += blockDim.x) {
     const int g = i / bb, e = i - g * bb;
@@ -491,7 +539,7 @@ __global__ void __launch_bounds__(256) qb_wfinish_kernel(int op, int b, int ncat
   for (int e = threadIdx.x; e < bb; e += blockDim.x)
     w[e] = ((sh[0][e] + sh[1][e]) + (sh[2][e] + sh[3][e])) + ((sh[4][e] + sh[5][e]) + (sh[6][e] + sh[7][e]));
   __syncthreads();
-  if (threadIdx.x < 32) qb_small_ops(op, b, w, st, flag, tol);
+  if (threadIdx.x < 32) qb_small_ops(op, b, w, st, flag, tol, allow_one != 0, skip_out);
 }
 
 }  // namespace spca

@@ -1315,12 +1315,17 @@ int spca_qb_block(int64_t m, int c0, int b, double *q, int64_t ldq, const double
   int parts = 1;  // of the last sweep (its reduction)
   const int bb = b * b;  // factors: see qb_small_kernel
   double *M1 = factors + 6 * bb, *M12 = factors + 7 * bb, *M3 = factors + 8 * bb, *M34 = factors + 9 * bb;
+  // factors[10]: skip flags of the two second CholeskyQR passes (one-pass CholeskyQR for a
+  // well-conditioned block, decided on the device by op 1 / op 3)
+  double *skip1 = factors + 10 * bb, *skip2 = skip1 + 1;
+  static const bool cq2_always = getenv("SPCA_QB_CQ2") != nullptr;  // A/B knob: always two passes
   const unsigned rblocks = (unsigned)ceil_div((int64_t)b * ncat, 32);
   // from_g: the sweep's y rows are G_i (tensor map, row stride ldg), else the
   // contiguous scratch ybuf (one bulk copy per tile)
-  auto sweep = [&](bool from_g, const double *mt, const double *xx, double *out, int64_t ldo, int wp,
-                   int ww) -> cudaError_t {
+  auto sweep = [&](bool from_g, const double *mt, const double *xx, double *out, int64_t ldo, int wp, int ww,
+                   const double *skip = nullptr) -> cudaError_t {
     spca::QbSweepArgs a{};
+    a.skip = skip;
     const bool need_q = c0 > 0 && (xx != nullptr || wp);
     const int nslab = need_q ? (c0 + 15) / 16 : 0;
     const int kind = (xx ? spca::kQbX : 0) | (wp ? spca::kQbP : 0) | (ww ? spca::kQbW : 0) | (out ? spca::kQbOut : 0);
@@ -1356,12 +1361,14 @@ int spca_qb_block(int64_t m, int c0, int b, double *q, int64_t ldq, const double
     spca::qb_reduce_kernel<<<rblocks, 256, 0, st>>>(part, parts, b, ncat, dst, xtrans, c0);
     return cudaGetLastError();
   };
-  auto small = [&](int op, const double *r) -> cudaError_t {
-    spca::qb_small_kernel<<<1, 32, 0, st>>>(op, b, ncat, c0, r, factors, flag, tol);
+  auto small = [&](int op, const double *r, double *skip_out) -> cudaError_t {
+    spca::qb_small_kernel<<<1, 32, 0, st>>>(op, b, ncat, c0, r, factors, flag, tol, cq2_always ? 0 : 1, skip_out);
     return cudaGetLastError();
   };
-  auto wfinish = [&](int op) -> cudaError_t {  // reduction of the t^T t block + the b x b step
-    spca::qb_wfinish_kernel<<<1, 256, 0, st>>>(op, b, ncat, c0, part, parts, factors, flag, tol);
+  // reduction of the t^T t block + the b x b step; skip: the step was done by op 1 / op 3
+  auto wfinish = [&](int op, const double *skip, double *skip_out) -> cudaError_t {
+    spca::qb_wfinish_kernel<<<1, 256, 0, st>>>(op, b, ncat, c0, part, parts, factors, flag, tol, skip,
+                                               cq2_always ? 0 : 1, skip_out);
     return cudaGetLastError();
   };
   static const bool sync_each = getenv("SPCA_QB_SYNC") != nullptr;  // debugging: fault localisation
@@ -1375,20 +1382,20 @@ int spca_qb_block(int64_t m, int c0, int b, double *q, int64_t ldq, const double
   // S1: y = G_i - Q X; [y^T Q | y^T y] (kept for the B update)
   QB_TRY(sweep(true, nullptr, c0 ? x : nullptr, ybuf, b, c0 ? 1 : 0, 1));
   QB_TRY(reduce(p_out, nullptr));
-  QB_TRY(small(1, p_out));
-  // S2: Q1 = y R1^-1, Q1^T Q1
-  QB_TRY(sweep(false, M1, nullptr, nullptr, 0, 0, 1));
-  QB_TRY(wfinish(2));
+  QB_TRY(small(1, p_out, skip1));
+  // S2: Q1 = y R1^-1, Q1^T Q1 (skipped on the device for a well-conditioned y)
+  QB_TRY(sweep(false, M1, nullptr, nullptr, 0, 0, 1, skip1));
+  QB_TRY(wfinish(2, skip1, nullptr));
   if (c0 > 0) {  // S3: Q^T Q2 (Q2 = y R1^-1 R2^-1), kept transposed as the next X
     QB_TRY(sweep(false, M12, nullptr, nullptr, 0, 1, 0));
     QB_TRY(reduce(red, xt));
   }
   // S4: z = Q2 - Q (Q^T Q2), z^T z
   QB_TRY(sweep(false, M12, c0 ? xt : nullptr, ybuf, b, 0, 1));
-  QB_TRY(wfinish(3));
-  // S5: Z1 = z R3^-1, Z1^T Z1
-  QB_TRY(sweep(false, M3, nullptr, nullptr, 0, 0, 1));
-  QB_TRY(wfinish(4));
+  QB_TRY(wfinish(3, nullptr, skip2));
+  // S5: Z1 = z R3^-1, Z1^T Z1 (skipped on the device for a well-conditioned z)
+  QB_TRY(sweep(false, M3, nullptr, nullptr, 0, 0, 1, skip2));
+  QB_TRY(wfinish(4, skip2, nullptr));
   // S6: Q_i = z R3^-1 R4^-1 into Q's columns [c0, c0 + b)
   QB_TRY(sweep(false, M34, nullptr, q + c0, ldq, 0, 0));
 #undef QB_TRY
