@@ -256,6 +256,21 @@ int spca_qb_block(int64_t m, int c0, int b, double *q, int64_t ldq, const double
 int spca_gaussian_device(double *out, int64_t count, uint64_t seed, uint64_t stream_id, const double *w,
                          const uint64_t *k, const double *f, double r_tail, double inv_r, void *stream);
 
+/* ---- post-pass: the B side of one QB block (qb.py:96 and :115-118) -----
+ * spca_qb_omega_proj: X = B[:c0] Omega_i (c0 x b, row-major), B row-major
+ * (row stride ldb), omega pointing at column c0 of Omega (row stride ldo);
+ * ws: spca_qb_omega_proj_ws(n, c0, b) doubles (fixed-order split-K partials).
+ * spca_qb_b_rows: rows [c0, c0 + b) of B,
+ *   B_i = R_i^-T (H[:, c0:c0+b]^T - (y^T Q + X^T) B[:c0]),
+ * h pointing at column c0 of H (row stride ldh), p_out = spca_qb_block's
+ * [y^T Q | y^T y] (b x (c0 + b)), r_i = its factors[5], b_out pointing at
+ * row c0 of B (row stride ldb). Device pointers, b even in [2, 16]. */
+int64_t spca_qb_omega_proj_ws(int64_t n, int c0_max, int b);
+int spca_qb_omega_proj(int64_t n, int c0, int b, const double *bm, int64_t ldb, const double *omega, int64_t ldo,
+                       double *x, double *ws, int64_t ws_elems, void *stream);
+int spca_qb_b_rows(int64_t n, int c0, int b, const double *bm, int64_t ldb, const double *h, int64_t ldh,
+                   const double *p_out, const double *x, const double *r_i, double *b_out, void *stream);
+
 int spca_last_error(spca_handle_t h, int *code, int64_t *bad_row, char *msg,
                     size_t msg_len);
 

@@ -59,6 +59,11 @@ SIGNATURES = {
                               c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "spca_gaussian_device": (c_int, [c_void_p, c_int64, ctypes.c_uint64, ctypes.c_uint64, c_void_p, c_void_p,
                                      c_void_p, c_double, c_double, c_void_p]),
+    "spca_qb_omega_proj_ws": (c_int64, [c_int64, c_int, c_int]),
+    "spca_qb_omega_proj": (c_int, [c_int64, c_int, c_int, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
+                                   c_int64, c_void_p]),
+    "spca_qb_b_rows": (c_int, [c_int64, c_int, c_int, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
+                               c_void_p, c_void_p, c_void_p]),
     "spca_last_error": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int64), c_char_p, c_size_t]),
     "spca_kernel_launches": (c_int64, [c_void_p]),
     "spca_enable_kernel_timing": (c_int, [c_void_p, c_int]),

@@ -101,6 +101,20 @@ __host__ __device__ inline uint64_t raw_at(uint64_t k, uint64_t key0, uint64_t k
 
 __host__ __device__ inline double next_double(uint64_t v) { return (double)(v >> 11) * (1.0 / 9007199254740992.0); }
 
+// raw draws pos + lane (lane = 0..31) of one warp: the 9 Philox blocks that
+// cover them are computed once (lanes 0..8) and their words handed out by
+// shuffles (each block serves four draws)
+__device__ __forceinline__ uint64_t warp_raw(int64_t pos, int lane, uint64_t key0, uint64_t key1) {
+  uint64_t b[4] = {0, 0, 0, 0};
+  const uint64_t base = (uint64_t)pos >> 2;
+  if (lane < 9) philox_block(base + lane + 1, key0, key1, b);
+  const int idx = (int)(pos & 3) + lane;  // draw index from the first block's word 0
+  const int src = idx >> 2, wd = idx & 3;
+  const uint64_t w0 = __shfl_sync(0xffffffffu, b[0], src), w1 = __shfl_sync(0xffffffffu, b[1], src);
+  const uint64_t w2 = __shfl_sync(0xffffffffu, b[2], src), w3 = __shfl_sync(0xffffffffu, b[3], src);
+  return wd == 0 ? w0 : (wd == 1 ? w1 : (wd == 2 ? w2 : w3));
+}
+
 struct Walk {
   const Tables *t;  // in shared memory
   uint64_t key0, key1;
@@ -198,7 +212,7 @@ __global__ void __launch_bounds__(256) gauss_walk(Tables tab_in, uint64_t key0, 
   while (after < 0) {
     if (first < 0 && pos >= A) first = pos;
     const int64_t kk = pos + lane;
-    const uint64_t r = raw_at((uint64_t)kk, key0, key1);
+    const uint64_t r = warp_raw(pos, lane, key0, key1);
     const int idx = (int)(r & 0xff);
     const uint64_t rabs = (r >> 9) & kMask52;
     const bool fast = rabs < tab.k[idx];

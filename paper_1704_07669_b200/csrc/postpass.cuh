@@ -543,3 +543,136 @@ __global__ void __launch_bounds__(256) qb_wfinish_kernel(int op, int b, int ncat
 }
 
 }  // namespace spca
+
+namespace spca {
+
+// ------------------------------------------------ B side of a QB block
+// The two n-long products of a block (qb.py:96 and :115-118) on fp64 CUDA
+// cores: they read the accepted rows of B (c0 x n, up to 384 MB at config 5)
+// once each, where library GEMMs of these skinny shapes ran at 1-3 TB/s.
+//
+// X = B[:c0] Omega_i (c0 x b), K = n split over the CTAs: a CTA stages its
+// K-chunk of Omega_i (chunk x b) in shared memory; warp w takes rows
+// w, w + 8, ... in groups of R, every lane a strided subset of the chunk's
+// k, accumulating R x b sums that are butterfly-reduced across the warp in a
+// fixed pattern; partials [chunk][c0][b] are reduced in a fixed order by
+// qb_reduce_kernel (bitwise reproducible).
+template <int B>
+__global__ void __launch_bounds__(256, 2) qb_omega_proj_kernel(int64_t n, int c0, const double *__restrict__ bm,
+                                                               int64_t ldb, const double *__restrict__ om,
+                                                               int64_t ldo, int64_t kchunk,
+                                                               double *__restrict__ part) {
+  extern __shared__ __align__(16) double osm[];  // [B][kchunk]: lane-consecutive k, conflict-free
+  constexpr int R = 2, U = 8;  // rows per warp pass, 32-wide k steps in flight (R * U loads per lane)
+  const int64_t k0 = (int64_t)blockIdx.x * kchunk;
+  const int kn = (int)(kchunk < n - k0 ? kchunk : n - k0);
+  const int kc = (int)kchunk;
+#pragma unroll 8
+  for (int i = threadIdx.x; i < kn * B; i += blockDim.x) {  // eight loads in flight per thread
+    const int k = i / B, j = i - k * B;
+    osm[j * kc + k] = __ldg(om + (k0 + k) * ldo + j);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *p = part + (size_t)blockIdx.x * c0 * B;
+  for (int r0 = warp * R; r0 < c0; r0 += 8 * R) {
+    double acc[R][B];
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+      for (int j = 0; j < B; ++j) acc[q][j] = 0.0;
+    for (int kb = 0; kb < kn; kb += 32 * U) {
+      double bv[U][R];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = kb + 32 * u + lane;
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+          bv[u][q] = (k < kn && r0 + q < c0) ? __ldg(bm + (size_t)(r0 + q) * ldb + k0 + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = kb + 32 * u + lane;
+        if (k < kn) {
+#pragma unroll
+          for (int j = 0; j < B; ++j) {
+            const double ov = osm[j * kc + k];
+#pragma unroll
+            for (int q = 0; q < R; ++q) acc[q][j] = fma(bv[u][q], ov, acc[q][j]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        double v = acc[q][j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        acc[q][j] = v;
+      }
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (r0 + q < c0)
+#pragma unroll
+          for (int j = 0; j < B; ++j) p[(size_t)(r0 + q) * B + j] = acc[q][j];
+  }
+}
+
+// B_i (rows [c0, c0 + b) of B, all n columns) in one pass over B[:c0]:
+//   B_i = R_i^-T (H_i^T - (y^T Q + X^T) B[:c0])       (qb.py:115-118)
+// one thread per column k: rhs = H[k, c0:c0+b] - M B[:c0, k] with
+// M = y^T Q + X^T (b x c0, in shared memory, read as broadcasts), then the
+// lower-triangular solve with R_i^T by forward substitution.
+template <int B>
+__global__ void __launch_bounds__(256) qb_b_rows_kernel(int64_t n, int c0, const double *__restrict__ bm,
+                                                        int64_t ldb, const double *__restrict__ h, int64_t ldh,
+                                                        const double *__restrict__ p_out,
+                                                        const double *__restrict__ x,
+                                                        const double *__restrict__ ri, double *__restrict__ bout) {
+  extern __shared__ __align__(16) double msm[];  // [c0][B]: M^T, then R_i (B x B)
+  double *rs = msm + (size_t)c0 * B;
+  const int ncat = c0 + B;
+  for (int i = threadIdx.x; i < c0 * B; i += blockDim.x) {
+    const int r = i / B, j = i - r * B;
+    msm[i] = p_out[(size_t)j * ncat + r] + x[(size_t)r * B + j];
+  }
+  for (int i = threadIdx.x; i < B * B; i += blockDim.x) rs[i] = ri[i];
+  __syncthreads();
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double acc[B];
+#pragma unroll
+  for (int j = 0; j < B; ++j) acc[j] = h[k * ldh + j];
+  int r = 0;
+  for (; r + 8 <= c0; r += 8) {  // eight loads of B in flight
+    double bv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bv[u] = __ldg(bm + (size_t)(r + u) * ldb + k);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double *mr = msm + (r + u) * B;
+#pragma unroll
+      for (int j = 0; j < B; ++j) acc[j] = fma(-mr[j], bv[u], acc[j]);
+    }
+  }
+  for (; r < c0; ++r) {
+    const double bv = __ldg(bm + (size_t)r * ldb + k);
+    const double *mr = msm + r * B;
+#pragma unroll
+    for (int j = 0; j < B; ++j) acc[j] = fma(-mr[j], bv, acc[j]);
+  }
+  // R_i^T z = acc: z_j = (acc_j - sum_{i<j} R[i][j] z_i) / R[j][j]
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    double s = acc[j];
+#pragma unroll
+    for (int i = 0; i < j; ++i) s = fma(-rs[i * B + j], acc[i], s);
+    acc[j] = s / rs[j * B + j];
+    bout[(size_t)j * ldb + k] = acc[j];
+  }
+}
+
+}  // namespace spca

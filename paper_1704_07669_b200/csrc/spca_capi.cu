@@ -1402,6 +1402,99 @@ int spca_qb_block(int64_t m, int c0, int b, double *q, int64_t ldq, const double
   return SPCA_OK;
 }
 
+// --- the B side of a QB block (postpass.cuh): X = B[:c0] Omega_i and B_i
+extern "C++" {
+namespace {
+int64_t qb_proj_chunk(int64_t n, int sms) {
+  int64_t kc = (n + 2 * (int64_t)sms - 1) / (2 * sms);  // about two CTAs per SM
+  kc = std::max<int64_t>(32, (kc + 31) / 32 * 32);
+  return std::min<int64_t>(kc, 1536);  // shared-memory stage: kc x b doubles <= 192 KB
+}
+template <int B>
+cudaError_t qb_proj_launch(int64_t n, int c0, const double *bm, int64_t ldb, const double *om, int64_t ldo,
+                           double *x, double *ws, int sms, cudaStream_t st) {
+  const int64_t kc = qb_proj_chunk(n, sms);
+  const int chunks = (int)((n + kc - 1) / kc);
+  const size_t smem = (size_t)kc * B * sizeof(double);
+  static std::once_flag once;
+  static cudaError_t ae = cudaSuccess;
+  std::call_once(once, [] {
+    ae = cudaFuncSetAttribute(spca::qb_omega_proj_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              1536 * B * (int)sizeof(double));
+  });
+  if (ae != cudaSuccess) return ae;
+  spca::qb_omega_proj_kernel<B><<<chunks, 256, smem, st>>>(n, c0, bm, ldb, om, ldo, kc, ws);
+  spca::qb_reduce_kernel<<<(unsigned)ceil_div((int64_t)c0 * B, 32), 256, 0, st>>>(ws, chunks, c0, B, x, nullptr, 0);
+  return cudaGetLastError();
+}
+template <int B>
+cudaError_t qb_brows_launch(int64_t n, int c0, const double *bm, int64_t ldb, const double *h, int64_t ldh,
+                            const double *p_out, const double *x, const double *ri, double *bout, cudaStream_t st) {
+  const size_t smem = ((size_t)c0 * B + B * B) * sizeof(double);
+  spca::qb_b_rows_kernel<B><<<(unsigned)ceil_div(n, 256), 256, smem, st>>>(n, c0, bm, ldb, h, ldh, p_out, x, ri,
+                                                                           bout);
+  return cudaGetLastError();
+}
+}  // namespace
+}  // extern "C++"
+
+int64_t spca_qb_omega_proj_ws(int64_t n, int c0_max, int b) {
+  if (n < 1 || c0_max < 0 || b < 1) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t kc = qb_proj_chunk(n, sms);
+  return ((n + kc - 1) / kc) * (int64_t)std::max(c0_max, 1) * b;
+}
+
+int spca_qb_omega_proj(int64_t n, int c0, int b, const double *bm, int64_t ldb, const double *omega, int64_t ldo,
+                       double *x, double *ws, int64_t ws_elems, void *stream) {
+  if (n < 1 || c0 < 1 || b < 2 || b > spca::kQbMaxB || (b & 1) || !bm || !omega || !x || !ws)
+    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "qb_omega_proj: unsupported arguments (n %lld c0 %d b %d)",
+                   (long long)n, c0, b);
+  if (ws_elems < spca_qb_omega_proj_ws(n, c0, b))
+    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "qb_omega_proj: workspace too small");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  switch (b) {
+    case 2: e = qb_proj_launch<2>(n, c0, bm, ldb, omega, ldo, x, ws, sms, st); break;
+    case 4: e = qb_proj_launch<4>(n, c0, bm, ldb, omega, ldo, x, ws, sms, st); break;
+    case 6: e = qb_proj_launch<6>(n, c0, bm, ldb, omega, ldo, x, ws, sms, st); break;
+    case 8: e = qb_proj_launch<8>(n, c0, bm, ldb, omega, ldo, x, ws, sms, st); break;
+    case 10: e = qb_proj_launch<10>(n, c0, bm, ldb, omega, ldo, x, ws, sms, st); break;
+    case 12: e = qb_proj_launch<12>(n, c0, bm, ldb, omega, ldo, x, ws, sms, st); break;
+    case 14: e = qb_proj_launch<14>(n, c0, bm, ldb, omega, ldo, x, ws, sms, st); break;
+    default: e = qb_proj_launch<16>(n, c0, bm, ldb, omega, ldo, x, ws, sms, st); break;
+  }
+  if (e != cudaSuccess) return set_err(nullptr, SPCA_ERR_CUDA, -1, "qb_omega_proj: %s", cudaGetErrorString(e));
+  return SPCA_OK;
+}
+
+int spca_qb_b_rows(int64_t n, int c0, int b, const double *bm, int64_t ldb, const double *h, int64_t ldh,
+                   const double *p_out, const double *x, const double *r_i, double *b_out, void *stream) {
+  if (n < 1 || c0 < 0 || c0 + b > spca::kQbMaxCat || b < 2 || b > spca::kQbMaxB || (b & 1) || !h || !p_out ||
+      !r_i || !b_out || (c0 > 0 && (!bm || !x)))
+    return set_err(nullptr, SPCA_ERR_CONFIG, -1, "qb_b_rows: unsupported arguments (n %lld c0 %d b %d)",
+                   (long long)n, c0, b);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  switch (b) {
+    case 2: e = qb_brows_launch<2>(n, c0, bm, ldb, h, ldh, p_out, x, r_i, b_out, st); break;
+    case 4: e = qb_brows_launch<4>(n, c0, bm, ldb, h, ldh, p_out, x, r_i, b_out, st); break;
+    case 6: e = qb_brows_launch<6>(n, c0, bm, ldb, h, ldh, p_out, x, r_i, b_out, st); break;
+    case 8: e = qb_brows_launch<8>(n, c0, bm, ldb, h, ldh, p_out, x, r_i, b_out, st); break;
+    case 10: e = qb_brows_launch<10>(n, c0, bm, ldb, h, ldh, p_out, x, r_i, b_out, st); break;
+    case 12: e = qb_brows_launch<12>(n, c0, bm, ldb, h, ldh, p_out, x, r_i, b_out, st); break;
+    case 14: e = qb_brows_launch<14>(n, c0, bm, ldb, h, ldh, p_out, x, r_i, b_out, st); break;
+    default: e = qb_brows_launch<16>(n, c0, bm, ldb, h, ldh, p_out, x, r_i, b_out, st); break;
+  }
+  if (e != cudaSuccess) return set_err(nullptr, SPCA_ERR_CUDA, -1, "qb_b_rows: %s", cudaGetErrorString(e));
+  return SPCA_OK;
+}
+
 int spca_center_correct(spca_handle_t h, int64_t m_total, const double *gsum, double *mean_out,
                         int mean_where) {
   if (!h) return set_err(nullptr, SPCA_ERR_STATE, -1, "null handle");
