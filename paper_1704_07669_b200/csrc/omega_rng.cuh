@@ -24,12 +24,13 @@
 // value starts merges with the true one within a few values) and walks the
 // chain 32 draws at a time: a ballot over 32 consecutive draws finds the
 // first one that is not a fast-path start; every draw before it is a value
-// start, and lane 0 evaluates the slow start alone. Pass 1 counts the value
-// starts inside each segment and records the first start at or after the
-// segment's beginning (entry) and after its end (exit); segment w + 1 is
-// the true chain exactly when entry[w + 1] == exit[w] (segment 0 starts at
-// draw 0, the true start), which the scan checks; pass 2 walks again and
-// writes value j = offset[w] + local index.
+// start, and lane 0 evaluates the slow start alone. The walk counts the
+// value starts inside each segment, stages their values at w L + i and
+// records the first start at or after the segment's beginning (entry) and
+// after its end (exit); segment w + 1 is the true chain exactly when
+// entry[w + 1] == exit[w] (segment 0 starts at draw 0, the true start),
+// which the scan checks while it forms the offsets; a gather moves value i
+// of segment w to j = offset[w] + i.
 //
 // Exactness: the fast path and accepted layer values are x = rabs * w[idx]
 // (one IEEE product, no contraction): exact. The layer and tail tests use
@@ -182,7 +183,10 @@ __device__ inline SlowValue slow_value(const Walk &W, int64_t pos) {
 
 // Walk the chain of value starts over segment w = [A, A + L) of the raw
 // stream (one warp). PASS 1: cnt[w], entry[w], exit_[w]. PASS 2: values
-// j = off[w] + i (j < count) into out, tail events appended at ev.
+// j = off[w] + i (j < count) into out, tail events appended at ev. PASS 3
+// (the default): PASS 1 and the values staged at out[w L + i] (a segment
+// holds at most L values), tail events with that staged index; gauss_gather
+// then moves them to j = off[w] + i — one walk instead of two.
 template <int PASS>
 __global__ void __launch_bounds__(256) gauss_walk(Tables tab_in, uint64_t key0, uint64_t key1, int64_t L,
                                                   int64_t margin, int nseg, int64_t *cnt, int64_t *entry,
@@ -207,7 +211,9 @@ __global__ void __launch_bounds__(256) gauss_walk(Tables tab_in, uint64_t key0, 
   const int64_t A = (int64_t)w * L, E = A + L;
   int64_t pos = w == 0 ? 0 : A - margin;  // always a value start (speculatively before A)
   int64_t n_in = 0, first = -1, after = -1;
-  int64_t j = PASS == 2 ? off[w] : 0;
+  int64_t j = PASS == 2 ? off[w] : (PASS == 3 ? (int64_t)w * L : 0);
+  constexpr bool WR = PASS >= 2;
+  const int64_t cap = PASS == 3 ? INT64_MAX : count;
   bool und = false;
   while (after < 0) {
     if (first < 0 && pos >= A) first = pos;
@@ -222,9 +228,9 @@ __global__ void __launch_bounds__(256) gauss_walk(Tables tab_in, uint64_t key0, 
     const bool mine = lane < p && kk >= A && kk < E;
     const unsigned mm = __ballot_sync(0xffffffffu, mine);
     if (first < 0 && mm) first = pos + (__ffs(mm) - 1);
-    if (PASS == 2 && mine) {
+    if (WR && mine) {
       const int64_t jj = j + __popc(mm & ((1u << lane) - 1));
-      if (jj < count) {
+      if (jj < cap) {
         double x = __dmul_rn((double)rabs, tab.w[idx]);
         if ((r >> 8) & 1) x = -x;
         out[jj] = x;
@@ -249,7 +255,7 @@ __global__ void __launch_bounds__(256) gauss_walk(Tables tab_in, uint64_t key0, 
       if (pos >= A) {
         if (lane == 0) {
           und |= sv.undecided != 0;
-          if (PASS == 2 && j < count) {
+          if (WR && j < cap) {
             out[j] = sv.v;
             if (sv.tail) {
               const unsigned long long e = atomicAdd(ev_n, 1ull);
@@ -266,7 +272,7 @@ __global__ void __launch_bounds__(256) gauss_walk(Tables tab_in, uint64_t key0, 
     if (PASS == 2 && j >= count) break;
   }
   if (lane == 0) {
-    if (PASS == 1) {
+    if (PASS != 2) {
       cnt[w] = n_in;
       entry[w] = first < 0 ? after : first;
       exit_[w] = after;
@@ -307,6 +313,16 @@ __global__ void gauss_scan(const int64_t *cnt, const int64_t *entry, const int64
     run += cnt[w];
   }
   if (bad) atomicOr(flags, 1);
+}
+
+// staged values of segment w (PASS 3) -> their places j = off[w] + i (< count)
+__global__ void __launch_bounds__(256) gauss_gather(const double *__restrict__ stage, int64_t L,
+                                                    const int64_t *cnt, const int64_t *off, double *out,
+                                                    int64_t count) {
+  const int w = blockIdx.x;
+  const int64_t c = cnt[w], o = off[w];
+  const double *src = stage + (size_t)w * L;
+  for (int64_t i = threadIdx.x; i < c && o + i < count; i += blockDim.x) out[o + i] = src[i];
 }
 
 __global__ void gauss_patch(double *out, const int64_t *j, const double *v, int64_t n) {

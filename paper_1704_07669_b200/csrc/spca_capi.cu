@@ -1554,6 +1554,7 @@ int spca_gaussian_device(double *out, int64_t count, uint64_t seed, uint64_t str
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  ensure_pool(dev);  // the staging buffer stays in the stream-ordered pool between calls
   const int64_t want_seg = (int64_t)sms * 32;  // ~4 resident warps of 8 per SM
   int64_t L = std::max<int64_t>(1024, (n_raw + want_seg - 1) / want_seg);
   L = (L + 31) / 32 * 32;
@@ -1564,11 +1565,17 @@ int spca_gaussian_device(double *out, int64_t count, uint64_t seed, uint64_t str
     unsigned long long ev_n;
     int flags, undecided;
   };
+  // staged values of the single walk (PASS 3): nseg x L doubles
+  double *stage = nullptr;
+  if (cudaMallocAsync((void **)&stage, (size_t)nseg * L * sizeof(double), st) != cudaSuccess)
+    return set_err(nullptr, SPCA_ERR_CUDA, -1, "gaussian_device: staging allocation failed");
   char *buf = nullptr;
   const size_t seg_bytes = (size_t)nseg * 8;
   const size_t bytes = 4 * seg_bytes + sizeof(Ctl) + (size_t)ev_cap * sizeof(TailEvent) + 64;
-  if (cudaMallocAsync((void **)&buf, bytes, st) != cudaSuccess)
+  if (cudaMallocAsync((void **)&buf, bytes, st) != cudaSuccess) {
+    cudaFreeAsync(stage, st);
     return set_err(nullptr, SPCA_ERR_CUDA, -1, "gaussian_device: allocation of %zu bytes failed", bytes);
+  }
   int64_t *cnt = (int64_t *)buf, *entry = cnt + nseg, *exit_ = entry + nseg, *off = exit_ + nseg;
   Ctl *ctl = (Ctl *)(off + nseg);
   TailEvent *ev = (TailEvent *)(((uintptr_t)(ctl + 1) + 31) & ~(uintptr_t)31);
@@ -1578,13 +1585,14 @@ int spca_gaussian_device(double *out, int64_t count, uint64_t seed, uint64_t str
   const unsigned blocks = (unsigned)((nseg + 7) / 8);
   const uint64_t key0 = seed, key1 = stream_id;
   cudaMemsetAsync(ctl, 0, sizeof(Ctl), st);
-  gauss_walk<1><<<blocks, 256, 0, st>>>(tab, key0, key1, L, margin, nseg, cnt, entry, exit_, nullptr, out, count,
-                                        ev, ev_cap, &ctl->ev_n, &ctl->undecided);
+  gauss_walk<3><<<blocks, 256, 0, st>>>(tab, key0, key1, L, margin, nseg, cnt, entry, exit_, nullptr, stage,
+                                        count, ev, ev_cap, &ctl->ev_n, &ctl->undecided);
   gauss_scan<<<1, 1024, 0, st>>>(cnt, entry, exit_, nseg, count, off, &ctl->flags);
-  gauss_walk<2><<<blocks, 256, 0, st>>>(tab, key0, key1, L, margin, nseg, cnt, entry, exit_, off, out, count, ev,
-                                        ev_cap, &ctl->ev_n, &ctl->undecided);
+  gauss_gather<<<nseg, 256, 0, st>>>(stage, L, cnt, off, out, count);
+  std::vector<int64_t> hoff;
   if (cudaGetLastError() != cudaSuccess || cudaMemcpyAsync(&hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st) ||
       cudaStreamSynchronize(st) != cudaSuccess) {
+    cudaFreeAsync(stage, st);
     cudaFreeAsync(buf, st);
     return set_err(nullptr, SPCA_ERR_CUDA, -1, "gaussian_device: kernel failed: %s",
                    cudaGetErrorString(cudaGetLastError()));
@@ -1598,16 +1606,27 @@ int spca_gaussian_device(double *out, int64_t count, uint64_t seed, uint64_t str
     hev.resize(hc.ev_n);
     std::vector<int64_t> pj(hc.ev_n);
     std::vector<double> pv(hc.ev_n);
-    if (cudaMemcpy(hev.data(), ev, hc.ev_n * sizeof(TailEvent), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    hoff.resize(nseg);
+    if (cudaMemcpy(hev.data(), ev, hc.ev_n * sizeof(TailEvent), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(hoff.data(), off, (size_t)nseg * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
       rc = set_err(nullptr, SPCA_ERR_CUDA, -1, "gaussian_device: event copy failed");
     } else {
+      size_t np = 0;  // staged index w L + i -> value index off[w] + i (tails past count dropped)
       for (size_t i = 0; i < hev.size(); ++i) {
+        const int64_t w = hev[i].j / L, jj = hoff[w] + (hev[i].j - w * L);
+        if (jj >= count) continue;
         const double xx = (-inv_r) * std::log1p(-next_double(hev[i].u1));
-        pj[i] = hev[i].j;
-        pv[i] = hev[i].neg ? -(r_tail + xx) : r_tail + xx;
+        pj[np] = jj;
+        pv[np] = hev[i].neg ? -(r_tail + xx) : r_tail + xx;
+        ++np;
       }
+      hev.resize(np);
+      pj.resize(np);
+      pv.resize(np);
       int64_t *dj = nullptr;
-      if (cudaMallocAsync((void **)&dj, hev.size() * 16, st) != cudaSuccess ||
+      if (np == 0) {
+        // every tail lay past the requested count
+      } else if (cudaMallocAsync((void **)&dj, hev.size() * 16, st) != cudaSuccess ||
           cudaMemcpyAsync(dj, pj.data(), hev.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
           cudaMemcpyAsync(dj + hev.size(), pv.data(), hev.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess) {
         rc = set_err(nullptr, SPCA_ERR_CUDA, -1, "gaussian_device: patch upload failed");
@@ -1622,6 +1641,7 @@ int spca_gaussian_device(double *out, int64_t count, uint64_t seed, uint64_t str
         rc = set_err(nullptr, SPCA_ERR_CUDA, -1, "gaussian_device: patch sync failed");
     }
   }
+  cudaFreeAsync(stage, st);
   cudaFreeAsync(buf, st);
   return rc;
 }

@@ -51,8 +51,12 @@ int tc_launch_lpad(int64_t l) { return l <= 64 ? 64 : 128; }
 // units and again from L2 by the H units one stage later, so about two
 // chunks must stay resident in the 126 MB L2: R0 * n * 4 B ~ 40 MB by default
 // (SPCA_TC_CHUNK_MB). Whole 256-row tile pairs, at most 8192 rows.
-int64_t tc_chunk_rows(int64_t n, int64_t /*l*/) {
-  int64_t mb = 40;
+int64_t tc_chunk_rows(int64_t n, int64_t l) {
+  // l_pad 128 sketches carry twice the MMA work per K block, so the chunk's
+  // DRAM re-read weighs less than per-chunk fixed costs: 80 MB measured best
+  // at config 3 (10.5 vs 11.2 ms at 40 MB; 120-240 MB slower again), 40 MB at
+  // config 2 (round-2 sweeps, profiles/r5_chunk_unit_sweep.txt)
+  int64_t mb = l > 64 ? 80 : 40;
   if (const char *e = getenv("SPCA_TC_CHUNK_MB")) mb = std::max<int64_t>(1, atoll(e));  // tuning knob
   int64_t r = (int64_t)(mb << 20) / (4 * n);
   // wide rows: at least 1024 rows (H units of a full 32 K blocks; config 5,
