@@ -76,3 +76,24 @@ def test_fused_qb_flags_deficient_block_and_general_path_repairs(golden):
     approx = res.q @ res.b
     want = torch.from_numpy(ref.q @ ref.b).to(dev)
     assert _rel(approx, want) < 1e-9
+
+
+def test_fused_qb_ill_conditioned_blocks_two_pass_path():
+    """Blocks with cond(y) ~ 1e3 (columns of G scaled over three decades
+    within every block) exceed the one-pass CholeskyQR bound (cond_F <= 16)
+    and run both CholeskyQR passes on the device; the result still matches
+    the reference's blocked_qb (oracle) at 1e-10 and Q stays orthonormal."""
+    g, h, om = _sketch(20000, 400, 60, seed=11)
+    scale = np.tile(np.logspace(0, -3, 10), 6)
+    g = g * scale[None, :]
+    h = h * scale[None, :]
+    om = om * scale[None, :]
+    dev = torch.device("cuda")
+    gt, ht, ot = (torch.from_numpy(x).to(dev) for x in (g, h, om))
+    fused = QB._blocked_qb_fused(gt, ht, ot, 10, dev)
+    assert fused is not None
+    ref = O.oracle_qb(g, h, om, 10)
+    assert _rel(fused.q, torch.from_numpy(ref.q).to(dev)) < 1e-10
+    assert _rel(fused.b, torch.from_numpy(ref.b).to(dev)) < 1e-10
+    eye = torch.eye(60, dtype=torch.float64, device=dev)
+    assert float((fused.q.T @ fused.q - eye).abs().max()) < 1e-12
