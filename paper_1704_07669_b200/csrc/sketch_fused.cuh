@@ -96,6 +96,8 @@ struct FusedArgs {
   int *ready;               // [C] reduced row slices
   int *hdone;               // [C] finished H units
   int *hseq;                // [2X] H units applied to column tile x (chunk-major)
+  int *trdy;                // [C][2T] reduced row slices per 128-row tile (S = the tile's G is complete)
+  int tile_ready;           // H units wait per 128-row tile of G^T (trdy) instead of for the whole chunk
   int accumulate;           // H of the launch's first chunk adds to hpart
   int64_t first_row;        // global index of the launch's first row
   const float *a;           // the launch's rows (row_base = 0) and their stride, for the
@@ -311,7 +313,12 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       const bool hstats = NORM && f.kind == 1 && f.nk > 0;
       if (hstats) {  // the row shifts / scales of chunk c come from its G reductions
         if (ptx::elect_one()) {
-          ptx::spin_until_geq(&args.ready[f.c], fused_real_tiles(sc, f.c) * sc.S);
+          if (args.tile_ready) {  // every tile this unit reads
+            const int t0 = f.k0 >> 2, t1 = (f.k0 + f.nk - 1) >> 2;
+            for (int t = t0; t <= t1; ++t) ptx::spin_until_geq(&args.trdy[f.c * 2 * sc.T + t], sc.S);
+          } else {
+            ptx::spin_until_geq(&args.ready[f.c], fused_real_tiles(sc, f.c) * sc.S);
+          }
           ptx::fence_proxy_async_global();
         }
         __syncwarp();
@@ -387,7 +394,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
       const FusedUnit f = fused_decode(sc, u);
       const int gslot = f.c % kSlots;
-      if (f.kind == 1 && f.nk > 0 && !(args.dbg & 16384)) {  // G^T of chunk c must be complete
+      const bool hwait = f.kind == 1 && f.nk > 0 && !(args.dbg & 16384);
+      if (hwait && !args.tile_ready) {  // G^T of chunk c must be complete
         if (ptx::elect_one()) {
           ptx::spin_until_geq(&args.ready[f.c], fused_real_tiles(sc, f.c) * sc.S);
           ptx::fence_proxy_async_global();
@@ -395,8 +403,17 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         __syncwarp();
       }
       if (lane == 0) SPCA_TRACE(ui, 7);
+      int wtile = -1;  // tile_ready: last 128-row tile of G^T known complete
 #pragma unroll 1
       for (int kb = 0; kb < f.nk; ++kb, ++gkb) {
+        if (hwait && args.tile_ready && ((f.k0 + kb) >> 2) != wtile) {  // the block's rows' G^T
+          wtile = (f.k0 + kb) >> 2;
+          if (ptx::elect_one()) {
+            ptx::spin_until_geq(&args.trdy[f.c * 2 * sc.T + wtile], sc.S);
+            ptx::fence_proxy_async_global();
+          }
+          __syncwarp();
+        }
         const int s = gkb % C::NB;
         if (gkb >= C::NB) ptx::mbar_wait(&bars.b_empty[s], ((gkb / C::NB) - 1) & 1);
         if (ptx::elect_one()) {
@@ -999,7 +1016,10 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           ptx::fence_proxy_async_global();
           __threadfence();
           ptx::named_bar(2, kTcEpi);
-          if (e == 0) atomicAdd(&args.ready[f.c], 1);
+          if (e == 0) {
+            atomicAdd(&args.trdy[f.c * twoT + tile], 1);
+            atomicAdd(&args.ready[f.c], 1);
+          }
         }
       } else {  // ------------------------------------------------ H epilogue
         const bool real = tile < sc.nx;

@@ -267,7 +267,7 @@ int tc_setup(spca_sketch *h) {
   CK(h, dalloc(h, &h->gpart, (size_t)h->gpart_elems * 4));
   // ordering counters of one launch (at most flush_every chunks)
   h->tc_ctr_chunks = h->flush_every;
-  CK(h, dalloc(h, &h->tc_ctr, (size_t)(h->tc_ctr_chunks * (2 * s.T + 2) + 2 * s.X) * 4));
+  CK(h, dalloc(h, &h->tc_ctr, (size_t)(h->tc_ctr_chunks * (4 * s.T + 2) + 2 * s.X) * 4));
   if (getenv("SPCA_TC_TRACE")) {
     CK(h, dalloc(h, &h->trace, (size_t)kTraceWords * 8));
     CK(h, cudaMemsetAsync(h->trace, 0, (size_t)kTraceWords * 8, h->stream));
@@ -312,7 +312,10 @@ int tc_register_source(spca_sketch *h, const void *a, int64_t rows, int64_t lda)
 // the G^T reduction. Every wait still points at a unit dealt earlier for
 // 0.5 <= lag <= 3 (H(c) after G(c); G(c)'s slot reuse after H(c - kSlots)).
 int tc_unit_order(spca_sketch *h, FusedSched &s) {
-  double lag = 2.0;
+  // with per-tile G^T readiness (args.tile_ready) a chunk's H units can follow
+  // its G units one stage later: l_pad 64 1.630 -> 1.601 ms at config 2 (A's
+  // DRAM reads 8.4 -> 6.6 GB); l_pad 128 measured equal at lag 1 and 2
+  double lag = h->tc_lp == 64 ? 1.0 : 2.0;
   if (const char *e = getenv("SPCA_TC_LAGF")) lag = std::max(0.5, std::min((double)kMaxLag, atof(e)));
   const int TS = s.T * s.S, TlS = s.Tl * s.S, XR = s.X * s.RS, P = TS + XR;
   if (s.C >= 32768 || std::max(TS, XR) >= 32768) {  // outside the table encoding: closed form
@@ -424,7 +427,7 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
     ta_g3 = &fa_g3;
     ta_h2 = &fa_h2;
   }
-  const size_t ctr_words = (size_t)s.C * (2 * s.T + 2) + 2 * s.X;
+  const size_t ctr_words = (size_t)s.C * (4 * s.T + 2) + 2 * s.X;
   const int grid = 2 * std::max(1, std::min(h->max_pairs, s.total));
 #if SPCA_BULK_EPI
   // H units add into the running H at L2 (bulk reduce-add): a launch that
@@ -461,6 +464,9 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   args.ready = h->tc_ctr + (size_t)s.C * 2 * s.T;
   args.hdone = args.ready + s.C;
   args.hseq = args.hdone + s.C;
+  args.trdy = args.hseq + 2 * s.X;  // [C][2T]
+  static const int tile_ready = getenv("SPCA_TC_TILE_READY") ? atoi(getenv("SPCA_TC_TILE_READY")) : 1;
+  args.tile_ready = tile_ready;
   args.accumulate = h->chunks_since_flush > 0 ? 1 : 0;
   args.first_row = h->rows_done;
   args.a = (const float *)a;
