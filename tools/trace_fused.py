@@ -81,7 +81,7 @@ sc = sched(rows, n, R0)
 ncl = len(t) // 2
 
 
-def host_order_kinds(s, lag=float(os.environ.get("SPCA_TC_LAGF", "2.0"))):
+def host_order_kinds(s, lag=float(os.environ.get("SPCA_TC_LAGF", "1.0" if l <= 64 else "2.0"))):
     # the host-built unit order of tc_unit_order (tc_host.cuh): G units of chunk
     # c at c*P + r, H units at c*P + TS + lag*P + r + 0.25, stable sort
     TS, XR = s["T"] * s["S"], s["X"] * s["RS"]
