@@ -182,7 +182,24 @@ __global__ void __launch_bounds__(kQbThreads, 2) qb_sweep_kernel(const __grid_co
   // column tiles of the reduction: [0, ntq) Q columns 8 nt.., [ntq, ntq + NH) t columns
   const int ntq = WP ? (c0 + 7) / 8 : 0;
   const int nlive = ntq + (WW ? NH : 0);
-  const int kspl = nlive >= kQbWarps ? 1 : (nlive >= 4 ? 2 : (nlive >= 2 ? 4 : 8));  // row groups
+  // row groups: the split minimising the busiest warp's share of part B,
+  // ceil(nlive / (warps / kspl)) tiles of tr / kspl rows each (at most
+  // kQbNtw tiles per warp; ties to fewer groups). nlive = 10 (c0 = 60) was
+  // dealt 2 tiles to two warps and 1 to the rest (kspl 1); kspl 2 gives 3
+  // half-height tiles to every column group.
+  int kspl = 8;
+  {
+    int best = 1 << 30;
+    for (int k = 1; k <= kQbWarps; k *= 2) {
+      const int per = (nlive + kQbWarps / k - 1) / (kQbWarps / k);
+      if (per > kQbNtw) continue;
+      const int cost = per * (kQbWarps / k);  // per / k in units of 1 / warps
+      if (cost < best) {
+        best = cost;
+        kspl = k;
+      }
+    }
+  }
   const int cgs = kQbWarps / kspl;                                                  // column-tile stride
   const int rsub = warp % kspl, cg = warp / kspl;
   double acc[kQbNtw][4];
