@@ -46,6 +46,7 @@ struct spca_sketch {
   int64_t gpart_elems = 0;
   void *tc_ws = nullptr;         // tensor-core G^T slots [kSlots][2][lpad][R0]
   size_t tc_ws_bytes = 0;
+  int tc_gt_kparts = 2;          // G^T parts per slot (hi / lo, or 1 raw)
   int *tc_ctr = nullptr;         // per-launch ordering counters of the pass kernel
   int tc_lp = 64;                // l_pad of one pass-kernel launch (64 or 128)
   int tc_groups = 1;             // column groups of 128 (l > 128): one launch each

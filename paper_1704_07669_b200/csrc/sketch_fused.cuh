@@ -74,6 +74,9 @@ struct FusedSched {
   int X, nx;      // H: 256-column tile pairs, real 128-column tiles over n
   int RS, hseg;   // H: row segments per chunk, K blocks per segment
   int D;          // stage lag of a chunk's H units behind its G units
+  int Gr;         // column groups of 128 sketched together (l > 128: each unit
+                  // covers one group; a unit's groups are dealt side by side, so
+                  // they read the same A tile at the same time: one DRAM read)
   int total;      // pair units in this launch
   const int *order;  // device: unit u -> kind << 30 | chunk << 15 | index (null: closed form, lag D)
 };
@@ -98,6 +101,10 @@ struct FusedArgs {
   int *hseq;                // [2X] H units applied to column tile x (chunk-major)
   int *trdy;                // [C][2T] reduced row slices per 128-row tile (S = the tile's G is complete)
   int tile_ready;           // H units wait per 128-row tile of G^T (trdy) instead of for the whole chunk
+  int64_t gpart_group;      // elements of gpart per column group (Gr > 1)
+  int64_t gT_group;         // elements of gT per column group
+  int gT_rows_group;        // rows of the G^T tensor map per column group
+  int ctr_group;            // ordering-counter words per column group
   int accumulate;           // H of the launch's first chunk adds to hpart
   int64_t first_row;        // global index of the launch's first row
   const float *a;           // the launch's rows (row_base = 0) and their stride, for the
@@ -122,9 +129,21 @@ struct FusedArgs {
 
 };
 
+// The state of column group g of a unit: Omega^T rows, partial / G^T slots,
+// output columns, ordering counters (identical to the launch's for g = 0)
+struct GroupView {
+  int wy0;            // first Omega^T row of the group
+  int gt_row0;        // first row of the group's G^T slots in the tensor map
+  float *gpart, *gT, *g_out, *hpart;
+  const float *left, *wsum;
+  int *seg_cnt, *ready, *hdone, *hseq, *trdy;
+  int colsum_on;
+};
+
 struct FusedUnit {
   int kind;   // 0 = G, 1 = H
   int c;      // chunk
+  int g;      // column group (0 unless Gr > 1)
   int a, b;   // G: tile pair, segment; H: column-tile pair, row segment
   int k0, nk; // first K block and count (G: over n; H: over the chunk's rows)
   int rows;   // rows of chunk c
@@ -134,12 +153,16 @@ struct FusedUnit {
 // units of a chunk come D stages after its G units, which leaves the G^T
 // reduction of the chunk D - 1 stages of slack (A of D + 1 chunks in L2).
 __host__ __device__ inline int fused_total(const FusedSched &s) {
-  const int TS = s.T * s.S, TlS = s.Tl * s.S, XR = s.X * s.RS;
+  const int TS = s.T * s.S * s.Gr, TlS = s.Tl * s.S * s.Gr, XR = s.X * s.RS * s.Gr;
   return (s.C - 1) * TS + TlS + s.C * XR;
 }
 
+// MULTI = false: a one-group launch (l_pad 64 always is), the group
+// arithmetic folds away
+template <bool MULTI = true>
 __host__ __device__ __forceinline__ FusedUnit fused_decode(const FusedSched &s, int u) {
-  const int TS = s.T * s.S, TlS = s.Tl * s.S, XR = s.X * s.RS, F = TS + XR, D = s.D;
+  const int Gr = MULTI ? s.Gr : 1;
+  const int TS = s.T * s.S * Gr, TlS = s.Tl * s.S * Gr, XR = s.X * s.RS * Gr, F = TS + XR, D = s.D;
   int kind = 0, c = 0, r = 0;
 #ifdef __CUDA_ARCH__
   if (s.order) {  // host-built order (tc_unit_order): any lag, including fractional stages
@@ -199,6 +222,8 @@ __host__ __device__ __forceinline__ FusedUnit fused_decode(const FusedSched &s, 
   FusedUnit f;
   f.kind = kind;
   f.c = c;
+  f.g = r % Gr;  // a unit's column groups are adjacent in the sequence
+  r /= Gr;
   f.rows = c == s.C - 1 ? s.rows_last : s.R0;
   if (kind == 0) {
     f.a = r / s.S;
@@ -212,6 +237,28 @@ __host__ __device__ __forceinline__ FusedUnit fused_decode(const FusedSched &s, 
     f.nk = max(0, min(s.hseg, (f.rows + 31) / 32 - f.k0));
   }
   return f;
+}
+
+template <int LPAD>
+__device__ __forceinline__ GroupView group_view(const FusedArgs &a, int g) {
+  if (LPAD == 64) g = 0;  // l_pad 64 sketches are one group: the offsets fold away
+  GroupView v;
+  const int64_t w = (int64_t)g * a.ctr_group;
+  v.wy0 = a.wy0 + g * LPAD;
+  v.gt_row0 = g * a.gT_rows_group;
+  v.gpart = a.gpart + g * a.gpart_group;
+  v.gT = a.gT + g * a.gT_group;
+  v.g_out = a.g_out + g * LPAD;
+  v.hpart = a.hpart + g * LPAD;
+  v.left = a.left ? a.left + g * LPAD : nullptr;
+  v.wsum = a.wsum ? a.wsum + g * LPAD : nullptr;
+  v.seg_cnt = a.seg_cnt + w;
+  v.ready = a.ready + w;
+  v.hdone = a.hdone + w;
+  v.hseq = a.hseq + w;
+  v.trdy = a.trdy + w;
+  v.colsum_on = a.colsum_on && g == 0;
+  return v;
 }
 
 __device__ __forceinline__ int fused_real_tiles(const FusedSched &s, int c) {
@@ -307,7 +354,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     int gkb = 0;
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl) {
-      const FusedUnit f = fused_decode(sc, u);
+      const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, f.g);
       const int rbase = args.row_base + f.c * sc.R0;
       const int tile = 2 * f.a + (int)rank;
       const bool hstats = NORM && f.kind == 1 && f.nk > 0;
@@ -315,9 +363,9 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         if (ptx::elect_one()) {
           if (args.tile_ready) {  // every tile this unit reads
             const int t0 = f.k0 >> 2, t1 = (f.k0 + f.nk - 1) >> 2;
-            for (int t = t0; t <= t1; ++t) ptx::spin_until_geq(&args.trdy[f.c * 2 * sc.T + t], sc.S);
+            for (int t = t0; t <= t1; ++t) ptx::spin_until_geq(&gv.trdy[f.c * 2 * sc.T + t], sc.S);
           } else {
-            ptx::spin_until_geq(&args.ready[f.c], fused_real_tiles(sc, f.c) * sc.S);
+            ptx::spin_until_geq(&gv.ready[f.c], fused_real_tiles(sc, f.c) * sc.S);
           }
           ptx::fence_proxy_async_global();
         }
@@ -392,12 +440,13 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     int gkb = 0, ui = 0;
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
-      const FusedUnit f = fused_decode(sc, u);
+      const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, f.g);
       const int gslot = f.c % kSlots;
       const bool hwait = f.kind == 1 && f.nk > 0 && !(args.dbg & 16384);
       if (hwait && !args.tile_ready) {  // G^T of chunk c must be complete
         if (ptx::elect_one()) {
-          ptx::spin_until_geq(&args.ready[f.c], fused_real_tiles(sc, f.c) * sc.S);
+          ptx::spin_until_geq(&gv.ready[f.c], fused_real_tiles(sc, f.c) * sc.S);
           ptx::fence_proxy_async_global();
         }
         __syncwarp();
@@ -409,7 +458,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         if (hwait && args.tile_ready && ((f.k0 + kb) >> 2) != wtile) {  // the block's rows' G^T
           wtile = (f.k0 + kb) >> 2;
           if (ptx::elect_one()) {
-            ptx::spin_until_geq(&args.trdy[f.c * 2 * sc.T + wtile], sc.S);
+            ptx::spin_until_geq(&gv.trdy[f.c * 2 * sc.T + wtile], sc.S);
             ptx::fence_proxy_async_global();
           }
           __syncwarp();
@@ -429,7 +478,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             // completing on its own barrier (its converters split them)
             constexpr int HR = LPAD / 2;
             ptx::mbar_arrive_expect_tx(&bars.b_full[s], C::BH_BYTES);
-            const int y = (f.kind == 0 ? args.wy0 : gslot * LPAD) + HR * (int)rank;
+            const int y = (f.kind == 0 ? gv.wy0 : gv.gt_row0 + gslot * LPAD) + HR * (int)rank;
             ptx::tma_load_2d_hint(st, f.kind == 0 ? &tWhi : &tGT, &bars.b_full[s], k, y, keep);
           }
 #else
@@ -440,8 +489,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           constexpr int HR = LPAD / 2;  // rows per B box
           // rows of W_hi / W_lo in the maps: Omega^T (G units) or G^T slot (H units)
           const CUtensorMap *mh = f.kind == 0 ? &tWhi : &tGT, *ml = f.kind == 0 ? &tWlo : &tGT;
-          const int yh = f.kind == 0 ? args.wy0 : 2 * gslot * LPAD,
-                    yl = f.kind == 0 ? args.wy0 : (2 * gslot + 1) * LPAD;
+          const int yh = f.kind == 0 ? gv.wy0 : gv.gt_row0 + 2 * gslot * LPAD,
+                    yl = f.kind == 0 ? gv.wy0 : gv.gt_row0 + (2 * gslot + 1) * LPAD;
           if constexpr (C::STACKED) {
             const CUtensorMap *m01 = rank == 0 ? mh : ml;
             const int y01 = rank == 0 ? yh : yl;
@@ -449,7 +498,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             ptx::tma_load_2d_pair(st + C::BH_BYTES, m01, bar, k, y01 + HR, keep);
             ptx::tma_load_2d_pair(st + 2 * C::BH_BYTES, mh, bar, k, yh + HR * (int)rank, keep);
           } else if (SPCA_BCOMB) {  // this CTA's hi and lo rows: one box of LPAD rows
-            const int yc = f.kind == 0 ? 2 * args.wy0 + LPAD * (int)rank : (2 * gslot + (int)rank) * LPAD;
+            const int yc = f.kind == 0 ? 2 * gv.wy0 + LPAD * (int)rank : gv.gt_row0 + (2 * gslot + (int)rank) * LPAD;
             ptx::tma_load_2d_pair(st, mh, bar, k, yc, keep);
           } else {
             ptx::tma_load_2d_pair(st, mh, bar, k, yh + HR * (int)rank, keep);
@@ -467,7 +516,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       unsigned long long *ct_ = args.trace + 256 * kTraceStride + 4 * kTraceMma + 6 * kTraceConv;
       int gkb = 0;
       for (int u = cid; u < sc.total && gkb < kTraceMma; u += ncl) {
-        const FusedUnit f = fused_decode(sc, u);
+        const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, f.g);
         for (int kb = 0; kb < f.nk && gkb < kTraceMma; ++kb, ++gkb) {
           ptx::mbar_wait(&bars.kb_empty[gkb % C::NS], (gkb / C::NS) & 1);
           ct_[gkb] = clock64();
@@ -481,7 +531,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       int gkb = 0, gq = 0, ui = 0;
 #pragma unroll 1
       for (int u = cid; u < sc.total; u += ncl, ++ui) {
-        const FusedUnit f = fused_decode(sc, u);
+        const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, f.g);
 #pragma unroll 1
         for (int kb = 0; kb < f.nk; ++kb, ++gkb) {
           if (lane == 0 && kb == 0) SPCA_TRACE(ui, 5);
@@ -528,7 +579,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     int gkb = 0, ui = 0, gpa = 0;  // gpa: A slot pairs consumed (SPCA_PAIRA)
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
-      const FusedUnit f = fused_decode(sc, u);
+      const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, f.g);
       float cs = 0.f, cc = 0.f;   // H: column sum (fp32 Kahan over the unit)
       // fused normalisation, G units: shift every value of the row by its first
       // value a0 (d = a - a0; exact for nearby values) and sum d, d^2 (Kahan)
@@ -729,7 +781,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     int gq = 0, ui = 0;
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
-      const FusedUnit f = fused_decode(sc, u);
+      const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, f.g);
       const int nq = (f.nk + kPromote - 1) / kPromote;
       float racc[64];
 #pragma unroll
@@ -770,11 +823,11 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         float chk = 0.f;
         if (tile < fused_real_tiles(sc, f.c) && !(args.dbg & 131072)) {
           if (f.c >= kSlots) {
-            if (lane == 0) ptx::spin_until_geq(&args.ready[f.c - kSlots], sc.nt * sc.S);
+            if (lane == 0) ptx::spin_until_geq(&gv.ready[f.c - kSlots], sc.nt * sc.S);
             __syncwarp();
           }
           float4 *gp = reinterpret_cast<float4 *>(
-              args.gpart + ((((size_t)(f.c % kSlots) * 2 * sc.T + tile) * sc.S + f.b) * 128 + t) * LPAD + c0);
+              gv.gpart + ((((size_t)(f.c % kSlots) * 2 * sc.T + tile) * sc.S + f.b) * 128 + t) * LPAD + c0);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             gp[i] = make_float4(racc[4 * i], racc[4 * i + 1], racc[4 * i + 2], racc[4 * i + 3]);
@@ -808,7 +861,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     int ui = 0;
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
-      const FusedUnit f = fused_decode(sc, u);
+      const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, f.g);
       const int tile = 2 * f.a + (int)rank;
       const int sb = ui % C::NSTG;  // staging buffer of this unit
       ptx::mbar_wait(&bars.epi_full[sb], (ui / C::NSTG) & 1);
@@ -836,12 +890,12 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           stg_bad[e] = 0;
         } else if (real) {
           // the partial slot was last used kSlots chunks ago: its slices must be reduced
-          if (f.c >= kSlots && e == 0) ptx::spin_until_geq(&args.ready[f.c - kSlots], sc.nt * sc.S);
+          if (f.c >= kSlots && e == 0) ptx::spin_until_geq(&gv.ready[f.c - kSlots], sc.nt * sc.S);
           ptx::named_bar(2, kTcEpi);
           // copy the staged tile to its partial slot, NQ consecutive lanes per row
           // (each warp store covers whole rows: coalesced)
           float4 *gp = reinterpret_cast<float4 *>(
-              args.gpart + (((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 * LPAD);
+              gv.gpart + (((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 * LPAD);
           const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF + sb * C::STG_BYTES);
 #if SPCA_BULK_EPI
           if (e == 0) {  // the whole staged tile -> its partial slot, one bulk copy
@@ -899,20 +953,20 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
 #endif
           __threadfence();
           ptx::named_bar(2, kTcEpi);
-          int *cnt = &args.seg_cnt[f.c * twoT + tile];
+          int *cnt = &gv.seg_cnt[f.c * twoT + tile];
           if (e == 0) {
             atomicAdd(cnt, 1);
             ptx::spin_until_geq(cnt, sc.S);  // every segment's partial is in
-            if (f.c >= kSlots) ptx::spin_until_geq(&args.hdone[f.c - kSlots], sc.nx * sc.RS);
+            if (f.c >= kSlots) ptx::spin_until_geq(&gv.hdone[f.c - kSlots], sc.nx * sc.RS);
           }
           ptx::named_bar(2, kTcEpi);
           // reduce this segment's slice of the tile's rows over the S partials (fixed order)
           const int r0 = (f.b * 128) / sc.S, r1 = ((f.b + 1) * 128) / sc.S;
-          const float *p0 = args.gpart + (((size_t)gslot * twoT + tile) * sc.S) * 128 * LPAD;
+          const float *p0 = gv.gpart + (((size_t)gslot * twoT + tile) * sc.S) * 128 * LPAD;
 #if SPCA_BRAW
-          float *ghi = args.gT + (size_t)gslot * LPAD * sc.R0;  // raw G^T of the slot
+          float *ghi = gv.gT + (size_t)gslot * LPAD * sc.R0;  // raw G^T of the slot
 #else
-          float *ghi = args.gT + (size_t)(2 * gslot) * LPAD * sc.R0;
+          float *ghi = gv.gT + (size_t)(2 * gslot) * LPAD * sc.R0;
           float *glo = ghi + (size_t)LPAD * sc.R0;
 #endif
           if (NORM) {
@@ -975,23 +1029,23 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
               }
               float a4[4] = {acc.x, acc.y, acc.z, acc.w};
               float b4[4] = {acc.x, acc.y, acc.z, acc.w};  // B operand of the H units
-              if (args.left != nullptr && valid) {  // co-sketch: H += A^T L
+              if (gv.left != nullptr && valid) {  // co-sketch: H += A^T L
                 const float4 l4 = __ldg(reinterpret_cast<const float4 *>(
-                                            args.left + ((int64_t)f.c * sc.R0 + rc) * args.gld) + q);
+                                            gv.left + ((int64_t)f.c * sc.R0 + rc) * args.gld) + q);
                 b4[0] = l4.x; b4[1] = l4.y; b4[2] = l4.z; b4[3] = l4.w;
               }
               if (NORM) {  // G_hat = (d Omega - mean_d * 1^T Omega) / norm; the H units take G_hat / norm
                 const float md = sl_stat[r][0], inv = sl_stat[r][1];
-                const float4 w4 = __ldg(reinterpret_cast<const float4 *>(args.wsum) + q);
+                const float4 w4 = __ldg(reinterpret_cast<const float4 *>(gv.wsum) + q);
                 const float ws[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                   a4[j] = fmaf(-md, ws[j], a4[j]) * inv;
-                  b4[j] = (args.left != nullptr ? b4[j] : a4[j]) * inv;
+                  b4[j] = (gv.left != nullptr ? b4[j] : a4[j]) * inv;
                 }
               }
               if (valid)
-                reinterpret_cast<float4 *>(args.g_out + ((int64_t)f.c * sc.R0 + rc) * args.gld)[q] =
+                reinterpret_cast<float4 *>(gv.g_out + ((int64_t)f.c * sc.R0 + rc) * args.gld)[q] =
                     make_float4(a4[0], a4[1], a4[2], a4[3]);
 #if SPCA_BRAW
 #pragma unroll
@@ -1017,8 +1071,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           __threadfence();
           ptx::named_bar(2, kTcEpi);
           if (e == 0) {
-            atomicAdd(&args.trdy[f.c * twoT + tile], 1);
-            atomicAdd(&args.ready[f.c], 1);
+            atomicAdd(&gv.trdy[f.c * twoT + tile], 1);
+            atomicAdd(&gv.ready[f.c], 1);
           }
         }
       } else {  // ------------------------------------------------ H epilogue
@@ -1027,21 +1081,21 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         const int col = tile * 128 + e;
         double csv = 0.0;
         if (real) {
-          if (e == 0) ptx::spin_until_geq(&args.hseq[tile], seq);
+          if (e == 0) ptx::spin_until_geq(&gv.hseq[tile], seq);
           ptx::named_bar(2, kTcEpi);
 #if SPCA_BULK_EPI
           {  // H row e += staged row e, one bulk reduce-add per row (at L2); the launch
              // zeroed H when it does not accumulate (the first unit of a tile adds to 0)
             const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF + sb * C::STG_BYTES);
             if (col < args.n) {
-              ptx::bulk_reduce_add_f32(args.hpart + (int64_t)col * args.gld, stg0 + e * LPAD * 4, LPAD * 4);
+              ptx::bulk_reduce_add_f32(gv.hpart + (int64_t)col * args.gld, stg0 + e * LPAD * 4, LPAD * 4);
               ptx::bulk_commit();
               ptx::bulk_wait_read0();
             }
           }
 #else
           {  // H rows of the tile's columns, NQ consecutive lanes per column (coalesced)
-            float *hp0 = args.hpart + (int64_t)tile * 128 * args.gld;
+            float *hp0 = gv.hpart + (int64_t)tile * 128 * args.gld;
             const bool overwrite = !args.accumulate && seq == 0;
             const uint32_t stg0 = ptx::smem_u32(smem + C::STG_OFF + sb * C::STG_BYTES);
             const int items = min(128, args.n - tile * 128) * NQ;
@@ -1074,7 +1128,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         }
         ptx::mbar_arrive(&bars.epi_empty[sb]);
         if (real) {
-          if (col < args.n && args.colsum_on) {
+          if (col < args.n && gv.colsum_on) {
             if (args.carry) {
               const double y = csv - __ldcg(args.carry + col);
               const double s0 = __ldcg(args.colsum + col);
@@ -1094,8 +1148,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           __threadfence();
           ptx::named_bar(2, kTcEpi);
           if (e == 0) {
-            ptx::st_release(&args.hseq[tile], seq + 1);
-            atomicAdd(&args.hdone[f.c], 1);
+            ptx::st_release(&gv.hseq[tile], seq + 1);
+            atomicAdd(&gv.hdone[f.c], 1);
           }
         }
       }

@@ -76,8 +76,19 @@ int tc_unit_kb() {
   return u;
 }
 
+// l > 128: the column groups of 128 run in ONE launch (units of every group
+// of a tile / column stripe dealt side by side, so each A tile is read from
+// DRAM once for all groups) unless fused row normalisation is on (its row
+// statistics are written by group 0's reductions) or SPCA_TC_SEQ_GROUPS is set
+// (one launch per group, each reading A).
+bool tc_merged_groups(const spca_sketch *h) {
+  static const bool seq = getenv("SPCA_TC_SEQ_GROUPS") != nullptr;
+  return h->tc_groups > 1 && !h->normalize && !seq;
+}
+
 FusedSched tc_base_sched(const spca_sketch *h) {
   FusedSched s{};
+  s.Gr = 1;
   const int U = tc_unit_kb();
   s.R0 = (int)h->chunk_rows;
   s.nt = s.R0 / 128;
@@ -87,7 +98,12 @@ FusedSched tc_base_sched(const spca_sketch *h) {
   // segments are dealt to consecutive pairs: S must not exceed the pairs of
   // the grid (else a pair would wait on its own later unit). Wide n gets
   // longer segments instead (S <= max_pairs / 2).
-  const int max_seg = std::max(1, h->max_pairs / 2);
+  // (merged column groups deal a tile's segments of every group side by side:
+  // the span S * groups keeps the same bound)
+  // (sized for every group whether or not this launch merges them, so the
+  // buffers allocated at setup fit either way)
+  const int gcap = std::max(1, h->tc_groups);
+  const int max_seg = std::max(1, h->max_pairs / (2 * gcap));
   s.S = (int)std::min<int64_t>(ceil_div(s.nkb, U), max_seg);
   s.kseg = (int)ceil_div(s.nkb, s.S);
   s.S = (int)ceil_div(s.nkb, s.kseg);
@@ -257,17 +273,20 @@ int tc_setup(spca_sketch *h) {
   constexpr int kGtParts = 2;
 #endif
   const FusedSched s = tc_base_sched(h);
-  // G^T (raw, or hi / lo) of kSlots chunks of one launch: [kSlots][parts x lp rows][R0], one TMA map
-  h->tc_ws_bytes = (size_t)kSlots * kGtParts * lp * s.R0 * 4;
+  // G^T (raw, or hi / lo) of kSlots chunks of one launch: [groups][kSlots][parts x lp rows][R0], one
+  // TMA map (groups: the column groups a merged launch sketches together)
+  const int ng = std::max(1, h->tc_groups);  // room for a merged launch of every group
+  h->tc_gt_kparts = kGtParts;
+  h->tc_ws_bytes = (size_t)ng * kSlots * kGtParts * lp * s.R0 * 4;
   CK(h, dalloc(h, &h->tc_ws, h->tc_ws_bytes));
-  rc = encode_2d(h, &h->tm_gT, h->tc_ws, (uint64_t)s.R0, (uint64_t)kSlots * kGtParts * lp, (uint64_t)s.R0 * 4,
-                 32, gbox);
+  rc = encode_2d(h, &h->tm_gT, h->tc_ws, (uint64_t)s.R0, (uint64_t)ng * kSlots * kGtParts * lp,
+                 (uint64_t)s.R0 * 4, 32, gbox);
   if (rc) return rc;
-  h->gpart_elems = (int64_t)kSlots * 2 * s.T * s.S * 128 * lp;
-  CK(h, dalloc(h, &h->gpart, (size_t)h->gpart_elems * 4));
-  // ordering counters of one launch (at most flush_every chunks)
+  h->gpart_elems = (int64_t)kSlots * 2 * s.T * s.S * 128 * lp;  // per group
+  CK(h, dalloc(h, &h->gpart, (size_t)ng * h->gpart_elems * 4));
+  // ordering counters of one launch (at most flush_every chunks), per group
   h->tc_ctr_chunks = h->flush_every;
-  CK(h, dalloc(h, &h->tc_ctr, (size_t)(h->tc_ctr_chunks * (4 * s.T + 2) + 2 * s.X) * 4));
+  CK(h, dalloc(h, &h->tc_ctr, (size_t)ng * (h->tc_ctr_chunks * (4 * s.T + 2) + 2 * s.X) * 4));
   if (getenv("SPCA_TC_TRACE")) {
     CK(h, dalloc(h, &h->trace, (size_t)kTraceWords * 8));
     CK(h, cudaMemsetAsync(h->trace, 0, (size_t)kTraceWords * 8, h->stream));
@@ -317,7 +336,7 @@ int tc_unit_order(spca_sketch *h, FusedSched &s) {
   // DRAM reads 8.4 -> 6.6 GB); l_pad 128 measured equal at lag 1 and 2
   double lag = h->tc_lp == 64 ? 1.0 : 2.0;
   if (const char *e = getenv("SPCA_TC_LAGF")) lag = std::max(0.5, std::min((double)kMaxLag, atof(e)));
-  const int TS = s.T * s.S, TlS = s.Tl * s.S, XR = s.X * s.RS, P = TS + XR;
+  const int TS = s.T * s.S * s.Gr, TlS = s.Tl * s.S * s.Gr, XR = s.X * s.RS * s.Gr, P = TS + XR;
   if (s.C >= 32768 || std::max(TS, XR) >= 32768) {  // outside the table encoding: closed form
     s.order = nullptr;
     return SPCA_OK;
@@ -388,6 +407,8 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   if ((lda % 4) != 0 || (reinterpret_cast<uintptr_t>(a) % 16) != 0)
     return set_err(h, SPCA_ERR_CONFIG, -1, "tensor-core path needs 16-byte aligned rows");
   FusedSched s = tc_base_sched(h);
+  const bool merged = tc_merged_groups(h);
+  s.Gr = merged ? h->tc_groups : 1;
   s.C = (int)ceil_div(rows, s.R0);
   s.rows_last = (int)(rows - (int64_t)(s.C - 1) * s.R0);
   s.ntl = (int)ceil_div(s.rows_last, 128);
@@ -427,15 +448,15 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
     ta_g3 = &fa_g3;
     ta_h2 = &fa_h2;
   }
-  const size_t ctr_words = (size_t)s.C * (4 * s.T + 2) + 2 * s.X;
+  const size_t ctr_words = (size_t)s.C * (4 * s.T + 2) + 2 * s.X;  // per group
   const int grid = 2 * std::max(1, std::min(h->max_pairs, s.total));
 #if SPCA_BULK_EPI
   // H units add into the running H at L2 (bulk reduce-add): a launch that
   // starts a flush period starts from zero instead of overwriting
   if (h->chunks_since_flush == 0) CK(h, cudaMemsetAsync(h->hpart, 0, (size_t)h->n * h->lpad * 4, h->stream));
 #endif
-  for (int grp = 0; grp < h->tc_groups; ++grp) {
-  CK(h, cudaMemsetAsync(h->tc_ctr, 0, ctr_words * 4, h->stream));
+  for (int grp = 0; grp < (merged ? 1 : h->tc_groups); ++grp) {
+  CK(h, cudaMemsetAsync(h->tc_ctr, 0, (size_t)s.Gr * ctr_words * 4, h->stream));
   FusedArgs args{};
   args.s = s;
   args.n = (int)h->n;
@@ -465,6 +486,10 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   args.hdone = args.ready + s.C;
   args.hseq = args.hdone + s.C;
   args.trdy = args.hseq + 2 * s.X;  // [C][2T]
+  args.ctr_group = (int)ctr_words;   // group g's counters at + g * ctr_words
+  args.gpart_group = h->gpart_elems;
+  args.gT_group = (int64_t)kSlots * h->tc_gt_kparts * h->tc_lp * s.R0;
+  args.gT_rows_group = kSlots * h->tc_gt_kparts * h->tc_lp;
   static const int tile_ready = getenv("SPCA_TC_TILE_READY") ? atoi(getenv("SPCA_TC_TILE_READY")) : 1;
   args.tile_ready = tile_ready;
   args.accumulate = h->chunks_since_flush > 0 ? 1 : 0;
