@@ -705,3 +705,38 @@ def test_full_size_properties(config):
     assert torch.equal(st.h, st2.h) and torch.equal(st.g, st2.g) and torch.equal(st.col_sums, st2.col_sums)
     del a, st, st2, ay
     torch.cuda.empty_cache()
+
+
+def test_merged_column_groups_bitwise_equal_to_one_launch_per_group(tmp_path):
+    """l > 128 (column groups of 128): the merged launch (every group in one
+    pass-kernel launch, csrc/tc_host.cuh tc_merged_groups) gives the same
+    G, H and column sums bit for bit as one launch per group
+    (SPCA_TC_SEQ_GROUPS=1, read once per process: a subprocess each)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_1704_07669_b200 as P
+m, n, l = 3000, 2000, 300
+gen = torch.Generator(device="cuda").manual_seed(4)
+a = torch.randn(m, n, device="cuda", dtype=torch.float32, generator=gen)
+om = np.random.default_rng(5).standard_normal((n, l))
+sk = P.GpuSketch(n, om, np.float32, precision="tc", rows_hint=m)
+sk.push(a, 0, final=True)
+g, h, cs, rows = sk.finish(on_device=True)
+np.savez(sys.argv[1], g=g.cpu().numpy(), h=h.cpu().numpy(), cs=cs.cpu().numpy())
+''' % root
+    outs = []
+    for seq in (False, True):
+        env = dict(os.environ)
+        env.pop("SPCA_TC_SEQ_GROUPS", None)
+        if seq:
+            env["SPCA_TC_SEQ_GROUPS"] = "1"
+        out = str(tmp_path / f"sk_{int(seq)}.npz")
+        subprocess.run([sys.executable, "-c", script, out], env=env, check=True, timeout=300)
+        outs.append(np.load(out))
+    for k in ("g", "h", "cs"):
+        assert np.array_equal(outs[0][k], outs[1][k]), k
