@@ -279,8 +279,13 @@ struct PairBars {
   uint32_t tmem_base;
 };
 
-template <int LPAD, bool NORM, bool SHIFT = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<LPAD>::THREADS, 1)
+// DUAL: clusters of four CTAs = two CTA pairs sketching two column groups of
+// the same rows (l_pad 256 as two groups of 128): pair 0 loads every A tile
+// once and multicasts it to the matching CTA of pair 1 (each A tile leaves
+// L2 once for both groups), pair p computes group p. Cluster dims come from
+// the launch (2 or 4).
+template <int LPAD, bool NORM, bool SHIFT = false, bool DUAL = false>
+__global__ void __launch_bounds__(TcCfg<LPAD>::THREADS, 1)
 tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ CUtensorMap tAh,
                const __grid_constant__ CUtensorMap tWhi, const __grid_constant__ CUtensorMap tWlo,
                const __grid_constant__ CUtensorMap tGT,
@@ -299,9 +304,15 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
   __shared__ float sl_stat[128][2];                   // norm, G slice reduction: mean_d, inv per row
   const FusedSched &sc = args.s;
 
+  static_assert(!DUAL || (!NORM && !SPCA_PAIRA && LPAD == 128), "dual pairs: plain / shift l_pad 128");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = ptx::cluster_rank();
-  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t crank = ptx::cluster_rank();
+  const uint32_t rank = crank & 1u;              // rank in the CTA pair
+  const uint32_t pid = DUAL ? crank >> 1 : 0u;   // pair in the cluster = column group (DUAL)
+  const uint32_t leader = crank & ~1u;           // the pair's leader CTA (cluster rank)
+  const uint16_t pmask = (uint16_t)(3u << (2 * pid));  // the pair's cluster ranks
+  constexpr int CS = DUAL ? 4 : 2;               // CTAs per cluster
+  const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
   unsigned long long *trace = args.trace ? args.trace + (size_t)blockIdx.x * kTraceStride : nullptr;
   if (trace && threadIdx.x == 0) trace[0] = ptx::globaltimer();
 
@@ -309,7 +320,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     for (int s = 0; s < C::NA; ++s) {
       ptx::mbar_init(&bars.a_full[s], 1);
       // the four warps of one converter group; paired slots: both groups (barriers [0, NP))
-      ptx::mbar_init(&bars.a_empty[s], SPCA_PAIRA ? 8 : 4);
+      // DUAL: pair 0's slot is also released by the matching CTA of pair 1 (multicast)
+      ptx::mbar_init(&bars.a_empty[s], SPCA_PAIRA ? 8 : ((DUAL && pid == 0) ? 8 : 4));
     }
     for (int s = 0; s < C::NS; ++s) {
       ptx::mbar_init(&bars.kb_full[s], 2 * 4);  // one converter group (4 warps) in each CTA
@@ -354,8 +366,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     int gkb = 0;
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl) {
-      const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
-      const GroupView gv = group_view<LPAD>(args, f.g);
+      const FusedUnit f = fused_decode<(LPAD != 64) && !DUAL>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, DUAL ? (int)pid : f.g);
       const int rbase = args.row_base + f.c * sc.R0;
       const int tile = 2 * f.a + (int)rank;
       const bool hstats = NORM && f.kind == 1 && f.nk > 0;
@@ -424,7 +436,18 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             }
             const int kx = (args.dbg & 2048) ? 0 : (f.k0 + kb) * 32;  // profiling knob: L2-resident A
             const int ry = (args.dbg & 2048) ? 0 : rbase;
-            if (f.kind == 0) {  // 128 rows x 32 k, row-major (swizzled)
+            if (DUAL) {
+              // pair 0 fetches the tile once for both pairs: same offset in this CTA and in
+              // the matching CTA of pair 1 (whose producer only posts its expected bytes)
+              if (pid == 0) {
+                const uint16_t mc = (uint16_t)((1u << crank) | (1u << (crank + 2)));
+                if (f.kind == 0)
+                  ptx::tma_load_2d_mc(st, &tAg, &bars.a_full[s], kx, ry + tile * 128, mc, keep);
+                else
+                  ptx::tma_load_2d_mc(st, &tAh, &bars.a_full[s], tile * 128,
+                                      ry + ((args.dbg & 2048) ? 0 : (f.k0 + kb) * 32), mc, drop);
+              }
+            } else if (f.kind == 0) {  // 128 rows x 32 k, row-major (swizzled)
               ptx::tma_load_2d_hint(st, &tAg, &bars.a_full[s], kx, ry + tile * 128, keep);
             } else {            // 32 rows x 128 columns, one unswizzled box
               ptx::tma_load_2d_hint(st, &tAh, &bars.a_full[s], tile * 128, ry + ((args.dbg & 2048) ? 0 : (f.k0 + kb) * 32), drop);
@@ -440,8 +463,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     int gkb = 0, ui = 0;
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
-      const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
-      const GroupView gv = group_view<LPAD>(args, f.g);
+      const FusedUnit f = fused_decode<(LPAD != 64) && !DUAL>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, DUAL ? (int)pid : f.g);
       const int gslot = f.c % kSlots;
       const bool hwait = f.kind == 1 && f.nk > 0 && !(args.dbg & 16384);
       if (hwait && !args.tile_ready) {  // G^T of chunk c must be complete
@@ -467,7 +490,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         if (gkb >= C::NB) ptx::mbar_wait(&bars.b_empty[s], ((gkb / C::NB) - 1) & 1);
         if (ptx::elect_one()) {
           uint8_t *st = smem + C::B_OFF + s * C::B_STAGE;
-          const uint32_t bar = ptx::mapa(ptx::smem_u32(&bars.b_full[s]), 0);
+          const uint32_t bar = ptx::mapa(ptx::smem_u32(&bars.b_full[s]), leader);
           const int k = (f.k0 + kb) * 32;
 #if SPCA_BRAW
           (void)bar;
@@ -516,8 +539,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       unsigned long long *ct_ = args.trace + 256 * kTraceStride + 4 * kTraceMma + 6 * kTraceConv;
       int gkb = 0;
       for (int u = cid; u < sc.total && gkb < kTraceMma; u += ncl) {
-        const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
-      const GroupView gv = group_view<LPAD>(args, f.g);
+        const FusedUnit f = fused_decode<(LPAD != 64) && !DUAL>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, DUAL ? (int)pid : f.g);
         for (int kb = 0; kb < f.nk && gkb < kTraceMma; ++kb, ++gkb) {
           ptx::mbar_wait(&bars.kb_empty[gkb % C::NS], (gkb / C::NS) & 1);
           ct_[gkb] = clock64();
@@ -531,8 +554,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       int gkb = 0, gq = 0, ui = 0;
 #pragma unroll 1
       for (int u = cid; u < sc.total; u += ncl, ++ui) {
-        const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
-      const GroupView gv = group_view<LPAD>(args, f.g);
+        const FusedUnit f = fused_decode<(LPAD != 64) && !DUAL>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, DUAL ? (int)pid : f.g);
 #pragma unroll 1
         for (int kb = 0; kb < f.nk; ++kb, ++gkb) {
           if (lane == 0 && kb == 0) SPCA_TRACE(ui, 5);
@@ -559,11 +582,11 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             if (!(args.dbg & 2))
               tc_mma_stage2<LPAD>(tmem + C::A_TMEM + 64 * ks, tmem + buf * C::ACC_COLS,
                                   bdesc0 + (uint64_t)((bs * C::B_STAGE) >> 4), first);
-            ptx::mma2_commit_both(&bars.kb_empty[ks]);
+            ptx::mma2_commit_both(&bars.kb_empty[ks], pmask);
 #if !SPCA_RELAY
-            ptx::mma2_commit_both(&bars.b_empty[bs]);
+            ptx::mma2_commit_both(&bars.b_empty[bs], pmask);
 #endif
-            if ((kb % kPromote) == kPromote - 1 || kb == f.nk - 1) ptx::mma2_commit_both(&bars.acc_full[buf]);
+            if ((kb % kPromote) == kPromote - 1 || kb == f.nk - 1) ptx::mma2_commit_both(&bars.acc_full[buf], pmask);
           }
           __syncwarp();
         }
@@ -575,12 +598,12 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     const int t = ct & 127;    // TMEM lane: G row / H column within the tile
     const int grp = ct >> 7;   // converts the K blocks kb = grp (mod kGroups)
     const uint32_t lane_base = tmem + ((uint32_t)(t & ~31) << 16);
-    const uint32_t kbfull_l = ptx::mapa(ptx::smem_u32(&bars.kb_full[0]), 0);
+    const uint32_t kbfull_l = ptx::mapa(ptx::smem_u32(&bars.kb_full[0]), leader);
     int gkb = 0, ui = 0, gpa = 0;  // gpa: A slot pairs consumed (SPCA_PAIRA)
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
-      const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
-      const GroupView gv = group_view<LPAD>(args, f.g);
+      const FusedUnit f = fused_decode<(LPAD != 64) && !DUAL>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, DUAL ? (int)pid : f.g);
       float cs = 0.f, cc = 0.f;   // H: column sum (fp32 Kahan over the unit)
       // fused normalisation, G units: shift every value of the row by its first
       // value a0 (d = a - a0; exact for nearby values) and sum d, d^2 (Kahan)
@@ -705,7 +728,12 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         // can go back to TMA (one lane's arrive would not order the other lanes'
         // outstanding shared loads against the next TMA write)
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&bars.a_empty[ab]);
+        if (lane == 0) {
+          ptx::mbar_arrive(&bars.a_empty[ab]);
+          // DUAL, pair 1: the slot's data came from pair 0's multicast; its producer
+          // refills this CTA's slot too, so it waits for this release as well
+          if (DUAL && pid == 1) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&bars.a_empty[ab]), crank - 2));
+        }
         if (gk >= C::NS) {
           ptx::mbar_wait(&bars.kb_empty[ts], ((gk / C::NS) - 1) & 1);
 #if SPCA_RELAY
@@ -776,13 +804,13 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     const int t = pt & 127;              // TMEM lane: G row / H column within the tile
     const int c0 = (pt >> 7) * 64;       // this thread's 64 output columns
     const uint32_t lane_base = tmem + ((uint32_t)(t & ~31) << 16);
-    const uint32_t accempty_l = ptx::mapa(ptx::smem_u32(&bars.acc_empty[0]), 0);
+    const uint32_t accempty_l = ptx::mapa(ptx::smem_u32(&bars.acc_empty[0]), leader);
     const uint32_t stg_row = ptx::smem_u32(smem + C::STG_OFF + t * LPAD * 4);
     int gq = 0, ui = 0;
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
-      const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
-      const GroupView gv = group_view<LPAD>(args, f.g);
+      const FusedUnit f = fused_decode<(LPAD != 64) && !DUAL>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, DUAL ? (int)pid : f.g);
       const int nq = (f.nk + kPromote - 1) / kPromote;
       float racc[64];
 #pragma unroll
@@ -861,8 +889,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
     int ui = 0;
 #pragma unroll 1
     for (int u = cid; u < sc.total; u += ncl, ++ui) {
-      const FusedUnit f = fused_decode<LPAD != 64>(sc, u);
-      const GroupView gv = group_view<LPAD>(args, f.g);
+      const FusedUnit f = fused_decode<(LPAD != 64) && !DUAL>(sc, u);
+      const GroupView gv = group_view<LPAD>(args, DUAL ? (int)pid : f.g);
       const int tile = 2 * f.a + (int)rank;
       const int sb = ui % C::NSTG;  // staging buffer of this unit
       ptx::mbar_wait(&bars.epi_full[sb], (ui / C::NSTG) & 1);

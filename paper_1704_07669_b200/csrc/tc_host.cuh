@@ -85,6 +85,19 @@ bool tc_merged_groups(const spca_sketch *h) {
   static const bool seq = getenv("SPCA_TC_SEQ_GROUPS") != nullptr;
   return h->tc_groups > 1 && !h->normalize && !seq;
 }
+int tc_max_quads();
+// Two column groups of 128 (l_pad 256, config 5) as one launch of clusters of
+// four, a CTA pair per group, each A tile fetched once and multicast to both
+// pairs (tc_pass_kernel<.., DUAL>). Opt-in (SPCA_TC_DUAL=1): bitwise equal to
+// the default, but measured slower — config 5 63.4 vs 55.7 ms, 20 000 rows
+// 24.1 vs 20.6 ms: only 33 clusters of four fit (132 SMs instead of 148) and
+// the two pairs run in lockstep (pair 0 refills a slot only after both pairs
+// consumed it), which costs more than the halved A traffic saves
+// (profiles/r5_dual_groups.txt). Fused normalisation keeps one launch per group.
+bool tc_dual_groups(const spca_sketch *h) {
+  static const bool on = getenv("SPCA_TC_DUAL") != nullptr && atoi(getenv("SPCA_TC_DUAL")) != 0;
+  return on && h->tc_groups == 2 && h->tc_lp == 128 && tc_merged_groups(h) && tc_max_quads() >= 1;
+}
 
 FusedSched tc_base_sched(const spca_sketch *h) {
   FusedSched s{};
@@ -179,7 +192,38 @@ int tc_set_smem_attrs() {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcCfg<LPAD>::SMEM) !=
         cudaSuccess)
       return 1;
+  if (LPAD == 128)
+    for (auto k : {tc_pass_kernel<128, false, false, true>, tc_pass_kernel<128, false, true, true>})
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcCfg<128>::SMEM) !=
+          cudaSuccess)
+        return 1;
   return 0;
+}
+
+// Clusters of four (two CTA pairs, DUAL) that can be resident at once
+int tc_max_quads() {
+  static int cached[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && cached[dev] > 0) return cached[dev];
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(4, 1, 1);
+  cfg.blockDim = dim3(TcCfg<128>::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = TcCfg<128>::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 4;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, tc_pass_kernel<128, false, false, true>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (dev >= 0 && dev < 64) cached[dev] = nc;
+  return nc;
 }
 
 // CTA pairs that can be resident at once: the persistent pass needs every
@@ -407,8 +451,10 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   if ((lda % 4) != 0 || (reinterpret_cast<uintptr_t>(a) % 16) != 0)
     return set_err(h, SPCA_ERR_CONFIG, -1, "tensor-core path needs 16-byte aligned rows");
   FusedSched s = tc_base_sched(h);
-  const bool merged = tc_merged_groups(h);
-  s.Gr = merged ? h->tc_groups : 1;
+  const bool dual = tc_dual_groups(h);
+  const bool merged = dual || tc_merged_groups(h);
+  s.Gr = (merged && !dual) ? h->tc_groups : 1;  // DUAL: each unit covers both groups (one per pair)
+  const int ngroups = merged ? h->tc_groups : 1;  // groups one launch sketches
   s.C = (int)ceil_div(rows, s.R0);
   s.rows_last = (int)(rows - (int64_t)(s.C - 1) * s.R0);
   s.ntl = (int)ceil_div(s.rows_last, 128);
@@ -449,14 +495,15 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
     ta_h2 = &fa_h2;
   }
   const size_t ctr_words = (size_t)s.C * (4 * s.T + 2) + 2 * s.X;  // per group
-  const int grid = 2 * std::max(1, std::min(h->max_pairs, s.total));
+  const int cs = dual ? 4 : 2;  // CTAs per cluster
+  const int grid = cs * std::max(1, std::min(dual ? tc_max_quads() : h->max_pairs, s.total));
 #if SPCA_BULK_EPI
   // H units add into the running H at L2 (bulk reduce-add): a launch that
   // starts a flush period starts from zero instead of overwriting
   if (h->chunks_since_flush == 0) CK(h, cudaMemsetAsync(h->hpart, 0, (size_t)h->n * h->lpad * 4, h->stream));
 #endif
   for (int grp = 0; grp < (merged ? 1 : h->tc_groups); ++grp) {
-  CK(h, cudaMemsetAsync(h->tc_ctr, 0, (size_t)s.Gr * ctr_words * 4, h->stream));
+  CK(h, cudaMemsetAsync(h->tc_ctr, 0, (size_t)ngroups * ctr_words * 4, h->stream));
   FusedArgs args{};
   args.s = s;
   args.n = (int)h->n;
@@ -503,6 +550,7 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   auto kern = h->tc_lp == 64
                   ? (h->normalize ? tc_pass_kernel<64, true>
                                   : (h->shift_on ? tc_pass_kernel<64, false, true> : tc_pass_kernel<64, false>))
+                  : dual ? (h->shift_on ? tc_pass_kernel<128, false, true, true> : tc_pass_kernel<128, false, false, true>)
                   : (h->normalize ? tc_pass_kernel<128, true>
                                   : (h->shift_on ? tc_pass_kernel<128, false, true> : tc_pass_kernel<128, false>));
   const unsigned threads = h->tc_lp == 64 ? TcCfg<64>::THREADS : TcCfg<128>::THREADS;
@@ -518,35 +566,39 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
   } else {
     CK(h, cudaEventCreateWithFlags(&ps.last, cudaEventDisableTiming));
   }
-#if SPCA_PAIRA
-  kern<<<grid, threads, smem, h->stream>>>(*ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, *ta_g3, *ta_h2, args);
-#else
-  (void)ta_g3;
-  (void)ta_h2;
   {
     // Cooperative launch: the driver co-schedules the whole grid (every CTA
     // resident at once, whatever else runs on the device), which the
     // persistent pass's inter-CTA waits rely on; a grid that cannot be
     // co-resident fails here (cudaErrorCooperativeLaunchTooLarge) instead of
-    // hanging. The kernel's cluster shape (2, 1, 1) is compiled in.
+    // hanging. Clusters of two CTAs (a pair), or four (DUAL: two pairs).
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3((unsigned)grid, 1, 1);
     lc.blockDim = dim3(threads, 1, 1);
     lc.dynamicSmemBytes = smem;
     lc.stream = h->stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = h->tc_coop ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = (unsigned)cs;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
     lc.attrs = at;
-    lc.numAttrs = 1;
+    lc.numAttrs = 2;
+#if SPCA_PAIRA
+    cudaError_t le = cudaLaunchKernelEx(&lc, kern, *ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, *ta_g3, *ta_h2, args);
+#else
+    (void)ta_g3;
+    (void)ta_h2;
     cudaError_t le = cudaLaunchKernelEx(&lc, kern, *ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, args);
+#endif
     if (le != cudaSuccess) {
       cudaGetLastError();
-      return set_err(h, SPCA_ERR_CUDA, -1, "pass kernel launch (grid %d, cooperative %d) failed: %s", grid,
-                     h->tc_coop ? 1 : 0, cudaGetErrorString(le));
+      return set_err(h, SPCA_ERR_CUDA, -1, "pass kernel launch (grid %d, cluster %d, cooperative %d) failed: %s",
+                     grid, cs, h->tc_coop ? 1 : 0, cudaGetErrorString(le));
     }
   }
-#endif
   CK_LAUNCH(h);
   CK(h, cudaEventRecord(ps.last, h->stream));
   }

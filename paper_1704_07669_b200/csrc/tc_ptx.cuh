@@ -179,12 +179,22 @@ __device__ __forceinline__ void mma2_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, u
       : "memory");
 }
 // arrive on the mbarrier at the same offset in both CTAs of the pair when all
-// prior pair MMAs of this thread complete
-__device__ __forceinline__ void mma2_commit_both(uint64_t *bar) {
+// prior pair MMAs of this thread complete (mask: the pair's two cluster ranks)
+__device__ __forceinline__ void mma2_commit_both(uint64_t *bar, uint16_t mask = 3) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
-      "h"((uint16_t)3)
+      "h"(mask)
+      : "memory");
+}
+// TMA tensor load delivered to the same shared-memory offset of every CTA in
+// `mask` (cluster ranks), completing on the mbarrier at the same offset in each
+__device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y,
+                                               uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "h"(mask), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, float4 v) {
