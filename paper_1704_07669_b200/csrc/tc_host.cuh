@@ -125,7 +125,9 @@ FusedSched tc_base_sched(const spca_sketch *h) {
   const int rkb = s.R0 / 32;
   // H units: row segments of up to 48 K blocks (config 3, 80-block chunks:
   // two segments of 40 ran 17% faster than three of 27)
-  s.RS = (int)ceil_div(rkb, std::max(U, 48));
+  int hu = std::max(U, 48);
+  if (const char *e = getenv("SPCA_TC_HSEG")) hu = std::max(1, atoi(e));  // tuning knob: K blocks per H unit
+  s.RS = (int)ceil_div(rkb, hu);
   s.hseg = (int)ceil_div(rkb, s.RS);
   s.RS = (int)ceil_div(rkb, s.hseg);
   s.D = 2;  // measured: one extra stage of slack removes the H units' waits for G^T
