@@ -67,6 +67,16 @@ def parse():
     return p.parse_args()
 
 
+def workload_config(workload: str, cs: dict, m_total: int, m_rank: int, world: int, mode: str) -> dict:
+    """The `config` object of a bench line: the workload alone, so both arms
+    (ours and --impl reference) print the same object for the same run."""
+    return {"workload": workload, "m": int(m_total), "m_per_gpu": int(m_rank), "n": cs["n"], "l": cs["l"],
+            "k": cs["k"], "rank": cs["rank"], "spectrum": cs["spectrum"], "noise": cs["noise"],
+            "parallelism": f"row-shard x{world} ({mode})",
+            "l2": "inputs larger than L2" if m_rank * cs["n"] * 4 >= (512 << 20)
+                  else "L2 flushed before every timed step"}
+
+
 def scaling_mode(args) -> str:
     if args.scaling != "auto":
         return args.scaling
@@ -285,8 +295,9 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * sec,
         "higher_is_better": True, "scaling": scaling_mode(args), "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": args.config if full else f"{args.config} row prefix", "m": m, "n": n, "l": l,
-                   "k": cs["k"], "block_rows": br},
+        "config": workload_config(args.config if full else f"{args.config} row prefix", cs, m, m, world,
+                                  scaling_mode(args)),
+        "precision": "fp64 (numpy / BLAS)", "block_rows": br,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "cores_physical": phys, "kind": kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -599,14 +610,14 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": mode, "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": args.config, "m": m_total, "m_per_gpu": m, "n": n, "l": l, "k": cs["k"],
-                   "rank": cs["rank"], "spectrum": cs["spectrum"], "noise": cs["noise"],
-                   "precision": "3xTF32 tcgen05" if used_tc else ("DMMA fp64" if args.dtype == "f64" else "FFMA"),
-                   "parallelism": f"row-shard x{world} ({mode})",
-                   "l2": ("inputs larger than L2 (A is %.1f GB per GPU)" % (bytes_per_rank / 1e9)
-                          if flush is None else
-                          "L2 flushed before every timed step (512 MB write, untimed; A is %.0f MB)"
-                          % (bytes_per_rank / 1e6))},
+        # the workload only (identical in the reference arm's line); how this arm
+        # computes it is in "precision"
+        "config": workload_config(args.config, cs, m_total, m, world, mode),
+        "precision": "3xTF32 tcgen05" if used_tc else ("DMMA fp64" if args.dtype == "f64" else "FFMA"),
+        "l2": ("inputs larger than L2 (A is %.1f GB per GPU)" % (bytes_per_rank / 1e9)
+               if flush is None else
+               "L2 flushed before every timed step (512 MB write, untimed; A is %.0f MB)"
+               % (bytes_per_rank / 1e6)),
         "roofline": roofline,
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
