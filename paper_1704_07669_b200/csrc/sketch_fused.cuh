@@ -282,10 +282,12 @@ struct PairBars {
 // DUAL: clusters of four CTAs = two CTA pairs sketching two column groups of
 // the same rows (l_pad 256 as two groups of 128): pair 0 loads every A tile
 // once and multicasts it to the matching CTA of pair 1 (each A tile leaves
-// L2 once for both groups), pair p computes group p. Cluster dims come from
-// the launch (2 or 4).
+// L2 once for both groups), pair p computes group p. The cluster shape is
+// compiled in (2, or 4 for DUAL): with the shape given as a launch attribute
+// the cooperative launch failed under ncu (LaunchFailed, round 2 session 4),
+// and the driver lists the smoke test's kernels with ncu.
 template <int LPAD, bool NORM, bool SHIFT = false, bool DUAL = false>
-__global__ void __launch_bounds__(TcCfg<LPAD>::THREADS, 1)
+__global__ void __cluster_dims__(DUAL ? 4 : 2, 1, 1) __launch_bounds__(TcCfg<LPAD>::THREADS, 1)
 tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ CUtensorMap tAh,
                const __grid_constant__ CUtensorMap tWhi, const __grid_constant__ CUtensorMap tWlo,
                const __grid_constant__ CUtensorMap tGT,

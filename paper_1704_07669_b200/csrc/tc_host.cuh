@@ -403,6 +403,47 @@ int tc_unit_order(spca_sketch *h, FusedSched &s) {
     if ((int)keys.size() != s.total) return set_err(h, SPCA_ERR_STATE, -1, "unit order size mismatch");
     std::vector<int> ord(keys.size());
     for (size_t i = 0; i < keys.size(); ++i) ord[i] = keys[i].second;
+    // Round alignment. Unit u runs on pair u mod ncl, so units [j ncl, (j + 1) ncl)
+    // form a "round" that the pairs execute at about the same time. The W = S Gr
+    // units of one G tile pair wait for one another in their epilogues (K-split
+    // reduction): a tile whose units straddle a round boundary makes the earlier
+    // round's CTAs wait a whole unit (~16 us) for the later round's. Where a tile
+    // would straddle, the rest of the round is filled with the next H units of an
+    // EARLIER chunk instead (their G^T dependencies were dealt at least a stage
+    // before; the relative order of the H units, and so every summation order,
+    // is unchanged: results stay bitwise equal). SPCA_TC_ALIGN=0 turns it off.
+    static const int align_on = getenv("SPCA_TC_ALIGN") ? atoi(getenv("SPCA_TC_ALIGN")) : 1;
+    const int ncl = std::max(1, std::min(h->max_pairs, s.total));
+    const int W = s.S * s.Gr;
+    if (align_on && W > 1 && W <= ncl) {
+      std::vector<int> out;
+      out.reserve(ord.size());
+      std::vector<char> taken(ord.size(), 0);
+      size_t hscan = 0;  // next candidate filler (H units are pulled in sequence order)
+      for (size_t i = 0; i < ord.size(); ++i) {
+        if (taken[i]) continue;
+        const int e = ord[i], kind = e >> 30, c = (e >> 15) & 0x7fff, r = e & 0x7fff;
+        if (kind == 0 && r % W == 0) {
+          int rem = ncl - (int)(out.size() % (size_t)ncl);
+          if (rem < W) {  // the tile would straddle: fill the round with H units of earlier chunks
+            hscan = std::max(hscan, i + 1);
+            while (rem > 0 && hscan < ord.size()) {
+              const int eh = ord[hscan];
+              if (!taken[hscan] && (eh >> 30) == 1) {
+                if (((eh >> 15) & 0x7fff) >= c) break;  // its own G units are not dealt yet
+                taken[hscan] = 1;
+                out.push_back(eh);
+                --rem;
+              }
+              ++hscan;
+              if (hscan > i + 4 * (size_t)P) break;  // bounded look-ahead
+            }
+          }
+        }
+        out.push_back(e);
+      }
+      if (out.size() == ord.size()) ord.swap(out);
+    }
     if ((int64_t)ord.size() > h->order_cap) {
       dfree(h, h->order_dev);
       h->order_dev = nullptr;
@@ -579,15 +620,11 @@ int tc_launch_rows(spca_sketch *h, const void *a, int64_t lda, int64_t rows) {
     lc.blockDim = dim3(threads, 1, 1);
     lc.dynamicSmemBytes = smem;
     lc.stream = h->stream;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[1];  // the cluster shape (cs) is compiled into the kernel
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = h->tc_coop ? 1 : 0;
-    at[1].id = cudaLaunchAttributeClusterDimension;
-    at[1].val.clusterDim.x = (unsigned)cs;
-    at[1].val.clusterDim.y = 1;
-    at[1].val.clusterDim.z = 1;
     lc.attrs = at;
-    lc.numAttrs = 2;
+    lc.numAttrs = 1;
 #if SPCA_PAIRA
     cudaError_t le = cudaLaunchKernelEx(&lc, kern, *ta_g, *ta_h, h->tm_whi, h->tm_wlo, h->tm_gT, *ta_g3, *ta_h2, args);
 #else
