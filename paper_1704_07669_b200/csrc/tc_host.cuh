@@ -411,8 +411,13 @@ int tc_unit_order(spca_sketch *h, FusedSched &s) {
     // would straddle, the rest of the round is filled with the next H units of an
     // EARLIER chunk instead (their G^T dependencies were dealt at least a stage
     // before; the relative order of the H units, and so every summation order,
-    // is unchanged: results stay bitwise equal). SPCA_TC_ALIGN=0 turns it off.
-    static const int align_on = getenv("SPCA_TC_ALIGN") ? atoi(getenv("SPCA_TC_ALIGN")) : 1;
+    // is unchanged: results stay bitwise equal). Opt-in (SPCA_TC_ALIGN=1): measured
+    // SLOWER (config 2 1.634 -> 1.696 ms, config 3 10.85 -> 11.92, config 5 60.5 ->
+    // 66.5): with tiles pinned to round starts the pairs' G / H mix becomes static
+    // (4 to 68 G units per pair instead of 49 to 57) and H units cost ~20% more than
+    // G units; the default order's 79-unit stages rotate over the 74 pairs
+    // (profiles/r6_align_ab.txt).
+    static const int align_on = getenv("SPCA_TC_ALIGN") ? atoi(getenv("SPCA_TC_ALIGN")) : 0;
     const int ncl = std::max(1, std::min(h->max_pairs, s.total));
     const int W = s.S * s.Gr;
     if (align_on && W > 1 && W <= ncl) {
