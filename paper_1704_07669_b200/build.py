@@ -50,6 +50,10 @@ if os.environ.get("SPCA_BUILD_PROMO_GP") is not None:  # G partials written by t
     FLAGS.append("-DSPCA_PROMO_GP=" + os.environ["SPCA_BUILD_PROMO_GP"])
 if os.environ.get("SPCA_BUILD_STACKED") is not None:  # experiment: l_pad=64 MMA form
     FLAGS.append("-DSPCA_STACKED_64=" + os.environ["SPCA_BUILD_STACKED"])
+if os.environ.get("SPCA_BUILD_GROUPS") is not None:  # experiment: converter groups for l_pad 64 (2 / 3)
+    FLAGS.append("-DSPCA_GROUPS_64=" + os.environ["SPCA_BUILD_GROUPS"])
+if os.environ.get("SPCA_BUILD_KPAIR") is not None:  # experiment: K blocks per MMA-warp iteration, l_pad 64 (0: one, 1: two)
+    FLAGS.append("-DSPCA_KPAIR=" + os.environ["SPCA_BUILD_KPAIR"])
 
 
 def _stale() -> bool:

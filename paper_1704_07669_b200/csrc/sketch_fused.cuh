@@ -74,6 +74,7 @@ struct FusedSched {
   int X, nx;      // H: 256-column tile pairs, real 128-column tiles over n
   int RS, hseg;   // H: row segments per chunk, K blocks per segment
   int D;          // stage lag of a chunk's H units behind its G units
+  int kp;         // every unit's K block count is a multiple of kp (TcCfg::KP; kseg, hseg too)
   int Gr;         // column groups of 128 sketched together (l > 128: each unit
                   // covers one group; a unit's groups are dealt side by side, so
                   // they read the same A tile at the same time: one DRAM read)
@@ -236,6 +237,9 @@ __host__ __device__ __forceinline__ FusedUnit fused_decode(const FusedSched &s, 
     f.k0 = f.b * s.hseg;
     f.nk = max(0, min(s.hseg, (f.rows + 31) / 32 - f.k0));
   }
+  // whole MMA-warp iterations: an odd tail takes one more K block, which reads
+  // zeros (columns >= n / rows beyond the launch are TMA out-of-bounds fill)
+  if (s.kp > 1) f.nk = (f.nk + s.kp - 1) / s.kp * s.kp;
   return f;
 }
 
@@ -299,10 +303,10 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ PairBars<LPAD> bars;
-  __shared__ double stg_cs[C::NSTG][kGroups * 128];  // H: per converter group, column-sum partial
+  __shared__ double stg_cs[C::NSTG][C::GROUPS * 128];  // H: per converter group, column-sum partial
   __shared__ int stg_bad[128];              // G epilogue: row of the tile has a non-finite partial
   __shared__ __align__(16) float sst[C::NA][64];      // norm, H blocks: a0 and 1/norm of the block's 32 rows
-  __shared__ double stg_rs[C::NSTG][2][kGroups * 128];  // norm, G units: per group sums of d and d^2
+  __shared__ double stg_rs[C::NSTG][2][C::GROUPS * 128];  // norm, G units: per group sums of d and d^2
   __shared__ float sl_stat[128][2];                   // norm, G slice reduction: mean_d, inv per row
   const FusedSched &sc = args.s;
 
@@ -326,7 +330,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       ptx::mbar_init(&bars.a_empty[s], SPCA_PAIRA ? 8 : ((DUAL && pid == 0) ? 8 : 4));
     }
     for (int s = 0; s < C::NS; ++s) {
-      ptx::mbar_init(&bars.kb_full[s], 2 * 4);  // one converter group (4 warps) in each CTA
+      ptx::mbar_init(&bars.kb_full[s], 2 * 4 * C::KP);  // KP converter groups (4 warps each) in each CTA
       ptx::mbar_init(&bars.kb_empty[s], 1);
     }
     for (int s = 0; s < C::NB; ++s) {
@@ -338,7 +342,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       ptx::mbar_init(&bars.acc_empty[s], 2 * C::PROMO_WARPS);
     }
     for (int s = 0; s < C::NSTG; ++s) {
-      ptx::mbar_init(&bars.epi_full[s], kTcConv + 32 * C::PROMO_WARPS);  // converters (column sums) + promoters
+      ptx::mbar_init(&bars.epi_full[s], C::CONV + 32 * C::PROMO_WARPS);  // converters (column sums) + promoters
       ptx::mbar_init(&bars.epi_empty[s], kTcEpi);
     }
     ptx::fence_mbar_init();
@@ -544,7 +548,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         const FusedUnit f = fused_decode<(LPAD != 64) && !DUAL>(sc, u);
       const GroupView gv = group_view<LPAD>(args, DUAL ? (int)pid : f.g);
         for (int kb = 0; kb < f.nk && gkb < kTraceMma; ++kb, ++gkb) {
-          ptx::mbar_wait(&bars.kb_empty[gkb % C::NS], (gkb / C::NS) & 1);
+          ptx::mbar_wait(&bars.kb_empty[(gkb % C::NS) / C::KP], (gkb / C::NS) & 1);
           ct_[gkb] = clock64();
         }
       }
@@ -559,7 +563,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         const FusedUnit f = fused_decode<(LPAD != 64) && !DUAL>(sc, u);
       const GroupView gv = group_view<LPAD>(args, DUAL ? (int)pid : f.g);
 #pragma unroll 1
-        for (int kb = 0; kb < f.nk; ++kb, ++gkb) {
+        for (int kb = 0; kb < f.nk; kb += C::KP, gkb += C::KP) {
           if (lane == 0 && kb == 0) SPCA_TRACE(ui, 5);
           const int ks = gkb % C::NS, bs = gkb % C::NB;
           const int q = gq + kb / kPromote, buf = q & 1;
@@ -573,32 +577,37 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           if (mt) mt[0] = clock64();
           if (first && q >= 2) ptx::mbar_wait(&bars.acc_empty[buf], ((q >> 1) - 1) & 1);
           if (mt) mt[1] = clock64();
-          ptx::mbar_wait(&bars.kb_full[ks], (gkb / C::NS) & 1);
+          ptx::mbar_wait(&bars.kb_full[ks / C::KP], (gkb / C::NS) & 1);
           if (mt) mt[2] = clock64();
 #if !SPCA_RELAY
+          static_assert(C::KP == 1, "the B ring handshake through the MMA warp is per K block");
           ptx::mbar_wait(&bars.b_full[bs], (gkb / C::NB) & 1);
 #endif
           if (mt) mt[3] = clock64();
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
-            if (!(args.dbg & 2))
-              tc_mma_stage2<LPAD>(tmem + C::A_TMEM + 64 * ks, tmem + buf * C::ACC_COLS,
-                                  bdesc0 + (uint64_t)((bs * C::B_STAGE) >> 4), first);
-            ptx::mma2_commit_both(&bars.kb_empty[ks], pmask);
+            if (!(args.dbg & 2)) {
+#pragma unroll
+              for (int j = 0; j < C::KP; ++j)  // the iteration's K blocks: operand stages ks + j, B stages (gkb + j) % NB
+                tc_mma_stage2<LPAD>(tmem + C::A_TMEM + 64 * (ks + j), tmem + buf * C::ACC_COLS,
+                                    bdesc0 + (uint64_t)((((gkb + j) % C::NB) * C::B_STAGE) >> 4), first && j == 0);
+            }
+            ptx::mma2_commit_both(&bars.kb_empty[ks / C::KP], pmask);
 #if !SPCA_RELAY
             ptx::mma2_commit_both(&bars.b_empty[bs], pmask);
 #endif
-            if ((kb % kPromote) == kPromote - 1 || kb == f.nk - 1) ptx::mma2_commit_both(&bars.acc_full[buf], pmask);
+            if (((kb + C::KP - 1) % kPromote) == kPromote - 1 || kb + C::KP >= f.nk)
+              ptx::mma2_commit_both(&bars.acc_full[buf], pmask);
           }
           __syncwarp();
         }
         gq += (f.nk + kPromote - 1) / kPromote;
       }
     }
-  } else if (warp >= 4 && warp < 4 + kTcConv / 32) {  // -------------------- converters
+  } else if (warp >= 4 && warp < 4 + C::CONV / 32) {  // -------------------- converters
     const int ct = threadIdx.x - 128;
     const int t = ct & 127;    // TMEM lane: G row / H column within the tile
-    const int grp = ct >> 7;   // converts the K blocks kb = grp (mod kGroups)
+    const int grp = ct >> 7;   // converts the K blocks kb = grp (mod GROUPS)
     const uint32_t lane_base = tmem + ((uint32_t)(t & ~31) << 16);
     const uint32_t kbfull_l = ptx::mapa(ptx::smem_u32(&bars.kb_full[0]), leader);
     int gkb = 0, ui = 0, gpa = 0;  // gpa: A slot pairs consumed (SPCA_PAIRA)
@@ -616,7 +625,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       }
       if (ct == 0) SPCA_TRACE(ui, 0);
 #pragma unroll 1
-      for (int kb = grp; kb < f.nk; kb += kGroups) {
+      for (int kb = grp; kb < f.nk; kb += C::GROUPS) {
         const int gk = gkb + kb;
 #if SPCA_PAIRA
         const int ga = gpa + (kb >> 1), ab = ga % C::NP;  // A slot pair of this block
@@ -747,7 +756,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           if (DUAL && pid == 1) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&bars.a_empty[ab]), crank - 2));
         }
         if (gk >= C::NS) {
-          ptx::mbar_wait(&bars.kb_empty[ts], ((gk / C::NS) - 1) & 1);
+          ptx::mbar_wait(&bars.kb_empty[ts / C::KP], ((gk / C::NS) - 1) & 1);
 #if SPCA_RELAY
           // block gk - NS is done: its B stage goes back to this CTA's B producer
           // (one arrival per block: lane 0 of the group's first warp)
@@ -787,7 +796,7 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
 #endif
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(kbfull_l + 8 * ts);
+        if (lane == 0) ptx::mbar_arrive_cluster(kbfull_l + 8 * (ts / C::KP));
         if (ctr) ctr[5] = clock64();
       }
 #if SPCA_PAIRA
@@ -922,8 +931,14 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           if (NORM) {  // this segment's row sums of d, d^2 (the two converter groups, in order)
             double *rp = reinterpret_cast<double *>(args.rstat_part) +
                          ((((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 + e) * 2;
-            rp[0] = stg_rs[sb][0][e] + stg_rs[sb][0][128 + e];
-            rp[1] = stg_rs[sb][1][e] + stg_rs[sb][1][128 + e];
+            double r0s = stg_rs[sb][0][e], r1s = stg_rs[sb][1][e];
+#pragma unroll
+            for (int g2 = 1; g2 < C::GROUPS; ++g2) {
+              r0s += stg_rs[sb][0][g2 * 128 + e];
+              r1s += stg_rs[sb][1][g2 * 128 + e];
+            }
+            rp[0] = r0s;
+            rp[1] = r1s;
           }
           flagged = stg_bad[e] != 0;
           ptx::named_bar(2, kTcEpi);  // every flag read before it is cleared for the next unit
@@ -963,8 +978,14 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           if (NORM) {  // this segment's row sums of d, d^2 (the two converter groups, in order)
             double *rp = reinterpret_cast<double *>(args.rstat_part) +
                          ((((size_t)gslot * twoT + tile) * sc.S + f.b) * 128 + e) * 2;
-            rp[0] = stg_rs[sb][0][e] + stg_rs[sb][0][128 + e];
-            rp[1] = stg_rs[sb][1][e] + stg_rs[sb][1][128 + e];
+            double r0s = stg_rs[sb][0][e], r1s = stg_rs[sb][1][e];
+#pragma unroll
+            for (int g2 = 1; g2 < C::GROUPS; ++g2) {
+              r0s += stg_rs[sb][0][g2 * 128 + e];
+              r1s += stg_rs[sb][1][g2 * 128 + e];
+            }
+            rp[0] = r0s;
+            rp[1] = r1s;
           }
           ptx::named_bar(2, kTcEpi);
           flagged = stg_bad[e] != 0;
@@ -1164,7 +1185,9 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             }
           }
 #endif
-          csv = stg_cs[sb][e] + stg_cs[sb][128 + e];
+          csv = stg_cs[sb][e];
+#pragma unroll
+          for (int g2 = 1; g2 < C::GROUPS; ++g2) csv += stg_cs[sb][g2 * 128 + e];
         }
         ptx::mbar_arrive(&bars.epi_empty[sb]);
         if (real) {

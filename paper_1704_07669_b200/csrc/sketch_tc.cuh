@@ -42,8 +42,28 @@ namespace spca {
 // TMEM lane quarter; group g takes the K blocks kb = g mod 2), then the
 // promoter warps (fold each accumulator period into fp32 registers and stage
 // the unit's result; 64 output columns per warp) and 4 epilogue warps.
-constexpr int kGroups = 2;      // converter groups
-constexpr int kTcConv = 128 * kGroups;  // converter threads
+// converter groups (TcCfg<LPAD>::GROUPS): group g takes the K blocks kb = g (mod
+// GROUPS). Two. Three for l_pad 64 (768 threads, 80 registers, ~70 bytes of
+// spills) measured no better: the skeleton (no loads, no MMAs, no epilogue)
+// went 1.013 -> 0.964 ms, the full pass 1.667 -> 1.694 ms, and one of two runs
+// hung (profiles/r6_groups_ab.txt) - the converter stage's group count is not
+// what bounds the pipeline.
+#ifndef SPCA_GROUPS_64
+#define SPCA_GROUPS_64 2
+#endif
+// K blocks per iteration of the MMA-issuing warp (l_pad 64). That warp's loop
+// is serial - wait for the operand stage, fence, issue, commit - and its waits
+// and commits cost 60-100 cycles each: with one K block per iteration it took
+// 620-750 cycles per block (fine trace, profiles/r6_fine_trace.txt: 396 cycles
+// of "issue + commit" with NO MMAs issued) against 384 tensor cycles, while the
+// converters ran five blocks ahead - the issuing warp bounded the pipeline.
+// With 2, the two converter groups' blocks 2j and 2j + 1 share one "stage full"
+// barrier and one commit: one wait, 24 MMAs, one commit per iteration. Every
+// unit then has an even number of K blocks (FusedSched::kp; an odd tail gets
+// one more block of TMA zero fill).
+#ifndef SPCA_KPAIR
+#define SPCA_KPAIR 1
+#endif
 constexpr int kTcEpi = 128;     // epilogue threads
 constexpr uint32_t kTmemCols = 512;
 #ifndef SPCA_PROMOTE
@@ -145,9 +165,13 @@ struct TcCfg {
   static constexpr bool STACKED = LPAD == 64 && SPCA_STACKED_64;
   static constexpr int ACC_COLS = STACKED ? 128 : LPAD;  // one accumulator
   static constexpr int NS = (kTmemCols - 2 * ACC_COLS) / 64;  // TMEM A operand stages
+  static constexpr int KP = (LPAD == 64 && SPCA_KPAIR && !SPCA_PAIRA) ? 2 : 1;  // K blocks per MMA-warp iteration
+  static_assert(NS % KP == 0 && SPCA_PROMOTE % KP == 0, "operand stages / accumulator period in whole iterations");
   // B ring: deep enough to cover an L2 round trip (~1-2 us) at the MMA rate
+  static constexpr int GROUPS = LPAD == 64 ? SPCA_GROUPS_64 : 2;  // converter groups
+  static constexpr int CONV = 128 * GROUPS;                       // converter threads
   static constexpr int PROMO_WARPS = 4 * (LPAD / 64);  // promoters: 64 output columns per thread
-  static constexpr int PROMO_BASE = 128 + kTcConv;     // first promoter thread
+  static constexpr int PROMO_BASE = 128 + CONV;        // first promoter thread
   static constexpr int EPI_BASE = PROMO_BASE + 32 * PROMO_WARPS;  // first epilogue thread
   static constexpr int THREADS = EPI_BASE + kTcEpi;
   static constexpr uint32_t A_BYTES = 128 * 32 * 4;   // raw A tile (16 KB)

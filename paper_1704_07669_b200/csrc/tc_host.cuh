@@ -117,8 +117,9 @@ FusedSched tc_base_sched(const spca_sketch *h) {
   // buffers allocated at setup fit either way)
   const int gcap = std::max(1, h->tc_groups);
   const int max_seg = std::max(1, h->max_pairs / (2 * gcap));
+  s.kp = h->tc_lp == 64 ? TcCfg<64>::KP : TcCfg<128>::KP;  // K blocks per MMA-warp iteration
   s.S = (int)std::min<int64_t>(ceil_div(s.nkb, U), max_seg);
-  s.kseg = (int)ceil_div(s.nkb, s.S);
+  s.kseg = (int)(ceil_div(ceil_div(s.nkb, s.S), s.kp) * s.kp);
   s.S = (int)ceil_div(s.nkb, s.kseg);
   s.nx = (int)ceil_div(h->n, 128);
   s.X = (int)ceil_div(s.nx, 2);
@@ -128,7 +129,7 @@ FusedSched tc_base_sched(const spca_sketch *h) {
   int hu = std::max(U, 48);
   if (const char *e = getenv("SPCA_TC_HSEG")) hu = std::max(1, atoi(e));  // tuning knob: K blocks per H unit
   s.RS = (int)ceil_div(rkb, hu);
-  s.hseg = (int)ceil_div(rkb, s.RS);
+  s.hseg = (int)(ceil_div(ceil_div(rkb, s.RS), s.kp) * s.kp);
   s.RS = (int)ceil_div(rkb, s.hseg);
   s.D = 2;  // measured: one extra stage of slack removes the H units' waits for G^T
   if (const char *e = getenv("SPCA_TC_LAG")) s.D = std::max(1, std::min(kMaxLag, atoi(e)));  // tuning knob
