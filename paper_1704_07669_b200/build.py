@@ -54,6 +54,8 @@ if os.environ.get("SPCA_BUILD_GROUPS") is not None:  # experiment: converter gro
     FLAGS.append("-DSPCA_GROUPS_64=" + os.environ["SPCA_BUILD_GROUPS"])
 if os.environ.get("SPCA_BUILD_KPAIR") is not None:  # experiment: K blocks per MMA-warp iteration, l_pad 64 (0: one, 1: two)
     FLAGS.append("-DSPCA_KPAIR=" + os.environ["SPCA_BUILD_KPAIR"])
+if os.environ.get("SPCA_BUILD_GTEAM") is not None:  # experiment: G slice reductions on their own two warps (0/1)
+    FLAGS.append("-DSPCA_GRED_TEAM=" + os.environ["SPCA_BUILD_GTEAM"])
 
 
 def _stale() -> bool:

@@ -311,6 +311,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
   const FusedSched &sc = args.s;
 
   static_assert(!DUAL || (!NORM && !SPCA_PAIRA && LPAD == 128), "dual pairs: plain / shift l_pad 128");
+  // G slice reductions on their own two warps (fused normalisation keeps them on the epilogue warps)
+  constexpr bool GTEAM = C::GT && !NORM && !DUAL;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = ptx::cluster_rank();
   const uint32_t rank = crank & 1u;              // rank in the CTA pair
@@ -363,6 +365,132 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
   ptx::cluster_sync();  // both CTAs' barriers exist before any cross-CTA arrive
   ptx::tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
+
+  // Phase B of a G unit's epilogue, once every K segment of the tile has written
+  // its partial: reduce THIS segment's slice of the tile's rows over the S
+  // partials in fixed order -> G rows (output), the split G^T operand of the H
+  // units, the readiness counters. Run by the epilogue warps (nth = 128) or by
+  // the reduction team (GTEAM: warp 3 and the last warp, nth = 64).
+  auto g_phase_b = [&](const FusedUnit &f, const GroupView &gv, const int tile, const int e, const int nth,
+                       const uint32_t barid) {
+    constexpr int NQ = LPAD / 4;
+    const int twoT = 2 * sc.T;
+    const int gslot = f.c % kSlots;
+    // reduce this segment's slice of the tile's rows over the S partials (fixed order)
+    const int r0 = (f.b * 128) / sc.S, r1 = ((f.b + 1) * 128) / sc.S;
+    const float *p0 = gv.gpart + (((size_t)gslot * twoT + tile) * sc.S) * 128 * LPAD;
+#if SPCA_BRAW
+    float *ghi = gv.gT + (size_t)gslot * LPAD * sc.R0;  // raw G^T of the slot
+#else
+    float *ghi = gv.gT + (size_t)(2 * gslot) * LPAD * sc.R0;
+    float *glo = ghi + (size_t)LPAD * sc.R0;
+#endif
+    if (NORM) {
+      // row statistics of the slice over the S segments (fixed order, fp64):
+      // mean_d = mean(a) - a0, norm = ||a - mean(a)||, from sums of d = a - a0
+      if (e < r1 - r0) {
+        const int r = r0 + e, rc = tile * 128 + r;
+        const double *rp = reinterpret_cast<const double *>(args.rstat_part) +
+                           (((size_t)gslot * twoT + tile) * sc.S * 128 + r) * 2;
+        double t1 = 0.0, t2 = 0.0;
+        for (int z = 0; z < sc.S; ++z) {
+          t1 += __ldcg(rp + (size_t)z * 256);
+          t2 += __ldcg(rp + (size_t)z * 256 + 1);
+        }
+        const double md = t1 / (double)args.n;
+        const double nrm = sqrt(fmax(t2 - t1 * md, 0.0));
+        const double inv = nrm > 0.0 ? 1.0 / nrm : 1.0;
+        const bool valid = rc < f.rows;
+        const int64_t grow = (int64_t)f.c * sc.R0 + rc;
+        sl_stat[r][0] = (float)md;
+        sl_stat[r][1] = (float)inv;
+        const size_t so = (size_t)gslot * sc.R0 + rc;
+        args.row_a0[so] = valid ? __ldg(args.a + grow * args.lda) : 0.f;
+        args.row_inv[so] = valid ? (float)inv : 1.f;
+        if (valid) args.row_coef[grow] = md * inv;
+      }
+      ptx::named_bar(barid, nth);
+    }
+    // items = (row, 8-column group), ROW fastest: consecutive threads take
+    // consecutive rows, so each G^T store of a warp covers consecutive rows
+    // of one G^T row (coalesced; the row-major order scattered them one
+    // row of G^T per lane: 1.5 ms of config 3's pass); a thread's two
+    // float4 loads per partial fill one 32-byte sector
+    const int nrs = r1 - r0;
+    constexpr int NO = LPAD / 8;  // 8-column groups
+#pragma unroll 1
+    for (int it = e; it < nrs * NO; it += nth) {
+      const int r = r0 + it % nrs, o = it / nrs;
+      const int rc = tile * 128 + r;  // row within the chunk
+      const bool valid = rc < f.rows;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int q = 2 * o + h2;
+        // partials of other CTAs: read through L2 (.cg), never a stale L1 line
+        const float4 *src = reinterpret_cast<const float4 *>(p0 + (size_t)r * LPAD) + q;
+        float4 acc = __ldcg(src);
+        int z = 1;
+        for (; z + 4 <= sc.S; z += 4) {  // four loads in flight, added in order z
+          float4 b4[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) b4[j] = __ldcg(src + (size_t)(z + j) * 128 * NQ);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc.x += b4[j].x; acc.y += b4[j].y; acc.z += b4[j].z; acc.w += b4[j].w;
+          }
+        }
+        for (; z < sc.S; ++z) {
+          const float4 b4 = __ldcg(src + (size_t)z * 128 * NQ);
+          acc.x += b4.x; acc.y += b4.y; acc.z += b4.z; acc.w += b4.w;
+        }
+        float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+        float b4[4] = {acc.x, acc.y, acc.z, acc.w};  // B operand of the H units
+        if (gv.left != nullptr && valid) {  // co-sketch: H += A^T L
+          const float4 l4 = __ldg(reinterpret_cast<const float4 *>(
+                                      gv.left + ((int64_t)f.c * sc.R0 + rc) * args.gld) + q);
+          b4[0] = l4.x; b4[1] = l4.y; b4[2] = l4.z; b4[3] = l4.w;
+        }
+        if (NORM) {  // G_hat = (d Omega - mean_d * 1^T Omega) / norm; the H units take G_hat / norm
+          const float md = sl_stat[r][0], inv = sl_stat[r][1];
+          const float4 w4 = __ldg(reinterpret_cast<const float4 *>(gv.wsum) + q);
+          const float ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            a4[j] = fmaf(-md, ws[j], a4[j]) * inv;
+            b4[j] = (gv.left != nullptr ? b4[j] : a4[j]) * inv;
+          }
+        }
+        if (valid)
+          reinterpret_cast<float4 *>(gv.g_out + ((int64_t)f.c * sc.R0 + rc) * args.gld)[q] =
+              make_float4(a4[0], a4[1], a4[2], a4[3]);
+#if SPCA_BRAW
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ghi[(size_t)(4 * q + j) * sc.R0 + rc] = valid ? b4[j] : 0.f;
+#else
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (args.dbg & 32768) break;  // profiling knob: no G^T stores
+          float h1 = 0.f, l1 = 0.f;
+          if (valid) split3(b4[j], h1, l1);
+#if SPCA_BCOMB
+          ghi[(size_t)bcomb_row(4 * q + j, 0, LPAD) * sc.R0 + rc] = h1;
+          ghi[(size_t)bcomb_row(4 * q + j, 1, LPAD) * sc.R0 + rc] = l1;
+#else
+          ghi[(size_t)(4 * q + j) * sc.R0 + rc] = h1;
+          glo[(size_t)(4 * q + j) * sc.R0 + rc] = l1;
+#endif
+        }
+#endif
+      }
+    }
+    ptx::fence_proxy_async_global();
+    __threadfence();
+    ptx::named_bar(barid, nth);
+    if (e == 0) {
+      atomicAdd(&gv.trdy[f.c * twoT + tile], 1);
+      atomicAdd(&gv.ready[f.c], 1);
+    }
+  };
 
   if (warp == 0) {  // ---------------------------------------------- A producer
     // L2 policy of A: the G units' loads (from HBM) must survive until the H
@@ -903,6 +1031,25 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
       if (SPCA_BULK_EPI) ptx::fence_proxy_async_smem();  // the staging leaves through the TMA engine
       ptx::mbar_arrive(&bars.epi_full[sb]);
     }
+  } else if (GTEAM && (warp == 3 || (C::GT_THREADS == 64 && warp == C::THREADS / 32 - 1))) {  // reduction team
+    // G units only: wait (on the global segment counter) until every K segment of
+    // the unit's tile has published its partial, then run phase B. Decoupled from
+    // the epilogue warps: no local hand-off is needed, the counter says it all.
+    const int tb = (warp == 3 ? 0 : 32) + lane;
+#pragma unroll 1
+    for (int u = cid; u < sc.total; u += ncl) {
+      const FusedUnit f = fused_decode<(LPAD != 64) && !DUAL>(sc, u);
+      if (f.kind != 0 || (args.dbg & 16384)) continue;
+      const GroupView gv = group_view<LPAD>(args, DUAL ? (int)pid : f.g);
+      const int tile = 2 * f.a + (int)rank;
+      if (tile >= fused_real_tiles(sc, f.c)) continue;
+      if (tb == 0) {
+        ptx::spin_until_geq(&gv.seg_cnt[f.c * 2 * sc.T + tile], sc.S);  // every segment's partial is in
+        if (f.c >= kSlots) ptx::spin_until_geq(&gv.hdone[f.c - kSlots], sc.nx * sc.RS);
+      }
+      ptx::named_bar(3, C::GT_THREADS);
+      g_phase_b(f, gv, tile, tb, C::GT_THREADS, 3u);
+    }
   } else if (warp >= C::EPI_BASE / 32) {  // --------------------------------- epilogue
     const int e = threadIdx.x - C::EPI_BASE;  // row (G) / column (H) of the tile
     constexpr int NQ = LPAD / 4;             // 16-byte chunks per row
@@ -1015,125 +1162,19 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
           __threadfence();
           ptx::named_bar(2, kTcEpi);
           int *cnt = &gv.seg_cnt[f.c * twoT + tile];
-          if (e == 0) {
-            atomicAdd(cnt, 1);
-            ptx::spin_until_geq(cnt, sc.S);  // every segment's partial is in
-            if (f.c >= kSlots) ptx::spin_until_geq(&gv.hdone[f.c - kSlots], sc.nx * sc.RS);
-          }
-          ptx::named_bar(2, kTcEpi);
-          // reduce this segment's slice of the tile's rows over the S partials (fixed order)
-          const int r0 = (f.b * 128) / sc.S, r1 = ((f.b + 1) * 128) / sc.S;
-          const float *p0 = gv.gpart + (((size_t)gslot * twoT + tile) * sc.S) * 128 * LPAD;
-#if SPCA_BRAW
-          float *ghi = gv.gT + (size_t)gslot * LPAD * sc.R0;  // raw G^T of the slot
-#else
-          float *ghi = gv.gT + (size_t)(2 * gslot) * LPAD * sc.R0;
-          float *glo = ghi + (size_t)LPAD * sc.R0;
-#endif
-          if (NORM) {
-            // row statistics of the slice over the S segments (fixed order, fp64):
-            // mean_d = mean(a) - a0, norm = ||a - mean(a)||, from sums of d = a - a0
-            if (e < r1 - r0) {
-              const int r = r0 + e, rc = tile * 128 + r;
-              const double *rp = reinterpret_cast<const double *>(args.rstat_part) +
-                                 (((size_t)gslot * twoT + tile) * sc.S * 128 + r) * 2;
-              double t1 = 0.0, t2 = 0.0;
-              for (int z = 0; z < sc.S; ++z) {
-                t1 += __ldcg(rp + (size_t)z * 256);
-                t2 += __ldcg(rp + (size_t)z * 256 + 1);
-              }
-              const double md = t1 / (double)args.n;
-              const double nrm = sqrt(fmax(t2 - t1 * md, 0.0));
-              const double inv = nrm > 0.0 ? 1.0 / nrm : 1.0;
-              const bool valid = rc < f.rows;
-              const int64_t grow = (int64_t)f.c * sc.R0 + rc;
-              sl_stat[r][0] = (float)md;
-              sl_stat[r][1] = (float)inv;
-              const size_t so = (size_t)gslot * sc.R0 + rc;
-              args.row_a0[so] = valid ? __ldg(args.a + grow * args.lda) : 0.f;
-              args.row_inv[so] = valid ? (float)inv : 1.f;
-              if (valid) args.row_coef[grow] = md * inv;
+          if constexpr (GTEAM) {
+            // the reduction team (warp 3 + the last warp) takes the unit from here: it
+            // waits for the tile's other K segments and reduces this segment's slice,
+            // so these warps are free for the next unit's staged result at once
+            if (e == 0) atomicAdd(cnt, 1);
+          } else {
+            if (e == 0) {
+              atomicAdd(cnt, 1);
+              ptx::spin_until_geq(cnt, sc.S);  // every segment's partial is in
+              if (f.c >= kSlots) ptx::spin_until_geq(&gv.hdone[f.c - kSlots], sc.nx * sc.RS);
             }
             ptx::named_bar(2, kTcEpi);
-          }
-          // items = (row, 8-column group), ROW fastest: consecutive threads take
-          // consecutive rows, so each G^T store of a warp covers consecutive rows
-          // of one G^T row (coalesced; the row-major order scattered them one
-          // row of G^T per lane: 1.5 ms of config 3's pass); a thread's two
-          // float4 loads per partial fill one 32-byte sector
-          const int nrs = r1 - r0;
-          constexpr int NO = LPAD / 8;  // 8-column groups
-#pragma unroll 1
-          for (int it = e; it < nrs * NO; it += kTcEpi) {
-            const int r = r0 + it % nrs, o = it / nrs;
-            const int rc = tile * 128 + r;  // row within the chunk
-            const bool valid = rc < f.rows;
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              const int q = 2 * o + h2;
-              // partials of other CTAs: read through L2 (.cg), never a stale L1 line
-              const float4 *src = reinterpret_cast<const float4 *>(p0 + (size_t)r * LPAD) + q;
-              float4 acc = __ldcg(src);
-              int z = 1;
-              for (; z + 4 <= sc.S; z += 4) {  // four loads in flight, added in order z
-                float4 b4[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) b4[j] = __ldcg(src + (size_t)(z + j) * 128 * NQ);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  acc.x += b4[j].x; acc.y += b4[j].y; acc.z += b4[j].z; acc.w += b4[j].w;
-                }
-              }
-              for (; z < sc.S; ++z) {
-                const float4 b4 = __ldcg(src + (size_t)z * 128 * NQ);
-                acc.x += b4.x; acc.y += b4.y; acc.z += b4.z; acc.w += b4.w;
-              }
-              float a4[4] = {acc.x, acc.y, acc.z, acc.w};
-              float b4[4] = {acc.x, acc.y, acc.z, acc.w};  // B operand of the H units
-              if (gv.left != nullptr && valid) {  // co-sketch: H += A^T L
-                const float4 l4 = __ldg(reinterpret_cast<const float4 *>(
-                                            gv.left + ((int64_t)f.c * sc.R0 + rc) * args.gld) + q);
-                b4[0] = l4.x; b4[1] = l4.y; b4[2] = l4.z; b4[3] = l4.w;
-              }
-              if (NORM) {  // G_hat = (d Omega - mean_d * 1^T Omega) / norm; the H units take G_hat / norm
-                const float md = sl_stat[r][0], inv = sl_stat[r][1];
-                const float4 w4 = __ldg(reinterpret_cast<const float4 *>(gv.wsum) + q);
-                const float ws[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  a4[j] = fmaf(-md, ws[j], a4[j]) * inv;
-                  b4[j] = (gv.left != nullptr ? b4[j] : a4[j]) * inv;
-                }
-              }
-              if (valid)
-                reinterpret_cast<float4 *>(gv.g_out + ((int64_t)f.c * sc.R0 + rc) * args.gld)[q] =
-                    make_float4(a4[0], a4[1], a4[2], a4[3]);
-#if SPCA_BRAW
-#pragma unroll
-              for (int j = 0; j < 4; ++j) ghi[(size_t)(4 * q + j) * sc.R0 + rc] = valid ? b4[j] : 0.f;
-#else
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                if (args.dbg & 32768) break;  // profiling knob: no G^T stores
-                float h1 = 0.f, l1 = 0.f;
-                if (valid) split3(b4[j], h1, l1);
-#if SPCA_BCOMB
-                ghi[(size_t)bcomb_row(4 * q + j, 0, LPAD) * sc.R0 + rc] = h1;
-                ghi[(size_t)bcomb_row(4 * q + j, 1, LPAD) * sc.R0 + rc] = l1;
-#else
-                ghi[(size_t)(4 * q + j) * sc.R0 + rc] = h1;
-                glo[(size_t)(4 * q + j) * sc.R0 + rc] = l1;
-#endif
-              }
-#endif
-            }
-          }
-          ptx::fence_proxy_async_global();
-          __threadfence();
-          ptx::named_bar(2, kTcEpi);
-          if (e == 0) {
-            atomicAdd(&gv.trdy[f.c * twoT + tile], 1);
-            atomicAdd(&gv.ready[f.c], 1);
+            g_phase_b(f, gv, tile, e, kTcEpi, 2u);
           }
         }
       } else {  // ------------------------------------------------ H epilogue

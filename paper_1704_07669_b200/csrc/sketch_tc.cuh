@@ -64,6 +64,19 @@ namespace spca {
 #ifndef SPCA_KPAIR
 #define SPCA_KPAIR 1
 #endif
+// Experiment (off): G units' phase B (wait for the tile's other K segments,
+// slice reduction, G^T) on a reduction team - the idle warp 3 (1), or warp 3 and
+// one more warp (2) - instead of on the four epilogue warps, l_pad 64. The
+// epilogue warps are busy ~75% of the time and pick a G unit's staged result
+// up 6.8 us late at the median (r6_kpair.txt trace), which delays G^T and with
+// it the H units; but the slice reduction on 32 / 64 threads instead of 128 is
+// itself slower, and G^T's latency is what the H units wait for: config 2
+// 1.663 (off) -> 1.894 (one warp) / 1.729 ms (two warps, which also caps the
+// kernel at 80 registers: 21 warps put six on one SM sub-partition)
+// (profiles/r6_gteam_ab.txt).
+#ifndef SPCA_GRED_TEAM
+#define SPCA_GRED_TEAM 0
+#endif
 constexpr int kTcEpi = 128;     // epilogue threads
 constexpr uint32_t kTmemCols = 512;
 #ifndef SPCA_PROMOTE
@@ -173,7 +186,16 @@ struct TcCfg {
   static constexpr int PROMO_WARPS = 4 * (LPAD / 64);  // promoters: 64 output columns per thread
   static constexpr int PROMO_BASE = 128 + CONV;        // first promoter thread
   static constexpr int EPI_BASE = PROMO_BASE + 32 * PROMO_WARPS;  // first epilogue thread
-  static constexpr int THREADS = EPI_BASE + kTcEpi;
+  // one more warp when the G slice reductions run on their own team (with the idle warp 3)
+#ifdef SPCA_FINE_TRACE
+  static constexpr bool GT = false;  // warp 3 records MMA completions
+#else
+  static constexpr bool GT = LPAD == 64 && SPCA_GRED_TEAM;
+#endif
+  // team size: warp 3 alone (SPCA_GRED_TEAM 1), or with one more warp (2: 21 warps
+  // put six on one SM sub-partition, which caps the kernel at 80 registers)
+  static constexpr int GT_THREADS = SPCA_GRED_TEAM == 2 ? 64 : 32;
+  static constexpr int THREADS = EPI_BASE + kTcEpi + ((GT && GT_THREADS == 64) ? 32 : 0);
   static constexpr uint32_t A_BYTES = 128 * 32 * 4;   // raw A tile (16 KB)
   static constexpr uint32_t BH_BYTES = (LPAD / 2) * 32 * 4;  // l_pad/2 rows of one B matrix tile
   // B stage per CTA (rank r). Stacked: [R0 | R1 | R2] of 32 rows each:
