@@ -56,6 +56,8 @@ if os.environ.get("SPCA_BUILD_KPAIR") is not None:  # experiment: K blocks per M
     FLAGS.append("-DSPCA_KPAIR=" + os.environ["SPCA_BUILD_KPAIR"])
 if os.environ.get("SPCA_BUILD_GTEAM") is not None:  # experiment: G slice reductions on their own two warps (0/1)
     FLAGS.append("-DSPCA_GRED_TEAM=" + os.environ["SPCA_BUILD_GTEAM"])
+if os.environ.get("SPCA_BUILD_GWIDE") is not None:  # experiment: G slice reduction, ten loads in flight (0/1)
+    FLAGS.append("-DSPCA_GRED_WIDE=" + os.environ["SPCA_BUILD_GWIDE"])
 
 
 def _stale() -> bool:

@@ -430,6 +430,20 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
         const float4 *src = reinterpret_cast<const float4 *>(p0 + (size_t)r * LPAD) + q;
         float4 acc = __ldcg(src);
         int z = 1;
+#if SPCA_GRED_WIDE
+        // nine more loads in flight behind the first (config 2's ten K segments: one
+        // L2 round trip per half instead of four), added in order z as below: the
+        // reduction's latency is in front of G^T, which the H units wait for
+        for (; z + 9 <= sc.S; z += 9) {
+          float4 b9[9];
+#pragma unroll
+          for (int j = 0; j < 9; ++j) b9[j] = __ldcg(src + (size_t)(z + j) * 128 * NQ);
+#pragma unroll
+          for (int j = 0; j < 9; ++j) {
+            acc.x += b9[j].x; acc.y += b9[j].y; acc.z += b9[j].z; acc.w += b9[j].w;
+          }
+        }
+#endif
         for (; z + 4 <= sc.S; z += 4) {  // four loads in flight, added in order z
           float4 b4[4];
 #pragma unroll

@@ -74,6 +74,12 @@ namespace spca {
 // 1.663 (off) -> 1.894 (one warp) / 1.729 ms (two warps, which also caps the
 // kernel at 80 registers: 21 warps put six on one SM sub-partition)
 // (profiles/r6_gteam_ab.txt).
+// Experiment (off): G slice reduction with ten partial loads in flight per half
+// instead of 1 + 4 + 4 + 1 (same order of additions): config 2 1.694 vs 1.688 ms,
+// config 5 61.3 vs 61.9 ms - within noise (profiles/r6_gwide_ab.txt)
+#ifndef SPCA_GRED_WIDE
+#define SPCA_GRED_WIDE 0
+#endif
 #ifndef SPCA_GRED_TEAM
 #define SPCA_GRED_TEAM 0
 #endif
