@@ -575,3 +575,29 @@ def test_pass_beside_foreign_kernels():
         assert torch.equal(h1, h0) and torch.equal(g1, g0) and torch.equal(c1, c0)
     torch.cuda.synchronize()
     k.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,l", [(1089, 2080, 60), (257, 1000, 30), (2081, 4000, 120), (3000 + 33, 999 * 4, 60)])
+def test_padded_k_blocks_read_zero_fill_not_memory(m, n, l):
+    """Units are padded to whole MMA-warp iterations (an odd tail of 32-deep K
+    blocks takes one more block: csrc/sketch_fused.cuh fused_decode). The extra
+    block must come from TMA out-of-bounds zero fill: the matrix here is a view
+    into a larger buffer whose other columns and rows are NaN, so a block that
+    read memory beyond n or beyond the last row would poison G or H.
+    Odd K-block counts over n (G units) and over the rows (H units)."""
+    torch = pytest.importorskip("torch")
+    if not _tc_ok():
+        pytest.skip("tensor-core path unavailable")
+    ld = (n + 64 + 3) // 4 * 4  # 16-byte row stride, at least 64 spare columns
+    big = torch.full((m + 96, ld), float("nan"), dtype=torch.float32, device="cuda")
+    a = O.gaussian(m, n, seed=m + 1).astype(np.float32)
+    big[:m, :n] = torch.from_numpy(a).cuda()
+    om = O.gaussian(n, l, seed=n + 1)
+    st = P.sketch_pass(P.DeviceRowStream(big[:m, :n]), om, precision="tc")
+    assert np.isfinite(st.g).all() and np.isfinite(st.h).all() and np.isfinite(st.col_sums).all()
+    ref = O.oracle_sketch(O.row_blocks(a, 4096), om.astype(np.float32).astype(np.float64))
+    assert rel(st.g, ref.g) <= 2e-5 and rel(st.h, ref.h) <= 2e-5
+    # the same rows pushed in two pieces (a partial chunk in the middle of the stream)
+    s2 = P.sketch_pass(P.DeviceRowStream(big[:m, :n]), om, precision="tc", block_rows=m // 2 + 1)
+    assert np.array_equal(st.g, s2.g) and np.array_equal(st.h, s2.h)
