@@ -9,10 +9,10 @@
 //   col_sums += 1^T A_c      (inside the H units)
 //
 // A_c is read from HBM by the G units (TMA, L2 evict_last) and re-read by the
-// H units D stages later (evict_first). The re-read is meant to hit L2, but
-// with three 40 MB chunks live it mostly misses: ncu measures ~2.05x the
-// bytes of A read from DRAM at config 2 (8.2 GB per 4 GB pass; 512-row chunks
-// read 1.2x but run slower). The units form one global
+// H units a stage later (evict_first). The re-read is meant to hit L2, but
+// only about half of it does: ncu measures ~1.7x the bytes of A read from
+// DRAM at config 2 (7.0 GB per 4 GB pass at lag 1; 8.2 GB at lag 2; 512-row
+// chunks read 1.2x but run slower). The units form one global
 // sequence of stages {G(s), H(s-1)}, s = 0..C, dealt round robin to CTA
 // pairs (clusters of 2, one CTA per SM), so the H contraction of chunk c
 // overlaps the G contraction of chunk c+1 inside one launch and every pair
