@@ -184,7 +184,8 @@ struct TcCfg {
   static constexpr bool STACKED = LPAD == 64 && SPCA_STACKED_64;
   static constexpr int ACC_COLS = STACKED ? 128 : LPAD;  // one accumulator
   static constexpr int NS = (kTmemCols - 2 * ACC_COLS) / 64;  // TMEM A operand stages
-  static constexpr int KP = (LPAD == 64 && SPCA_KPAIR && !SPCA_PAIRA) ? 2 : 1;  // K blocks per MMA-warp iteration
+  // K blocks per MMA-warp iteration (SPCA_KPAIR: 1 = l_pad 64 only, 2 = l_pad 128 as well)
+  static constexpr int KP = ((LPAD == 64 || SPCA_KPAIR == 2) && SPCA_KPAIR && !SPCA_PAIRA) ? 2 : 1;
   static_assert(NS % KP == 0 && SPCA_PROMOTE % KP == 0, "operand stages / accumulator period in whole iterations");
   // B ring: deep enough to cover an L2 round trip (~1-2 us) at the MMA rate
   static constexpr int GROUPS = LPAD == 64 ? SPCA_GROUPS_64 : 2;  // converter groups
