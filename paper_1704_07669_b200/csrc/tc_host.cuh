@@ -70,8 +70,11 @@ int64_t tc_chunk_rows(int64_t n, int64_t l) {
 
 // K blocks (32 deep) per work unit: the G units split n, the H units split a
 // chunk's rows, both into pieces of about this size.
-int tc_unit_kb() {
-  int u = 32;
+// l_pad 64: 40 (config 2, n = 10 000: eight K segments of 40 / 34 blocks instead
+// of ten of 32 / 26 - G units about as long as the H units and a better balanced
+// last segment: 1.681 -> 1.668 ms in three alternating runs, profiles/r6_unit40.txt)
+int tc_unit_kb(int lp) {
+  int u = lp == 64 ? 40 : 32;
   if (const char *e = getenv("SPCA_TC_UNIT_KB")) u = std::max(1, atoi(e));  // tuning knob
   return u;
 }
@@ -102,7 +105,7 @@ bool tc_dual_groups(const spca_sketch *h) {
 FusedSched tc_base_sched(const spca_sketch *h) {
   FusedSched s{};
   s.Gr = 1;
-  const int U = tc_unit_kb();
+  const int U = tc_unit_kb(h->tc_lp);
   s.R0 = (int)h->chunk_rows;
   s.nt = s.R0 / 128;
   s.T = s.nt / 2;
