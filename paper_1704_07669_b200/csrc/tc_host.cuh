@@ -70,11 +70,13 @@ int64_t tc_chunk_rows(int64_t n, int64_t l) {
 
 // K blocks (32 deep) per work unit: the G units split n, the H units split a
 // chunk's rows, both into pieces of about this size.
-// l_pad 64: 40 (config 2, n = 10 000: eight K segments of 40 / 34 blocks instead
-// of ten of 32 / 26 - G units about as long as the H units and a better balanced
-// last segment: 1.681 -> 1.668 ms in three alternating runs, profiles/r6_unit40.txt)
+// (40 for l_pad 64 - config 2: eight K segments of 40 / 34 blocks instead of ten
+// of 32 / 26 - measured 0.8% faster in three alternating runs, 1.681 -> 1.668 ms,
+// but with 7.58 instead of 6.98 GB of DRAM reads per pass: not taken,
+// profiles/r6_unit40.txt)
 int tc_unit_kb(int lp) {
-  int u = lp == 64 ? 40 : 32;
+  (void)lp;
+  int u = 32;
   if (const char *e = getenv("SPCA_TC_UNIT_KB")) u = std::max(1, atoi(e));  // tuning knob
   return u;
 }

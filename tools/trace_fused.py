@@ -49,7 +49,7 @@ stat("MMA issue span (leader)", np.where(mm, u[:, :, 6] - u[:, :, 5], np.nan).ra
 stat("B producer dep-wait end - conv start", np.where(valid & (u[:, :, 7] > 0), u[:, :, 7] - u[:, :, 0], np.nan).ravel())
 
 # per unit kind (replicates fused_decode for the single launch of this run)
-def sched(m, n, R0, U=int(os.environ.get("SPCA_TC_UNIT_KB", "40" if l <= 64 else "32"))):
+def sched(m, n, R0, U=int(os.environ.get("SPCA_TC_UNIT_KB", "32"))):
     kp = 2 if l <= 64 else 1  # K blocks per MMA-warp iteration (TcCfg::KP): kseg / hseg are multiples
     nkb = -(-n // 32); S = min(-(-nkb // U), 37); kseg = -(-(-(-nkb // S)) // kp) * kp; S = -(-nkb // kseg)
     nt = R0 // 128; T = nt // 2; nx = -(-n // 128); X = -(-nx // 2)
