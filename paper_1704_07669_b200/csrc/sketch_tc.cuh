@@ -61,8 +61,16 @@ namespace spca {
 // barrier and one commit: one wait, 24 MMAs, one commit per iteration. Every
 // unit then has an even number of K blocks (FusedSched::kp; an odd tail gets
 // one more block of TMA zero fill).
+// Build option (SPCA_BUILD_KPAIR=1), off by default: it lifts the block rate
+// (G units 14.6 -> 11.8 us per 32 K blocks; passes whose A is L2-resident or
+// whose epilogue is idle run 5-9% faster), but the full config-2 pass is bound
+// elsewhere (G -> G^T latency against the L2 capacity): equal
+// in 20-pass bursts (1.670 vs 1.670 ms), 0.7% slower over 300 back-to-back
+// passes under the power cap (1.880 vs 1.867 ms) and 7% more DRAM reads
+// (6.98 vs 6.46 GB) because the faster G units put more data between a
+// tile's two reads (profiles/r6_kpair.txt, r6_kpair_sustained.txt).
 #ifndef SPCA_KPAIR
-#define SPCA_KPAIR 1
+#define SPCA_KPAIR 0
 #endif
 // Experiment (off): G units' phase B (wait for the tile's other K segments,
 // slice reduction, G^T) on a reduction team - the idle warp 3 (1), or warp 3 and
