@@ -580,9 +580,10 @@ def test_pass_beside_foreign_kernels():
 @pytest.mark.gpu
 @pytest.mark.parametrize("m,n,l", [(1089, 2080, 60), (257, 1000, 30), (2081, 4000, 120), (3000 + 33, 999 * 4, 60)])
 def test_padded_k_blocks_read_zero_fill_not_memory(m, n, l):
-    """Units are padded to whole MMA-warp iterations (an odd tail of 32-deep K
-    blocks takes one more block: csrc/sketch_fused.cuh fused_decode). The extra
-    block must come from TMA out-of-bounds zero fill: the matrix here is a view
+    """Partial K blocks (n or the row count not a multiple of 32) and, in builds
+    with paired MMA-warp iterations (SPCA_BUILD_KPAIR: an odd tail of 32-deep K
+    blocks takes one more block, csrc/sketch_fused.cuh fused_decode), whole extra
+    blocks must come from TMA out-of-bounds zero fill: the matrix here is a view
     into a larger buffer whose other columns and rows are NaN, so a block that
     read memory beyond n or beyond the last row would poison G or H.
     Odd K-block counts over n (G units) and over the rows (H units)."""
