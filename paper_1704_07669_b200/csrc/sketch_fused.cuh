@@ -836,17 +836,8 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
             }
           } else {
             const uint32_t raw = ptx::smem_u32(smem + s * C::A_BYTES + t * 4);  // column t
-            if (args.dbg & 524288) {  // profiling knob: row-style 16-byte loads (results are garbage)
-              const uint32_t row = ptx::smem_u32(smem + s * C::A_BYTES + t * 128);
-#pragma unroll
-              for (int q4 = 0; q4 < 8; ++q4) {
-                const float4 x = ptx::lds128(row + ((q4 ^ (t & 7)) << 4));
-                v[4 * q4] = x.x; v[4 * q4 + 1] = x.y; v[4 * q4 + 2] = x.z; v[4 * q4 + 3] = x.w;
-              }
-            } else {
 #pragma unroll
             for (int kq = 0; kq < 32; ++kq) v[kq] = ptx::lds32(raw + kq * 512);
-            }
             if (SHIFT) {  // column shift on the chunk's real rows only
               const float cj = __ldg(args.cshift + (2 * f.a + (int)rank) * 128 + t);
               const int r0 = (f.k0 + kb) * 32;
@@ -871,7 +862,6 @@ tc_pass_kernel(const __grid_constant__ CUtensorMap tAg, const __grid_constant__ 
 #pragma unroll
               for (int i = 0; i < 16; ++i) p16[i] = v[2 * i] + v[2 * i + 1];
             }
-            if (!(args.dbg & 262144))  // profiling knob: no column-sum reduction
 #pragma unroll
             for (int w = 8; w >= 1; w >>= 1)
 #pragma unroll
